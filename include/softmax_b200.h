@@ -1,0 +1,169 @@
+/*
+ * softmax_b200.h -- C ABI of the B200-native row-softmax hot path.
+ *
+ * This is the drop-in boundary for the reference's softmax entry point
+ * (/root/reference/pkg/src/softmax_kit/kernels.py:350-362,
+ *   softmax(m: Matrix2D, variant: KernelVariant, cfg: LaneConfig) -> Matrix2D)
+ * and its inner plugin point (kernels.py:283-339, variant_pipeline ->
+ * PhasePipeline(maxsub, exp, sumscale)).  The reference is Python + numba;
+ * its "FFI" for this path is the Python call, so the binding a maintainer adds
+ * is a ctypes stub.  Plain pointers and sizes only: no torch
+ * types cross this boundary.
+ *
+ * Conventions
+ *  - float32 row-major [rows, cols] with row pitch ld (elements, >= cols).
+ *  - Device entry points (sk_softmax_f32, sk_row_stats_f32, sk_normalize_f32,
+ *    sk_rescale_sumexp) are asynchronous on `stream` (a cudaStream_t, passed
+ *    as void* so the header does not need cuda_runtime.h); no host sync.
+ *  - Status codes map onto the reference error taxonomy (errors.py:4-21):
+ *      SK_ERR_ARGUMENT  -> ArgumentError      (tensor.py:43-57, kernels.py:304-305)
+ *      SK_ERR_NONFINITE -> NumericDomainError (kernels.py:342-347)
+ *      SK_ERR_RESOURCE  -> ResourceError      (tensor.py:98-101)
+ *      SK_ERR_CUDA      -> SoftmaxKitError    (no reference analogue)
+ *  - Thread-safe across streams: kernels have no global state; the optional
+ *    library-managed workspace is keyed by (device, stream).
+ */
+#ifndef SOFTMAX_B200_H_
+#define SOFTMAX_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SK_ABI_VERSION 1
+
+enum sk_status {
+  SK_OK = 0,
+  SK_ERR_ARGUMENT = 1,
+  SK_ERR_NONFINITE = 2,
+  SK_ERR_CUDA = 3,
+  SK_ERR_RESOURCE = 4,
+};
+
+/* Arithmetic mode = the variant ladder (kernels.py:76-96) collapsed to what
+ * changes the numbers on a GPU:
+ *   SK_MODE_CLIPPED   ReferenceClipped (ValueClip at -64, kernels.py:99, :147)
+ *   SK_MODE_EXACT     ReferenceInference, MklStyleScalar, VectorizedSum,
+ *                     FullVectorized (no clip, accurate exp)
+ *   SK_MODE_APPROX    FullVectorizedApproxExp (no clip, ex2.approx exp;
+ *                     tolerance 1e-5, bench.py:52)                           */
+enum sk_mode { SK_MODE_CLIPPED = 0, SK_MODE_EXACT = 1, SK_MODE_APPROX = 2 };
+
+/* Sentinel stored in *bad_row when no non-finite input was seen. */
+#define SK_NO_BAD_ROW 0xFFFFFFFFFFFFFFFFull
+
+int sk_abi_version(void);
+const char* sk_status_string(int status);
+/* Last CUDA error text seen by this thread (empty if none). */
+const char* sk_last_error(void);
+
+/*
+ * Fused row softmax on device buffers.  Replaces the three numba phase loops
+ * _maxsub_rows_scalar / _exp_rows_scalar / _sumscale_rows_scalar
+ * (kernels.py:136-189) with one pass over HBM where the shape allows.
+ *
+ *  x, y       device pointers, must not alias; y receives [rows, cols].
+ *  ldx, ldy   row pitches in elements (>= cols).
+ *  bad_row    device uint64; the kernels atomicMin() the index of any row
+ *             holding NaN/+-Inf into it.  Initialise it to SK_NO_BAD_ROW once;
+ *             it is only written on bad input.  May be NULL (then a
+ *             library-owned flag is used and not reported).
+ *  workspace  device scratch of sk_softmax_workspace_bytes() bytes, zeroed
+ *             once before first use (the kernels leave it zeroed), or NULL
+ *             for a library-managed per-(device, stream) workspace.
+ * rows == 0 is a no-op.  Returns SK_OK or an error status.
+ */
+int sk_softmax_f32(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
+                   int64_t ldy, int mode, unsigned long long* bad_row, void* workspace,
+                   size_t workspace_bytes, void* stream);
+
+size_t sk_softmax_workspace_bytes(int64_t rows, int64_t cols);
+
+/*
+ * Host-buffer softmax: the compat path behind softmax(Matrix2D, ...).
+ * Copies x_host to the device in row chunks, runs sk_softmax_f32 per chunk
+ * and copies each chunk back, pipelined over several streams so H2D, compute
+ * and D2H overlap; returns after y_host is complete.  Pinned (page-locked)
+ * host buffers give full PCIe bandwidth; pageable ones work, slower.
+ * On non-finite input returns SK_ERR_NONFINITE and stores the first bad row
+ * in *bad_row_out (y_host contents then unspecified).
+ */
+int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_t cols,
+                        int mode, int device, int64_t* bad_row_out);
+
+/*
+ * Column-shard building blocks (sharding.py): local per-row statistics of
+ * the [rows, cols] block x, merged across ranks with all-reduce(MAX) on
+ * row_max then all-reduce(SUM) on row_sum.  RowStats, kernels.py:108-112.
+ *   sk_row_stats_f32:  row_max[r] = max_c x[r,c];
+ *                      row_sum[r] = sum_c exp(clip(x[r,c] - row_max[r]))  (f64)
+ *   sk_rescale_sumexp: row_sum[r] *= exp(local_max[r] - global_max[r])
+ *   sk_normalize_f32:  y[r,c] = exp(clip(x[r,c] - row_max[r])) * (1/(float)row_sum[r])
+ */
+int sk_row_stats_f32(const float* x, int64_t rows, int64_t cols, int64_t ldx, int mode,
+                     float* row_max, double* row_sum, unsigned long long* bad_row,
+                     void* workspace, size_t workspace_bytes, void* stream);
+size_t sk_row_stats_workspace_bytes(int64_t rows, int64_t cols);
+int sk_rescale_sumexp(const float* local_max, const float* global_max, double* row_sum,
+                      int64_t rows, void* stream);
+int sk_normalize_f32(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
+                     int64_t ldy, int mode, const float* row_max, const double* row_sum,
+                     void* stream);
+
+/*
+ * Page-locked host memory for Matrix2D buffers (tensor.py:90-103 allocates
+ * with np.zeros; pinned memory lets sk_softmax_f32_host reach full PCIe
+ * bandwidth).  Returns NULL on failure (-> ResourceError).
+ */
+void* sk_alloc_pinned(size_t bytes);
+void sk_free_pinned(void* p);
+
+/*
+ * Process-wide tuning / test hooks (not needed for normal use):
+ *   "path"           -1 auto, 0 force K1 (rows in registers), 1 force TMA
+ *                    segments (K2/K3), 2 force split (K4)
+ *   "k1_lpr","k1_nv","k1_u"  force a K1 instantiation (lanes per row,
+ *                    float4s per lane, rows per lane-group batch)
+ *   "grid_mult"      K1 grid = SMs * occupancy * grid_mult (default 1)
+ *   "seg_len"        target segment length (floats) for K2/K3
+ *   "skip_max_shift" 1: shift by 0 instead of the row max -- the reference's
+ *                    _SKIP_MAX_SHIFT fault hook (kernels.py:103-105, :309-311);
+ *                    large logits then overflow and verification must fail.
+ */
+int sk_set_tuning(const char* key, int value);
+
+/*
+ * Launch plan that sk_softmax_f32 would use for this shape/alignment, as a
+ * short text ("k1_vec lpr=8 nv=4 u=2 grid=..." ...), for tests and bench logs.
+ * Writes at most buflen bytes (NUL-terminated); returns SK_OK.
+ */
+int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t x_addr,
+                     uint64_t y_addr, int device, char* buf, int buflen);
+
+/*
+ * Deterministic host-side input generators (tensor.py:106-121 and the
+ * BASELINE configs).  Element i of a fill depends only on (seed, i), so
+ * chunks [start, start+n) can be generated independently and in parallel.
+ *   sk_fill_uniform_f32: fill_uniform (tensor.py:106-121): Philox4x64-10
+ *       raw draw i (numpy np.random.Philox(key=seed)) -> ((u>>11)+0.5)*2^-53
+ *       -> low+(high-low)u in f64 -> f32 -> clamp into the open interval.
+ *   sk_fill_normal_f32: N(0, sigma^2): Box-Muller on raw draws (2i, 2i+1)
+ *       giving elements 2i (cos) and 2i+1 (sin), in f64, then f32.
+ *   sk_plant_f32: sets `count` distinct flat positions of x[0, total) to
+ *       `value`; positions = first distinct (raw % total) of the Philox stream
+ *       keyed by seed ^ 0x5EEDC0FFEE, in draw order.
+ * nthreads <= 0: use all hardware threads.
+ */
+int sk_fill_uniform_f32(float* dst, int64_t n, uint64_t seed, double low, double high,
+                        uint64_t start, int nthreads);
+int sk_fill_normal_f32(float* dst, int64_t n, uint64_t seed, double sigma, uint64_t start,
+                       int nthreads);
+int sk_plant_f32(float* x, int64_t total, int64_t count, uint64_t seed, float value);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SOFTMAX_B200_H_ */

@@ -1,0 +1,44 @@
+"""B200-native fp32 row softmax -- drop-in for softmax_kit's softmax entry point.
+
+Reference: /root/reference/pkg/src/softmax_kit/kernels.py:350-362
+(``softmax(m: Matrix2D, variant: KernelVariant, cfg: LaneConfig) -> Matrix2D``).
+The numeric work runs in hand-written sm_100a kernels behind the C ABI in
+include/softmax_b200.h (libsoftmax_b200.so); this package is the host-side
+mirror of the reference interface.  There is no CPU fallback.
+"""
+
+from .errors import ArgumentError, NumericDomainError, ResourceError, SoftmaxKitError
+from .lanes import LaneConfig
+from .tensor import FillSpec, Matrix2D, alloc_matrix, fill_uniform
+from .kernels import (
+    CLIP_FLOOR,
+    FLT_MIN_NORMAL,
+    LADDER,
+    KernelVariant,
+    RowStats,
+    row_stats_device,
+    softmax,
+    softmax_into,
+    variant_mode,
+)
+
+__all__ = [
+    "ArgumentError",
+    "NumericDomainError",
+    "ResourceError",
+    "SoftmaxKitError",
+    "LaneConfig",
+    "FillSpec",
+    "Matrix2D",
+    "alloc_matrix",
+    "fill_uniform",
+    "CLIP_FLOOR",
+    "FLT_MIN_NORMAL",
+    "LADDER",
+    "KernelVariant",
+    "RowStats",
+    "row_stats_device",
+    "softmax",
+    "softmax_into",
+    "variant_mode",
+]

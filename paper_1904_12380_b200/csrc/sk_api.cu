@@ -1,0 +1,662 @@
+// sk_api.cu -- C ABI (include/softmax_b200.h): launch planning, workspaces,
+// the pipelined host-buffer path, and the column-shard building blocks.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/softmax_b200.h"
+#include "sk_rows.cuh"
+#include "sk_seg.cuh"
+#include "sk_split.cuh"
+
+namespace sk {
+namespace {
+
+thread_local std::string g_last_error;
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  (void)cudaGetLastError();
+  if (e == cudaErrorMemoryAllocation) return SK_ERR_RESOURCE;
+  return SK_ERR_CUDA;
+}
+#define SK_CUDA(call)                                   \
+  do {                                                  \
+    cudaError_t _e = (call);                            \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+int arg_fail(const std::string& msg) {
+  g_last_error = msg;
+  return SK_ERR_ARGUMENT;
+}
+
+// ---------------------------------------------------------------- device info
+struct DevInfo {
+  int sms = 0;
+  bool coop = false;
+};
+DevInfo dev_info(int dev) {
+  static std::mutex mu;
+  static std::map<int, DevInfo> cache;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  DevInfo d;
+  cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+  int coop = 0;
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  d.coop = coop != 0;
+  cache[dev] = d;
+  return d;
+}
+
+// ------------------------------------------------------------ tuning overrides
+std::atomic<int> g_force_path{-1};  // -1 auto, 0 k1, 1 seg, 2 split
+// fault hook mirroring kernels._SKIP_MAX_SHIFT (kernels.py:103-105): when set the
+// kernels shift by 0 instead of the row max, so large logits overflow exp.
+std::atomic<int> g_skip_max_shift{0};
+float shift_scale() { return g_skip_max_shift.load() ? 0.0f : 1.0f; }
+std::atomic<int> g_k1_lpr{0}, g_k1_nv{0}, g_k1_u{0}, g_grid_mult{0}, g_seg_len{0};
+
+// ------------------------------------------------------------------ K1 table
+using K1Fn = void (*)(const float*, float*, int64_t, int, int64_t, int64_t,
+                      unsigned long long*, float);
+struct K1Entry {
+  int vec, lpr, nv, u;
+  K1Fn fn[3];
+};
+#define SK_K1(VEC, LPR, NV, U)                                                   \
+  K1Entry {                                                                      \
+    VEC, LPR, NV, U, {                                                           \
+      &k1_rows<kClipAccurate, VEC, LPR, NV, U>, &k1_rows<kAccurate, VEC, LPR, NV, U>, \
+          &k1_rows<kApprox, VEC, LPR, NV, U>                                     \
+    }                                                                            \
+  }
+const K1Entry kK1Table[] = {
+    // 128-bit path (cols % 4 == 0, 16-B aligned rows)
+    SK_K1(4, 4, 1, 4), SK_K1(4, 8, 1, 4), SK_K1(4, 16, 1, 4), SK_K1(4, 8, 2, 2),
+    SK_K1(4, 8, 4, 1), SK_K1(4, 8, 4, 2), SK_K1(4, 16, 2, 2), SK_K1(4, 16, 2, 1),
+    SK_K1(4, 16, 4, 1), SK_K1(4, 16, 4, 2), SK_K1(4, 32, 1, 4), SK_K1(4, 32, 2, 2),
+    SK_K1(4, 32, 4, 1), SK_K1(4, 32, 8, 1), SK_K1(4, 32, 1, 2), SK_K1(4, 32, 2, 1),
+    // 32-bit path (any pitch / alignment)
+    SK_K1(1, 8, 1, 4), SK_K1(1, 16, 1, 4), SK_K1(1, 32, 1, 4), SK_K1(1, 16, 4, 2),
+    SK_K1(1, 32, 2, 2), SK_K1(1, 32, 4, 1), SK_K1(1, 32, 8, 1), SK_K1(1, 32, 16, 1),
+    SK_K1(1, 32, 32, 1),
+};
+#undef SK_K1
+
+const K1Entry* k1_find(int vec, int lpr, int nv, int u) {
+  for (const auto& e : kK1Table)
+    if (e.vec == vec && e.lpr == lpr && e.nv == nv && e.u == u) return &e;
+  return nullptr;
+}
+
+// default K1 shape per row length (covers cols <= 1024)
+void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u) {
+  if (vec == 4) {
+    if (cols <= 16) { lpr = 4; nv = 1; u = 4; }
+    else if (cols <= 32) { lpr = 8; nv = 1; u = 4; }
+    else if (cols <= 64) { lpr = 16; nv = 1; u = 4; }
+    else if (cols <= 128) { lpr = 8; nv = 4; u = 2; }
+    else if (cols <= 256) { lpr = 16; nv = 4; u = 1; }
+    else if (cols <= 512) { lpr = 32; nv = 4; u = 1; }
+    else { lpr = 32; nv = 8; u = 1; }
+  } else {
+    if (cols <= 8) { lpr = 8; nv = 1; u = 4; }
+    else if (cols <= 16) { lpr = 16; nv = 1; u = 4; }
+    else if (cols <= 32) { lpr = 32; nv = 1; u = 4; }
+    else if (cols <= 64) { lpr = 16; nv = 4; u = 2; }
+    else if (cols <= 128) { lpr = 32; nv = 4; u = 1; }
+    else if (cols <= 256) { lpr = 32; nv = 8; u = 1; }
+    else if (cols <= 512) { lpr = 32; nv = 16; u = 1; }
+    else { lpr = 32; nv = 32; u = 1; }
+  }
+}
+
+// --------------------------------------------------------------- seg table
+using SegFn = void (*)(const float*, float*, int64_t, int64_t, int64_t, int64_t, int, int,
+                       unsigned*, RowPartial*, unsigned long long*, float);
+template <int NV>
+SegFn seg_fn(int mode) {
+  switch (mode) {
+    case kClipAccurate: return &k_seg<kClipAccurate, NV>;
+    case kAccurate: return &k_seg<kAccurate, NV>;
+    default: return &k_seg<kApprox, NV>;
+  }
+}
+constexpr int kSegNV = 4;
+constexpr int kSegMaxThreads = 512;
+constexpr int64_t kSegCap = int64_t(kSegMaxThreads) * kSegNV * 4;  // 8192 floats / CTA
+
+// Occupancy per (kernel, block, smem, device), cached: the query is not free
+// and sk_softmax_f32 is called once per softmax.
+int occupancy(const void* fn, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(fn, threads, smem, dev);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem) != cudaSuccess) {
+    (void)cudaGetLastError();
+    nb = 0;
+  }
+  std::lock_guard<std::mutex> g(mu);
+  cache[key] = nb;
+  return nb;
+}
+
+// --------------------------------------------------------------- planning
+enum PathKind { kPathK1 = 0, kPathSeg = 1, kPathSplit = 2 };
+
+struct Plan {
+  PathKind kind = kPathK1;
+  // K1
+  const K1Entry* k1 = nullptr;
+  // seg
+  int nseg = 1, seglen = 0, threads = 0;
+  size_t smem = 0;
+  // split
+  int nch = 0;
+  int64_t grid = 0;
+  bool vec = false;
+};
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct WsLayout {
+  size_t bad = 0, cnt = 0, part = 0, rmax = 0, rsum = 0, total = 0;
+};
+WsLayout ws_layout(int64_t rows, int64_t parts_per_row) {
+  WsLayout l;
+  l.bad = 0;
+  l.cnt = 256;
+  l.part = align_up(l.cnt + size_t(rows) * 4, 256);
+  l.rmax = align_up(l.part + size_t(rows) * size_t(parts_per_row) * sizeof(RowPartial), 256);
+  l.rsum = align_up(l.rmax + size_t(rows) * 4, 256);
+  l.total = align_up(l.rsum + size_t(rows) * 8, 256);
+  return l;
+}
+
+int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa, uint64_t ya,
+              int mode, int dev, Plan& p) {
+  const DevInfo di = dev_info(dev);
+  const bool vec = (cols % 4 == 0) && (ldx % 4 == 0) && (ldy % 4 == 0) && (xa % 16 == 0) &&
+                   (ya % 16 == 0);
+  p.vec = vec;
+  int force = g_force_path.load();
+  PathKind kind;
+  if (force >= 0) kind = static_cast<PathKind>(force);
+  else if (cols <= 1024) kind = kPathK1;
+  else if (vec) kind = kPathSeg;
+  else kind = kPathSplit;
+  if (kind == kPathK1 && cols > 1024) return arg_fail("k1 path needs cols <= 1024");
+  if (kind == kPathSeg && !vec) return arg_fail("seg path needs 16-B aligned rows");
+
+  if (kind == kPathK1) {
+    int lpr, nv, u;
+    k1_default(vec ? 4 : 1, cols, lpr, nv, u);
+    if (g_k1_lpr.load() > 0) { lpr = g_k1_lpr; nv = g_k1_nv; u = g_k1_u; }
+    const K1Entry* e = k1_find(vec ? 4 : 1, lpr, nv, u);
+    if (!e) return arg_fail("no K1 instantiation for the requested shape");
+    if (int64_t(lpr) * nv * e->vec < cols) return arg_fail("K1 shape does not cover cols");
+    p.kind = kPathK1;
+    p.k1 = e;
+    const int64_t rows_per_cta = int64_t(kRowsThreads / 32) * u * (32 / lpr);
+    const int64_t need = (rows + rows_per_cta - 1) / rows_per_cta;
+    int occ = occupancy(reinterpret_cast<const void*>(e->fn[mode]), kRowsThreads, 0);
+    int mult = g_grid_mult.load() > 0 ? g_grid_mult.load() : 1;
+    const int64_t cap = int64_t(di.sms) * std::max(occ, 1) * mult;
+    p.grid = std::max<int64_t>(1, std::min(need, cap));
+    return SK_OK;
+  }
+  if (kind == kPathSeg) {
+    int64_t target = g_seg_len.load() > 0 ? g_seg_len.load() : kSegCap;
+    target = std::min<int64_t>(target, kSegCap);
+    int64_t nseg = (cols + target - 1) / target;
+    int64_t seglen = align_up((cols + nseg - 1) / nseg, 4);
+    int threads = static_cast<int>(align_up((seglen / 4 + kSegNV - 1) / kSegNV, 32));
+    threads = std::max(threads, 64);
+    const size_t smem = size_t(kSegStages) * threads * kSegNV * 4 * sizeof(float);
+    SegFn fn = seg_fn<kSegNV>(mode);
+    const int occ = occupancy(reinterpret_cast<const void*>(fn), threads, smem);
+    const int64_t items = rows * nseg;
+    const int64_t cap = int64_t(di.sms) * std::max(occ, 1);
+    p.kind = kPathSeg;
+    p.nseg = static_cast<int>(nseg);
+    p.seglen = static_cast<int>(seglen);
+    p.threads = threads;
+    p.smem = smem;
+    p.grid = std::min(items, cap);
+    if (nseg > 1 && (!di.coop || nseg > p.grid || occ < 1)) {
+      if (force >= 0) return arg_fail("seg path cannot co-schedule this row split");
+      kind = kPathSplit;  // rows too long to co-schedule: fall through
+    } else {
+      return SK_OK;
+    }
+  }
+  p.kind = kPathSplit;
+  p.nch = static_cast<int>((cols + kSplitChunk - 1) / kSplitChunk);
+  p.grid = rows * p.nch;
+  return SK_OK;
+}
+
+size_t plan_ws_bytes(const Plan& p, int64_t rows) {
+  if (p.kind == kPathSeg) return ws_layout(rows, p.nseg).total;
+  if (p.kind == kPathSplit) return ws_layout(rows, p.nch).total;
+  return ws_layout(0, 0).total;
+}
+
+// ------------------------------------------------- library-managed workspace
+struct Ws {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+std::mutex g_ws_mu;
+std::map<std::pair<int, cudaStream_t>, Ws> g_ws;
+
+int get_ws(int dev, cudaStream_t s, size_t need, void** out) {
+  std::lock_guard<std::mutex> g(g_ws_mu);
+  Ws& w = g_ws[{dev, s}];
+  if (w.bytes < need) {
+    size_t nb = std::max(need, size_t(1) << 20);
+    if (w.ptr) SK_CUDA(cudaFreeAsync(w.ptr, s));
+    w.ptr = nullptr;
+    w.bytes = 0;
+    SK_CUDA(cudaMallocAsync(&w.ptr, nb, s));
+    SK_CUDA(cudaMemsetAsync(w.ptr, 0, nb, s));
+    // bad-row flag lives at offset 0: "no bad row"
+    SK_CUDA(cudaMemsetAsync(w.ptr, 0xFF, 8, s));
+    w.bytes = nb;
+  }
+  *out = w.ptr;
+  return SK_OK;
+}
+
+int check_common(const float* x, const void* y, int64_t rows, int64_t cols, int64_t ldx,
+                 int64_t ldy, int mode) {
+  if (rows < 0 || cols < 1) return arg_fail("need rows >= 0 and cols >= 1");
+  if (ldx < cols || ldy < cols) return arg_fail("row pitch must be >= cols");
+  if (mode < 0 || mode > 2) return arg_fail("mode must be SK_MODE_CLIPPED/EXACT/APPROX");
+  if (rows > 0 && (!x || !y)) return arg_fail("null buffer");
+  if (cols > (int64_t(1) << 40)) return arg_fail("cols too large");
+  return SK_OK;
+}
+
+int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t cols,
+                int64_t ldx, int64_t ldy, int mode, unsigned long long* bad, char* ws,
+                cudaStream_t s) {
+  if (p.kind == kPathK1) {
+    p.k1->fn[mode]<<<static_cast<unsigned>(p.grid), kRowsThreads, 0, s>>>(
+        x, y, rows, static_cast<int>(cols), ldx, ldy, bad, shift_scale());
+    SK_CUDA(cudaGetLastError());
+    return SK_OK;
+  }
+  if (p.kind == kPathSeg) {
+    const WsLayout l = ws_layout(rows, p.nseg);
+    unsigned* cnt = reinterpret_cast<unsigned*>(ws + l.cnt);
+    RowPartial* part = reinterpret_cast<RowPartial*>(ws + l.part);
+    SegFn fn = seg_fn<kSegNV>(mode);
+    int nseg = p.nseg, seglen = p.seglen;
+    float sh = shift_scale();
+    void* args[] = {(void*)&x,   (void*)&y,    (void*)&rows,   (void*)&cols,
+                    (void*)&ldx, (void*)&ldy,  (void*)&nseg,   (void*)&seglen,
+                    (void*)&cnt, (void*)&part, (void*)&bad,    (void*)&sh};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(p.grid));
+    cfg.blockDim = dim3(p.threads);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = p.nseg > 1 ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SK_CUDA(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(fn), args));
+    return SK_OK;
+  }
+  // split: stats -> combine -> normalize
+  const WsLayout l = ws_layout(rows, p.nch);
+  RowPartial* part = reinterpret_cast<RowPartial*>(ws + l.part);
+  float* rmax = reinterpret_cast<float*>(ws + l.rmax);
+  double* rsum = reinterpret_cast<double*>(ws + l.rsum);
+  const unsigned g = static_cast<unsigned>(rows * p.nch);
+  switch (mode) {
+    case kClipAccurate: k4_stats<kClipAccurate><<<g, kSplitThreads, 0, s>>>(x, rows, cols, ldx, p.nch, part, bad, shift_scale()); break;
+    case kAccurate: k4_stats<kAccurate><<<g, kSplitThreads, 0, s>>>(x, rows, cols, ldx, p.nch, part, bad, shift_scale()); break;
+    default: k4_stats<kApprox><<<g, kSplitThreads, 0, s>>>(x, rows, cols, ldx, p.nch, part, bad, shift_scale()); break;
+  }
+  SK_CUDA(cudaGetLastError());
+  k4_combine<<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, s>>>(part, rows, p.nch,
+                                                                          rmax, rsum);
+  SK_CUDA(cudaGetLastError());
+  const bool v4 = p.vec;
+#define SK_NORM(M)                                                                          \
+  if (v4)                                                                                   \
+    k4_normalize<M, 4><<<g, kSplitThreads, 0, s>>>(x, y, rows, cols, ldx, ldy, p.nch, rmax, \
+                                                   rsum);                                   \
+  else                                                                                      \
+    k4_normalize<M, 1><<<g, kSplitThreads, 0, s>>>(x, y, rows, cols, ldx, ldy, p.nch, rmax, rsum);
+  switch (mode) {
+    case kClipAccurate: SK_NORM(kClipAccurate); break;
+    case kAccurate: SK_NORM(kAccurate); break;
+    default: SK_NORM(kApprox); break;
+  }
+#undef SK_NORM
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}
+
+int softmax_dev(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx, int64_t ldy,
+                int mode, unsigned long long* bad, void* workspace, size_t ws_bytes,
+                cudaStream_t s) {
+  int st = check_common(x, y, rows, cols, ldx, ldy, mode);
+  if (st) return st;
+  if (rows == 0) return SK_OK;
+  if (reinterpret_cast<const char*>(x) < reinterpret_cast<const char*>(y) + rows * ldy * 4 &&
+      reinterpret_cast<const char*>(y) < reinterpret_cast<const char*>(x) + rows * ldx * 4)
+    return arg_fail("x and y must not alias");
+  int dev = 0;
+  SK_CUDA(cudaGetDevice(&dev));
+  Plan p;
+  st = make_plan(rows, cols, ldx, ldy, reinterpret_cast<uint64_t>(x),
+                 reinterpret_cast<uint64_t>(y), mode, dev, p);
+  if (st) return st;
+  const size_t need = plan_ws_bytes(p, rows);
+  char* ws = static_cast<char*>(workspace);
+  if (ws && ws_bytes < need) return arg_fail("workspace too small");
+  if (!ws) {
+    void* w = nullptr;
+    st = get_ws(dev, s, need, &w);
+    if (st) return st;
+    ws = static_cast<char*>(w);
+  }
+  if (!bad) bad = reinterpret_cast<unsigned long long*>(ws);  // library flag at offset 0
+  return launch_plan(p, x, y, rows, cols, ldx, ldy, mode, bad, ws, s);
+}
+
+// ------------------------------------------------ pipelined host-buffer path
+constexpr int kHostStreams = 3;
+struct HostCtx {
+  std::mutex mu;
+  bool init = false;
+  cudaStream_t st[kHostStreams] = {};
+  float* dx[kHostStreams] = {};
+  float* dy[kHostStreams] = {};
+  unsigned long long* dbad = nullptr;  // one bad-row flag per chunk
+  unsigned long long* hbad = nullptr;  // pinned mirror
+  int64_t flag_cap = 0;
+  size_t cap_bytes = 0;
+};
+std::mutex g_host_mu;
+std::map<int, HostCtx*> g_host;
+
+HostCtx* host_ctx(int dev) {
+  std::lock_guard<std::mutex> g(g_host_mu);
+  HostCtx*& c = g_host[dev];
+  if (!c) c = new HostCtx();
+  return c;
+}
+
+}  // namespace
+}  // namespace sk
+
+using namespace sk;
+
+extern "C" {
+
+int sk_abi_version(void) { return SK_ABI_VERSION; }
+
+const char* sk_status_string(int status) {
+  switch (status) {
+    case SK_OK: return "ok";
+    case SK_ERR_ARGUMENT: return "invalid argument";
+    case SK_ERR_NONFINITE: return "non-finite logits";
+    case SK_ERR_CUDA: return "cuda error";
+    case SK_ERR_RESOURCE: return "allocation failed";
+    default: return "unknown status";
+  }
+}
+
+const char* sk_last_error(void) { return g_last_error.c_str(); }
+
+void* sk_alloc_pinned(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+    g_last_error = "cudaHostAlloc failed";
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void sk_free_pinned(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int sk_set_tuning(const char* key, int value) {
+  if (!key) return SK_ERR_ARGUMENT;
+  std::string k(key);
+  if (k == "path") g_force_path = value;
+  else if (k == "k1_lpr") g_k1_lpr = value;
+  else if (k == "k1_nv") g_k1_nv = value;
+  else if (k == "k1_u") g_k1_u = value;
+  else if (k == "grid_mult") g_grid_mult = value;
+  else if (k == "seg_len") g_seg_len = value;
+  else if (k == "skip_max_shift") g_skip_max_shift = value;
+  else return arg_fail("unknown tuning key " + k);
+  return SK_OK;
+}
+
+size_t sk_softmax_workspace_bytes(int64_t rows, int64_t cols) {
+  if (rows <= 0 || cols <= 0) return ws_layout(0, 0).total;
+  const int64_t nseg = (cols + kSegCap - 1) / kSegCap;
+  const int64_t nch = (cols + kSplitChunk - 1) / kSplitChunk;
+  return std::max(ws_layout(rows, nseg).total, ws_layout(rows, nch).total);
+}
+
+int sk_softmax_f32(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
+                   int64_t ldy, int mode, unsigned long long* bad_row, void* workspace,
+                   size_t workspace_bytes, void* stream) {
+  return softmax_dev(x, y, rows, cols, ldx, ldy, mode, bad_row, workspace, workspace_bytes,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t x_addr,
+                     uint64_t y_addr, int device, char* buf, int buflen) {
+  if (!buf || buflen < 1) return arg_fail("null buffer");
+  int st = check_common(reinterpret_cast<const float*>(1), reinterpret_cast<const void*>(1),
+                        rows, cols, ldx, ldy, 0);
+  if (st) return st;
+  Plan p;
+  st = make_plan(rows, cols, ldx, ldy, x_addr, y_addr, 0, device, p);
+  if (st) return st;
+  if (p.kind == kPathK1)
+    snprintf(buf, buflen, "k1 vec=%d lpr=%d nv=%d u=%d threads=%d grid=%lld", p.k1->vec,
+             p.k1->lpr, p.k1->nv, p.k1->u, kRowsThreads, (long long)p.grid);
+  else if (p.kind == kPathSeg)
+    snprintf(buf, buflen, "%s nseg=%d seglen=%d threads=%d smem=%zu grid=%lld",
+             p.nseg == 1 ? "k2_tma" : "k3_coop", p.nseg, p.seglen, p.threads, p.smem,
+             (long long)p.grid);
+  else
+    snprintf(buf, buflen, "k4_split vec=%d nch=%d grid=%lld", p.vec ? 4 : 1, p.nch,
+             (long long)p.grid);
+  return SK_OK;
+}
+
+int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_t cols,
+                        int mode, int device, int64_t* bad_row_out) {
+  if (bad_row_out) *bad_row_out = -1;
+  int st = check_common(x_host, y_host, rows, cols, cols, cols, mode);
+  if (st) return st;
+  if (rows == 0) return SK_OK;
+  SK_CUDA(cudaSetDevice(device));
+  HostCtx* c = host_ctx(device);
+  std::lock_guard<std::mutex> g(c->mu);
+  if (!c->init) {
+    for (int i = 0; i < kHostStreams; ++i)
+      SK_CUDA(cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking));
+    c->init = true;
+  }
+  const int64_t row_bytes = cols * 4;
+  const int64_t total = rows * row_bytes;
+  // chunk: ~1/8 of the job, 2..32 MiB, whole rows
+  int64_t chunk_bytes = std::min<int64_t>(std::max<int64_t>(total / 8, 2 << 20), 32 << 20);
+  int64_t chunk_rows = std::max<int64_t>(1, chunk_bytes / row_bytes);
+  chunk_rows = std::min(chunk_rows, rows);
+  const size_t need = size_t(chunk_rows * row_bytes);
+  if (c->cap_bytes < need) {
+    for (int i = 0; i < kHostStreams; ++i) SK_CUDA(cudaStreamSynchronize(c->st[i]));
+    for (int i = 0; i < kHostStreams; ++i) {
+      if (c->dx[i]) cudaFree(c->dx[i]);
+      if (c->dy[i]) cudaFree(c->dy[i]);
+      c->dx[i] = c->dy[i] = nullptr;
+    }
+    c->cap_bytes = 0;
+    for (int i = 0; i < kHostStreams; ++i) {
+      SK_CUDA(cudaMalloc(&c->dx[i], need));
+      SK_CUDA(cudaMalloc(&c->dy[i], need));
+    }
+    c->cap_bytes = need;
+  }
+  const int64_t nchunks = (rows + chunk_rows - 1) / chunk_rows;
+  if (c->flag_cap < nchunks) {
+    if (c->dbad) cudaFree(c->dbad);
+    if (c->hbad) cudaFreeHost(c->hbad);
+    c->dbad = nullptr;
+    c->hbad = nullptr;
+    c->flag_cap = 0;
+    const int64_t cap = std::max<int64_t>(nchunks, 64);
+    SK_CUDA(cudaMalloc(&c->dbad, cap * sizeof(unsigned long long)));
+    SK_CUDA(cudaMemset(c->dbad, 0xFF, cap * sizeof(unsigned long long)));
+    SK_CUDA(cudaMallocHost(&c->hbad, cap * sizeof(unsigned long long)));
+    c->flag_cap = cap;
+  }
+  // chunk k on stream k % kHostStreams: H2D -> fused kernel -> D2H -> its flag.
+  // In-order streams make buffer reuse safe; the copy engines overlap H2D of one
+  // chunk with D2H of another.
+  for (int64_t k = 0; k < nchunks; ++k) {
+    const int i = static_cast<int>(k % kHostStreams);
+    const int64_t r0 = k * chunk_rows;
+    const int64_t nr = std::min(chunk_rows, rows - r0);
+    const size_t bytes = size_t(nr * row_bytes);
+    SK_CUDA(cudaMemcpyAsync(c->dx[i], x_host + r0 * cols, bytes, cudaMemcpyHostToDevice,
+                            c->st[i]));
+    st = softmax_dev(c->dx[i], c->dy[i], nr, cols, cols, cols, mode, c->dbad + k, nullptr, 0,
+                     c->st[i]);
+    if (st) return st;
+    SK_CUDA(cudaMemcpyAsync(y_host + r0 * cols, c->dy[i], bytes, cudaMemcpyDeviceToHost,
+                            c->st[i]));
+    SK_CUDA(cudaMemcpyAsync(c->hbad + k, c->dbad + k, sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, c->st[i]));
+  }
+  for (int i = 0; i < kHostStreams; ++i) SK_CUDA(cudaStreamSynchronize(c->st[i]));
+  for (int64_t k = 0; k < nchunks; ++k) {
+    if (c->hbad[k] != SK_NO_BAD_ROW) {
+      const int64_t row = k * chunk_rows + static_cast<int64_t>(c->hbad[k]);
+      SK_CUDA(cudaMemset(c->dbad, 0xFF, nchunks * sizeof(unsigned long long)));
+      if (bad_row_out) *bad_row_out = row;
+      g_last_error = "non-finite logits in row " + std::to_string(row);
+      return SK_ERR_NONFINITE;
+    }
+  }
+  return SK_OK;
+}
+
+size_t sk_row_stats_workspace_bytes(int64_t rows, int64_t cols) {
+  const int64_t nch = (cols + kSplitChunk - 1) / kSplitChunk;
+  return ws_layout(std::max<int64_t>(rows, 0), nch).total;
+}
+
+int sk_row_stats_f32(const float* x, int64_t rows, int64_t cols, int64_t ldx, int mode,
+                     float* row_max, double* row_sum, unsigned long long* bad_row,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+  int st = check_common(x, row_max, rows, cols, ldx, ldx, mode);
+  if (st) return st;
+  if (rows == 0) return SK_OK;
+  if (!row_sum) return arg_fail("null row_sum");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int dev = 0;
+  SK_CUDA(cudaGetDevice(&dev));
+  const int nch = static_cast<int>((cols + kSplitChunk - 1) / kSplitChunk);
+  const WsLayout l = ws_layout(rows, nch);
+  char* ws = static_cast<char*>(workspace);
+  if (ws && workspace_bytes < l.total) return arg_fail("workspace too small");
+  if (!ws) {
+    void* w = nullptr;
+    st = get_ws(dev, s, l.total, &w);
+    if (st) return st;
+    ws = static_cast<char*>(w);
+  }
+  if (!bad_row) bad_row = reinterpret_cast<unsigned long long*>(ws);
+  RowPartial* part = reinterpret_cast<RowPartial*>(ws + l.part);
+  const unsigned g = static_cast<unsigned>(rows * nch);
+  switch (mode) {
+    case kClipAccurate: k4_stats<kClipAccurate><<<g, kSplitThreads, 0, s>>>(x, rows, cols, ldx, nch, part, bad_row, shift_scale()); break;
+    case kAccurate: k4_stats<kAccurate><<<g, kSplitThreads, 0, s>>>(x, rows, cols, ldx, nch, part, bad_row, shift_scale()); break;
+    default: k4_stats<kApprox><<<g, kSplitThreads, 0, s>>>(x, rows, cols, ldx, nch, part, bad_row, shift_scale()); break;
+  }
+  SK_CUDA(cudaGetLastError());
+  k4_combine<<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, s>>>(part, rows, nch,
+                                                                          row_max, row_sum);
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}
+
+int sk_rescale_sumexp(const float* local_max, const float* global_max, double* row_sum,
+                      int64_t rows, void* stream) {
+  if (rows < 0) return arg_fail("rows < 0");
+  if (rows == 0) return SK_OK;
+  if (!local_max || !global_max || !row_sum) return arg_fail("null buffer");
+  k4_rescale<<<static_cast<unsigned>((rows + 255) / 256), 256, 0,
+               static_cast<cudaStream_t>(stream)>>>(local_max, global_max, row_sum, rows);
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}
+
+int sk_normalize_f32(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
+                     int64_t ldy, int mode, const float* row_max, const double* row_sum,
+                     void* stream) {
+  int st = check_common(x, y, rows, cols, ldx, ldy, mode);
+  if (st) return st;
+  if (rows == 0) return SK_OK;
+  if (!row_max || !row_sum) return arg_fail("null row statistics");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int nch = static_cast<int>((cols + kSplitChunk - 1) / kSplitChunk);
+  const unsigned g = static_cast<unsigned>(rows * nch);
+  const bool v4 = (cols % 4 == 0) && (ldx % 4 == 0) && (ldy % 4 == 0) &&
+                  (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
+                  (reinterpret_cast<uintptr_t>(y) % 16 == 0);
+#define SK_NORM(M)                                                                            \
+  if (v4)                                                                                     \
+    k4_normalize<M, 4><<<g, kSplitThreads, 0, s>>>(x, y, rows, cols, ldx, ldy, nch, row_max,  \
+                                                   row_sum);                                  \
+  else                                                                                        \
+    k4_normalize<M, 1><<<g, kSplitThreads, 0, s>>>(x, y, rows, cols, ldx, ldy, nch, row_max, row_sum);
+  switch (mode) {
+    case kClipAccurate: SK_NORM(kClipAccurate); break;
+    case kAccurate: SK_NORM(kAccurate); break;
+    default: SK_NORM(kApprox); break;
+  }
+#undef SK_NORM
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}
+
+}  // extern "C"

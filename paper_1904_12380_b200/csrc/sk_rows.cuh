@@ -1,0 +1,127 @@
+// sk_rows.cuh -- K1: short rows held in registers, LPR lanes per row.
+//
+// Replaces, for C <= 1024, the three reference phase loops
+//   _maxsub_rows_scalar  kernels.py:136-151
+//   _exp_rows_scalar     kernels.py:171-174
+//   _sumscale_rows_scalar kernels.py:177-189
+// with one pass: each row is read from HBM once (128-bit streaming loads when
+// the row pitch allows, 32-bit coalesced loads otherwise), reduced with
+// __shfl_xor inside an aligned group of LPR lanes, and written once.
+//
+// Work unit: one warp owns U * (32/LPR) consecutive rows per iteration; lane
+// `sl` of a row group holds vectors j*LPR+sl, j < NV, of VEC floats each, so a
+// warp-wide load instruction touches (32/LPR) rows * LPR*VEC*4 contiguous bytes.
+#pragma once
+#include "sk_common.cuh"
+
+namespace sk {
+
+constexpr int kRowsThreads = 256;
+
+template <int MODE, int VEC, int LPR, int NV, int U>
+__global__ void __launch_bounds__(kRowsThreads)
+    k1_rows(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int cols,
+            int64_t ldx, int64_t ldy, unsigned long long* __restrict__ bad_row,
+            float shift_scale) {
+  static_assert(VEC == 1 || VEC == 4, "VEC");
+  static_assert(LPR >= 1 && LPR <= 32 && (LPR & (LPR - 1)) == 0, "LPR");
+  constexpr int RPW = 32 / LPR;
+  constexpr int ROWS_ITER = U * RPW;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPR;
+  const int sl = lane % LPR;
+  const int64_t gwarp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarp = (int64_t(gridDim.x) * blockDim.x) >> 5;
+
+  for (int64_t base = gwarp * ROWS_ITER; base < rows; base += nwarp * ROWS_ITER) {
+    float v[U][NV][VEC];
+    bool bad[U];
+    // ---- one batch of loads: U*NV independent requests in flight per lane
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = base + u * RPW + sub;
+      const bool rv = r < rows;
+      const float* xr = x + (rv ? r : 0) * ldx;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const int c = (j * LPR + sl) * VEC;
+        if (rv && c < cols) {
+          if constexpr (VEC == 4) {
+            const float4 t = ld_stream4(xr + c);
+            v[u][j][0] = t.x; v[u][j][1] = t.y; v[u][j][2] = t.z; v[u][j][3] = t.w;
+          } else {
+            v[u][j][0] = ld_stream1(xr + c);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) v[u][j][k] = kPadLogit;
+        }
+      }
+    }
+    // ---- row max (strict-'>' scan == max for finite data) + finite check
+    float m[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float mu = kPadLogit;
+      bool b = false;
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+          mu = fmaxf(mu, v[u][j][k]);
+          b |= not_finite(v[u][j][k]);
+        }
+      bad[u] = b;
+      m[u] = group_max<LPR>(mu) * shift_scale;  // shift_scale = 0: fault hook
+    }
+    // ---- shift, clip, exp (kept in registers), row sum
+    float rcp[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = base + u * RPW + sub;
+      const bool rv = r < rows;
+      float s = 0.0f;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const int c = (j * LPR + sl) * VEC;
+        const bool ok = rv && c < cols;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+          const float e = shifted_exp<MODE>(v[u][j][k], m[u]);
+          v[u][j][k] = e;
+          s += ok ? e : 0.0f;
+        }
+      }
+      rcp[u] = recip_of_sum(group_sum<LPR>(static_cast<double>(s)));
+    }
+    // ---- scale + flush, write once
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = base + u * RPW + sub;
+      if (r >= rows) continue;
+      float* yr = y + r * ldy;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const int c = (j * LPR + sl) * VEC;
+        if (c < cols) {
+          if constexpr (VEC == 4) {
+            float4 t;
+            t.x = scale_flush(v[u][j][0], rcp[u]);
+            t.y = scale_flush(v[u][j][1], rcp[u]);
+            t.z = scale_flush(v[u][j][2], rcp[u]);
+            t.w = scale_flush(v[u][j][3], rcp[u]);
+            st_stream4(yr + c, t);
+          } else {
+            st_stream1(yr + c, scale_flush(v[u][j][0], rcp[u]));
+          }
+        }
+      }
+    }
+    // ---- non-finite input: report the smallest offending row (kernels.py:342-347)
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (bad[u]) atomicMin(bad_row, static_cast<unsigned long long>(base + u * RPW + sub));
+  }
+}
+
+}  // namespace sk

@@ -1,0 +1,163 @@
+// sk_split.cuh -- K4: split softmax = row statistics pass + normalize pass.
+//
+// Used for (a) column-sharded softmax across GPUs (the per-row (max, sum)
+// pair is all that crosses NVLink; see sharding.py) and (b) long rows whose
+// pitch or base is not 16-B aligned (no TMA), at 12 B/element.
+//
+//   k4_stats:   item (row, chunk) -> partial (m_k, s_k), s_k = sum exp(clip(x - m_k))
+//   k4_combine: per row M = max m_k, S = sum s_k * exp(m_k - M)      (f64, fixed order)
+//   k4_rescale: s *= exp(m_local - M_global)   (between the two all-reduces)
+//   k4_normalize: y = exp(clip(x - M)) * (1/(float)S), flush  -- the reference's
+//               own operation order (kernels.py:144-189) given the row stats.
+//
+// RowStats / row_stats (kernels.py:108-112, 272-276) is the (max, sum) pair.
+#pragma once
+#include "sk_common.cuh"
+#include "sk_seg.cuh"
+
+namespace sk {
+
+constexpr int kSplitThreads = 256;
+constexpr int kSplitPerThread = 16;
+constexpr int kSplitChunk = kSplitThreads * kSplitPerThread;  // 4096 floats
+
+__device__ __forceinline__ float block_max_256(float v, float* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = group_max<32>(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    float t = lane < (kSplitThreads / 32) ? red[lane] : kPadLogit;
+    t = group_max<32>(t);
+    if (lane == 0) red[32] = t;
+  }
+  __syncthreads();
+  const float r = red[32];
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ double block_sum_256(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = group_sum<32>(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    double t = lane < (kSplitThreads / 32) ? red[lane] : 0.0;
+    t = group_sum<32>(t);
+    if (lane == 0) red[32] = t;
+  }
+  __syncthreads();
+  const double r = red[32];
+  __syncthreads();
+  return r;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kSplitThreads)
+    k4_stats(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx, int nch,
+             RowPartial* __restrict__ partials, unsigned long long* __restrict__ bad_row,
+             float shift_scale) {
+  __shared__ float red_f[33];
+  __shared__ double red_d[33];
+  const int64_t w = blockIdx.x;
+  const int64_t row = w / nch;
+  const int ch = static_cast<int>(w - row * nch);
+  const int64_t c0 = int64_t(ch) * kSplitChunk;
+  const float* xr = x + row * ldx + c0;
+  const int64_t rem = cols - c0;
+  const int len = static_cast<int>(rem < kSplitChunk ? rem : kSplitChunk);
+  float v[kSplitPerThread];
+  float mt = kPadLogit;
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < kSplitPerThread; ++i) {
+    const int c = threadIdx.x + i * kSplitThreads;
+    v[i] = c < len ? ld_stream1(xr + c) : kPadLogit;
+    mt = fmaxf(mt, v[i]);
+    bad |= not_finite(v[i]);
+  }
+  if (bad) atomicMin(bad_row, static_cast<unsigned long long>(row));
+  const float m = block_max_256(mt, red_f) * shift_scale;
+  float st = 0.0f;
+#pragma unroll
+  for (int i = 0; i < kSplitPerThread; ++i) {
+    const int c = threadIdx.x + i * kSplitThreads;
+    const float e = shifted_exp<MODE>(v[i], m);
+    st += c < len ? e : 0.0f;
+  }
+  const double s = block_sum_256(static_cast<double>(st), red_d);
+  if (threadIdx.x == 0) {
+    RowPartial p;
+    p.m = m;
+    p.pad = 0.0f;
+    p.s = s;
+    partials[w] = p;
+  }
+}
+
+// one warp per row
+__global__ void k4_combine(const RowPartial* __restrict__ partials, int64_t rows, int nch,
+                           float* __restrict__ row_max, double* __restrict__ row_sum) {
+  const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const RowPartial* rp = partials + row * nch;
+  float M = kPadLogit;
+  for (int q = lane; q < nch; q += 32) M = fmaxf(M, rp[q].m);
+  M = group_max<32>(M);
+  double S = 0.0;
+  for (int q = lane; q < nch; q += 32)
+    S += rp[q].s * static_cast<double>(rp[q].m == M ? 1.0f : expf(rp[q].m - M));
+  S = group_sum<32>(S);
+  if (lane == 0) {
+    row_max[row] = M;
+    row_sum[row] = S;
+  }
+}
+
+__global__ void k4_rescale(const float* __restrict__ local_max,
+                           const float* __restrict__ global_max, double* __restrict__ sum,
+                           int64_t rows) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const float d = local_max[i] - global_max[i];
+  sum[i] *= static_cast<double>(d == 0.0f ? 1.0f : expf(d));
+}
+
+template <int MODE, int VEC>
+__global__ void __launch_bounds__(kSplitThreads)
+    k4_normalize(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
+                 int64_t ldx, int64_t ldy, int nch, const float* __restrict__ row_max,
+                 const double* __restrict__ row_sum) {
+  const int64_t w = blockIdx.x;
+  const int64_t row = w / nch;
+  const int ch = static_cast<int>(w - row * nch);
+  const int64_t c0 = int64_t(ch) * kSplitChunk;
+  const float* xr = x + row * ldx + c0;
+  float* yr = y + row * ldy + c0;
+  const int64_t rem = cols - c0;
+  const int len = static_cast<int>(rem < kSplitChunk ? rem : kSplitChunk);
+  const float M = row_max[row];
+  const float r = recip_of_sum(row_sum[row]);
+  if constexpr (VEC == 4) {
+#pragma unroll
+    for (int i = 0; i < kSplitPerThread / 4; ++i) {
+      const int c = 4 * (threadIdx.x + i * kSplitThreads);
+      if (c < len) {
+        const float4 t = ld_stream4(xr + c);
+        st_stream4(yr + c, make_float4(scale_flush(shifted_exp<MODE>(t.x, M), r),
+                                       scale_flush(shifted_exp<MODE>(t.y, M), r),
+                                       scale_flush(shifted_exp<MODE>(t.z, M), r),
+                                       scale_flush(shifted_exp<MODE>(t.w, M), r)));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kSplitPerThread; ++i) {
+      const int c = threadIdx.x + i * kSplitThreads;
+      if (c < len) st_stream1(yr + c, scale_flush(shifted_exp<MODE>(ld_stream1(xr + c), M), r));
+    }
+  }
+}
+
+}  // namespace sk

@@ -1,0 +1,262 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference.
+
+Gate (BASELINE.json north_star): max |d| <= 1e-6, max |d|/ref <=
+1e-5, max |rowsum - 1| <= 1e-5 against ReferenceClipped on identical inputs;
+1e-5 relative for the approximate-exp rung (reference bench.py:52).  Small
+cases compare straight against outputs of the reference itself
+(tests/golden); full configs against the C oracle, which is pinned
+bit-exact to the reference (test_oracle_golden.py).
+"""
+
+import numpy as np
+import pytest
+
+import paper_1904_12380_b200 as sk
+from paper_1904_12380_b200 import _native, configs
+from tests import gpu_util as gu
+
+pytestmark = pytest.mark.gpu
+
+MODES = {"clipped": 0, "inference": 1, "approx": 2}
+
+
+def assert_parity(oracle, y, ref, approx=False, what=""):
+    d = oracle.parity(y, ref, approx=approx)
+    assert d["ok"], (what, d)
+    return d
+
+
+@pytest.fixture(autouse=True)
+def _reset_tuning():
+    yield
+    for k, v in (("path", -1), ("k1_lpr", 0), ("grid_mult", 0), ("seg_len", 0),
+                 ("skip_max_shift", 0)):
+        _native.set_tuning(k, v)
+
+
+# ---------------------------------------------------------------- golden sweep
+def test_sweep_against_reference_outputs(golden, golden_meta, oracle):
+    for C in golden_meta["sweep"]:
+        x = golden[f"sweep/{C}/x"]
+        for rung, mode in MODES.items():
+            y, bad = gu.softmax_abi(x, mode)
+            assert bad == gu.NO_BAD
+            assert_parity(oracle, y, golden[f"sweep/{C}/{rung}"], approx=(mode == 2),
+                          what=(C, rung, gu.plan(*x.shape)))
+
+
+def test_spec_known_answers(golden, oracle):
+    for case in ("spec_123", "spec_zeros", "spec_single", "spec_big", "spec_clip"):
+        x = golden[f"{case}/x"]
+        for rung in ("clipped", "inference"):
+            y, _ = gu.softmax_abi(x, MODES[rung])
+            assert_parity(oracle, y, golden[f"{case}/{rung}"], what=(case, rung))
+    y, _ = gu.softmax_abi(np.array([[3.0]], np.float32))
+    assert y[0, 0] == 1.0
+    y, _ = gu.softmax_abi(np.zeros((1, 4), np.float32))
+    assert np.all(y == 0.25)
+    x = np.array([[0.0, -100.0]], np.float32)
+    assert gu.softmax_abi(x, 0)[0][0, 1] > 0
+    assert gu.softmax_abi(x, 1)[0][0, 1] == 0
+
+
+def test_config_rows_against_reference(golden, oracle):
+    for name in ("c1", "c3"):
+        y, _ = gu.softmax_abi(golden[f"{name}/x"], 0)
+        assert_parity(oracle, y, golden[f"{name}/clipped"], what=name)
+
+
+# ---------------------------------------------------------------- full configs
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_config_full_parity(name, oracle):
+    x = configs.generate(name)
+    ref = oracle.softmax_ref(x, True, nthreads=0)
+    y, bad = gu.softmax_abi(x, 0)
+    assert bad == gu.NO_BAD
+    d = assert_parity(oracle, y, ref, what=(name, gu.plan(*x.shape)))
+    print(name, gu.plan(*x.shape), d)
+
+
+@pytest.mark.parametrize("name,sample_rows", [("c4", 24), ("c5a", 8192), ("c5b", 6)])
+def test_config_full_size_properties(name, sample_rows, oracle):
+    """Full-size run: every row sums to 1, all outputs positive and finite,
+    and a seeded sample of rows matches the oracle."""
+    t = gu.torch()
+    spec = configs.get(name)
+    x = configs.generate(spec)
+    xd = t.from_numpy(x).cuda()
+    del x
+    yd = sk.softmax(xd, sk.KernelVariant.REFERENCE_CLIPPED)
+    t.cuda.synchronize()
+    rowsum = yd.double().sum(dim=1) if spec.cols <= 4096 else t.stack(
+        [yd[i].double().sum() for i in range(spec.rows)])
+    assert float((rowsum - 1).abs().max()) <= 1e-5
+    assert bool(t.isfinite(yd).all()) and float(yd.min()) > 0
+    rng = np.random.default_rng(7)
+    rows = np.unique(rng.integers(0, spec.rows, sample_rows))
+    xs = configs.generate(spec, 0, None)[rows] if spec.rows * spec.cols <= 1 << 27 else \
+        np.stack([configs.generate(spec, int(r), 1)[0] for r in rows])
+    ref = oracle.softmax_ref(xs, True, nthreads=0)
+    got = yd[t.from_numpy(rows).cuda()].cpu().numpy()
+    d = assert_parity(oracle, got, ref, what=(name, gu.plan(spec.rows, spec.cols)))
+    print(name, gu.plan(spec.rows, spec.cols), d)
+
+
+# ---------------------------------------------------------------- edge shapes
+EDGE_C = [1, 2, 3, 7, 49, 50, 51, 127, 128, 129, 1000, 1023, 1024, 1025, 4096, 4097, 8192,
+          8193, 12289, 65536, 65537, 262144]
+
+
+@pytest.mark.parametrize("C", EDGE_C)
+def test_edge_shapes(C, oracle):
+    rows = 37 if C <= 8193 else 5
+    x = np.empty((rows, C), np.float32)
+    from paper_1904_12380_b200 import tensor
+
+    tensor.fill_normal_array(x, C, 6.0)
+    if C > 5:
+        x[1, C // 2] = -300.0  # clip fires
+        x[2, :] -= 500.0       # large negative row (shift invariance)
+    for mode in (0, 1):
+        ref = oracle.softmax_ref(x, clip=(mode == 0))
+        y, bad = gu.softmax_abi(x, mode)
+        assert bad == gu.NO_BAD
+        assert_parity(oracle, y, ref, what=(C, mode, gu.plan(rows, C)))
+
+
+@pytest.mark.parametrize("C", [50, 128, 1000, 2048, 4097, 16384, 100000])
+def test_unaligned_and_strided(C, oracle):
+    rows = 9
+    x = np.empty((rows, C), np.float32)
+    from paper_1904_12380_b200 import tensor
+
+    tensor.fill_uniform_array(x, 11, -30, 30)
+    ref = oracle.softmax_ref(x)
+    for xo, yo, ldx, ldy in ((1, 0, None, None), (0, 3, None, None), (0, 0, C + 4, C + 8),
+                             (2, 1, C + 3, C + 5)):
+        y, _ = gu.softmax_abi(x, 0, x_offset=xo, y_offset=yo, ldx=ldx, ldy=ldy)
+        assert_parity(oracle, y, ref, what=(C, xo, yo, ldx, ldy))
+
+
+@pytest.mark.parametrize("path", [0, 1, 2])
+def test_every_path_on_same_input(path, oracle):
+    C = 1024 if path == 0 else 20000
+    x = configs.generate("c4", 0, 3)[:, :C].copy()
+    ref = oracle.softmax_ref(x)
+    _native.set_tuning("path", path)
+    y, _ = gu.softmax_abi(x, 0)
+    assert_parity(oracle, y, ref, what=path)
+
+
+def test_k1_instantiations_all_agree(oracle):
+    x = configs.generate("c2", 0, 999)
+    ref = oracle.softmax_ref(x)
+    for lpr, nv, u in ((8, 4, 1), (8, 4, 2), (16, 2, 2), (16, 4, 1), (32, 1, 4), (32, 4, 1)):
+        _native.set_tuning("k1_lpr", lpr)
+        _native.set_tuning("k1_nv", nv)
+        _native.set_tuning("k1_u", u)
+        y, _ = gu.softmax_abi(x, 0)
+        assert_parity(oracle, y, ref, what=(lpr, nv, u))
+
+
+def test_seg_lengths_all_agree(oracle):
+    x = configs.generate("c4", 0, 4)[:, :100000].copy()
+    ref = oracle.softmax_ref(x)
+    for sl in (2048, 4096, 8192):
+        _native.set_tuning("seg_len", sl)
+        y, _ = gu.softmax_abi(x, 0)
+        assert_parity(oracle, y, ref, what=sl)
+
+
+# ---------------------------------------------------------------- errors / faults
+@pytest.mark.parametrize("C", [50, 128, 1000, 4097, 8192, 70000])
+def test_nonfinite_reports_first_bad_row(C):
+    rows = 40
+    x = np.ones((rows, C), np.float32)
+    x[31, C - 1] = np.inf
+    x[17, C // 2] = np.nan
+    x[25, 0] = -np.inf
+    _, bad = gu.softmax_abi(x, 0)
+    assert bad == 17, gu.plan(rows, C)
+    t = gu.torch()
+    with pytest.raises(sk.NumericDomainError, match="row 17"):
+        sk.softmax(t.from_numpy(x).cuda(), sk.KernelVariant.REFERENCE_CLIPPED)
+    with pytest.raises(sk.NumericDomainError, match="row 17"):
+        sk.softmax(sk.Matrix2D.from_array(x), sk.KernelVariant.REFERENCE_CLIPPED)
+    # the flag was reset: a clean call succeeds afterwards
+    sk.softmax(t.ones(3, C, device="cuda"), sk.KernelVariant.REFERENCE_CLIPPED)
+
+
+def test_skip_max_shift_fault_is_caught(oracle):
+    """kernels._SKIP_MAX_SHIFT (reference kernels.py:103-105): without the max
+    shift, large logits overflow and the parity harness must FAIL."""
+    from paper_1904_12380_b200 import kernels
+
+    x = configs.generate("c1") + np.float32(80.0)
+    ref = oracle.softmax_ref(x)
+    t = gu.torch()
+    kernels._SKIP_MAX_SHIFT = True
+    try:
+        y = sk.softmax(t.from_numpy(x).cuda(), sk.KernelVariant.REFERENCE_CLIPPED).cpu().numpy()
+    finally:
+        kernels._SKIP_MAX_SHIFT = False
+    assert not oracle.parity(y, ref)["ok"]
+    y = sk.softmax(t.from_numpy(x).cuda(), sk.KernelVariant.REFERENCE_CLIPPED).cpu().numpy()
+    assert oracle.parity(y, ref)["ok"]
+
+
+# ---------------------------------------------------------------- invariants
+def test_shift_invariance_and_order():
+    x = configs.generate("c3", 0, None)[:256]
+    base, _ = gu.softmax_abi(x)
+    for c in (-50.0, -1.0, 1.0, 50.0):
+        y, _ = gu.softmax_abi(x + np.float32(c))
+        assert np.max(np.abs(y - base)) <= 1e-6
+    ranks_in = np.argsort(np.argsort(x[:8], axis=1, kind="stable"), axis=1)
+    y8 = base[:8]
+    # order preserved where inputs are distinct (ties/clip floor aside)
+    for r in range(8):
+        ux = x[r] > x[r].max() - 60
+        assert np.all(np.diff(y8[r][ux][np.argsort(x[r][ux])]) >= 0)
+    del ranks_in
+
+
+def test_deterministic_and_row_shard_bitwise():
+    """Same bits run to run, and a row block computed alone equals the same
+    rows of the whole matrix (row sharding needs no communication)."""
+    for name, split in (("c2", 20000), ("c1", 1024), ("c3", 4096)):
+        x = configs.generate(name)
+        y1, _ = gu.softmax_abi(x)
+        y2, _ = gu.softmax_abi(x)
+        assert np.array_equal(y1.view(np.uint32), y2.view(np.uint32))
+        a, _ = gu.softmax_abi(x[:split])
+        b, _ = gu.softmax_abi(x[split:])
+        assert np.array_equal(np.concatenate([a, b]).view(np.uint32), y1.view(np.uint32))
+    spec = configs.get("c4")
+    x = configs.generate(spec, 0, 16)
+    y, _ = gu.softmax_abi(x)
+    a, _ = gu.softmax_abi(x[5:9])
+    assert np.array_equal(a.view(np.uint32), y[5:9].view(np.uint32))
+
+
+def test_host_path_equals_device_path():
+    x = configs.generate("c3")
+    dev, _ = gu.softmax_abi(x)
+    m = sk.Matrix2D.from_array(x, pinned=True)
+    out = sk.softmax(m, sk.KernelVariant.REFERENCE_CLIPPED)
+    assert np.array_equal(out.view2d.view(np.uint32), dev.view(np.uint32))
+    pageable = sk.softmax(sk.Matrix2D.from_array(x), sk.KernelVariant.REFERENCE_CLIPPED)
+    assert np.array_equal(pageable.view2d.view(np.uint32), dev.view(np.uint32))
+    arr = sk.softmax(x, sk.KernelVariant.REFERENCE_CLIPPED)
+    assert np.array_equal(arr.view(np.uint32), dev.view(np.uint32))
+
+
+def test_every_variant_through_public_api(oracle):
+    x = configs.generate("c2", 0, 512)
+    t = gu.torch()
+    xd = t.from_numpy(x).cuda()
+    for v in sk.LADDER:
+        y = sk.softmax(xd, v).cpu().numpy()
+        ref = oracle.softmax_ref(x, clip=(v is sk.KernelVariant.REFERENCE_CLIPPED))
+        assert_parity(oracle, y, ref, approx=(v is sk.KernelVariant.FULL_VECTORIZED_APPROX_EXP),
+                      what=v)

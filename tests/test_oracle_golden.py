@@ -1,0 +1,95 @@
+"""The C oracle is pinned bit-for-bit to the reference's own outputs
+(tests/golden/*, produced by running /root/reference in the build container)."""
+
+import numpy as np
+import pytest
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+
+
+@pytest.mark.parametrize("case", ["spec_123", "spec_zeros", "spec_single", "spec_big", "spec_clip"])
+def test_spec_known_answers_bit_exact(golden, oracle, case):
+    x = golden[f"{case}/x"]
+    for rung, clip in (("clipped", True), ("inference", False)):
+        y = oracle.softmax_ref(x, clip)
+        assert np.array_equal(bits(y), bits(golden[f"{case}/{rung}"])), (case, rung)
+
+
+def test_spec_values(oracle):
+    # SPEC.md:175-177, :523 and SURVEY §4 known answers
+    y = oracle.softmax_ref(np.array([[1, 2, 3]], np.float32))
+    np.testing.assert_allclose(y[0], [0.09003057, 0.24472847, 0.66524096], atol=1e-6)
+    assert np.all(oracle.softmax_ref(np.zeros((1, 4), np.float32)) == 0.25)
+    assert oracle.softmax_ref(np.array([[3.0]], np.float32))[0, 0] == 1.0
+    x = np.array([[0.0, -100.0]], np.float32)
+    assert oracle.softmax_ref(x, clip=True)[0, 1] > 0  # ValueClip keeps it positive
+    assert oracle.softmax_ref(x, clip=False)[0, 1] == 0  # inference flushes to +0
+
+
+def test_sweep_bit_exact(golden, golden_meta, oracle):
+    for C in golden_meta["sweep"]:
+        x = golden[f"sweep/{C}/x"]
+        for rung, clip in (("clipped", True), ("inference", False)):
+            y = oracle.softmax_ref(x, clip)
+            assert np.array_equal(bits(y), bits(golden[f"sweep/{C}/{rung}"])), (C, rung)
+
+
+def test_config_rows_bit_exact(golden, oracle):
+    for name in ("c1", "c3"):
+        y = oracle.softmax_ref(golden[f"{name}/x"], True)
+        assert np.array_equal(bits(y), bits(golden[f"{name}/clipped"])), name
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_full_config_hash_matches_reference(golden_meta, oracle, name):
+    from paper_1904_12380_b200 import configs
+
+    meta = golden_meta["configs"][name]
+    x = configs.generate(name)
+    assert configs.sha256(x) == meta["input_sha256"]
+    y = oracle.softmax_ref(x, True, nthreads=0)
+    assert configs.sha256(y) == meta["ref_clipped_sha256"]
+
+
+def test_multithreaded_oracle_is_bitwise_single_threaded(oracle):
+    from paper_1904_12380_b200 import configs
+
+    x = configs.generate("c1")
+    a = oracle.softmax_ref(x, True, nthreads=1)
+    b = oracle.softmax_ref(x, True, nthreads=0)
+    assert np.array_equal(bits(a), bits(b))
+
+
+def test_nonfinite_rejected_with_first_row(oracle):
+    x = np.zeros((6, 5), np.float32)
+    x[4, 2] = np.inf
+    x[2, 0] = np.nan
+    with pytest.raises(ValueError, match="row 2"):
+        oracle.softmax_ref(x)
+
+
+def test_lane_reductions_match_reference(golden, oracle):
+    for W in (4, 8, 16):
+        for n in (1, 3, 7, 11, 64, 515):
+            a = golden[f"lanes/{W}/{n}/a"]
+            assert oracle.lanes_max(a, W) == golden[f"lanes/{W}/{n}/max"][0]
+            assert bits(oracle.lanes_sum(a, W)) == bits(golden[f"lanes/{W}/{n}/sum"][0])
+
+
+def test_philox_matches_numpy(oracle):
+    for seed, start, n in ((1, 0, 9), (7, 1001, 5), (123456789, 3, 17)):
+        want = np.random.Philox(key=seed).random_raw(start + n)[start:]
+        assert np.array_equal(oracle.philox_raw(seed, start, n), want)
+
+
+def test_metrics():
+    import oracle as o
+
+    ref = np.array([[0.25, 0.75]])
+    assert o.max_abs_err(ref, ref) == 0.0
+    assert o.max_rel_err(np.array([[0.5, 0.5]]), ref) == pytest.approx(1.0)
+    assert o.max_rowsum_dev(np.array([[0.5, 0.6]])) == pytest.approx(0.1)
+    assert o.max_rel_err(np.array([[np.nan, 1.0]]), ref) == float("inf")
+    assert o.max_rel_err(np.array([[1e-30, 1.0]]), np.array([[0.0, 1.0]])) == float("inf")
