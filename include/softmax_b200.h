@@ -71,9 +71,9 @@ const char* sk_last_error(void);
  *             holding NaN/+-Inf into it.  Initialise it to SK_NO_BAD_ROW once;
  *             it is only written on bad input.  May be NULL (then a
  *             library-owned flag is used and not reported).
- *  workspace  device scratch of sk_softmax_workspace_bytes() bytes, zeroed
- *             once before first use (the kernels leave it zeroed), or NULL
- *             for a library-managed per-(device, stream) workspace.
+ *  workspace  device scratch of sk_softmax_workspace_bytes() bytes (no
+ *             initialisation needed; launches on one stream may share it), or
+ *             NULL for a library-managed per-(device, stream) workspace.
  * rows == 0 is a no-op.  Returns SK_OK or an error status.
  */
 int sk_softmax_f32(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,

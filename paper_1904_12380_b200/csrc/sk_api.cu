@@ -150,8 +150,15 @@ int occupancy(const void* fn, int threads, size_t smem) {
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
   }
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  static std::map<std::pair<const void*, int>, size_t> smem_set;  // only ever raised
+  if (smem > 48 * 1024) {
+    std::lock_guard<std::mutex> g(mu);
+    size_t& cur = smem_set[{fn, dev}];
+    if (smem > cur) {
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      cur = smem;
+    }
+  }
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem) != cudaSuccess) {
     (void)cudaGetLastError();
@@ -313,6 +320,9 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
     unsigned* cnt = reinterpret_cast<unsigned*>(ws + l.cnt);
     RowPartial* part = reinterpret_cast<RowPartial*>(ws + l.part);
     SegFn fn = seg_fn<kSegNV>(mode);
+    // K3 row counters start at zero every launch (the workspace is shared by
+    // launches of different shapes, so no state is assumed across launches).
+    if (p.nseg > 1) SK_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(unsigned), s));
     int nseg = p.nseg, seglen = p.seglen;
     float sh = shift_scale();
     void* args[] = {(void*)&x,   (void*)&y,    (void*)&rows,   (void*)&cols,

@@ -17,9 +17,10 @@
 //      resident and items are taken in increasing order, so the wait cannot
 //      deadlock while nseg <= gridDim.x), then merges
 //         M = max_k m_k,   S = sum_k s_k * exp(m_k - M)      (f64, fixed order)
-//   5. writes y = max(e * exp(m_l - M), e^-64) * (1/S)  (clip mode; the max
-//      restores the ValueClip floor relative to the global max, since exp is
-//      monotone) -- HBM is read once and written once: 8 B/element.
+//   5. writes y = exp(clip(x - M)) * (1/S) from the registers (K2 reuses e;
+//      K3 recomputes exp against the merged M so every output is rounded as
+//      the reference rounds it) -- HBM is read once and written once:
+//      8 B/element.  Row counters are zeroed by the launcher before a K3 launch.
 //
 // Replaces kernels.py:136-189 for C > 1024 (and row_stats, kernels.py:272-276,
 // whose (max, sum) pair is exactly what step 4 exchanges).
@@ -137,7 +138,11 @@ __global__ void __launch_bounds__(1024)
     __syncthreads();
     const float m_l = red_f[32] * shift_scale;  // shift_scale = 0: fault hook
 
-    // ---- e = exp(clip(x - m_l)) kept in registers; local sum
+    // ---- local sum of e = exp(clip(x - m_l)).  K2 keeps e in registers (one
+    // exp per element, reference order); K3 keeps x and recomputes exp(x - M)
+    // against the merged row max below, so every output is rounded exactly as
+    // the reference rounds it (s = x - M in fp32, clip, expf, * 1/S).
+    const bool single = (nseg == 1);
     float st = 0.0f;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
@@ -145,7 +150,7 @@ __global__ void __launch_bounds__(1024)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const float e = shifted_exp<MODE>(v[i][c], m_l);
-        v[i][c] = e;
+        if (single) v[i][c] = e;
         st += ok ? e : 0.0f;
       }
     }
@@ -160,10 +165,9 @@ __global__ void __launch_bounds__(1024)
     __syncthreads();
     const double s_l = red_d[32];
 
-    float scale, floor_e = 0.0f, rcp;
-    if (nseg == 1) {
+    float M = m_l, rcp;
+    if (single) {
       rcp = recip_of_sum(s_l);
-      scale = 1.0f;
     } else {
       // ---- publish, wait for the row, merge (warp 0)
       if (warp == 0) {
@@ -182,32 +186,26 @@ __global__ void __launch_bounds__(1024)
         }
         __syncwarp();
         const RowPartial* rp = partials + row * nseg;
-        float M = kPadLogit;
-        for (int q = lane; q < nseg; q += 32) M = fmaxf(M, __ldcg(&rp[q].m));
-        M = group_max<32>(M);
+        float Mw = kPadLogit;
+        for (int q = lane; q < nseg; q += 32) Mw = fmaxf(Mw, __ldcg(&rp[q].m));
+        Mw = group_max<32>(Mw);
         double S = 0.0;
         for (int q = lane; q < nseg; q += 32) {
           const float mq = __ldcg(&rp[q].m);
-          S += __ldcg(&rp[q].s) * static_cast<double>(expf(mq - M));
+          S += __ldcg(&rp[q].s) * static_cast<double>(mq == Mw ? 1.0f : expf(mq - Mw));
         }
         S = group_sum<32>(S);
         if (lane == 0) {
-          bc_M = M;
+          bc_M = Mw;
           bc_S = S;
-          // second arrival: the last reader of this row resets the counter, so
-          // the workspace is clean for the next launch on this stream.
-          const unsigned old = atomicAdd(&row_cnt[row], 1u);
-          if (old == 2u * nseg - 1u) row_cnt[row] = 0u;
         }
       }
       __syncthreads();
-      const float M = bc_M;
+      M = bc_M;
       rcp = recip_of_sum(bc_S);
-      scale = (m_l == M) ? 1.0f : expf(m_l - M);
-      if (MODE == kClipAccurate) floor_e = expf(kClipFloor);
     }
 
-    // ---- y = max(e*scale, floor) * r, flush, streaming store straight from registers
+    // ---- y = exp(clip(x - M)) * r, flush, streaming store straight from registers
     float* yr = y + row * ldy + int64_t(seg) * seglen;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
@@ -215,14 +213,8 @@ __global__ void __launch_bounds__(1024)
       if (q < nvec) {
         float o[4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          float e = v[i][c];
-          if (nseg != 1) {
-            e = e * scale;
-            if (MODE == kClipAccurate) e = fmaxf(e, floor_e);
-          }
-          o[c] = scale_flush(e, rcp);
-        }
+        for (int c = 0; c < 4; ++c)
+          o[c] = scale_flush(single ? v[i][c] : shifted_exp<MODE>(v[i][c], M), rcp);
         st_stream4(yr + 4 * q, make_float4(o[0], o[1], o[2], o[3]));
       }
     }
