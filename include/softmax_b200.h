@@ -129,6 +129,8 @@ void sk_free_pinned(void* p);
  *                    float4s per lane, rows per lane-group batch)
  *   "grid_mult"      K1 grid = SMs * occupancy * grid_mult (default 1)
  *   "seg_len"        target segment length (floats) for K2/K3
+ *   "seg_align"      1 (default): K3 grid is a whole multiple of the row's
+ *                    segment count, so row groups never straddle CTAs
  *   "skip_max_shift" 1: shift by 0 instead of the row max -- the reference's
  *                    _SKIP_MAX_SHIFT fault hook (kernels.py:103-105, :309-311);
  *                    large logits then overflow and verification must fail.

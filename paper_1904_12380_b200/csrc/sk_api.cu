@@ -16,6 +16,7 @@
 #include "sk_rows.cuh"
 #include "sk_seg.cuh"
 #include "sk_split.cuh"
+#include "sk_lag.cuh"
 
 namespace sk {
 namespace {
@@ -66,50 +67,86 @@ std::atomic<int> g_force_path{-1};  // -1 auto, 0 k1, 1 seg, 2 split
 std::atomic<int> g_skip_max_shift{0};
 float shift_scale() { return g_skip_max_shift.load() ? 0.0f : 1.0f; }
 std::atomic<int> g_k1_lpr{0}, g_k1_nv{0}, g_k1_u{0}, g_grid_mult{0}, g_seg_len{0};
+std::atomic<int> g_seg_align{0};  // K3 grid = whole multiple of nseg (row groups never straddle)
+std::atomic<int> g_k1_pf{-1};     // -1: table default, 0/1 force register prefetch
+std::atomic<int> g_pdl{1};        // programmatic dependent launch on every kernel
+std::atomic<int> g_lag{2};        // K3 normalize lag in rounds
+std::atomic<int> g_k3_impl{0};    // 0: lagged two-pass (k3_lag), 1: smem-resident (k_seg)
+
+// Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.
+template <typename... Args>
+cudaError_t launch_k(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     bool coop, Args... args) {
+  void* argv[] = {static_cast<void*>(&args)...};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (coop) {
+    attr[n].id = cudaLaunchAttributeCooperative;
+    attr[n].val.cooperative = 1;
+    ++n;
+  } else if (g_pdl.load()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelExC(&cfg, fn, argv);
+}
 
 // ------------------------------------------------------------------ K1 table
 using K1Fn = void (*)(const float*, float*, int64_t, int, int64_t, int64_t,
                       unsigned long long*, float);
 struct K1Entry {
-  int vec, lpr, nv, u;
+  int vec, lpr, nv, u, pf;
   K1Fn fn[3];
 };
-#define SK_K1(VEC, LPR, NV, U)                                                   \
-  K1Entry {                                                                      \
-    VEC, LPR, NV, U, {                                                           \
-      &k1_rows<kClipAccurate, VEC, LPR, NV, U>, &k1_rows<kAccurate, VEC, LPR, NV, U>, \
-          &k1_rows<kApprox, VEC, LPR, NV, U>                                     \
-    }                                                                            \
+#define SK_K1(VEC, LPR, NV, U, PF)                                                         \
+  K1Entry {                                                                                \
+    VEC, LPR, NV, U, PF, {                                                                 \
+      &k1_rows<kClipAccurate, VEC, LPR, NV, U, PF>, &k1_rows<kAccurate, VEC, LPR, NV, U, PF>, \
+          &k1_rows<kApprox, VEC, LPR, NV, U, PF>                                           \
+    }                                                                                      \
   }
 const K1Entry kK1Table[] = {
     // 128-bit path (cols % 4 == 0, 16-B aligned rows)
-    SK_K1(4, 4, 1, 4), SK_K1(4, 8, 1, 4), SK_K1(4, 16, 1, 4), SK_K1(4, 8, 2, 2),
-    SK_K1(4, 8, 4, 1), SK_K1(4, 8, 4, 2), SK_K1(4, 16, 2, 2), SK_K1(4, 16, 2, 1),
-    SK_K1(4, 16, 4, 1), SK_K1(4, 16, 4, 2), SK_K1(4, 32, 1, 4), SK_K1(4, 32, 2, 2),
-    SK_K1(4, 32, 4, 1), SK_K1(4, 32, 8, 1), SK_K1(4, 32, 1, 2), SK_K1(4, 32, 2, 1),
+    SK_K1(4, 4, 1, 4, 0), SK_K1(4, 8, 1, 4, 0), SK_K1(4, 16, 1, 4, 0), SK_K1(4, 8, 2, 2, 0),
+    SK_K1(4, 8, 4, 1, 0), SK_K1(4, 8, 4, 2, 0), SK_K1(4, 16, 2, 2, 0), SK_K1(4, 16, 2, 1, 0),
+    SK_K1(4, 16, 4, 1, 0), SK_K1(4, 16, 4, 2, 0), SK_K1(4, 32, 1, 4, 0), SK_K1(4, 32, 2, 2, 0),
+    SK_K1(4, 32, 4, 1, 0), SK_K1(4, 32, 8, 1, 0), SK_K1(4, 32, 1, 2, 0), SK_K1(4, 32, 2, 1, 0),
+    SK_K1(4, 8, 4, 1, 1), SK_K1(4, 16, 2, 1, 1), SK_K1(4, 16, 4, 1, 1), SK_K1(4, 32, 2, 1, 1),
+    SK_K1(4, 32, 4, 1, 1), SK_K1(4, 32, 8, 1, 1), SK_K1(4, 16, 1, 4, 1), SK_K1(4, 8, 1, 4, 1),
     // 32-bit path (any pitch / alignment)
-    SK_K1(1, 8, 1, 4), SK_K1(1, 16, 1, 4), SK_K1(1, 32, 1, 4), SK_K1(1, 16, 4, 2),
-    SK_K1(1, 32, 2, 2), SK_K1(1, 32, 4, 1), SK_K1(1, 32, 8, 1), SK_K1(1, 32, 16, 1),
-    SK_K1(1, 32, 32, 1),
+    SK_K1(1, 8, 1, 4, 0), SK_K1(1, 16, 1, 4, 0), SK_K1(1, 32, 1, 4, 0), SK_K1(1, 16, 4, 2, 0),
+    SK_K1(1, 32, 2, 2, 0), SK_K1(1, 32, 4, 1, 0), SK_K1(1, 32, 8, 1, 0), SK_K1(1, 32, 16, 1, 0),
+    SK_K1(1, 32, 32, 1, 0), SK_K1(1, 16, 4, 2, 1), SK_K1(1, 16, 4, 1, 1),
 };
 #undef SK_K1
 
-const K1Entry* k1_find(int vec, int lpr, int nv, int u) {
+const K1Entry* k1_find(int vec, int lpr, int nv, int u, int pf) {
   for (const auto& e : kK1Table)
-    if (e.vec == vec && e.lpr == lpr && e.nv == nv && e.u == u) return &e;
+    if (e.vec == vec && e.lpr == lpr && e.nv == nv && e.u == u && e.pf == pf) return &e;
   return nullptr;
 }
 
-// default K1 shape per row length (covers cols <= 1024)
-void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u) {
+// default K1 shape per row length (covers cols <= 1024); grid multiplier:
+// 0 = persistent (SMs x occupancy), m > 0 = m x that many CTAs (waves).
+void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u, int& pf, int& gm) {
+  pf = 0;
+  gm = 1;
   if (vec == 4) {
     if (cols <= 16) { lpr = 4; nv = 1; u = 4; }
     else if (cols <= 32) { lpr = 8; nv = 1; u = 4; }
     else if (cols <= 64) { lpr = 16; nv = 1; u = 4; }
-    else if (cols <= 128) { lpr = 8; nv = 4; u = 2; }
-    else if (cols <= 256) { lpr = 16; nv = 4; u = 1; }
-    else if (cols <= 512) { lpr = 32; nv = 4; u = 1; }
-    else { lpr = 32; nv = 8; u = 1; }
+    else if (cols <= 128) { lpr = 16; nv = 2; u = 1; gm = 2; }
+    else if (cols <= 256) { lpr = 16; nv = 4; u = 1; gm = 4; }
+    else if (cols <= 512) { lpr = 32; nv = 4; u = 1; gm = 2; }
+    else { lpr = 32; nv = 8; u = 1; gm = 2; }
   } else {
     if (cols <= 8) { lpr = 8; nv = 1; u = 4; }
     else if (cols <= 16) { lpr = 16; nv = 1; u = 4; }
@@ -133,6 +170,17 @@ SegFn seg_fn(int mode) {
     default: return &k_seg<kApprox, NV>;
   }
 }
+using LagFn = void (*)(const float*, float*, int64_t, int64_t, int64_t, int64_t, int, int, int,
+                       unsigned*, RowPartial*, unsigned long long*, float);
+template <int NV>
+LagFn lag_fn(int mode) {
+  switch (mode) {
+    case kClipAccurate: return &k3_lag<kClipAccurate, NV>;
+    case kAccurate: return &k3_lag<kAccurate, NV>;
+    default: return &k3_lag<kApprox, NV>;
+  }
+}
+constexpr int kLagThreads = 256;
 constexpr int kSegNV = 4;
 constexpr int kSegMaxThreads = 512;
 constexpr int64_t kSegCap = int64_t(kSegMaxThreads) * kSegNV * 4;  // 8192 floats / CTA
@@ -176,8 +224,9 @@ struct Plan {
   PathKind kind = kPathK1;
   // K1
   const K1Entry* k1 = nullptr;
-  // seg
-  int nseg = 1, seglen = 0, threads = 0;
+  // seg (K2: nseg == 1; K3: nseg > 1)
+  int nseg = 1, seglen = 0, threads = 0, lag = 0;
+  bool k3_lag = false;
   size_t smem = 0;
   // split
   int nch = 0;
@@ -201,13 +250,21 @@ WsLayout ws_layout(int64_t rows, int64_t parts_per_row) {
   return l;
 }
 
+int plan_split(int64_t rows, int64_t cols, Plan& p) {
+  p.kind = kPathSplit;
+  p.nch = static_cast<int>((cols + kSplitChunk - 1) / kSplitChunk);
+  p.grid = rows * p.nch;
+  if (p.grid > int64_t(INT32_MAX)) return arg_fail("matrix too large for the split path");
+  return SK_OK;
+}
+
 int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa, uint64_t ya,
               int mode, int dev, Plan& p) {
   const DevInfo di = dev_info(dev);
   const bool vec = (cols % 4 == 0) && (ldx % 4 == 0) && (ldy % 4 == 0) && (xa % 16 == 0) &&
                    (ya % 16 == 0);
   p.vec = vec;
-  int force = g_force_path.load();
+  const int force = g_force_path.load();
   PathKind kind;
   if (force >= 0) kind = static_cast<PathKind>(force);
   else if (cols <= 1024) kind = kPathK1;
@@ -217,55 +274,64 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
   if (kind == kPathSeg && !vec) return arg_fail("seg path needs 16-B aligned rows");
 
   if (kind == kPathK1) {
-    int lpr, nv, u;
-    k1_default(vec ? 4 : 1, cols, lpr, nv, u);
+    int lpr, nv, u, pf, gm;
+    k1_default(vec ? 4 : 1, cols, lpr, nv, u, pf, gm);
     if (g_k1_lpr.load() > 0) { lpr = g_k1_lpr; nv = g_k1_nv; u = g_k1_u; }
-    const K1Entry* e = k1_find(vec ? 4 : 1, lpr, nv, u);
+    if (g_k1_pf.load() >= 0) pf = g_k1_pf.load();
+    if (g_grid_mult.load() > 0) gm = g_grid_mult.load();
+    const K1Entry* e = k1_find(vec ? 4 : 1, lpr, nv, u, pf);
     if (!e) return arg_fail("no K1 instantiation for the requested shape");
     if (int64_t(lpr) * nv * e->vec < cols) return arg_fail("K1 shape does not cover cols");
     p.kind = kPathK1;
     p.k1 = e;
     const int64_t rows_per_cta = int64_t(kRowsThreads / 32) * u * (32 / lpr);
     const int64_t need = (rows + rows_per_cta - 1) / rows_per_cta;
-    int occ = occupancy(reinterpret_cast<const void*>(e->fn[mode]), kRowsThreads, 0);
-    int mult = g_grid_mult.load() > 0 ? g_grid_mult.load() : 1;
-    const int64_t cap = int64_t(di.sms) * std::max(occ, 1) * mult;
+    const int occ = occupancy(reinterpret_cast<const void*>(e->fn[mode]), kRowsThreads, 0);
+    const int64_t cap = int64_t(di.sms) * std::max(occ, 1) * gm;
     p.grid = std::max<int64_t>(1, std::min(need, cap));
     return SK_OK;
   }
   if (kind == kPathSeg) {
     int64_t target = g_seg_len.load() > 0 ? g_seg_len.load() : kSegCap;
     target = std::min<int64_t>(target, kSegCap);
-    int64_t nseg = (cols + target - 1) / target;
-    int64_t seglen = align_up((cols + nseg - 1) / nseg, 4);
-    int threads = static_cast<int>(align_up((seglen / 4 + kSegNV - 1) / kSegNV, 32));
-    threads = std::max(threads, 64);
-    const size_t smem = size_t(kSegStages) * threads * kSegNV * 4 * sizeof(float);
-    SegFn fn = seg_fn<kSegNV>(mode);
-    const int occ = occupancy(reinterpret_cast<const void*>(fn), threads, smem);
-    const int64_t items = rows * nseg;
-    const int64_t cap = int64_t(di.sms) * std::max(occ, 1);
+    const int64_t nseg = (cols + target - 1) / target;
+    const int64_t seglen = align_up((cols + nseg - 1) / nseg, 4);
     p.kind = kPathSeg;
     p.nseg = static_cast<int>(nseg);
     p.seglen = static_cast<int>(seglen);
-    p.threads = threads;
-    p.smem = smem;
-    p.grid = std::min(items, cap);
-    if (nseg > 1 && (!di.coop || nseg > p.grid || occ < 1)) {
-      if (force >= 0) return arg_fail("seg path cannot co-schedule this row split");
-      kind = kPathSplit;  // rows too long to co-schedule: fall through
+    const int64_t items = rows * nseg;
+    if (nseg > 1 && g_k3_impl.load() == 0) {
+      // K3: lagged two-pass, 256 threads, NV float4 per thread
+      p.k3_lag = true;
+      p.threads = kLagThreads;
+      p.lag = std::max(0, g_lag.load());
+      p.smem = 0;
+      const int nv = seglen <= int64_t(kLagThreads) * 4 * 4 ? 4 : 8;
+      const LagFn fn = nv == 4 ? lag_fn<4>(mode) : lag_fn<8>(mode);
+      const int occ = occupancy(reinterpret_cast<const void*>(fn), p.threads, 0);
+      p.grid = std::min(items, int64_t(di.sms) * std::max(occ, 1));
     } else {
-      return SK_OK;
+      // K2 (nseg == 1) or smem-resident K3: TMA segments into a 2-stage ring
+      int threads = static_cast<int>(align_up((seglen / 4 + kSegNV - 1) / kSegNV, 32));
+      threads = std::max(threads, 64);
+      p.threads = threads;
+      p.smem = size_t(kSegStages) * threads * kSegNV * 4 * sizeof(float);
+      const SegFn fn = seg_fn<kSegNV>(mode);
+      const int occ = occupancy(reinterpret_cast<const void*>(fn), threads, p.smem);
+      p.grid = std::min(items, int64_t(di.sms) * std::max(occ, 1));
     }
+    if (nseg > 1 && g_seg_align.load() && p.grid >= nseg) p.grid = p.grid / nseg * nseg;
+    if (nseg > 1 && (!di.coop || nseg > p.grid)) {
+      if (force >= 0) return arg_fail("seg path cannot co-schedule this row split");
+      return plan_split(rows, cols, p);  // rows too long to co-schedule
+    }
+    return SK_OK;
   }
-  p.kind = kPathSplit;
-  p.nch = static_cast<int>((cols + kSplitChunk - 1) / kSplitChunk);
-  p.grid = rows * p.nch;
-  return SK_OK;
+  return plan_split(rows, cols, p);
 }
 
 size_t plan_ws_bytes(const Plan& p, int64_t rows) {
-  if (p.kind == kPathSeg) return ws_layout(rows, p.nseg).total;
+  if (p.kind == kPathSeg && p.nseg > 1) return ws_layout(rows, p.nseg).total;
   if (p.kind == kPathSplit) return ws_layout(rows, p.nch).total;
   return ws_layout(0, 0).total;
 }
@@ -306,71 +372,75 @@ int check_common(const float* x, const void* y, int64_t rows, int64_t cols, int6
   return SK_OK;
 }
 
+int launch_split(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
+                 int64_t ldy, int mode, bool v4, unsigned long long* bad, char* ws, int nch,
+                 bool normalize, float* rmax_out, double* rsum_out, cudaStream_t s) {
+  const WsLayout l = ws_layout(rows, nch);
+  RowPartial* part = reinterpret_cast<RowPartial*>(ws + l.part);
+  float* rmax = rmax_out ? rmax_out : reinterpret_cast<float*>(ws + l.rmax);
+  double* rsum = rsum_out ? rsum_out : reinterpret_cast<double*>(ws + l.rsum);
+  const dim3 g(static_cast<unsigned>(rows * nch));
+  const float sh = shift_scale();
+  const void* stats = mode == kClipAccurate ? reinterpret_cast<const void*>(&k4_stats<kClipAccurate>)
+                      : mode == kAccurate   ? reinterpret_cast<const void*>(&k4_stats<kAccurate>)
+                                            : reinterpret_cast<const void*>(&k4_stats<kApprox>);
+  SK_CUDA(launch_k(stats, g, dim3(kSplitThreads), 0, s, false, x, rows, cols, ldx, nch, part,
+                   bad, sh));
+  SK_CUDA(launch_k(reinterpret_cast<const void*>(&k4_combine),
+                   dim3(static_cast<unsigned>((rows * 32 + 255) / 256)), dim3(256), 0, s, false,
+                   static_cast<const RowPartial*>(part), rows, nch, rmax, rsum));
+  if (!normalize) return SK_OK;
+  const void* norm;
+  switch (mode) {
+    case kClipAccurate:
+      norm = v4 ? reinterpret_cast<const void*>(&k4_normalize<kClipAccurate, 4>)
+                : reinterpret_cast<const void*>(&k4_normalize<kClipAccurate, 1>);
+      break;
+    case kAccurate:
+      norm = v4 ? reinterpret_cast<const void*>(&k4_normalize<kAccurate, 4>)
+                : reinterpret_cast<const void*>(&k4_normalize<kAccurate, 1>);
+      break;
+    default:
+      norm = v4 ? reinterpret_cast<const void*>(&k4_normalize<kApprox, 4>)
+                : reinterpret_cast<const void*>(&k4_normalize<kApprox, 1>);
+  }
+  SK_CUDA(launch_k(norm, g, dim3(kSplitThreads), 0, s, false, x, y, rows, cols, ldx, ldy, nch,
+                   static_cast<const float*>(rmax), static_cast<const double*>(rsum)));
+  return SK_OK;
+}
+
 int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t cols,
                 int64_t ldx, int64_t ldy, int mode, unsigned long long* bad, char* ws,
                 cudaStream_t s) {
+  const float sh = shift_scale();
   if (p.kind == kPathK1) {
-    p.k1->fn[mode]<<<static_cast<unsigned>(p.grid), kRowsThreads, 0, s>>>(
-        x, y, rows, static_cast<int>(cols), ldx, ldy, bad, shift_scale());
-    SK_CUDA(cudaGetLastError());
+    SK_CUDA(launch_k(reinterpret_cast<const void*>(p.k1->fn[mode]),
+                     dim3(static_cast<unsigned>(p.grid)), dim3(kRowsThreads), 0, s, false, x, y,
+                     rows, static_cast<int>(cols), ldx, ldy, bad, sh));
     return SK_OK;
   }
   if (p.kind == kPathSeg) {
     const WsLayout l = ws_layout(rows, p.nseg);
     unsigned* cnt = reinterpret_cast<unsigned*>(ws + l.cnt);
     RowPartial* part = reinterpret_cast<RowPartial*>(ws + l.part);
-    SegFn fn = seg_fn<kSegNV>(mode);
+    const int nseg = p.nseg, seglen = p.seglen;
     // K3 row counters start at zero every launch (the workspace is shared by
     // launches of different shapes, so no state is assumed across launches).
-    if (p.nseg > 1) SK_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(unsigned), s));
-    int nseg = p.nseg, seglen = p.seglen;
-    float sh = shift_scale();
-    void* args[] = {(void*)&x,   (void*)&y,    (void*)&rows,   (void*)&cols,
-                    (void*)&ldx, (void*)&ldy,  (void*)&nseg,   (void*)&seglen,
-                    (void*)&cnt, (void*)&part, (void*)&bad,    (void*)&sh};
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(p.grid));
-    cfg.blockDim = dim3(p.threads);
-    cfg.dynamicSmemBytes = p.smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = p.nseg > 1 ? 1 : 0;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    SK_CUDA(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(fn), args));
+    if (nseg > 1) SK_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(unsigned), s));
+    if (p.k3_lag) {
+      const LagFn fn = p.seglen <= kLagThreads * 16 ? lag_fn<4>(mode) : lag_fn<8>(mode);
+      SK_CUDA(launch_k(reinterpret_cast<const void*>(fn), dim3(static_cast<unsigned>(p.grid)),
+                       dim3(p.threads), 0, s, true, x, y, rows, cols, ldx, ldy, nseg, seglen,
+                       p.lag, cnt, part, bad, sh));
+    } else {
+      SK_CUDA(launch_k(reinterpret_cast<const void*>(seg_fn<kSegNV>(mode)),
+                       dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), p.smem, s, nseg > 1,
+                       x, y, rows, cols, ldx, ldy, nseg, seglen, cnt, part, bad, sh));
+    }
     return SK_OK;
   }
-  // split: stats -> combine -> normalize
-  const WsLayout l = ws_layout(rows, p.nch);
-  RowPartial* part = reinterpret_cast<RowPartial*>(ws + l.part);
-  float* rmax = reinterpret_cast<float*>(ws + l.rmax);
-  double* rsum = reinterpret_cast<double*>(ws + l.rsum);
-  const unsigned g = static_cast<unsigned>(rows * p.nch);
-  switch (mode) {
-    case kClipAccurate: k4_stats<kClipAccurate><<<g, kSplitThreads, 0, s>>>(x, rows, cols, ldx, p.nch, part, bad, shift_scale()); break;
-    case kAccurate: k4_stats<kAccurate><<<g, kSplitThreads, 0, s>>>(x, rows, cols, ldx, p.nch, part, bad, shift_scale()); break;
-    default: k4_stats<kApprox><<<g, kSplitThreads, 0, s>>>(x, rows, cols, ldx, p.nch, part, bad, shift_scale()); break;
-  }
-  SK_CUDA(cudaGetLastError());
-  k4_combine<<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, s>>>(part, rows, p.nch,
-                                                                          rmax, rsum);
-  SK_CUDA(cudaGetLastError());
-  const bool v4 = p.vec;
-#define SK_NORM(M)                                                                          \
-  if (v4)                                                                                   \
-    k4_normalize<M, 4><<<g, kSplitThreads, 0, s>>>(x, y, rows, cols, ldx, ldy, p.nch, rmax, \
-                                                   rsum);                                   \
-  else                                                                                      \
-    k4_normalize<M, 1><<<g, kSplitThreads, 0, s>>>(x, y, rows, cols, ldx, ldy, p.nch, rmax, rsum);
-  switch (mode) {
-    case kClipAccurate: SK_NORM(kClipAccurate); break;
-    case kAccurate: SK_NORM(kAccurate); break;
-    default: SK_NORM(kApprox); break;
-  }
-#undef SK_NORM
-  SK_CUDA(cudaGetLastError());
-  return SK_OK;
+  return launch_split(x, y, rows, cols, ldx, ldy, mode, p.vec, bad, ws, p.nch, true, nullptr,
+                      nullptr, s);
 }
 
 int softmax_dev(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx, int64_t ldy,
@@ -470,6 +540,11 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "grid_mult") g_grid_mult = value;
   else if (k == "seg_len") g_seg_len = value;
   else if (k == "skip_max_shift") g_skip_max_shift = value;
+  else if (k == "seg_align") g_seg_align = value;
+  else if (k == "k1_pf") g_k1_pf = value;
+  else if (k == "pdl") g_pdl = value;
+  else if (k == "lag") g_lag = value;
+  else if (k == "k3_impl") g_k3_impl = value;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;
 }
@@ -498,12 +573,12 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
   st = make_plan(rows, cols, ldx, ldy, x_addr, y_addr, 0, device, p);
   if (st) return st;
   if (p.kind == kPathK1)
-    snprintf(buf, buflen, "k1 vec=%d lpr=%d nv=%d u=%d threads=%d grid=%lld", p.k1->vec,
-             p.k1->lpr, p.k1->nv, p.k1->u, kRowsThreads, (long long)p.grid);
+    snprintf(buf, buflen, "k1 vec=%d lpr=%d nv=%d u=%d pf=%d threads=%d grid=%lld", p.k1->vec,
+             p.k1->lpr, p.k1->nv, p.k1->u, p.k1->pf, kRowsThreads, (long long)p.grid);
   else if (p.kind == kPathSeg)
-    snprintf(buf, buflen, "%s nseg=%d seglen=%d threads=%d smem=%zu grid=%lld",
-             p.nseg == 1 ? "k2_tma" : "k3_coop", p.nseg, p.seglen, p.threads, p.smem,
-             (long long)p.grid);
+    snprintf(buf, buflen, "%s nseg=%d seglen=%d threads=%d smem=%zu lag=%d grid=%lld",
+             p.nseg == 1 ? "k2_tma" : (p.k3_lag ? "k3_lag" : "k3_smem"), p.nseg, p.seglen,
+             p.threads, p.smem, p.lag, (long long)p.grid);
   else
     snprintf(buf, buflen, "k4_split vec=%d nch=%d grid=%lld", p.vec ? 4 : 1, p.nch,
              (long long)p.grid);
@@ -615,18 +690,8 @@ int sk_row_stats_f32(const float* x, int64_t rows, int64_t cols, int64_t ldx, in
     ws = static_cast<char*>(w);
   }
   if (!bad_row) bad_row = reinterpret_cast<unsigned long long*>(ws);
-  RowPartial* part = reinterpret_cast<RowPartial*>(ws + l.part);
-  const unsigned g = static_cast<unsigned>(rows * nch);
-  switch (mode) {
-    case kClipAccurate: k4_stats<kClipAccurate><<<g, kSplitThreads, 0, s>>>(x, rows, cols, ldx, nch, part, bad_row, shift_scale()); break;
-    case kAccurate: k4_stats<kAccurate><<<g, kSplitThreads, 0, s>>>(x, rows, cols, ldx, nch, part, bad_row, shift_scale()); break;
-    default: k4_stats<kApprox><<<g, kSplitThreads, 0, s>>>(x, rows, cols, ldx, nch, part, bad_row, shift_scale()); break;
-  }
-  SK_CUDA(cudaGetLastError());
-  k4_combine<<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, s>>>(part, rows, nch,
-                                                                          row_max, row_sum);
-  SK_CUDA(cudaGetLastError());
-  return SK_OK;
+  return launch_split(x, nullptr, rows, cols, ldx, ldx, mode, false, bad_row, ws, nch, false,
+                      row_max, row_sum, s);
 }
 
 int sk_rescale_sumexp(const float* local_max, const float* global_max, double* row_sum,
@@ -634,9 +699,10 @@ int sk_rescale_sumexp(const float* local_max, const float* global_max, double* r
   if (rows < 0) return arg_fail("rows < 0");
   if (rows == 0) return SK_OK;
   if (!local_max || !global_max || !row_sum) return arg_fail("null buffer");
-  k4_rescale<<<static_cast<unsigned>((rows + 255) / 256), 256, 0,
-               static_cast<cudaStream_t>(stream)>>>(local_max, global_max, row_sum, rows);
-  SK_CUDA(cudaGetLastError());
+  SK_CUDA(launch_k(reinterpret_cast<const void*>(&k4_rescale),
+                   dim3(static_cast<unsigned>((rows + 255) / 256)), dim3(256), 0,
+                   static_cast<cudaStream_t>(stream), false, local_max, global_max, row_sum,
+                   rows));
   return SK_OK;
 }
 
@@ -653,19 +719,22 @@ int sk_normalize_f32(const float* x, float* y, int64_t rows, int64_t cols, int64
   const bool v4 = (cols % 4 == 0) && (ldx % 4 == 0) && (ldy % 4 == 0) &&
                   (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
                   (reinterpret_cast<uintptr_t>(y) % 16 == 0);
-#define SK_NORM(M)                                                                            \
-  if (v4)                                                                                     \
-    k4_normalize<M, 4><<<g, kSplitThreads, 0, s>>>(x, y, rows, cols, ldx, ldy, nch, row_max,  \
-                                                   row_sum);                                  \
-  else                                                                                        \
-    k4_normalize<M, 1><<<g, kSplitThreads, 0, s>>>(x, y, rows, cols, ldx, ldy, nch, row_max, row_sum);
+  const void* norm;
   switch (mode) {
-    case kClipAccurate: SK_NORM(kClipAccurate); break;
-    case kAccurate: SK_NORM(kAccurate); break;
-    default: SK_NORM(kApprox); break;
+    case kClipAccurate:
+      norm = v4 ? reinterpret_cast<const void*>(&k4_normalize<kClipAccurate, 4>)
+                : reinterpret_cast<const void*>(&k4_normalize<kClipAccurate, 1>);
+      break;
+    case kAccurate:
+      norm = v4 ? reinterpret_cast<const void*>(&k4_normalize<kAccurate, 4>)
+                : reinterpret_cast<const void*>(&k4_normalize<kAccurate, 1>);
+      break;
+    default:
+      norm = v4 ? reinterpret_cast<const void*>(&k4_normalize<kApprox, 4>)
+                : reinterpret_cast<const void*>(&k4_normalize<kApprox, 1>);
   }
-#undef SK_NORM
-  SK_CUDA(cudaGetLastError());
+  SK_CUDA(launch_k(norm, dim3(g), dim3(kSplitThreads), 0, s, false, x, y, rows, cols, ldx, ldy,
+                   nch, row_max, row_sum));
   return SK_OK;
 }
 

@@ -142,6 +142,16 @@ __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src
       : "memory");
 }
 
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// Every kernel waits for its stream predecessor's memory to be visible before
+// touching global memory, then immediately lets its own successor be
+// scheduled, so back-to-back launches overlap launch latency and tail.  Both
+// are no-ops when the launch did not carry the PDL attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---- global-scope acquire/release for cross-CTA row statistics --------------
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   unsigned v;

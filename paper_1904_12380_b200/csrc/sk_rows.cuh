@@ -18,109 +18,143 @@ namespace sk {
 
 constexpr int kRowsThreads = 256;
 
+template <int VEC, int LPR, int NV, int U>
+struct RowBatch {
+  float v[U][NV][VEC];
+};
+
+template <int VEC, int LPR, int NV, int U>
+__device__ __forceinline__ void k1_load(RowBatch<VEC, LPR, NV, U>& B, const float* __restrict__ x,
+                                        int64_t base, int64_t rows, int cols, int64_t ldx,
+                                        int sub, int sl) {
+  constexpr int RPW = 32 / LPR;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t r = base + u * RPW + sub;
+    const bool rv = r < rows;
+    const float* xr = x + (rv ? r : 0) * ldx;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int c = (j * LPR + sl) * VEC;
+      if (rv && c < cols) {
+        if constexpr (VEC == 4) {
+          const float4 t = ld_stream4(xr + c);
+          B.v[u][j][0] = t.x; B.v[u][j][1] = t.y; B.v[u][j][2] = t.z; B.v[u][j][3] = t.w;
+        } else {
+          B.v[u][j][0] = ld_stream1(xr + c);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) B.v[u][j][k] = kPadLogit;
+      }
+    }
+  }
+}
+
 template <int MODE, int VEC, int LPR, int NV, int U>
+__device__ __forceinline__ void k1_process(RowBatch<VEC, LPR, NV, U>& B, float* __restrict__ y,
+                                           int64_t base, int64_t rows, int cols, int64_t ldy,
+                                           int sub, int sl, unsigned long long* bad_row,
+                                           float shift_scale) {
+  constexpr int RPW = 32 / LPR;
+  // ---- row max (strict-'>' scan == max for finite data) + finite check
+  float m[U];
+  bool bad[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    float mu = kPadLogit;
+    bool b = false;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) {
+        mu = fmaxf(mu, B.v[u][j][k]);
+        b |= not_finite(B.v[u][j][k]);
+      }
+    bad[u] = b;
+    m[u] = group_max<LPR>(mu) * shift_scale;  // shift_scale = 0: fault hook
+  }
+  // ---- shift, clip, exp (kept in registers), row sum
+  float rcp[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const bool rv = base + u * RPW + sub < rows;
+    float s = 0.0f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const bool ok = rv && (j * LPR + sl) * VEC < cols;
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) {
+        const float e = shifted_exp<MODE>(B.v[u][j][k], m[u]);
+        B.v[u][j][k] = e;
+        s += ok ? e : 0.0f;
+      }
+    }
+    rcp[u] = recip_of_sum(group_sum<LPR>(static_cast<double>(s)));
+  }
+  // ---- scale + flush, write once
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t r = base + u * RPW + sub;
+    if (r >= rows) continue;
+    float* yr = y + r * ldy;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int c = (j * LPR + sl) * VEC;
+      if (c < cols) {
+        if constexpr (VEC == 4) {
+          st_stream4(yr + c, make_float4(scale_flush(B.v[u][j][0], rcp[u]),
+                                         scale_flush(B.v[u][j][1], rcp[u]),
+                                         scale_flush(B.v[u][j][2], rcp[u]),
+                                         scale_flush(B.v[u][j][3], rcp[u])));
+        } else {
+          st_stream1(yr + c, scale_flush(B.v[u][j][0], rcp[u]));
+        }
+      }
+    }
+  }
+  // ---- non-finite input: report the smallest offending row (kernels.py:342-347)
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (bad[u]) atomicMin(bad_row, static_cast<unsigned long long>(base + u * RPW + sub));
+}
+
+// PF = 1: software-pipelined -- the next batch's loads are issued before the
+// current batch is reduced, so each lane keeps 2*U*NV requests in flight.
+template <int MODE, int VEC, int LPR, int NV, int U, int PF>
 __global__ void __launch_bounds__(kRowsThreads)
     k1_rows(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int cols,
             int64_t ldx, int64_t ldy, unsigned long long* __restrict__ bad_row,
             float shift_scale) {
   static_assert(VEC == 1 || VEC == 4, "VEC");
   static_assert(LPR >= 1 && LPR <= 32 && (LPR & (LPR - 1)) == 0, "LPR");
-  constexpr int RPW = 32 / LPR;
-  constexpr int ROWS_ITER = U * RPW;
+  constexpr int ROWS_ITER = U * (32 / LPR);
   const int lane = threadIdx.x & 31;
   const int sub = lane / LPR;
   const int sl = lane % LPR;
   const int64_t gwarp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarp = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t stride = ((int64_t(gridDim.x) * blockDim.x) >> 5) * ROWS_ITER;
+  pdl_wait();
+  pdl_launch_dependents();
 
-  for (int64_t base = gwarp * ROWS_ITER; base < rows; base += nwarp * ROWS_ITER) {
-    float v[U][NV][VEC];
-    bool bad[U];
-    // ---- one batch of loads: U*NV independent requests in flight per lane
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t r = base + u * RPW + sub;
-      const bool rv = r < rows;
-      const float* xr = x + (rv ? r : 0) * ldx;
-#pragma unroll
-      for (int j = 0; j < NV; ++j) {
-        const int c = (j * LPR + sl) * VEC;
-        if (rv && c < cols) {
-          if constexpr (VEC == 4) {
-            const float4 t = ld_stream4(xr + c);
-            v[u][j][0] = t.x; v[u][j][1] = t.y; v[u][j][2] = t.z; v[u][j][3] = t.w;
-          } else {
-            v[u][j][0] = ld_stream1(xr + c);
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < VEC; ++k) v[u][j][k] = kPadLogit;
-        }
-      }
+  int64_t base = gwarp * ROWS_ITER;
+  if constexpr (PF) {
+    if (base >= rows) return;
+    RowBatch<VEC, LPR, NV, U> cur;
+    k1_load(cur, x, base, rows, cols, ldx, sub, sl);
+    for (; base < rows; base += stride) {
+      RowBatch<VEC, LPR, NV, U> nxt;
+      const bool more = base + stride < rows;
+      if (more) k1_load(nxt, x, base + stride, rows, cols, ldx, sub, sl);
+      k1_process<MODE>(cur, y, base, rows, cols, ldy, sub, sl, bad_row, shift_scale);
+      if (more) cur = nxt;
     }
-    // ---- row max (strict-'>' scan == max for finite data) + finite check
-    float m[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      float mu = kPadLogit;
-      bool b = false;
-#pragma unroll
-      for (int j = 0; j < NV; ++j)
-#pragma unroll
-        for (int k = 0; k < VEC; ++k) {
-          mu = fmaxf(mu, v[u][j][k]);
-          b |= not_finite(v[u][j][k]);
-        }
-      bad[u] = b;
-      m[u] = group_max<LPR>(mu) * shift_scale;  // shift_scale = 0: fault hook
+  } else {
+    for (; base < rows; base += stride) {
+      RowBatch<VEC, LPR, NV, U> cur;
+      k1_load(cur, x, base, rows, cols, ldx, sub, sl);
+      k1_process<MODE>(cur, y, base, rows, cols, ldy, sub, sl, bad_row, shift_scale);
     }
-    // ---- shift, clip, exp (kept in registers), row sum
-    float rcp[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t r = base + u * RPW + sub;
-      const bool rv = r < rows;
-      float s = 0.0f;
-#pragma unroll
-      for (int j = 0; j < NV; ++j) {
-        const int c = (j * LPR + sl) * VEC;
-        const bool ok = rv && c < cols;
-#pragma unroll
-        for (int k = 0; k < VEC; ++k) {
-          const float e = shifted_exp<MODE>(v[u][j][k], m[u]);
-          v[u][j][k] = e;
-          s += ok ? e : 0.0f;
-        }
-      }
-      rcp[u] = recip_of_sum(group_sum<LPR>(static_cast<double>(s)));
-    }
-    // ---- scale + flush, write once
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t r = base + u * RPW + sub;
-      if (r >= rows) continue;
-      float* yr = y + r * ldy;
-#pragma unroll
-      for (int j = 0; j < NV; ++j) {
-        const int c = (j * LPR + sl) * VEC;
-        if (c < cols) {
-          if constexpr (VEC == 4) {
-            float4 t;
-            t.x = scale_flush(v[u][j][0], rcp[u]);
-            t.y = scale_flush(v[u][j][1], rcp[u]);
-            t.z = scale_flush(v[u][j][2], rcp[u]);
-            t.w = scale_flush(v[u][j][3], rcp[u]);
-            st_stream4(yr + c, t);
-          } else {
-            st_stream1(yr + c, scale_flush(v[u][j][0], rcp[u]));
-          }
-        }
-      }
-    }
-    // ---- non-finite input: report the smallest offending row (kernels.py:342-347)
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (bad[u]) atomicMin(bad_row, static_cast<unsigned long long>(base + u * RPW + sub));
   }
 }
 

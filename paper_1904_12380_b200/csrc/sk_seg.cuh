@@ -73,6 +73,8 @@ __global__ void __launch_bounds__(1024)
                 &bars[stage]);
   };
 
+  pdl_wait();
+  pdl_launch_dependents();
   if (tid == 0) {
     for (int s = 0; s < kSegStages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();

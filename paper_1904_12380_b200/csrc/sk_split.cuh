@@ -59,6 +59,8 @@ __global__ void __launch_bounds__(kSplitThreads)
              float shift_scale) {
   __shared__ float red_f[33];
   __shared__ double red_d[33];
+  pdl_wait();
+  pdl_launch_dependents();
   const int64_t w = blockIdx.x;
   const int64_t row = w / nch;
   const int ch = static_cast<int>(w - row * nch);
@@ -98,6 +100,8 @@ __global__ void __launch_bounds__(kSplitThreads)
 // one warp per row
 __global__ void k4_combine(const RowPartial* __restrict__ partials, int64_t rows, int nch,
                            float* __restrict__ row_max, double* __restrict__ row_sum) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -118,6 +122,8 @@ __global__ void k4_combine(const RowPartial* __restrict__ partials, int64_t rows
 __global__ void k4_rescale(const float* __restrict__ local_max,
                            const float* __restrict__ global_max, double* __restrict__ sum,
                            int64_t rows) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= rows) return;
   const float d = local_max[i] - global_max[i];
@@ -129,6 +135,8 @@ __global__ void __launch_bounds__(kSplitThreads)
     k4_normalize(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
                  int64_t ldx, int64_t ldy, int nch, const float* __restrict__ row_max,
                  const double* __restrict__ row_sum) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int64_t w = blockIdx.x;
   const int64_t row = w / nch;
   const int ch = static_cast<int>(w - row * nch);

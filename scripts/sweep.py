@@ -1,0 +1,143 @@
+#!/usr/bin/env python
+"""Kernel-shape sweep on one GPU: device time per launch for each tuning.
+
+    python scripts/sweep.py --config c2 --reps 200
+
+Times back-to-back launches over rotating buffer pairs (> 3x L2) with CUDA
+events; prints one JSON line per variant to stdout.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+from paper_1904_12380_b200 import _native, configs  # noqa: E402
+
+K1_SHAPES = {
+    # (lpr, nv, u, pf) -- vec=4 entries instantiated in sk_api.cu
+    "c2": [(8, 4, 1, 0), (16, 2, 1, 0), (8, 4, 1, 1), (16, 2, 1, 1), (16, 1, 4, 1), (8, 1, 4, 1)],
+    "c5a": [(16, 4, 1, 0), (16, 4, 1, 1), (32, 2, 1, 1), (32, 2, 2, 0)],
+    "c3": [(32, 8, 1, 0), (32, 8, 1, 1)],
+}
+
+
+def bench_once(x, ys, rows, cols, reps, stream):
+    L = _native.lib()
+    R = len(ys)
+    flag = torch.full((1,), -1, dtype=torch.int64, device=x[0].device)
+
+    def launch(i):
+        _native.check(L.sk_softmax_f32(x[i % R].data_ptr(), ys[i % R].data_ptr(), rows, cols, cols,
+                                       cols, 0, flag.data_ptr(), None, 0, stream.cuda_stream))
+
+    with torch.cuda.stream(stream):
+        for i in range(10):
+            launch(i)
+        g = torch.cuda.CUDAGraph()
+        G = R * max(1, 32 // R)
+        with torch.cuda.graph(g, stream=stream):
+            for i in range(G):
+                launch(i)
+        g.replay()
+        stream.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        n = max(1, reps // G)
+        e0.record(stream)
+        for _ in range(n):
+            g.replay()
+        e1.record(stream)
+    stream.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / (n * G)
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--config", default="c2")
+    p.add_argument("--reps", type=int, default=200)
+    p.add_argument("--seg-lens", default="4096,8192")
+    p.add_argument("--grid-mults", default="1,2")
+    args = p.parse_args()
+    spec = configs.get(args.config)
+    x_host = configs.generate(spec)
+    dev = torch.device("cuda", 0)
+    pair = 8 * spec.rows * spec.cols
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    R = max(2, -(-3 * l2 // pair))
+    xs = [torch.from_numpy(x_host).to(dev)]
+    xs += [xs[0].clone() for _ in range(R - 1)]
+    ys = [torch.empty_like(xs[0]) for _ in range(R)]
+    s = torch.cuda.Stream(dev)
+    rows, cols = spec.rows, spec.cols
+    out = []
+
+    def record(tag, us):
+        d = {"config": spec.name, "variant": tag, "us": us,
+             "gbs": 8.0 * rows * cols / us / 1e3,
+             "plan": _native.describe_plan(rows, cols, cols, cols, xs[0].data_ptr(),
+                                           ys[0].data_ptr(), 0)}
+        print(json.dumps(d), flush=True)
+        out.append(d)
+
+    record("default", bench_once(xs, ys, rows, cols, args.reps, s))
+    if cols <= 1024:
+        _native.set_tuning("pdl", 0)
+        record("default pdl=0", bench_once(xs, ys, rows, cols, args.reps, s))
+        _native.set_tuning("pdl", 1)
+        for lpr, nv, u, pf in K1_SHAPES.get(spec.name, []):
+            for gm in map(int, args.grid_mults.split(",")):
+                _native.set_tuning("k1_lpr", lpr)
+                _native.set_tuning("k1_nv", nv)
+                _native.set_tuning("k1_u", u)
+                _native.set_tuning("k1_pf", pf)
+                _native.set_tuning("grid_mult", gm)
+                try:
+                    record(f"k1 lpr={lpr} nv={nv} u={u} pf={pf} gm={gm}",
+                           bench_once(xs, ys, rows, cols, args.reps, s))
+                except Exception as e:  # noqa: BLE001
+                    print(json.dumps({"variant": f"{lpr},{nv},{u},{pf}", "error": str(e)}))
+        _native.set_tuning("k1_lpr", 0)
+        _native.set_tuning("k1_pf", -1)
+        _native.set_tuning("grid_mult", 0)
+    else:
+        for lag in (0, 1, 2, 4):
+            _native.set_tuning("lag", lag)
+            for sl in map(int, args.seg_lens.split(",")):
+                _native.set_tuning("seg_len", sl)
+                record(f"k3_lag seg_len={sl} lag={lag}", bench_once(xs, ys, rows, cols, args.reps, s))
+        _native.set_tuning("lag", 2)
+        _native.set_tuning("seg_len", 0)
+        _native.set_tuning("k3_impl", 1)
+        record("k3_smem", bench_once(xs, ys, rows, cols, args.reps, s))
+        _native.set_tuning("k3_impl", 0)
+        _native.set_tuning("path", 2)
+        record("split(k4)", bench_once(xs, ys, rows, cols, max(10, args.reps // 4), s))
+        _native.set_tuning("path", -1)
+    # copy roofline in the same run: D2D copy of the same bytes (bound_probe analog)
+    a = xs[0]
+    b = ys[0]
+    with torch.cuda.stream(s):
+        for _ in range(5):
+            b.copy_(a)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for i in range(50):
+            ys[i % R].copy_(xs[i % R])
+        e1.record(s)
+    s.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / 50
+    print(json.dumps({"config": spec.name, "variant": "torch copy_ (same bytes)", "us": us,
+                      "gbs": 8.0 * rows * cols / us / 1e3}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
