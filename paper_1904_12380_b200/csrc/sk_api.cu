@@ -16,7 +16,7 @@
 #include "sk_rows.cuh"
 #include "sk_seg.cuh"
 #include "sk_split.cuh"
-#include "sk_lag.cuh"
+#include "sk_chunk.cuh"
 
 namespace sk {
 namespace {
@@ -70,8 +70,8 @@ std::atomic<int> g_k1_lpr{0}, g_k1_nv{0}, g_k1_u{0}, g_grid_mult{0}, g_seg_len{0
 std::atomic<int> g_seg_align{0};  // K3 grid = whole multiple of nseg (row groups never straddle)
 std::atomic<int> g_k1_pf{-1};     // -1: table default, 0/1 force register prefetch
 std::atomic<int> g_pdl{1};        // programmatic dependent launch on every kernel
-std::atomic<int> g_lag{2};        // K3 normalize lag in rounds
-std::atomic<int> g_k3_impl{0};    // 0: lagged two-pass (k3_lag), 1: smem-resident (k_seg)
+std::atomic<int> g_chunk_mb{24};  // K3 row-chunk size (MB of input) kept L2 resident
+std::atomic<int> g_k3_impl{0};    // 0: L2-chunked two-pass (k3_chunk), 1: smem-resident (k_seg)
 
 // Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.
 template <typename... Args>
@@ -170,17 +170,15 @@ SegFn seg_fn(int mode) {
     default: return &k_seg<kApprox, NV>;
   }
 }
-using LagFn = void (*)(const float*, float*, int64_t, int64_t, int64_t, int64_t, int, int, int,
-                       unsigned*, RowPartial*, unsigned long long*, float);
 template <int NV>
-LagFn lag_fn(int mode) {
+const void* chunk_fn(int mode) {
   switch (mode) {
-    case kClipAccurate: return &k3_lag<kClipAccurate, NV>;
-    case kAccurate: return &k3_lag<kAccurate, NV>;
-    default: return &k3_lag<kApprox, NV>;
+    case kClipAccurate: return reinterpret_cast<const void*>(&k3_chunk<kClipAccurate, NV>);
+    case kAccurate: return reinterpret_cast<const void*>(&k3_chunk<kAccurate, NV>);
+    default: return reinterpret_cast<const void*>(&k3_chunk<kApprox, NV>);
   }
 }
-constexpr int kLagThreads = 256;
+constexpr int64_t kChunkSeg = 4096;  // default K3 segment (256 threads x 4 float4)
 constexpr int kSegNV = 4;
 constexpr int kSegMaxThreads = 512;
 constexpr int64_t kSegCap = int64_t(kSegMaxThreads) * kSegNV * 4;  // 8192 floats / CTA
@@ -225,8 +223,9 @@ struct Plan {
   // K1
   const K1Entry* k1 = nullptr;
   // seg (K2: nseg == 1; K3: nseg > 1)
-  int nseg = 1, seglen = 0, threads = 0, lag = 0;
-  bool k3_lag = false;
+  int nseg = 1, seglen = 0, threads = 0;
+  bool k3_chunk = false;
+  int64_t chunk_rows = 0;
   size_t smem = 0;
   // split
   int nch = 0;
@@ -292,7 +291,8 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     return SK_OK;
   }
   if (kind == kPathSeg) {
-    int64_t target = g_seg_len.load() > 0 ? g_seg_len.load() : kSegCap;
+    const bool chunked = cols > kSegCap && g_k3_impl.load() == 0;
+    int64_t target = g_seg_len.load() > 0 ? g_seg_len.load() : (chunked ? kChunkSeg : kSegCap);
     target = std::min<int64_t>(target, kSegCap);
     const int64_t nseg = (cols + target - 1) / target;
     const int64_t seglen = align_up((cols + nseg - 1) / nseg, 4);
@@ -301,15 +301,18 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     p.seglen = static_cast<int>(seglen);
     const int64_t items = rows * nseg;
     if (nseg > 1 && g_k3_impl.load() == 0) {
-      // K3: lagged two-pass, 256 threads, NV float4 per thread
-      p.k3_lag = true;
-      p.threads = kLagThreads;
-      p.lag = std::max(0, g_lag.load());
+      // K3: L2-chunked two-pass, 256 threads, NV float4 per thread
+      p.k3_chunk = true;
+      p.threads = kChunkThreads;
       p.smem = 0;
-      const int nv = seglen <= int64_t(kLagThreads) * 4 * 4 ? 4 : 8;
-      const LagFn fn = nv == 4 ? lag_fn<4>(mode) : lag_fn<8>(mode);
-      const int occ = occupancy(reinterpret_cast<const void*>(fn), p.threads, 0);
-      p.grid = std::min(items, int64_t(di.sms) * std::max(occ, 1));
+      const int nv = seglen <= int64_t(kChunkThreads) * 4 * 4 ? 4 : 8;
+      const void* fn = nv == 4 ? chunk_fn<4>(mode) : chunk_fn<8>(mode);
+      const int occ = occupancy(fn, p.threads, 0);
+      p.grid = int64_t(di.sms) * std::max(occ, 1);
+      const int64_t chunk_bytes = int64_t(std::max(1, g_chunk_mb.load())) << 20;
+      p.chunk_rows = std::max<int64_t>(1, chunk_bytes / (cols * 4));
+      p.chunk_rows = std::min(p.chunk_rows, rows);
+      return SK_OK;  // no co-residency requirement: the kernel boundary is the barrier
     } else {
       // K2 (nseg == 1) or smem-resident K3: TMA segments into a 2-stage ring
       int threads = static_cast<int>(align_up((seglen / 4 + kSegNV - 1) / kSegNV, 32));
@@ -427,11 +430,21 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
     // K3 row counters start at zero every launch (the workspace is shared by
     // launches of different shapes, so no state is assumed across launches).
     if (nseg > 1) SK_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(unsigned), s));
-    if (p.k3_lag) {
-      const LagFn fn = p.seglen <= kLagThreads * 16 ? lag_fn<4>(mode) : lag_fn<8>(mode);
-      SK_CUDA(launch_k(reinterpret_cast<const void*>(fn), dim3(static_cast<unsigned>(p.grid)),
-                       dim3(p.threads), 0, s, true, x, y, rows, cols, ldx, ldy, nseg, seglen,
-                       p.lag, cnt, part, bad, sh));
+    if (p.k3_chunk) {
+      const void* fn = p.seglen <= kChunkThreads * 16 ? chunk_fn<4>(mode) : chunk_fn<8>(mode);
+      float* rmax = reinterpret_cast<float*>(ws + l.rmax);
+      double* rsum = reinterpret_cast<double*>(ws + l.rsum);
+      const int64_t nchunks = (rows + p.chunk_rows - 1) / p.chunk_rows;
+      for (int64_t k = 0; k <= nchunks; ++k) {
+        const int64_t s0 = k * p.chunk_rows;
+        const int64_t sr = k < nchunks ? std::min(p.chunk_rows, rows - s0) : 0;
+        const int64_t n0 = (k - 1) * p.chunk_rows;
+        const int64_t nr = k >= 1 ? std::min(p.chunk_rows, rows - n0) : 0;
+        const int wait_first = k == 0 ? 1 : 0;
+        SK_CUDA(launch_k(fn, dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), 0, s, false, x,
+                         y, cols, ldx, ldy, nseg, seglen, s0, sr, std::max<int64_t>(n0, 0), nr,
+                         wait_first, cnt, part, rmax, rsum, bad, sh));
+      }
     } else {
       SK_CUDA(launch_k(reinterpret_cast<const void*>(seg_fn<kSegNV>(mode)),
                        dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), p.smem, s, nseg > 1,
@@ -543,7 +556,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "seg_align") g_seg_align = value;
   else if (k == "k1_pf") g_k1_pf = value;
   else if (k == "pdl") g_pdl = value;
-  else if (k == "lag") g_lag = value;
+  else if (k == "chunk_mb") g_chunk_mb = value;
   else if (k == "k3_impl") g_k3_impl = value;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;
@@ -551,7 +564,7 @@ int sk_set_tuning(const char* key, int value) {
 
 size_t sk_softmax_workspace_bytes(int64_t rows, int64_t cols) {
   if (rows <= 0 || cols <= 0) return ws_layout(0, 0).total;
-  const int64_t nseg = (cols + kSegCap - 1) / kSegCap;
+  const int64_t nseg = (cols + kChunkSeg - 1) / kChunkSeg;
   const int64_t nch = (cols + kSplitChunk - 1) / kSplitChunk;
   return std::max(ws_layout(rows, nseg).total, ws_layout(rows, nch).total);
 }
@@ -576,9 +589,9 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
     snprintf(buf, buflen, "k1 vec=%d lpr=%d nv=%d u=%d pf=%d threads=%d grid=%lld", p.k1->vec,
              p.k1->lpr, p.k1->nv, p.k1->u, p.k1->pf, kRowsThreads, (long long)p.grid);
   else if (p.kind == kPathSeg)
-    snprintf(buf, buflen, "%s nseg=%d seglen=%d threads=%d smem=%zu lag=%d grid=%lld",
-             p.nseg == 1 ? "k2_tma" : (p.k3_lag ? "k3_lag" : "k3_smem"), p.nseg, p.seglen,
-             p.threads, p.smem, p.lag, (long long)p.grid);
+    snprintf(buf, buflen, "%s nseg=%d seglen=%d threads=%d smem=%zu chunk_rows=%lld grid=%lld",
+             p.nseg == 1 ? "k2_tma" : (p.k3_chunk ? "k3_chunk" : "k3_smem"), p.nseg, p.seglen,
+             p.threads, p.smem, (long long)p.chunk_rows, (long long)p.grid);
   else
     snprintf(buf, buflen, "k4_split vec=%d nch=%d grid=%lld", p.vec ? 4 : 1, p.nch,
              (long long)p.grid);
