@@ -141,6 +141,15 @@ void sk_free_pinned(void* p);
 int sk_set_tuning(const char* key, int value);
 
 /*
+ * Accuracy diagnostic of the kernels' exponential: sweeps every fp32 value in
+ * [lo, hi] (hi <= 0) through the packed and scalar exp paths of `mode` and
+ * reports the worst error vs the double-precision exp, in fp32 ulps of the
+ * true result and as a relative error.  Synchronous.  (Reference exp:
+ * kernels.py:171-174.)
+ */
+int sk_exp_accuracy(int mode, float lo, float hi, double* max_ulp, double* max_rel, int device);
+
+/*
  * Launch plan that sk_softmax_f32 would use for this shape/alignment, as a
  * short text ("k1_vec lpr=8 nv=4 u=2 grid=..." ...), for tests and bench logs.
  * Writes at most buflen bytes (NUL-terminated); returns SK_OK.

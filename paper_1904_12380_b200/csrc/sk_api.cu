@@ -372,6 +372,8 @@ int check_common(const float* x, const void* y, int64_t rows, int64_t cols, int6
   if (mode < 0 || mode > 2) return arg_fail("mode must be SK_MODE_CLIPPED/EXACT/APPROX");
   if (rows > 0 && (!x || !y)) return arg_fail("null buffer");
   if (cols > (int64_t(1) << 40)) return arg_fail("cols too large");
+  // clip mode skips the sub-normal flush: every output >= e^-64 / cols is normal
+  if (mode == 0 && cols > int64_t(13000000000)) return arg_fail("cols too large for clip mode");
   return SK_OK;
 }
 

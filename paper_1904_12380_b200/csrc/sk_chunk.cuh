@@ -113,24 +113,24 @@ __global__ void __launch_bounds__(kChunkThreads)
         }
       }
       float mt = kPadLogit;
-      bool bad = false;
-#pragma unroll
-      for (int i = 0; i < NV; ++i)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          mt = fmaxf(mt, v[i][c]);
-          bad |= not_finite(v[i][c]);
-        }
-      if (bad) atomicMin(bad_row, static_cast<unsigned long long>(row));
-      const float m_l = cta_max(mt, red) * shift_scale;  // shift_scale = 0: fault hook
-      float st = 0.0f;
+      u64 z = f2pk(0.0f, 0.0f);
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
-        const bool ok = tid + i * kChunkThreads < nvec;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) st += ok ? shifted_exp<MODE>(v[i][c], m_l) : 0.0f;
+        mt = fmaxf(mt, fmaxf(fmaxf(v[i][0], v[i][1]), fmaxf(v[i][2], v[i][3])));
+        z = nf_acc2(nf_acc2(z, v[i][0], v[i][1]), v[i][2], v[i][3]);
       }
-      const double s_l = cta_sum(static_cast<double>(st), red);
+      if (nf_bad(z)) atomicMin(bad_row, static_cast<unsigned long long>(row));
+      const float m_l = cta_max(mt, red) * shift_scale;  // shift_scale = 0: fault hook
+      u64 acc = f2pk(0.0f, 0.0f);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        float2 a = sexp2<MODE>(v[i][0], v[i][1], m_l);
+        float2 b = sexp2<MODE>(v[i][2], v[i][3], m_l);
+        if (!(tid + i * kChunkThreads < nvec)) a = b = make_float2(0.0f, 0.0f);
+        acc = f2add(f2add(acc, f2pk(a.x, a.y)), f2pk(b.x, b.y));
+      }
+      const float2 acc2 = f2up(acc);
+      const double s_l = cta_sum(static_cast<double>(acc2.x + acc2.y), red);
       if (tid == 0) {
         RowPartial p;
         p.m = m_l;
@@ -188,11 +188,11 @@ __global__ void __launch_bounds__(kChunkThreads)
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
         const int q = tid + i * kChunkThreads;
-        if (q < nvec)
-          st_stream4(ys + 4 * q, make_float4(scale_flush(shifted_exp<MODE>(t[i].x, M), rcp),
-                                             scale_flush(shifted_exp<MODE>(t[i].y, M), rcp),
-                                             scale_flush(shifted_exp<MODE>(t[i].z, M), rcp),
-                                             scale_flush(shifted_exp<MODE>(t[i].w, M), rcp)));
+        if (q < nvec) {
+          const float2 a = scale2<MODE>(sexp2<MODE>(t[i].x, t[i].y, M), rcp);
+          const float2 b = scale2<MODE>(sexp2<MODE>(t[i].z, t[i].w, M), rcp);
+          st_stream4(ys + 4 * q, make_float4(a.x, a.y, b.x, b.y));
+        }
       }
     }
   }

@@ -26,17 +26,122 @@ constexpr float kClipFloor = -64.0f;                  // kernels.py:99
 constexpr float kFltMinNormal = 1.1754943508222875e-38f;  // kernels.py:101
 constexpr float kPadLogit = -FLT_MAX;                 // padding for max (finite!)
 
+// ---- packed fp32x2 arithmetic (sm_100a FADD2/FMUL2/FFMA2) -----------------
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 f2pk(float a, float b) {
+  u64 r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2up(u64 r) {
+  float2 v;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ u64 f2add(u64 a, u64 b) {
+  u64 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 f2sub(u64 a, u64 b) {
+  u64 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 f2mul(u64 a, u64 b) {
+  u64 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 f2mul_ftz(u64 a, u64 b) {
+  u64 d;
+  asm("mul.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 f2fma(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ float ex2_ftz(float t) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(t));
+  return r;
+}
+
+// ---- the exponential used on the hot path -----------------------------------
+// exp(s) for a shifted logit s <= 0, clamped first at the mode's floor:
+//   clip mode  : -64 (the reference's ValueClip, kernels.py:147 -- exactly
+//                `s > -64 ? s : -64`, since fmaxf(s, -64) is that for non-NaN s)
+//   other modes: -104 (every exp below FLT_MIN flushes to 0 in the output
+//                anyway, kernels.py:186-188; the floor keeps the arithmetic finite)
+// Accurate modes: with L = log2(e) = L_hi + L_lo,
+//   t  = fl(s * L_hi)                     (MUFU argument)
+//   d  = (s*L_hi - t) * ln2 + s*(L_lo*ln2)  (the rounding error of t, exact via FMA)
+//   e  = ex2(t) * (1 + d)                 (one MUFU.EX2 per element)
+// so the MUFU sees one rounded argument and the lost low bits are put back by
+// a first-order correction (|d| < 4e-6).  Measured accuracy is reported by
+// sk_exp_accuracy() and tests/test_gpu_parity.py::test_exp_accuracy_exhaustive.
+// Everything except the clamp and the MUFU runs as packed fp32x2 (FFMA2 etc.),
+// ~5 issue slots per element instead of ~10 for libdevice expf.
+constexpr float kLog2eHi = 1.44269502162933349609375f;            // fp32(log2 e)
+constexpr float kLog2eLoLn2 = 1.925963033500011079e-08f * 0.69314718055994530942f;
+constexpr float kLn2 = 0.69314718055994530942f;
+constexpr float kLog2e = 1.4426950408889634f;
+
+template <int MODE>
+__device__ __forceinline__ constexpr float exp_floor() {
+  return MODE == kClipAccurate ? kClipFloor : -104.0f;
+}
+
+// (x0, x1) -> (exp(clamp(x0 - m)), exp(clamp(x1 - m)))
+template <int MODE>
+__device__ __forceinline__ float2 sexp2(float x0, float x1, float m) {
+  const float2 s = f2up(f2sub(f2pk(x0, x1), f2pk(m, m)));
+  const float s0 = fmaxf(s.x, exp_floor<MODE>()), s1 = fmaxf(s.y, exp_floor<MODE>());
+  const u64 S = f2pk(s0, s1);
+  if (MODE == kApprox) {
+    const float2 t = f2up(f2mul(S, f2pk(kLog2e, kLog2e)));
+    return make_float2(ex2_ftz(t.x), ex2_ftz(t.y));
+  }
+  const u64 tn = f2mul(S, f2pk(-kLog2eHi, -kLog2eHi));      // -t
+  const u64 d1 = f2fma(S, f2pk(kLog2eHi, kLog2eHi), tn);    // s*L_hi - t (exact)
+  const u64 d = f2fma(d1, f2pk(kLn2, kLn2), f2mul(S, f2pk(kLog2eLoLn2, kLog2eLoLn2)));
+  const float2 t = f2up(tn);
+  const u64 p = f2pk(ex2_ftz(-t.x), ex2_ftz(-t.y));
+  return f2up(f2fma(p, d, p));
+}
+
+template <int MODE>
+__device__ __forceinline__ float sexp1(float x, float m) {
+  const float s = fmaxf(x - m, exp_floor<MODE>());
+  if (MODE == kApprox) return ex2_ftz(s * kLog2e);
+  const float t = s * kLog2eHi;
+  const float d = fmaf(fmaf(s, kLog2eHi, -t), kLn2, s * kLog2eLoLn2);
+  const float p = ex2_ftz(t);
+  return fmaf(p, d, p);
+}
+
+// Backwards-compatible scalar name used by the split kernels.
 template <int MODE>
 __device__ __forceinline__ float shifted_exp(float x, float m) {
-  float s = x - m;
-  if (MODE == kClipAccurate) s = s > kClipFloor ? s : kClipFloor;
-  if (MODE == kApprox) {
-    float r;
-    // ex2.approx.ftz: 2^(s*log2e); rel. error ~2^-22 + |s|*log2e*2^-24
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s * 1.4426950408889634f));
-    return r;
-  }
-  return expf(s);  // CUDA libdevice expf, <= 2 ulp (compiled without fast-math)
+  return sexp1<MODE>(x, m);
+}
+
+// Output scale y = e * r with the reference's flush of sub-normal results to
+// +0 (kernels.py:186-188).  In clip mode every output is >= e^-64 / C, which is
+// normal for C < 1.3e10 (checked by the launcher), so the flush cannot fire and
+// a plain multiply is bit-identical; otherwise the ftz multiply flushes exactly
+// the results below FLT_MIN.
+template <int MODE>
+__device__ __forceinline__ float2 scale2(float2 e, float r) {
+  const u64 E = f2pk(e.x, e.y), R = f2pk(r, r);
+  return f2up(MODE == kClipAccurate ? f2mul(E, R) : f2mul_ftz(E, R));
+}
+template <int MODE>
+__device__ __forceinline__ float scale1(float e, float r) {
+  const float y = e * r;
+  return (MODE != kClipAccurate && y < kFltMinNormal) ? 0.0f : y;
 }
 
 // Output scale with the reference's flush-to-zero of sub-normal results.
@@ -48,6 +153,16 @@ __device__ __forceinline__ float scale_flush(float e, float r) {
 // IEEE round-to-nearest reciprocal of the fp32-rounded sum (kernels.py:184).
 __device__ __forceinline__ float recip_of_sum(double s) {
   return __frcp_rn(__double2float_rn(s));
+}
+
+// Non-finite accumulator: z += x * 0 stays +-0 for finite x and turns NaN for
+// any +-Inf/NaN; packed, half an issue slot per element.
+__device__ __forceinline__ u64 nf_acc2(u64 z, float a, float b) {
+  return f2fma(f2pk(a, b), f2pk(0.0f, 0.0f), z);
+}
+__device__ __forceinline__ bool nf_bad(u64 z) {
+  const float2 v = f2up(z);
+  return !(v.x == 0.0f && v.y == 0.0f);
 }
 
 // Non-finite detector: true iff |x| is Inf or x is NaN.  One FSETP per element.

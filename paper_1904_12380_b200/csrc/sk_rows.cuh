@@ -20,8 +20,13 @@ constexpr int kRowsThreads = 256;
 
 template <int VEC, int LPR, int NV, int U>
 struct RowBatch {
-  float v[U][NV][VEC];
+  float v[U][NV * VEC];  // element e of lane-row u sits at column col<>(e)
 };
+
+template <int VEC, int LPR>
+__device__ __forceinline__ int k1_col(int e, int sl) {
+  return ((e / VEC) * LPR + sl) * VEC + (e % VEC);
+}
 
 template <int VEC, int LPR, int NV, int U>
 __device__ __forceinline__ void k1_load(RowBatch<VEC, LPR, NV, U>& B, const float* __restrict__ x,
@@ -39,39 +44,45 @@ __device__ __forceinline__ void k1_load(RowBatch<VEC, LPR, NV, U>& B, const floa
       if (rv && c < cols) {
         if constexpr (VEC == 4) {
           const float4 t = ld_stream4(xr + c);
-          B.v[u][j][0] = t.x; B.v[u][j][1] = t.y; B.v[u][j][2] = t.z; B.v[u][j][3] = t.w;
+          B.v[u][4 * j] = t.x; B.v[u][4 * j + 1] = t.y;
+          B.v[u][4 * j + 2] = t.z; B.v[u][4 * j + 3] = t.w;
         } else {
-          B.v[u][j][0] = ld_stream1(xr + c);
+          B.v[u][j] = ld_stream1(xr + c);
         }
       } else {
 #pragma unroll
-        for (int k = 0; k < VEC; ++k) B.v[u][j][k] = kPadLogit;
+        for (int k = 0; k < VEC; ++k) B.v[u][j * VEC + k] = kPadLogit;
       }
     }
   }
 }
 
-template <int MODE, int VEC, int LPR, int NV, int U>
+// One batch: max -> exp -> sum -> scale -> store, all in registers.
+// FULL: cols == LPR*NV*VEC, so no lane holds padding and the sum needs no mask.
+template <int MODE, bool FULL, int VEC, int LPR, int NV, int U>
 __device__ __forceinline__ void k1_process(RowBatch<VEC, LPR, NV, U>& B, float* __restrict__ y,
                                            int64_t base, int64_t rows, int cols, int64_t ldy,
                                            int sub, int sl, unsigned long long* bad_row,
                                            float shift_scale) {
   constexpr int RPW = 32 / LPR;
-  // ---- row max (strict-'>' scan == max for finite data) + finite check
+  constexpr int E = NV * VEC;
+  // ---- row max (== the strict-'>' scan for finite data) + finite check
   float m[U];
   bool bad[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     float mu = kPadLogit;
-    bool b = false;
+    u64 z = f2pk(0.0f, 0.0f);
 #pragma unroll
-    for (int j = 0; j < NV; ++j)
-#pragma unroll
-      for (int k = 0; k < VEC; ++k) {
-        mu = fmaxf(mu, B.v[u][j][k]);
-        b |= not_finite(B.v[u][j][k]);
-      }
-    bad[u] = b;
+    for (int e = 0; e + 1 < E; e += 2) {
+      mu = fmaxf(mu, fmaxf(B.v[u][e], B.v[u][e + 1]));
+      z = nf_acc2(z, B.v[u][e], B.v[u][e + 1]);
+    }
+    if constexpr (E % 2) {
+      mu = fmaxf(mu, B.v[u][E - 1]);
+      z = nf_acc2(z, B.v[u][E - 1], 0.0f);
+    }
+    bad[u] = nf_bad(z);
     m[u] = group_max<LPR>(mu) * shift_scale;  // shift_scale = 0: fault hook
   }
   // ---- shift, clip, exp (kept in registers), row sum
@@ -79,20 +90,32 @@ __device__ __forceinline__ void k1_process(RowBatch<VEC, LPR, NV, U>& B, float* 
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const bool rv = base + u * RPW + sub < rows;
-    float s = 0.0f;
+    u64 acc = f2pk(0.0f, 0.0f);
 #pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      const bool ok = rv && (j * LPR + sl) * VEC < cols;
-#pragma unroll
-      for (int k = 0; k < VEC; ++k) {
-        const float e = shifted_exp<MODE>(B.v[u][j][k], m[u]);
-        B.v[u][j][k] = e;
-        s += ok ? e : 0.0f;
+    for (int e = 0; e + 1 < E; e += 2) {
+      float2 ex = sexp2<MODE>(B.v[u][e], B.v[u][e + 1], m[u]);
+      B.v[u][e] = ex.x;
+      B.v[u][e + 1] = ex.y;
+      if constexpr (!FULL) {
+        if (!(rv && k1_col<VEC, LPR>(e, sl) < cols)) ex.x = 0.0f;
+        if (!(rv && k1_col<VEC, LPR>(e + 1, sl) < cols)) ex.y = 0.0f;
       }
+      acc = f2add(acc, f2pk(ex.x, ex.y));
+    }
+    float s;
+    {
+      const float2 a = f2up(acc);
+      s = a.x + a.y;
+    }
+    if constexpr (E % 2) {
+      float ex = sexp1<MODE>(B.v[u][E - 1], m[u]);
+      B.v[u][E - 1] = ex;
+      if (!FULL && !(rv && k1_col<VEC, LPR>(E - 1, sl) < cols)) ex = 0.0f;
+      s += ex;
     }
     rcp[u] = recip_of_sum(group_sum<LPR>(static_cast<double>(s)));
   }
-  // ---- scale + flush, write once
+  // ---- scale (+ flush), write once
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const int64_t r = base + u * RPW + sub;
@@ -101,14 +124,14 @@ __device__ __forceinline__ void k1_process(RowBatch<VEC, LPR, NV, U>& B, float* 
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const int c = (j * LPR + sl) * VEC;
-      if (c < cols) {
+      if (FULL || c < cols) {
         if constexpr (VEC == 4) {
-          st_stream4(yr + c, make_float4(scale_flush(B.v[u][j][0], rcp[u]),
-                                         scale_flush(B.v[u][j][1], rcp[u]),
-                                         scale_flush(B.v[u][j][2], rcp[u]),
-                                         scale_flush(B.v[u][j][3], rcp[u])));
+          const float2 a = scale2<MODE>(make_float2(B.v[u][4 * j], B.v[u][4 * j + 1]), rcp[u]);
+          const float2 b =
+              scale2<MODE>(make_float2(B.v[u][4 * j + 2], B.v[u][4 * j + 3]), rcp[u]);
+          st_stream4(yr + c, make_float4(a.x, a.y, b.x, b.y));
         } else {
-          st_stream1(yr + c, scale_flush(B.v[u][j][0], rcp[u]));
+          st_stream1(yr + c, scale1<MODE>(B.v[u][j], rcp[u]));
         }
       }
     }
@@ -117,6 +140,18 @@ __device__ __forceinline__ void k1_process(RowBatch<VEC, LPR, NV, U>& B, float* 
 #pragma unroll
   for (int u = 0; u < U; ++u)
     if (bad[u]) atomicMin(bad_row, static_cast<unsigned long long>(base + u * RPW + sub));
+}
+
+template <int MODE, int VEC, int LPR, int NV, int U>
+__device__ __forceinline__ void k1_process_any(RowBatch<VEC, LPR, NV, U>& B,
+                                               float* __restrict__ y, int64_t base,
+                                               int64_t rows, int cols, int64_t ldy, int sub,
+                                               int sl, unsigned long long* bad_row,
+                                               float shift_scale) {
+  if (cols == LPR * NV * VEC)
+    k1_process<MODE, true>(B, y, base, rows, cols, ldy, sub, sl, bad_row, shift_scale);
+  else
+    k1_process<MODE, false>(B, y, base, rows, cols, ldy, sub, sl, bad_row, shift_scale);
 }
 
 // PF = 1: software-pipelined -- the next batch's loads are issued before the
@@ -146,14 +181,14 @@ __global__ void __launch_bounds__(kRowsThreads)
       RowBatch<VEC, LPR, NV, U> nxt;
       const bool more = base + stride < rows;
       if (more) k1_load(nxt, x, base + stride, rows, cols, ldx, sub, sl);
-      k1_process<MODE>(cur, y, base, rows, cols, ldy, sub, sl, bad_row, shift_scale);
+      k1_process_any<MODE>(cur, y, base, rows, cols, ldy, sub, sl, bad_row, shift_scale);
       if (more) cur = nxt;
     }
   } else {
     for (; base < rows; base += stride) {
       RowBatch<VEC, LPR, NV, U> cur;
       k1_load(cur, x, base, rows, cols, ldx, sub, sl);
-      k1_process<MODE>(cur, y, base, rows, cols, ldy, sub, sl, bad_row, shift_scale);
+      k1_process_any<MODE>(cur, y, base, rows, cols, ldy, sub, sl, bad_row, shift_scale);
     }
   }
 }

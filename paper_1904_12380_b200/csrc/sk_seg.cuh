@@ -120,15 +120,13 @@ __global__ void __launch_bounds__(1024)
 
     // ---- local max + finite check
     float mt = kPadLogit;
-    bool bad = false;
+    u64 z = f2pk(0.0f, 0.0f);
 #pragma unroll
-    for (int i = 0; i < NV; ++i)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        mt = fmaxf(mt, v[i][c]);
-        bad |= not_finite(v[i][c]);
-      }
-    if (bad) atomicMin(bad_row, static_cast<unsigned long long>(row));
+    for (int i = 0; i < NV; ++i) {
+      mt = fmaxf(mt, fmaxf(fmaxf(v[i][0], v[i][1]), fmaxf(v[i][2], v[i][3])));
+      z = nf_acc2(nf_acc2(z, v[i][0], v[i][1]), v[i][2], v[i][3]);
+    }
+    if (nf_bad(z)) atomicMin(bad_row, static_cast<unsigned long long>(row));
     mt = group_max<32>(mt);
     if (lane == 0) red_f[warp] = mt;
     __syncthreads();
@@ -145,17 +143,20 @@ __global__ void __launch_bounds__(1024)
     // against the merged row max below, so every output is rounded exactly as
     // the reference rounds it (s = x - M in fp32, clip, expf, * 1/S).
     const bool single = (nseg == 1);
-    float st = 0.0f;
+    u64 acc = f2pk(0.0f, 0.0f);
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const bool ok = tid + i * static_cast<int>(blockDim.x) < nvec;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float e = shifted_exp<MODE>(v[i][c], m_l);
-        if (single) v[i][c] = e;
-        st += ok ? e : 0.0f;
+      float2 a = sexp2<MODE>(v[i][0], v[i][1], m_l);
+      float2 b = sexp2<MODE>(v[i][2], v[i][3], m_l);
+      if (single) {
+        v[i][0] = a.x; v[i][1] = a.y; v[i][2] = b.x; v[i][3] = b.y;
       }
+      if (!ok) a = b = make_float2(0.0f, 0.0f);
+      acc = f2add(f2add(acc, f2pk(a.x, a.y)), f2pk(b.x, b.y));
     }
+    const float2 acc2 = f2up(acc);
+    const float st = acc2.x + acc2.y;
     double sd = group_sum<32>(static_cast<double>(st));
     if (lane == 0) red_d[warp] = sd;
     __syncthreads();
@@ -213,11 +214,17 @@ __global__ void __launch_bounds__(1024)
     for (int i = 0; i < NV; ++i) {
       const int q = tid + i * blockDim.x;
       if (q < nvec) {
-        float o[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          o[c] = scale_flush(single ? v[i][c] : shifted_exp<MODE>(v[i][c], M), rcp);
-        st_stream4(yr + 4 * q, make_float4(o[0], o[1], o[2], o[3]));
+        float2 a, b;
+        if (single) {
+          a = make_float2(v[i][0], v[i][1]);
+          b = make_float2(v[i][2], v[i][3]);
+        } else {
+          a = sexp2<MODE>(v[i][0], v[i][1], M);
+          b = sexp2<MODE>(v[i][2], v[i][3], M);
+        }
+        a = scale2<MODE>(a, rcp);
+        b = scale2<MODE>(b, rcp);
+        st_stream4(yr + 4 * q, make_float4(a.x, a.y, b.x, b.y));
       }
     }
     __syncthreads();  // red_* / bc_* reuse in the next item

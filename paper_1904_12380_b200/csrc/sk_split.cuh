@@ -70,24 +70,29 @@ __global__ void __launch_bounds__(kSplitThreads)
   const int len = static_cast<int>(rem < kSplitChunk ? rem : kSplitChunk);
   float v[kSplitPerThread];
   float mt = kPadLogit;
-  bool bad = false;
+  u64 z = f2pk(0.0f, 0.0f);
 #pragma unroll
   for (int i = 0; i < kSplitPerThread; ++i) {
     const int c = threadIdx.x + i * kSplitThreads;
     v[i] = c < len ? ld_stream1(xr + c) : kPadLogit;
-    mt = fmaxf(mt, v[i]);
-    bad |= not_finite(v[i]);
   }
-  if (bad) atomicMin(bad_row, static_cast<unsigned long long>(row));
-  const float m = block_max_256(mt, red_f) * shift_scale;
-  float st = 0.0f;
 #pragma unroll
-  for (int i = 0; i < kSplitPerThread; ++i) {
-    const int c = threadIdx.x + i * kSplitThreads;
-    const float e = shifted_exp<MODE>(v[i], m);
-    st += c < len ? e : 0.0f;
+  for (int i = 0; i < kSplitPerThread; i += 2) {
+    mt = fmaxf(mt, fmaxf(v[i], v[i + 1]));
+    z = nf_acc2(z, v[i], v[i + 1]);
   }
-  const double s = block_sum_256(static_cast<double>(st), red_d);
+  if (nf_bad(z)) atomicMin(bad_row, static_cast<unsigned long long>(row));
+  const float m = block_max_256(mt, red_f) * shift_scale;
+  u64 acc = f2pk(0.0f, 0.0f);
+#pragma unroll
+  for (int i = 0; i < kSplitPerThread; i += 2) {
+    float2 e = sexp2<MODE>(v[i], v[i + 1], m);
+    if (!(static_cast<int>(threadIdx.x) + i * kSplitThreads < len)) e.x = 0.0f;
+    if (!(static_cast<int>(threadIdx.x) + (i + 1) * kSplitThreads < len)) e.y = 0.0f;
+    acc = f2add(acc, f2pk(e.x, e.y));
+  }
+  const float2 acc2 = f2up(acc);
+  const double s = block_sum_256(static_cast<double>(acc2.x + acc2.y), red_d);
   if (threadIdx.x == 0) {
     RowPartial p;
     p.m = m;
@@ -153,17 +158,16 @@ __global__ void __launch_bounds__(kSplitThreads)
       const int c = 4 * (threadIdx.x + i * kSplitThreads);
       if (c < len) {
         const float4 t = ld_stream4(xr + c);
-        st_stream4(yr + c, make_float4(scale_flush(shifted_exp<MODE>(t.x, M), r),
-                                       scale_flush(shifted_exp<MODE>(t.y, M), r),
-                                       scale_flush(shifted_exp<MODE>(t.z, M), r),
-                                       scale_flush(shifted_exp<MODE>(t.w, M), r)));
+        const float2 a = scale2<MODE>(sexp2<MODE>(t.x, t.y, M), r);
+        const float2 b = scale2<MODE>(sexp2<MODE>(t.z, t.w, M), r);
+        st_stream4(yr + c, make_float4(a.x, a.y, b.x, b.y));
       }
     }
   } else {
 #pragma unroll
     for (int i = 0; i < kSplitPerThread; ++i) {
       const int c = threadIdx.x + i * kSplitThreads;
-      if (c < len) st_stream1(yr + c, scale_flush(shifted_exp<MODE>(ld_stream1(xr + c), M), r));
+      if (c < len) st_stream1(yr + c, scale1<MODE>(sexp1<MODE>(ld_stream1(xr + c), M), r));
     }
   }
 }

@@ -260,3 +260,23 @@ def test_every_variant_through_public_api(oracle):
         ref = oracle.softmax_ref(x, clip=(v is sk.KernelVariant.REFERENCE_CLIPPED))
         assert_parity(oracle, y, ref, approx=(v is sk.KernelVariant.FULL_VECTORIZED_APPROX_EXP),
                       what=v)
+
+
+# ---------------------------------------------------------------- exp accuracy
+def test_exp_accuracy_exhaustive():
+    """Every fp32 in [-64, 0] (the ValueClip range; ~1.1e9 values) and in
+    [-88, -64] through the kernels' exponential vs the double exp.  The
+    reference's glibc expf is within 0.5 ulp, so kernel-vs-reference per-element
+    differences are bounded by max_ulp + 0.5 (SPEC.md:146-147 examples)."""
+    import ctypes
+
+    L = _native.lib()
+    for mode, lo, hi, ulp_bound in ((0, -64.0, 0.0, 2.5), (1, -87.0, 0.0, 2.5),
+                                    (2, -87.0, 0.0, 200.0)):
+        u = ctypes.c_double()
+        r = ctypes.c_double()
+        _native.check(L.sk_exp_accuracy(mode, lo, hi, ctypes.byref(u), ctypes.byref(r), 0))
+        print(f"mode {mode} [{lo}, {hi}]: max {u.value:.3f} ulp, max rel {r.value:.3e}")
+        assert u.value <= ulp_bound, (mode, u.value)
+        if mode == 2:
+            assert r.value <= 1e-5  # FullVectorizedApproxExp tolerance, bench.py:52
