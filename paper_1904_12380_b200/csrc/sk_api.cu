@@ -71,6 +71,7 @@ std::atomic<int> g_seg_align{0};  // K3 grid = whole multiple of nseg (row group
 std::atomic<int> g_k1_pf{-1};     // -1: table default, 0/1 force register prefetch
 std::atomic<int> g_pdl{1};        // programmatic dependent launch on every kernel
 std::atomic<int> g_chunk_mb{24};  // K3 row-chunk size (MB of input) kept L2 resident
+std::atomic<int> g_chunk_occ_div{2};  // K3 grid = SMs*occupancy/div: two launches co-reside
 std::atomic<int> g_k3_impl{0};    // 0: L2-chunked two-pass (k3_chunk), 1: smem-resident (k_seg)
 
 // Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.
@@ -308,7 +309,8 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
       const int nv = seglen <= int64_t(kChunkThreads) * 4 * 4 ? 4 : 8;
       const void* fn = nv == 4 ? chunk_fn<4>(mode) : chunk_fn<8>(mode);
       const int occ = occupancy(fn, p.threads, 0);
-      p.grid = int64_t(di.sms) * std::max(occ, 1);
+      const int div = std::max(1, g_chunk_occ_div.load());
+      p.grid = std::max<int64_t>(di.sms, int64_t(di.sms) * std::max(occ, 1) / div);
       const int64_t chunk_bytes = int64_t(std::max(1, g_chunk_mb.load())) << 20;
       p.chunk_rows = std::max<int64_t>(1, chunk_bytes / (cols * 4));
       p.chunk_rows = std::min(p.chunk_rows, rows);
@@ -559,6 +561,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "k1_pf") g_k1_pf = value;
   else if (k == "pdl") g_pdl = value;
   else if (k == "chunk_mb") g_chunk_mb = value;
+  else if (k == "chunk_occ_div") g_chunk_occ_div = value;
   else if (k == "k3_impl") g_k3_impl = value;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;
