@@ -156,8 +156,15 @@ __device__ __forceinline__ void k1_process_any(RowBatch<VEC, LPR, NV, U>& B,
 
 // PF = 1: software-pipelined -- the next batch's loads are issued before the
 // current batch is reduced, so each lane keeps 2*U*NV requests in flight.
+// Occupancy floor: >= 3 CTAs (24 warps) per SM for the register-heavy shapes,
+// >= 4 otherwise, so there are always enough warps to cover HBM latency.
+template <int VEC, int NV, int U, int PF>
+constexpr int k1_min_blocks() {
+  return NV * VEC * U * (PF ? 2 : 1) >= 32 ? 3 : 4;
+}
+
 template <int MODE, int VEC, int LPR, int NV, int U, int PF>
-__global__ void __launch_bounds__(kRowsThreads)
+__global__ void __launch_bounds__(kRowsThreads, (k1_min_blocks<VEC, NV, U, PF>()))
     k1_rows(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int cols,
             int64_t ldx, int64_t ldy, unsigned long long* __restrict__ bad_row,
             float shift_scale) {
