@@ -129,10 +129,11 @@ void sk_free_pinned(void* p);
  *                    float4s per lane, rows per lane-group batch)
  *   "grid_mult"      K1 grid = SMs * occupancy * grid_mult (default 1)
  *   "seg_len"        target segment length (floats) for K2/K3
- *   "chunk_mb"       K3 row-chunk size in MB (default 24, L2 resident)
+ *   "chunk_mb"       K3 re-read distance / row-chunk size in MB (default 24)
  *   "chunk_occ_div"  K3 grid = SMs * occupancy / div (default 2: consecutive
  *                    launches co-reside so STATS(k+1) overlaps NORMALIZE(k-1))
- *   "k3_impl"        0 (default) L2-chunked K3, 1 smem-resident cooperative K3
+ *   "k3_impl"        0 (default) one-launch ordered task queue, 1 smem-resident
+ *                    cooperative, 2 one launch per L2-sized row chunk
  *   "k1_pf", "pdl"   K1 register prefetch (-1 table default), PDL on launches (1)
  *   "seg_align"      1 (default): K3 grid is a whole multiple of the row's
  *                    segment count, so row groups never straddle CTAs

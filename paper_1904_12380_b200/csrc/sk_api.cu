@@ -17,6 +17,7 @@
 #include "sk_seg.cuh"
 #include "sk_split.cuh"
 #include "sk_chunk.cuh"
+#include "sk_dyn.cuh"
 
 namespace sk {
 namespace {
@@ -72,7 +73,7 @@ std::atomic<int> g_k1_pf{-1};     // -1: table default, 0/1 force register prefe
 std::atomic<int> g_pdl{1};        // programmatic dependent launch on every kernel
 std::atomic<int> g_chunk_mb{24};  // K3 row-chunk size (MB of input) kept L2 resident
 std::atomic<int> g_chunk_occ_div{2};  // K3 grid = SMs*occupancy/div: two launches co-reside
-std::atomic<int> g_k3_impl{0};    // 0: L2-chunked two-pass (k3_chunk), 1: smem-resident (k_seg)
+std::atomic<int> g_k3_impl{0};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
 
 // Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.
 template <typename... Args>
@@ -172,6 +173,14 @@ SegFn seg_fn(int mode) {
   }
 }
 template <int NV>
+const void* dyn_fn(int mode) {
+  switch (mode) {
+    case kClipAccurate: return reinterpret_cast<const void*>(&k3_dyn<kClipAccurate, NV>);
+    case kAccurate: return reinterpret_cast<const void*>(&k3_dyn<kAccurate, NV>);
+    default: return reinterpret_cast<const void*>(&k3_dyn<kApprox, NV>);
+  }
+}
+template <int NV>
 const void* chunk_fn(int mode) {
   switch (mode) {
     case kClipAccurate: return reinterpret_cast<const void*>(&k3_chunk<kClipAccurate, NV>);
@@ -225,7 +234,7 @@ struct Plan {
   const K1Entry* k1 = nullptr;
   // seg (K2: nseg == 1; K3: nseg > 1)
   int nseg = 1, seglen = 0, threads = 0;
-  bool k3_chunk = false;
+  int k3 = 0;  // 0 none/K2, 1 dyn, 2 smem, 3 chunk
   int64_t chunk_rows = 0;
   size_t smem = 0;
   // split
@@ -236,14 +245,18 @@ struct Plan {
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// [0] bad-row flag (8 B) | [8] task counter (8 B) | row counters | row ready
+// flags | partials | row max | row sum.  [8, part) is zeroed before a K3 launch.
 struct WsLayout {
-  size_t bad = 0, cnt = 0, part = 0, rmax = 0, rsum = 0, total = 0;
+  size_t bad = 0, ctrl = 8, cnt = 0, ready = 0, part = 0, rmax = 0, rsum = 0, total = 0;
 };
 WsLayout ws_layout(int64_t rows, int64_t parts_per_row) {
   WsLayout l;
   l.bad = 0;
+  l.ctrl = 8;
   l.cnt = 256;
-  l.part = align_up(l.cnt + size_t(rows) * 4, 256);
+  l.ready = align_up(l.cnt + size_t(rows) * 4, 256);
+  l.part = align_up(l.ready + size_t(rows) * 4, 256);
   l.rmax = align_up(l.part + size_t(rows) * size_t(parts_per_row) * sizeof(RowPartial), 256);
   l.rsum = align_up(l.rmax + size_t(rows) * 4, 256);
   l.total = align_up(l.rsum + size_t(rows) * 8, 256);
@@ -301,22 +314,31 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     p.nseg = static_cast<int>(nseg);
     p.seglen = static_cast<int>(seglen);
     const int64_t items = rows * nseg;
-    if (nseg > 1 && g_k3_impl.load() == 0) {
-      // K3: L2-chunked two-pass, 256 threads, NV float4 per thread
-      p.k3_chunk = true;
+    const int impl = g_k3_impl.load();
+    if (nseg > 1 && (impl == 0 || impl == 2)) {
       p.threads = kChunkThreads;
       p.smem = 0;
       const int nv = seglen <= int64_t(kChunkThreads) * 4 * 4 ? 4 : 8;
-      const void* fn = nv == 4 ? chunk_fn<4>(mode) : chunk_fn<8>(mode);
+      const void* fn = impl == 0 ? (nv == 4 ? dyn_fn<4>(mode) : dyn_fn<8>(mode))
+                                 : (nv == 4 ? chunk_fn<4>(mode) : chunk_fn<8>(mode));
       const int occ = occupancy(fn, p.threads, 0);
-      const int div = std::max(1, g_chunk_occ_div.load());
-      p.grid = std::max<int64_t>(di.sms, int64_t(di.sms) * std::max(occ, 1) / div);
       const int64_t chunk_bytes = int64_t(std::max(1, g_chunk_mb.load())) << 20;
       p.chunk_rows = std::max<int64_t>(1, chunk_bytes / (cols * 4));
       p.chunk_rows = std::min(p.chunk_rows, rows);
-      return SK_OK;  // no co-residency requirement: the kernel boundary is the barrier
+      if (impl == 0) {
+        // K3 dyn: one launch, ordered task queue, lag = chunk_rows rows
+        p.k3 = 1;
+        p.grid = int64_t(di.sms) * std::max(occ, 1);
+      } else {
+        // K3 chunk: one launch per row chunk (+1)
+        p.k3 = 3;
+        const int div = std::max(1, g_chunk_occ_div.load());
+        p.grid = std::max<int64_t>(di.sms, int64_t(di.sms) * std::max(occ, 1) / div);
+      }
+      return SK_OK;  // no co-residency requirement
     } else {
       // K2 (nseg == 1) or smem-resident K3: TMA segments into a 2-stage ring
+      if (nseg > 1) p.k3 = 2;
       int threads = static_cast<int>(align_up((seglen / 4 + kSegNV - 1) / kSegNV, 32));
       threads = std::max(threads, 64);
       p.threads = threads;
@@ -433,8 +455,8 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
     const int nseg = p.nseg, seglen = p.seglen;
     // K3 row counters start at zero every launch (the workspace is shared by
     // launches of different shapes, so no state is assumed across launches).
-    if (nseg > 1) SK_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(unsigned), s));
-    if (p.k3_chunk) {
+    if (nseg > 1 && p.k3 != 1) SK_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(unsigned), s));
+    if (p.k3 == 3) {
       const void* fn = p.seglen <= kChunkThreads * 16 ? chunk_fn<4>(mode) : chunk_fn<8>(mode);
       float* rmax = reinterpret_cast<float*>(ws + l.rmax);
       double* rsum = reinterpret_cast<double*>(ws + l.rsum);
@@ -449,6 +471,17 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
                          y, cols, ldx, ldy, nseg, seglen, s0, sr, std::max<int64_t>(n0, 0), nr,
                          wait_first, cnt, part, rmax, rsum, bad, sh));
       }
+    } else if (p.k3 == 1) {
+      const void* fn = p.seglen <= kChunkThreads * 16 ? dyn_fn<4>(mode) : dyn_fn<8>(mode);
+      unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ws + l.ctrl);
+      unsigned* ready = reinterpret_cast<unsigned*>(ws + l.ready);
+      float* rmax = reinterpret_cast<float*>(ws + l.rmax);
+      double* rsum = reinterpret_cast<double*>(ws + l.rsum);
+      SK_CUDA(cudaMemsetAsync(ws + l.ctrl, 0, l.part - l.ctrl, s));
+      const int64_t lag = p.chunk_rows;
+      SK_CUDA(launch_k(fn, dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), 0, s, false, x, y,
+                       rows, cols, ldx, ldy, nseg, seglen, lag, ctr, cnt, ready, part, rmax, rsum,
+                       bad, sh));
     } else {
       SK_CUDA(launch_k(reinterpret_cast<const void*>(seg_fn<kSegNV>(mode)),
                        dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), p.smem, s, nseg > 1,
@@ -595,7 +628,8 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
              p.k1->lpr, p.k1->nv, p.k1->u, p.k1->pf, kRowsThreads, (long long)p.grid);
   else if (p.kind == kPathSeg)
     snprintf(buf, buflen, "%s nseg=%d seglen=%d threads=%d smem=%zu chunk_rows=%lld grid=%lld",
-             p.nseg == 1 ? "k2_tma" : (p.k3_chunk ? "k3_chunk" : "k3_smem"), p.nseg, p.seglen,
+             p.nseg == 1 ? "k2_tma" : (p.k3 == 1 ? "k3_dyn" : p.k3 == 3 ? "k3_chunk" : "k3_smem"),
+             p.nseg, p.seglen,
              p.threads, p.smem, (long long)p.chunk_rows, (long long)p.grid);
   else
     snprintf(buf, buflen, "k4_split vec=%d nch=%d grid=%lld", p.vec ? 4 : 1, p.nch,

@@ -1,0 +1,180 @@
+// sk_dyn.cuh -- K3: long rows, one launch, ordered dynamic task queue.
+//
+// Rows longer than one CTA holds (C > 8192) are cut into nseg segments of
+// `seglen` floats.  There are two task kinds per (row, segment):
+//
+//   S (stats):     stream the segment from HBM into registers, reduce
+//                  m = max and s = sum exp(clip(x - m)) over the CTA, store
+//                  the partial; the segment whose atomic arrival on the row
+//                  counter is the last one merges the row
+//                      M = max_k m_k,  S = sum_k s_k * exp(m_k - M)  (f64, fixed order)
+//                  stores (M, S) and release-stores the row's ready flag.
+//   N (normalize): acquire the row's ready flag, re-read the segment (it was
+//                  read `lag` rows earlier, so it is still in L2) and write
+//                  y = exp(clip(x - M)) * (1/(float)S) -- the reference's own
+//                  operation order (kernels.py:144-189) for every element.
+//
+// CTAs claim tasks from a global counter in this order:
+//      S(rows 0..lag-1),  then for r = 0, 1, ...:  S(row r+lag), N(row r)
+// so reads of new rows and read+writes of old rows are interleaved finely and
+// the re-read distance is `lag` rows (sized to a slice of the 126 MB L2).
+// S tasks never wait, and an N task only waits for S tasks with smaller
+// indices -- already claimed by running CTAs -- so there is no deadlock and no
+// co-residency requirement: a plain launch, no grid barrier, no per-chunk
+// launches.  HBM traffic: one read + one write per element (8 B/element) when
+// the re-read hits L2.  Replaces kernels.py:136-189 for long rows.
+#pragma once
+#include "sk_common.cuh"
+#include "sk_seg.cuh"
+#include "sk_chunk.cuh"
+
+namespace sk {
+
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int MODE, int NV>
+__global__ void __launch_bounds__(kChunkThreads)
+    k3_dyn(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
+           int64_t ldx, int64_t ldy, int nseg, int seglen, int64_t lag,
+           unsigned long long* __restrict__ task_ctr, unsigned* __restrict__ row_cnt,
+           unsigned* __restrict__ row_ready, RowPartial* __restrict__ partials,
+           float* __restrict__ row_max, double* __restrict__ row_sum,
+           unsigned long long* __restrict__ bad_row, float shift_scale) {
+  __shared__ ChunkRed red;
+  __shared__ unsigned long long task_sh;
+  const int tid = threadIdx.x;
+  pdl_wait();
+  pdl_launch_dependents();
+  const uint64_t keep = policy_evict_last();
+  const uint64_t drop = policy_evict_first();
+  const int64_t ns = nseg;
+  const int64_t head = lag * ns;                  // S tasks of rows [0, lag)
+  const int64_t pairs = (rows - lag) * 2 * ns;    // (S(r+lag), N(r)) blocks
+  const int64_t total = 2 * rows * ns;
+
+  for (;;) {
+    if (tid == 0) task_sh = atomicAdd(task_ctr, 1ull);
+    __syncthreads();
+    const int64_t t = static_cast<int64_t>(task_sh);
+    __syncthreads();
+    if (t >= total) break;
+    bool stats;
+    int64_t row;
+    int seg;
+    if (t < head) {
+      stats = true;
+      row = t / ns;
+      seg = static_cast<int>(t % ns);
+    } else if (t - head < pairs) {
+      const int64_t u = t - head;
+      const int64_t r = u / (2 * ns);
+      const int64_t w = u % (2 * ns);
+      stats = w < ns;
+      row = stats ? r + lag : r;
+      seg = static_cast<int>(stats ? w : w - ns);
+    } else {
+      const int64_t u = t - head - pairs;
+      stats = false;
+      row = rows - lag + u / ns;
+      seg = static_cast<int>(u % ns);
+    }
+    const int64_t c0 = int64_t(seg) * seglen;
+    const int64_t rem = cols - c0;
+    const int nvec = static_cast<int>((rem < seglen ? rem : seglen) >> 2);
+    const float* xs = x + row * ldx + c0;
+
+    if (stats) {
+      float v[NV][4];
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int q = tid + i * kChunkThreads;
+        if (q < nvec) {
+          const float4 tt = ld_hint4(xs + 4 * q, keep);
+          v[i][0] = tt.x; v[i][1] = tt.y; v[i][2] = tt.z; v[i][3] = tt.w;
+        } else {
+          v[i][0] = v[i][1] = v[i][2] = v[i][3] = kPadLogit;
+        }
+      }
+      float mt = kPadLogit;
+      u64 z = f2pk(0.0f, 0.0f);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        mt = fmaxf(mt, fmaxf(fmaxf(v[i][0], v[i][1]), fmaxf(v[i][2], v[i][3])));
+        z = nf_acc2(nf_acc2(z, v[i][0], v[i][1]), v[i][2], v[i][3]);
+      }
+      if (nf_bad(z)) atomicMin(bad_row, static_cast<unsigned long long>(row));
+      const float m_l = cta_max(mt, red) * shift_scale;  // shift_scale = 0: fault hook
+      u64 acc = f2pk(0.0f, 0.0f);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        float2 a = sexp2<MODE>(v[i][0], v[i][1], m_l);
+        float2 b = sexp2<MODE>(v[i][2], v[i][3], m_l);
+        if (!(tid + i * kChunkThreads < nvec)) a = b = make_float2(0.0f, 0.0f);
+        acc = f2add(f2add(acc, f2pk(a.x, a.y)), f2pk(b.x, b.y));
+      }
+      const float2 acc2 = f2up(acc);
+      const double s_l = cta_sum(static_cast<double>(acc2.x + acc2.y), red);
+      if (tid == 0) {
+        RowPartial p;
+        p.m = m_l;
+        p.pad = 0.0f;
+        p.s = s_l;
+        partials[row * ns + seg] = p;
+        __threadfence();
+        const unsigned old = atomicAdd(&row_cnt[row], 1u);
+        red.last = (old == static_cast<unsigned>(nseg) - 1u);
+      }
+      __syncthreads();
+      if (red.last) {  // last arrival merges the row (fixed order: deterministic)
+        __threadfence();
+        const RowPartial* rp = partials + row * ns;
+        float mq = kPadLogit;
+        for (int q = tid; q < nseg; q += kChunkThreads) mq = fmaxf(mq, __ldcg(&rp[q].m));
+        const float M = cta_max(mq, red);
+        double sq = 0.0;
+        for (int q = tid; q < nseg; q += kChunkThreads) {
+          const float m = __ldcg(&rp[q].m);
+          sq += __ldcg(&rp[q].s) * static_cast<double>(m == M ? 1.0f : expf(m - M));
+        }
+        const double S = cta_sum(sq, red);
+        if (tid == 0) {
+          row_max[row] = M;
+          row_sum[row] = S;
+          __threadfence();
+          st_release_gpu(&row_ready[row], 1u);
+        }
+      }
+    } else {
+      if (tid == 0) {
+        unsigned sleep = 32;
+        while (ld_acquire_gpu(&row_ready[row]) == 0u) {
+          __nanosleep(sleep);
+          if (sleep < 512) sleep <<= 1;
+        }
+      }
+      __syncthreads();
+      const float M = __ldcg(&row_max[row]);
+      const float rcp = recip_of_sum(__ldcg(&row_sum[row]));
+      float* ys = y + row * ldy + c0;
+      float4 tv[NV];
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int q = tid + i * kChunkThreads;
+        if (q < nvec) tv[i] = ld_hint4(xs + 4 * q, drop);
+      }
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int q = tid + i * kChunkThreads;
+        if (q < nvec) {
+          const float2 a = scale2<MODE>(sexp2<MODE>(tv[i].x, tv[i].y, M), rcp);
+          const float2 b = scale2<MODE>(sexp2<MODE>(tv[i].z, tv[i].w, M), rcp);
+          st_stream4(ys + 4 * q, make_float4(a.x, a.y, b.x, b.y));
+        }
+      }
+    }
+  }
+}
+
+}  // namespace sk

@@ -111,16 +111,16 @@ def main():
         _native.set_tuning("pdl", 0)
         record("default pdl=0", bench_once(xs, ys, rows, cols, args.reps, s))
         _native.set_tuning("pdl", 1)
-        for div in (1, 2, 3):
-            _native.set_tuning("chunk_occ_div", div)
-            for mb in (16, 24, 32):
+        for impl, mbs in ((0, (8, 16, 24, 32, 48)), (2, (32,))):
+            _native.set_tuning("k3_impl", impl)
+            for mb in mbs:
                 _native.set_tuning("chunk_mb", mb)
                 for sl in map(int, args.seg_lens.split(",")):
                     _native.set_tuning("seg_len", sl)
-                    record(f"k3_chunk seg_len={sl} chunk_mb={mb} div={div}",
+                    record(f"k3 impl={impl} seg_len={sl} chunk_mb={mb}",
                            bench_once(xs, ys, rows, cols, args.reps, s))
+        _native.set_tuning("k3_impl", 0)
         _native.set_tuning("chunk_mb", 24)
-        _native.set_tuning("chunk_occ_div", 2)
         _native.set_tuning("seg_len", 0)
         _native.set_tuning("k3_impl", 1)
         record("k3_smem", bench_once(xs, ys, rows, cols, args.reps, s))
