@@ -18,6 +18,7 @@
 #include "sk_split.cuh"
 #include "sk_chunk.cuh"
 #include "sk_dyn.cuh"
+#include "sk_warp3.cuh"
 
 namespace sk {
 namespace {
@@ -173,6 +174,15 @@ SegFn seg_fn(int mode) {
   }
 }
 template <int NV>
+const void* warp3_fn(int mode) {
+  switch (mode) {
+    case kClipAccurate: return reinterpret_cast<const void*>(&k3_warp<kClipAccurate, NV>);
+    case kAccurate: return reinterpret_cast<const void*>(&k3_warp<kAccurate, NV>);
+    default: return reinterpret_cast<const void*>(&k3_warp<kApprox, NV>);
+  }
+}
+constexpr int64_t kWarpSeg = 1024;  // K3 warp task: 32 lanes x 8 float4
+template <int NV>
 const void* dyn_fn(int mode) {
   switch (mode) {
     case kClipAccurate: return reinterpret_cast<const void*>(&k3_dyn<kClipAccurate, NV>);
@@ -305,16 +315,31 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     return SK_OK;
   }
   if (kind == kPathSeg) {
-    const bool chunked = cols > kSegCap && g_k3_impl.load() == 0;
+    const int impl0 = g_k3_impl.load();
+    const bool chunked = cols > kSegCap && impl0 != 1;
+    const bool warp3 = cols > kSegCap && impl0 == 3;
     int64_t target = g_seg_len.load() > 0 ? g_seg_len.load() : (chunked ? kChunkSeg : kSegCap);
+    if (warp3) target = g_seg_len.load() == 2048 ? 2048 : kWarpSeg;
     target = std::min<int64_t>(target, kSegCap);
     const int64_t nseg = (cols + target - 1) / target;
-    const int64_t seglen = align_up((cols + nseg - 1) / nseg, 4);
+    // warp tasks use fixed-size segments (the last one shorter)
+    const int64_t seglen = warp3 ? target : align_up((cols + nseg - 1) / nseg, 4);
     p.kind = kPathSeg;
     p.nseg = static_cast<int>(nseg);
     p.seglen = static_cast<int>(seglen);
     const int64_t items = rows * nseg;
     const int impl = g_k3_impl.load();
+    if (nseg > 1 && impl == 3) {
+      p.k3 = 4;
+      p.threads = kWarp3Threads;
+      p.smem = 0;
+      const void* fn = seglen == 2048 ? warp3_fn<16>(mode) : warp3_fn<8>(mode);
+      const int occ = occupancy(fn, p.threads, 0);
+      const int64_t chunk_bytes = int64_t(std::max(1, g_chunk_mb.load())) << 20;
+      p.chunk_rows = std::min(rows, std::max<int64_t>(1, chunk_bytes / (cols * 4)));
+      p.grid = int64_t(di.sms) * std::max(occ, 1);
+      return SK_OK;
+    }
     if (nseg > 1 && (impl == 0 || impl == 2)) {
       p.threads = kChunkThreads;
       p.smem = 0;
@@ -455,7 +480,7 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
     const int nseg = p.nseg, seglen = p.seglen;
     // K3 row counters start at zero every launch (the workspace is shared by
     // launches of different shapes, so no state is assumed across launches).
-    if (nseg > 1 && p.k3 != 1) SK_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(unsigned), s));
+    if (nseg > 1 && p.k3 != 1 && p.k3 != 4) SK_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(unsigned), s));
     if (p.k3 == 3) {
       const void* fn = p.seglen <= kChunkThreads * 16 ? chunk_fn<4>(mode) : chunk_fn<8>(mode);
       float* rmax = reinterpret_cast<float*>(ws + l.rmax);
@@ -471,6 +496,17 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
                          y, cols, ldx, ldy, nseg, seglen, s0, sr, std::max<int64_t>(n0, 0), nr,
                          wait_first, cnt, part, rmax, rsum, bad, sh));
       }
+    } else if (p.k3 == 4) {
+      const void* fn = p.seglen == 2048 ? warp3_fn<16>(mode) : warp3_fn<8>(mode);
+      unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ws + l.ctrl);
+      unsigned* ready = reinterpret_cast<unsigned*>(ws + l.ready);
+      float* rmax = reinterpret_cast<float*>(ws + l.rmax);
+      double* rsum = reinterpret_cast<double*>(ws + l.rsum);
+      SK_CUDA(cudaMemsetAsync(ws + l.ctrl, 0, l.part - l.ctrl, s));
+      const int64_t lag = p.chunk_rows;
+      SK_CUDA(launch_k(fn, dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), 0, s, false, x, y,
+                       rows, cols, ldx, ldy, nseg, lag, ctr, cnt, ready, part, rmax, rsum, bad,
+                       sh));
     } else if (p.k3 == 1) {
       const void* fn = p.seglen <= kChunkThreads * 16 ? dyn_fn<4>(mode) : dyn_fn<8>(mode);
       unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ws + l.ctrl);
@@ -602,7 +638,7 @@ int sk_set_tuning(const char* key, int value) {
 
 size_t sk_softmax_workspace_bytes(int64_t rows, int64_t cols) {
   if (rows <= 0 || cols <= 0) return ws_layout(0, 0).total;
-  const int64_t nseg = (cols + kChunkSeg - 1) / kChunkSeg;
+  const int64_t nseg = (cols + kWarpSeg - 1) / kWarpSeg;
   const int64_t nch = (cols + kSplitChunk - 1) / kSplitChunk;
   return std::max(ws_layout(rows, nseg).total, ws_layout(rows, nch).total);
 }
@@ -628,7 +664,11 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
              p.k1->lpr, p.k1->nv, p.k1->u, p.k1->pf, kRowsThreads, (long long)p.grid);
   else if (p.kind == kPathSeg)
     snprintf(buf, buflen, "%s nseg=%d seglen=%d threads=%d smem=%zu chunk_rows=%lld grid=%lld",
-             p.nseg == 1 ? "k2_tma" : (p.k3 == 1 ? "k3_dyn" : p.k3 == 3 ? "k3_chunk" : "k3_smem"),
+             p.nseg == 1 ? "k2_tma"
+                         : (p.k3 == 1   ? "k3_dyn"
+                            : p.k3 == 3 ? "k3_chunk"
+                            : p.k3 == 4 ? "k3_warp"
+                                        : "k3_smem"),
              p.nseg, p.seglen,
              p.threads, p.smem, (long long)p.chunk_rows, (long long)p.grid);
   else

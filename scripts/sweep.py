@@ -63,7 +63,7 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--config", default="c2")
     p.add_argument("--reps", type=int, default=200)
-    p.add_argument("--seg-lens", default="4096,8192")
+    p.add_argument("--seg-lens", default="1024,2048,4096")
     p.add_argument("--grid-mults", default="1,2")
     args = p.parse_args()
     spec = configs.get(args.config)
@@ -111,7 +111,7 @@ def main():
         _native.set_tuning("pdl", 0)
         record("default pdl=0", bench_once(xs, ys, rows, cols, args.reps, s))
         _native.set_tuning("pdl", 1)
-        for impl, mbs in ((0, (8, 16, 24, 32, 48)), (2, (32,))):
+        for impl, mbs in ((3, (8, 16, 24, 32, 48)), (0, (24, 32))):
             _native.set_tuning("k3_impl", impl)
             for mb in mbs:
                 _native.set_tuning("chunk_mb", mb)

@@ -159,6 +159,26 @@ def test_k1_instantiations_all_agree(oracle):
         assert_parity(oracle, y, ref, what=(lpr, nv, u))
 
 
+@pytest.mark.parametrize("impl", [0, 1, 2, 3])
+def test_every_k3_implementation(impl, oracle):
+    """Long-row kernels: ordered CTA queue (0), smem-resident cooperative (1),
+    per-chunk launches (2), ordered warp queue (3) -- all against the oracle,
+    on a ragged width (last segment partial) and several chunk sizes."""
+    x = configs.generate("c4", 0, 40)[:, :200_004].copy()
+    x[3, 777] = -500.0
+    ref = oracle.softmax_ref(x)
+    _native.set_tuning("k3_impl", impl)
+    try:
+        for mb in (1, 3, 24):
+            _native.set_tuning("chunk_mb", mb)
+            y, bad = gu.softmax_abi(x, 0)
+            assert bad == gu.NO_BAD
+            assert_parity(oracle, y, ref, what=(impl, mb, gu.plan(*x.shape)))
+    finally:
+        _native.set_tuning("k3_impl", 0)
+        _native.set_tuning("chunk_mb", 24)
+
+
 def test_seg_lengths_all_agree(oracle):
     x = configs.generate("c4", 0, 4)[:, :100000].copy()
     ref = oracle.softmax_ref(x)
