@@ -130,6 +130,7 @@ void sk_free_pinned(void* p);
  *   "grid_mult"      K1 grid = SMs * occupancy * grid_mult (default 1)
  *   "seg_len"        target segment length (floats) for K2/K3
  *   "chunk_mb"       K3 re-read distance / row-chunk size in MB (default 24)
+ *   "claim_batch"    K3 queue tasks claimed per atomic (default 4)
  *   "chunk_occ_div"  K3 grid = SMs * occupancy / div (default 2: consecutive
  *                    launches co-reside so STATS(k+1) overlaps NORMALIZE(k-1))
  *   "k3_impl"        0 (default) one-launch ordered task queue, 1 smem-resident

@@ -73,7 +73,8 @@ std::atomic<int> g_seg_align{0};  // K3 grid = whole multiple of nseg (row group
 std::atomic<int> g_k1_pf{-1};     // -1: table default, 0/1 force register prefetch
 std::atomic<int> g_pdl{1};        // programmatic dependent launch on every kernel
 std::atomic<int> g_chunk_mb{24};  // K3 row-chunk size (MB of input) kept L2 resident
-std::atomic<int> g_chunk_occ_div{2};  // K3 grid = SMs*occupancy/div: two launches co-reside
+std::atomic<int> g_chunk_occ_div{2};
+std::atomic<int> g_claim_batch{4};   // K3 queue: tasks claimed per atomic  // K3 grid = SMs*occupancy/div: two launches co-reside
 std::atomic<int> g_k3_impl{0};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
 
 // Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.
@@ -504,9 +505,10 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
       double* rsum = reinterpret_cast<double*>(ws + l.rsum);
       SK_CUDA(cudaMemsetAsync(ws + l.ctrl, 0, l.part - l.ctrl, s));
       const int64_t lag = p.chunk_rows;
+      const int batch = std::max(1, g_claim_batch.load());
       SK_CUDA(launch_k(fn, dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), 0, s, false, x, y,
-                       rows, cols, ldx, ldy, nseg, lag, ctr, cnt, ready, part, rmax, rsum, bad,
-                       sh));
+                       rows, cols, ldx, ldy, nseg, lag, batch, ctr, cnt, ready, part, rmax, rsum,
+                       bad, sh));
     } else if (p.k3 == 1) {
       const void* fn = p.seglen <= kChunkThreads * 16 ? dyn_fn<4>(mode) : dyn_fn<8>(mode);
       unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ws + l.ctrl);
@@ -515,9 +517,10 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
       double* rsum = reinterpret_cast<double*>(ws + l.rsum);
       SK_CUDA(cudaMemsetAsync(ws + l.ctrl, 0, l.part - l.ctrl, s));
       const int64_t lag = p.chunk_rows;
+      const int batch = std::max(1, g_claim_batch.load());
       SK_CUDA(launch_k(fn, dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), 0, s, false, x, y,
-                       rows, cols, ldx, ldy, nseg, seglen, lag, ctr, cnt, ready, part, rmax, rsum,
-                       bad, sh));
+                       rows, cols, ldx, ldy, nseg, seglen, lag, batch, ctr, cnt, ready, part, rmax,
+                       rsum, bad, sh));
     } else {
       SK_CUDA(launch_k(reinterpret_cast<const void*>(seg_fn<kSegNV>(mode)),
                        dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), p.smem, s, nseg > 1,
@@ -631,6 +634,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "pdl") g_pdl = value;
   else if (k == "chunk_mb") g_chunk_mb = value;
   else if (k == "chunk_occ_div") g_chunk_occ_div = value;
+  else if (k == "claim_batch") g_claim_batch = value;
   else if (k == "k3_impl") g_k3_impl = value;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;

@@ -37,7 +37,7 @@ __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
 template <int MODE, int NV>
 __global__ void __launch_bounds__(kChunkThreads)
     k3_dyn(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
-           int64_t ldx, int64_t ldy, int nseg, int seglen, int64_t lag,
+           int64_t ldx, int64_t ldy, int nseg, int seglen, int64_t lag, int batch,
            unsigned long long* __restrict__ task_ctr, unsigned* __restrict__ row_cnt,
            unsigned* __restrict__ row_ready, RowPartial* __restrict__ partials,
            float* __restrict__ row_max, double* __restrict__ row_sum,
@@ -54,11 +54,17 @@ __global__ void __launch_bounds__(kChunkThreads)
   const int64_t pairs = (rows - lag) * 2 * ns;    // (S(r+lag), N(r)) blocks
   const int64_t total = 2 * rows * ns;
 
+  int k = batch;
+  unsigned long long cur = 0;
   for (;;) {
-    if (tid == 0) task_sh = atomicAdd(task_ctr, 1ull);
-    __syncthreads();
-    const int64_t t = static_cast<int64_t>(task_sh);
-    __syncthreads();
+    if (k == batch) {  // claim `batch` tasks with one atomic
+      if (tid == 0) task_sh = atomicAdd(task_ctr, static_cast<unsigned long long>(batch));
+      __syncthreads();
+      cur = task_sh;
+      __syncthreads();
+      k = 0;
+    }
+    const int64_t t = static_cast<int64_t>(cur) + k++;
     if (t >= total) break;
     bool stats;
     int64_t row;

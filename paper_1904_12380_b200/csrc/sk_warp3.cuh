@@ -54,7 +54,7 @@ __device__ __forceinline__ void w3_decode(int64_t t, int64_t rows, int64_t ns, i
 template <int MODE, int NV>
 __global__ void __launch_bounds__(kWarp3Threads)
     k3_warp(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
-            int64_t ldx, int64_t ldy, int nseg, int64_t lag,
+            int64_t ldx, int64_t ldy, int nseg, int64_t lag, int batch,
             unsigned long long* __restrict__ task_ctr, unsigned* __restrict__ row_cnt,
             unsigned* __restrict__ row_ready, RowPartial* __restrict__ partials,
             float* __restrict__ row_max, double* __restrict__ row_sum,
@@ -68,13 +68,18 @@ __global__ void __launch_bounds__(kWarp3Threads)
   const int64_t ns = nseg;
   const int64_t total = 2 * rows * ns;
 
-  unsigned long long next = 0;
-  if (lane == 0) next = atomicAdd(task_ctr, 1ull);
-  next = __shfl_sync(0xffffffffu, next, 0);
+  // Tasks are claimed `batch` at a time (one atomic per batch: a single counter
+  // sustains only ~0.5 G atomics/s); the next batch is claimed while the last
+  // task of the current one runs.
+  unsigned long long cur = 0, next = 0;
+  if (lane == 0) cur = atomicAdd(task_ctr, static_cast<unsigned long long>(batch));
+  cur = __shfl_sync(0xffffffffu, cur, 0);
+  int k = 0;
   for (;;) {
-    const int64_t t = static_cast<int64_t>(next);
+    const int64_t t = static_cast<int64_t>(cur) + k;
     if (t >= total) break;
-    if (lane == 0) next = atomicAdd(task_ctr, 1ull);  // claim ahead; used next iteration
+    if (k == batch - 1 && lane == 0)
+      next = atomicAdd(task_ctr, static_cast<unsigned long long>(batch));
     bool stats;
     int64_t row;
     int seg;
@@ -163,7 +168,10 @@ __global__ void __launch_bounds__(kWarp3Threads)
         }
       }
     }
-    next = __shfl_sync(0xffffffffu, next, 0);
+    if (++k == batch) {
+      cur = __shfl_sync(0xffffffffu, next, 0);
+      k = 0;
+    }
   }
 }
 
