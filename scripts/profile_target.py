@@ -31,6 +31,11 @@ def main():
     p.add_argument("--rows", type=int, default=0, help="use only the first N rows")
     p.add_argument("--mode", type=int, default=0)
     args = p.parse_args()
+    import os
+
+    for kv in os.environ.get("SK_TUNING", "").split():
+        k, v = kv.split("=")
+        _native.set_tuning(k, int(v))
     spec = configs.get(args.config)
     rows = args.rows or spec.rows
     x = configs.generate(spec)[:rows] if spec.plant_count else configs.generate(spec, 0, rows)
