@@ -73,8 +73,9 @@ std::atomic<int> g_seg_align{0};  // K3 grid = whole multiple of nseg (row group
 std::atomic<int> g_k1_pf{-1};     // -1: table default, 0/1 force register prefetch
 std::atomic<int> g_pdl{1};        // programmatic dependent launch on every kernel
 std::atomic<int> g_chunk_mb{24};  // K3 row-chunk size (MB of input) kept L2 resident
+std::atomic<int> g_chunk_mb_set{0};  // chunk_mb explicitly tuned (overrides the K3 warp lag)
 std::atomic<int> g_chunk_occ_div{2};
-std::atomic<int> g_claim_batch{4};   // K3 queue: tasks claimed per atomic  // K3 grid = SMs*occupancy/div: two launches co-reside
+std::atomic<int> g_claim_batch{0};   // K3 warp queue: tasks per atomic claim (0 = static)  // K3 grid = SMs*occupancy/div: two launches co-reside
 std::atomic<int> g_k3_impl{0};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
 
 // Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.
@@ -336,9 +337,14 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
       p.smem = 0;
       const void* fn = seglen == 2048 ? warp3_fn<16>(mode) : warp3_fn<8>(mode);
       const int occ = occupancy(fn, p.threads, 0);
-      const int64_t chunk_bytes = int64_t(std::max(1, g_chunk_mb.load())) << 20;
-      p.chunk_rows = std::min(rows, std::max<int64_t>(1, chunk_bytes / (cols * 4)));
       p.grid = int64_t(di.sms) * std::max(occ, 1);
+      // re-read distance: 1.5x the in-flight window (one task per resident warp)
+      // unless chunk_mb overrides it; the window plus the lag stay well inside L2
+      const int64_t window = p.grid * (p.threads / 32) * seglen * 4;
+      int64_t lag_bytes = window * 3 / 2;
+      if (g_chunk_mb_set.load()) lag_bytes = int64_t(std::max(1, g_chunk_mb.load())) << 20;
+      p.chunk_rows = std::min(rows, std::max<int64_t>(1, lag_bytes / (cols * 4)));
+      if (g_claim_batch.load() == 0 && (!di.coop || occ < 1)) return plan_split(rows, cols, p);
       return SK_OK;
     }
     if (nseg > 1 && (impl == 0 || impl == 2)) {
@@ -505,10 +511,10 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
       double* rsum = reinterpret_cast<double*>(ws + l.rsum);
       SK_CUDA(cudaMemsetAsync(ws + l.ctrl, 0, l.part - l.ctrl, s));
       const int64_t lag = p.chunk_rows;
-      const int batch = std::max(1, g_claim_batch.load());
-      SK_CUDA(launch_k(fn, dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), 0, s, false, x, y,
-                       rows, cols, ldx, ldy, nseg, lag, batch, ctr, cnt, ready, part, rmax, rsum,
-                       bad, sh));
+      const int batch = std::max(0, g_claim_batch.load());
+      SK_CUDA(launch_k(fn, dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), 0, s,
+                       batch == 0, x, y, rows, cols, ldx, ldy, nseg, lag, batch, ctr, cnt, ready,
+                       part, rmax, rsum, bad, sh));
     } else if (p.k3 == 1) {
       const void* fn = p.seglen <= kChunkThreads * 16 ? dyn_fn<4>(mode) : dyn_fn<8>(mode);
       unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ws + l.ctrl);
@@ -632,7 +638,10 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "seg_align") g_seg_align = value;
   else if (k == "k1_pf") g_k1_pf = value;
   else if (k == "pdl") g_pdl = value;
-  else if (k == "chunk_mb") g_chunk_mb = value;
+  else if (k == "chunk_mb") {
+    g_chunk_mb = value > 0 ? value : 24;
+    g_chunk_mb_set = value > 0;
+  }
   else if (k == "chunk_occ_div") g_chunk_occ_div = value;
   else if (k == "claim_batch") g_claim_batch = value;
   else if (k == "k3_impl") g_k3_impl = value;

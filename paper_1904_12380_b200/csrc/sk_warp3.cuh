@@ -23,6 +23,12 @@ namespace sk {
 
 constexpr int kWarp3Threads = 256;
 
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v)
+               : "memory");
+  return old;
+}
 __device__ __forceinline__ void st_release_gpu_u32(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -68,17 +74,23 @@ __global__ void __launch_bounds__(kWarp3Threads)
   const int64_t ns = nseg;
   const int64_t total = 2 * rows * ns;
 
-  // Tasks are claimed `batch` at a time (one atomic per batch: a single counter
-  // sustains only ~0.5 G atomics/s); the next batch is claimed while the last
-  // task of the current one runs.
+  // batch == 0: static round-robin -- warp w runs tasks w, w+W, w+2W, ... (no
+  //   atomics; the in-flight window is exactly one task per warp; the launch is
+  //   cooperative so every warp is resident, which keeps the waits deadlock-free).
+  // batch >= 1: tasks claimed `batch` at a time from the global counter (one
+  //   atomic per batch: a single counter sustains only ~0.5 G atomics/s).
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t gwarp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   unsigned long long cur = 0, next = 0;
-  if (lane == 0) cur = atomicAdd(task_ctr, static_cast<unsigned long long>(batch));
-  cur = __shfl_sync(0xffffffffu, cur, 0);
+  if (batch > 0) {
+    if (lane == 0) cur = atomicAdd(task_ctr, static_cast<unsigned long long>(batch));
+    cur = __shfl_sync(0xffffffffu, cur, 0);
+  }
   int k = 0;
-  for (;;) {
-    const int64_t t = static_cast<int64_t>(cur) + k;
+  for (int64_t it = 0;; ++it) {
+    const int64_t t = batch > 0 ? static_cast<int64_t>(cur) + k : gwarp + it * nwarps;
     if (t >= total) break;
-    if (k == batch - 1 && lane == 0)
+    if (batch > 0 && k == batch - 1 && lane == 0)
       next = atomicAdd(task_ctr, static_cast<unsigned long long>(batch));
     bool stats;
     int64_t row;
@@ -123,12 +135,12 @@ __global__ void __launch_bounds__(kWarp3Threads)
         p.pad = 0.0f;
         p.s = s_l;
         partials[row * ns + seg] = p;
-        __threadfence();
-        last = atomicAdd(&row_cnt[row], 1u) == static_cast<unsigned>(nseg) - 1u;
+        // release our partial / acquire everyone else's if we are last
+        last = atom_add_acq_rel_gpu(&row_cnt[row], 1u) == static_cast<unsigned>(nseg) - 1u;
       }
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {  // merge the row (fixed order: deterministic)
-        __threadfence();
+        __syncwarp();
         const RowPartial* rp = partials + row * ns;
         float mq = kPadLogit;
         for (int q = lane; q < nseg; q += 32) mq = fmaxf(mq, __ldcg(&rp[q].m));
@@ -142,16 +154,15 @@ __global__ void __launch_bounds__(kWarp3Threads)
         if (lane == 0) {
           row_max[row] = M;
           row_sum[row] = S;
-          __threadfence();
           st_release_gpu_u32(&row_ready[row], 1u);
         }
       }
     } else {
       if (lane == 0) {
-        unsigned sleep = 32;
+        unsigned sleep = 20;
         while (ld_acquire_gpu(&row_ready[row]) == 0u) {
           __nanosleep(sleep);
-          if (sleep < 512) sleep <<= 1;
+          if (sleep < 320) sleep <<= 1;
         }
       }
       __syncwarp();
@@ -168,7 +179,7 @@ __global__ void __launch_bounds__(kWarp3Threads)
         }
       }
     }
-    if (++k == batch) {
+    if (batch > 0 && ++k == batch) {
       cur = __shfl_sync(0xffffffffu, next, 0);
       k = 0;
     }

@@ -111,9 +111,9 @@ def main():
         _native.set_tuning("pdl", 0)
         record("default pdl=0", bench_once(xs, ys, rows, cols, args.reps, s))
         _native.set_tuning("pdl", 1)
-        for impl, mbs, sls in ((3, (16, 24, 32), (1024, 2048)), (0, (24, 32), (4096,))):
+        for impl, mbs, sls in ((3, (0, 16, 32, 48), (1024, 2048)),):
             _native.set_tuning("k3_impl", impl)
-            for b in (1, 4, 16):
+            for b in (0, 4):
                 _native.set_tuning("claim_batch", b)
                 for mb in mbs:
                     _native.set_tuning("chunk_mb", mb)
@@ -121,9 +121,10 @@ def main():
                         _native.set_tuning("seg_len", sl)
                         record(f"k3 impl={impl} seg_len={sl} chunk_mb={mb} batch={b}",
                                bench_once(xs, ys, rows, cols, args.reps, s))
-        _native.set_tuning("claim_batch", 4)
+        _native.set_tuning("claim_batch", 0)
+        _native.set_tuning("chunk_mb", 0)
         _native.set_tuning("k3_impl", 0)
-        _native.set_tuning("chunk_mb", 24)
+        _native.set_tuning("chunk_mb", 0)
         _native.set_tuning("seg_len", 0)
         _native.set_tuning("k3_impl", 1)
         record("k3_smem", bench_once(xs, ys, rows, cols, args.reps, s))

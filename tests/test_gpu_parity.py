@@ -159,7 +159,7 @@ def test_k1_instantiations_all_agree(oracle):
         assert_parity(oracle, y, ref, what=(lpr, nv, u))
 
 
-@pytest.mark.parametrize("impl", [0, 1, 2, 3])
+@pytest.mark.parametrize("impl", [0, 1, 2, 3, "3b"])
 def test_every_k3_implementation(impl, oracle):
     """Long-row kernels: ordered CTA queue (0), smem-resident cooperative (1),
     per-chunk launches (2), ordered warp queue (3) -- all against the oracle,
@@ -167,16 +167,20 @@ def test_every_k3_implementation(impl, oracle):
     x = configs.generate("c4", 0, 40)[:, :200_004].copy()
     x[3, 777] = -500.0
     ref = oracle.softmax_ref(x)
+    if impl == "3b":  # warp queue with batched atomic claims instead of static tasks
+        impl = 3
+        _native.set_tuning("claim_batch", 4)
     _native.set_tuning("k3_impl", impl)
     try:
-        for mb in (1, 3, 24):
+        for mb in (1, 3, 0):
             _native.set_tuning("chunk_mb", mb)
             y, bad = gu.softmax_abi(x, 0)
             assert bad == gu.NO_BAD
             assert_parity(oracle, y, ref, what=(impl, mb, gu.plan(*x.shape)))
     finally:
+        _native.set_tuning("claim_batch", 0)
         _native.set_tuning("k3_impl", 0)
-        _native.set_tuning("chunk_mb", 24)
+        _native.set_tuning("chunk_mb", 0)
 
 
 def test_seg_lengths_all_agree(oracle):
