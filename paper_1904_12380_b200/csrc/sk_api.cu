@@ -19,6 +19,7 @@
 #include "sk_chunk.cuh"
 #include "sk_dyn.cuh"
 #include "sk_warp3.cuh"
+#include "sk_reg3.cuh"
 
 namespace sk {
 namespace {
@@ -176,6 +177,14 @@ SegFn seg_fn(int mode) {
   }
 }
 template <int NV>
+const void* reg3_fn(int mode) {
+  switch (mode) {
+    case kClipAccurate: return reinterpret_cast<const void*>(&k3_reg<kClipAccurate, NV>);
+    case kAccurate: return reinterpret_cast<const void*>(&k3_reg<kAccurate, NV>);
+    default: return reinterpret_cast<const void*>(&k3_reg<kApprox, NV>);
+  }
+}
+template <int NV>
 const void* warp3_fn(int mode) {
   switch (mode) {
     case kClipAccurate: return reinterpret_cast<const void*>(&k3_warp<kClipAccurate, NV>);
@@ -319,9 +328,9 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
   if (kind == kPathSeg) {
     const int impl0 = g_k3_impl.load();
     const bool chunked = cols > kSegCap && impl0 != 1;
-    const bool warp3 = cols > kSegCap && impl0 == 3;
+    const bool warp3 = cols > kSegCap && (impl0 == 3 || impl0 == 4);
     int64_t target = g_seg_len.load() > 0 ? g_seg_len.load() : (chunked ? kChunkSeg : kSegCap);
-    if (warp3) target = g_seg_len.load() == 2048 ? 2048 : kWarpSeg;
+    if (warp3) target = g_seg_len.load() == 2048 ? 2048 : g_seg_len.load() == 512 ? 512 : kWarpSeg;
     target = std::min<int64_t>(target, kSegCap);
     const int64_t nseg = (cols + target - 1) / target;
     // warp tasks use fixed-size segments (the last one shorter)
@@ -331,6 +340,19 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     p.seglen = static_cast<int>(seglen);
     const int64_t items = rows * nseg;
     const int impl = g_k3_impl.load();
+    if (nseg > 1 && impl == 4) {
+      // K3 registers: static warp tasks, cooperative
+      p.k3 = 5;
+      p.threads = kReg3Threads;
+      p.smem = 0;
+      const void* fn = seglen == 2048 ? reg3_fn<16>(mode)
+                       : seglen == 512 ? reg3_fn<4>(mode) : reg3_fn<8>(mode);
+      const int occ = occupancy(fn, p.threads, 0);
+      p.grid = int64_t(di.sms) * std::max(occ, 1);
+      const int64_t warps = p.grid * (p.threads / 32);
+      if (!di.coop || occ < 1 || nseg > warps) return plan_split(rows, cols, p);
+      return SK_OK;
+    }
     if (nseg > 1 && impl == 3) {
       p.k3 = 4;
       p.threads = kWarp3Threads;
@@ -487,7 +509,7 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
     const int nseg = p.nseg, seglen = p.seglen;
     // K3 row counters start at zero every launch (the workspace is shared by
     // launches of different shapes, so no state is assumed across launches).
-    if (nseg > 1 && p.k3 != 1 && p.k3 != 4) SK_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(unsigned), s));
+    if (nseg > 1 && p.k3 != 1 && p.k3 != 4 && p.k3 != 5) SK_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(unsigned), s));
     if (p.k3 == 3) {
       const void* fn = p.seglen <= kChunkThreads * 16 ? chunk_fn<4>(mode) : chunk_fn<8>(mode);
       float* rmax = reinterpret_cast<float*>(ws + l.rmax);
@@ -503,6 +525,15 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
                          y, cols, ldx, ldy, nseg, seglen, s0, sr, std::max<int64_t>(n0, 0), nr,
                          wait_first, cnt, part, rmax, rsum, bad, sh));
       }
+    } else if (p.k3 == 5) {
+      const void* fn = p.seglen == 2048 ? reg3_fn<16>(mode)
+                       : p.seglen == 512 ? reg3_fn<4>(mode) : reg3_fn<8>(mode);
+      unsigned* ready = reinterpret_cast<unsigned*>(ws + l.ready);
+      float* rmax = reinterpret_cast<float*>(ws + l.rmax);
+      double* rsum = reinterpret_cast<double*>(ws + l.rsum);
+      SK_CUDA(cudaMemsetAsync(ws + l.ctrl, 0, l.part - l.ctrl, s));
+      SK_CUDA(launch_k(fn, dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), 0, s, true, x, y,
+                       rows, cols, ldx, ldy, nseg, cnt, ready, part, rmax, rsum, bad, sh));
     } else if (p.k3 == 4) {
       const void* fn = p.seglen == 2048 ? warp3_fn<16>(mode) : warp3_fn<8>(mode);
       unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ws + l.ctrl);
@@ -651,7 +682,7 @@ int sk_set_tuning(const char* key, int value) {
 
 size_t sk_softmax_workspace_bytes(int64_t rows, int64_t cols) {
   if (rows <= 0 || cols <= 0) return ws_layout(0, 0).total;
-  const int64_t nseg = (cols + kWarpSeg - 1) / kWarpSeg;
+  const int64_t nseg = (cols + 512 - 1) / 512;  // smallest K3 segment
   const int64_t nch = (cols + kSplitChunk - 1) / kSplitChunk;
   return std::max(ws_layout(rows, nseg).total, ws_layout(rows, nch).total);
 }
@@ -681,6 +712,7 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
                          : (p.k3 == 1   ? "k3_dyn"
                             : p.k3 == 3 ? "k3_chunk"
                             : p.k3 == 4 ? "k3_warp"
+                            : p.k3 == 5 ? "k3_reg"
                                         : "k3_smem"),
              p.nseg, p.seglen,
              p.threads, p.smem, (long long)p.chunk_rows, (long long)p.grid);

@@ -111,9 +111,10 @@ def main():
         _native.set_tuning("pdl", 0)
         record("default pdl=0", bench_once(xs, ys, rows, cols, args.reps, s))
         _native.set_tuning("pdl", 1)
-        for impl, mbs, sls in ((3, (0, 16, 32, 48), (1024, 2048)),):
+        for impl, mbs, sls, bs in ((4, (0,), (512, 1024, 2048), (0,)),
+                                   (3, (0,), (2048,), (0, 4))):
             _native.set_tuning("k3_impl", impl)
-            for b in (0, 4):
+            for b in bs:
                 _native.set_tuning("claim_batch", b)
                 for mb in mbs:
                     _native.set_tuning("chunk_mb", mb)

@@ -159,7 +159,7 @@ def test_k1_instantiations_all_agree(oracle):
         assert_parity(oracle, y, ref, what=(lpr, nv, u))
 
 
-@pytest.mark.parametrize("impl", [0, 1, 2, 3, "3b"])
+@pytest.mark.parametrize("impl", [0, 1, 2, 3, "3b", 4])
 def test_every_k3_implementation(impl, oracle):
     """Long-row kernels: ordered CTA queue (0), smem-resident cooperative (1),
     per-chunk launches (2), ordered warp queue (3) -- all against the oracle,
