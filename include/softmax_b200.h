@@ -130,11 +130,13 @@ void sk_free_pinned(void* p);
  *   "grid_mult"      K1 grid = SMs * occupancy * grid_mult (default 1)
  *   "seg_len"        target segment length (floats) for K2/K3
  *   "chunk_mb"       K3 re-read distance / row-chunk size in MB (default 24)
- *   "claim_batch"    K3 queue tasks claimed per atomic (default 4)
  *   "chunk_occ_div"  K3 grid = SMs * occupancy / div (default 2: consecutive
  *                    launches co-reside so STATS(k+1) overlaps NORMALIZE(k-1))
- *   "k3_impl"        0 (default) one-launch ordered task queue, 1 smem-resident
- *                    cooperative, 2 one launch per L2-sized row chunk
+ *   "k3_impl"        long rows: 3 (default) warp-task queue with L2 re-read,
+ *                    0 CTA-task queue, 1 smem-resident cooperative, 2 one launch
+ *                    per L2-sized row chunk, 4 register-resident warp tasks
+ *   "claim_batch"    K3 warp queue: 0 (default) static round-robin tasks on a
+ *                    cooperative grid, n > 0 tasks claimed n per atomic
  *   "k1_pf", "pdl"   K1 register prefetch (-1 table default), PDL on launches (1)
  *   "seg_align"      1 (default): K3 grid is a whole multiple of the row's
  *                    segment count, so row groups never straddle CTAs

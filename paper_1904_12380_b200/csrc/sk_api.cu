@@ -77,7 +77,7 @@ std::atomic<int> g_chunk_mb{24};  // K3 row-chunk size (MB of input) kept L2 res
 std::atomic<int> g_chunk_mb_set{0};  // chunk_mb explicitly tuned (overrides the K3 warp lag)
 std::atomic<int> g_chunk_occ_div{2};
 std::atomic<int> g_claim_batch{0};   // K3 warp queue: tasks per atomic claim (0 = static)  // K3 grid = SMs*occupancy/div: two launches co-reside
-std::atomic<int> g_k3_impl{0};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
+std::atomic<int> g_k3_impl{3};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
 
 // Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.
 template <typename... Args>
@@ -149,7 +149,7 @@ void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u, int& pf, int& 
     if (cols <= 16) { lpr = 4; nv = 1; u = 4; }
     else if (cols <= 32) { lpr = 8; nv = 1; u = 4; }
     else if (cols <= 64) { lpr = 16; nv = 1; u = 4; }
-    else if (cols <= 128) { lpr = 16; nv = 2; u = 1; gm = 2; }
+    else if (cols <= 128) { lpr = 8; nv = 4; u = 1; gm = 2; }
     else if (cols <= 256) { lpr = 16; nv = 4; u = 1; gm = 4; }
     else if (cols <= 512) { lpr = 32; nv = 4; u = 1; gm = 2; }
     else { lpr = 32; nv = 8; u = 1; gm = 2; }
@@ -330,7 +330,8 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     const bool chunked = cols > kSegCap && impl0 != 1;
     const bool warp3 = cols > kSegCap && (impl0 == 3 || impl0 == 4);
     int64_t target = g_seg_len.load() > 0 ? g_seg_len.load() : (chunked ? kChunkSeg : kSegCap);
-    if (warp3) target = g_seg_len.load() == 2048 ? 2048 : g_seg_len.load() == 512 ? 512 : kWarpSeg;
+    if (warp3)  // warp tasks: 2048 floats (default) or 1024 / 512
+      target = g_seg_len.load() == 1024 ? 1024 : g_seg_len.load() == 512 ? 512 : 2048;
     target = std::min<int64_t>(target, kSegCap);
     const int64_t nseg = (cols + target - 1) / target;
     // warp tasks use fixed-size segments (the last one shorter)
