@@ -114,6 +114,19 @@ int sk_normalize_f32(const float* x, float* y, int64_t rows, int64_t cols, int64
                      void* stream);
 
 /*
+ * The reference's three phases as separate kernels (NOT the hot path; the
+ * fused sk_softmax_f32 is).  They back variant_pipeline() / the GPU phase
+ * profile (kernels.py:283-339, profiler.py:96-133):
+ *   sk_maxsub_f32    y = x - rowmax, clamped at -64 if clip  (kernels.py:136-151)
+ *   sk_exp_f32       buf = exp(buf) in place, mode as sk_softmax_f32 (kernels.py:171-174)
+ *   sk_sumscale_f32  buf *= 1/(float)sum(row) (f64 sum), sub-normal -> +0 (kernels.py:177-189)
+ */
+int sk_maxsub_f32(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
+                  int64_t ldy, int clip, void* stream);
+int sk_exp_f32(float* buf, int64_t n, int mode, void* stream);
+int sk_sumscale_f32(float* buf, int64_t rows, int64_t cols, int64_t ld, void* stream);
+
+/*
  * Page-locked host memory for Matrix2D buffers (tensor.py:90-103 allocates
  * with np.zeros; pinned memory lets sk_softmax_f32_host reach full PCIe
  * bandwidth).  Returns NULL on failure (-> ResourceError).

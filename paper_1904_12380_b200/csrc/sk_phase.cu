@@ -1,0 +1,126 @@
+// sk_phase.cu -- the reference's three softmax phases as separate kernels.
+//
+// Not the hot path: the fused kernels (K1-K4) are.  These exist so the GPU
+// can reproduce the reference's phase structure -- variant_pipeline /
+// PhasePipeline (kernels.py:283-339) and the Fig. 2 phase profile
+// (profiler.py:96-133) -- with the same per-phase semantics:
+//
+//   sk_maxsub_f32    kernels.py:136-151  y = x - rowmax (ValueClip at -64 if clip)
+//   sk_exp_f32       kernels.py:171-174  buf = exp(buf), elementwise, in place
+//   sk_sumscale_f32  kernels.py:177-189  S = sum(row) (f64), r = 1/(float)S,
+//                                        y = e*r, y < FLT_MIN -> +0, in place
+//
+// One CTA per row, grid-stride over columns, any row pitch / alignment.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/softmax_b200.h"
+#include "sk_common.cuh"
+
+namespace sk {
+namespace {
+
+constexpr int kPhaseThreads = 256;
+
+__device__ __forceinline__ float cta_reduce_max(float v, float* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = group_max<32>(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  float m = red[0];
+  for (int w = 1; w < kPhaseThreads / 32; ++w) m = fmaxf(m, red[w]);
+  __syncthreads();
+  return m;
+}
+__device__ __forceinline__ double cta_reduce_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = group_sum<32>(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = red[0];
+  for (int w = 1; w < kPhaseThreads / 32; ++w) s += red[w];
+  __syncthreads();
+  return s;
+}
+
+__global__ void __launch_bounds__(kPhaseThreads)
+    k_maxsub(const float* __restrict__ x, float* __restrict__ y, int64_t cols, int64_t ldx,
+             int64_t ldy, int clip, float shift_scale) {
+  __shared__ float red[kPhaseThreads / 32];
+  const float* xr = x + int64_t(blockIdx.x) * ldx;
+  float* yr = y + int64_t(blockIdx.x) * ldy;
+  float m = kPadLogit;
+  for (int64_t c = threadIdx.x; c < cols; c += kPhaseThreads) m = fmaxf(m, xr[c]);
+  m = cta_reduce_max(m, red) * shift_scale;
+  for (int64_t c = threadIdx.x; c < cols; c += kPhaseThreads) {
+    const float s = xr[c] - m;
+    yr[c] = clip ? (s > kClipFloor ? s : kClipFloor) : s;
+  }
+}
+
+template <int MODE>
+__global__ void k_exp(float* __restrict__ buf, int64_t n) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    buf[i] = sexp1<MODE>(buf[i], 0.0f);
+}
+
+__global__ void __launch_bounds__(kPhaseThreads)
+    k_sumscale(float* __restrict__ buf, int64_t cols, int64_t ld) {
+  __shared__ double red[kPhaseThreads / 32];
+  float* r = buf + int64_t(blockIdx.x) * ld;
+  double s = 0.0;
+  for (int64_t c = threadIdx.x; c < cols; c += kPhaseThreads) s += static_cast<double>(r[c]);
+  s = cta_reduce_sum(s, red);
+  const float rcp = recip_of_sum(s);
+  for (int64_t c = threadIdx.x; c < cols; c += kPhaseThreads) r[c] = scale_flush(r[c], rcp);
+}
+
+bool bad_shape(const void* a, const void* b, int64_t rows, int64_t cols, int64_t ld1,
+               int64_t ld2) {
+  return rows < 0 || cols < 1 || ld1 < cols || ld2 < cols || rows > INT32_MAX ||
+         (rows > 0 && (!a || !b));
+}
+
+}  // namespace
+}  // namespace sk
+
+extern "C" {
+
+int sk_maxsub_f32(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
+                  int64_t ldy, int clip, void* stream) {
+  if (sk::bad_shape(x, y, rows, cols, ldx, ldy)) return SK_ERR_ARGUMENT;
+  if (rows == 0) return SK_OK;
+  sk::k_maxsub<<<static_cast<unsigned>(rows), sk::kPhaseThreads, 0,
+                 static_cast<cudaStream_t>(stream)>>>(x, y, cols, ldx, ldy, clip ? 1 : 0, 1.0f);
+  return cudaGetLastError() == cudaSuccess ? SK_OK : SK_ERR_CUDA;
+}
+
+int sk_exp_f32(float* buf, int64_t n, int mode, void* stream) {
+  if (n < 0 || (n > 0 && !buf) || mode < 0 || mode > 2) return SK_ERR_ARGUMENT;
+  if (n == 0) return SK_OK;
+  int sms = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (n + 255) / 256;
+  const unsigned grid = static_cast<unsigned>(want < int64_t(sms) * 16 ? want : int64_t(sms) * 16);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  switch (mode) {
+    case 0: sk::k_exp<sk::kClipAccurate><<<grid, 256, 0, s>>>(buf, n); break;
+    case 1: sk::k_exp<sk::kAccurate><<<grid, 256, 0, s>>>(buf, n); break;
+    default: sk::k_exp<sk::kApprox><<<grid, 256, 0, s>>>(buf, n); break;
+  }
+  return cudaGetLastError() == cudaSuccess ? SK_OK : SK_ERR_CUDA;
+}
+
+int sk_sumscale_f32(float* buf, int64_t rows, int64_t cols, int64_t ld, void* stream) {
+  if (sk::bad_shape(buf, buf, rows, cols, ld, ld)) return SK_ERR_ARGUMENT;
+  if (rows == 0) return SK_OK;
+  sk::k_sumscale<<<static_cast<unsigned>(rows), sk::kPhaseThreads, 0,
+                   static_cast<cudaStream_t>(stream)>>>(buf, cols, ld);
+  return cudaGetLastError() == cudaSuccess ? SK_OK : SK_ERR_CUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,54 @@
+"""GPU tests of the phase pipeline, profiler, bound probe and CLI."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1904_12380_b200 as sk
+from paper_1904_12380_b200 import bench_cli, bound_probe, configs, phases, profiler
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("C", [1, 50, 1000, 4097, 70000])
+def test_phase_pipeline_matches_fused(C, oracle):
+    x = configs.generate("c4", 0, 7)[:, :C].copy()
+    xd = torch.from_numpy(x).cuda()
+    for v in (sk.KernelVariant.REFERENCE_CLIPPED, sk.KernelVariant.REFERENCE_INFERENCE):
+        pipe = phases.variant_pipeline(v, *x.shape)
+        buf = torch.empty_like(xd)
+        pipe.maxsub(xd, buf)
+        pipe.exp(buf)
+        pipe.sumscale(buf)
+        ref = oracle.softmax_ref(x, v is sk.KernelVariant.REFERENCE_CLIPPED)
+        assert oracle.parity(buf.cpu().numpy(), ref)["ok"], (C, v)
+
+
+def test_profiler_and_probe_on_gpu():
+    m = sk.Matrix2D.from_array(configs.generate("c3"))
+    t = profiler.time_phases(m, sk.KernelVariant.REFERENCE_CLIPPED, reps=20, warmup=3)
+    assert all(x.phase_sum <= x.whole for x in t)
+    w = profiler.time_whole(m, sk.KernelVariant.REFERENCE_CLIPPED, reps=20, warmup=3)
+    assert min(w) > 0
+    r = bound_probe.probe(m, sk.KernelVariant.REFERENCE_CLIPPED, reps=20, warmup=3)
+    print("c3 probe", r)
+    # the fused kernel moves the copy's bytes at the copy's speed: memory bound
+    assert r.verdict is bound_probe.Verdict.MEMORY_BOUND_LIKELY
+    s = bound_probe.probe_self_copy(m, reps=20, warmup=3)
+    assert s.verdict is bound_probe.Verdict.MEMORY_BOUND_LIKELY
+
+
+def test_cli_verify_and_bench(capsys):
+    assert bench_cli.main(["verify", "--reps", "5"]) == 0
+    out = capsys.readouterr().out
+    assert "verify: OK" in out
+    assert bench_cli.main(["bench", "--reps", "10", "--format", "csv",
+                           "--batch-size", "32", "--batch-size", "128"]) == 0
+    rows = capsys.readouterr().out.strip().splitlines()
+    assert rows[0].startswith("variant,batch,cols,median_ticks")
+    assert len(rows) == 1 + 2 * (len(sk.LADDER) + 1)
+    assert bench_cli.main(["probe", "--reps", "5", "--batch-size", "128"]) == 0
+    assert "CopyBaseline" in capsys.readouterr().out
+    assert bench_cli.main(["profile", "--reps", "5", "--batch-size", "8",
+                           "--variant", "ReferenceClipped"]) == 0
+    assert "Profiling Report" in capsys.readouterr().out
