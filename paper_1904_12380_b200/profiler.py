@@ -83,6 +83,15 @@ def _ticks(e0, e1) -> int:
     return int(round(e0.elapsed_time(e1) * 1e6))
 
 
+def _hold_stream(n_launches: int) -> None:
+    """Park the stream behind a device-side sleep while the host enqueues the
+    timed launches, so each event pair brackets GPU time only (not the
+    host's per-launch latency while the GPU sits idle)."""
+    import torch
+
+    torch.cuda._sleep(int(min(2e9, 2e5 + n_launches * 1.2e5)))  # ~60 us of cycles per launch
+
+
 def time_whole(m, variant: KernelVariant, reps: int, warmup: int = 10,
                cfg: LaneConfig = LaneConfig()) -> list[int]:
     """Device ticks of the fused softmax, one event pair per rep."""
@@ -96,6 +105,7 @@ def time_whole(m, variant: KernelVariant, reps: int, warmup: int = 10,
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(reps)]
+    _hold_stream(reps)
     for a, b in ev:
         a.record()
         softmax_into(x, y, variant, cfg, check_finite=False)
@@ -122,6 +132,7 @@ def time_phases(m, variant: KernelVariant, reps: int, warmup: int = 10,
         pipe.sumscale(dst)
     torch.cuda.synchronize()
     marks = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(reps)]
+    _hold_stream(3 * reps)
     for e in marks:
         e[0].record()
         e[1].record()
