@@ -153,6 +153,7 @@ void sk_free_pinned(void* p);
  *   "k1_pf", "pdl"   K1 register prefetch (-1 table default), PDL on launches (1)
  *   "seg_align"      1 (default): K3 grid is a whole multiple of the row's
  *                    segment count, so row groups never straddle CTAs
+ *   "host_chunk_kb"  sk_softmax_f32_host chunk size in KiB (0 = auto, ~1/16 of the job)
  *   "skip_max_shift" 1: shift by 0 instead of the row max -- the reference's
  *                    _SKIP_MAX_SHIFT fault hook (kernels.py:103-105, :309-311);
  *                    large logits then overflow and verification must fail.

@@ -599,13 +599,19 @@ int softmax_dev(const float* x, float* y, int64_t rows, int64_t cols, int64_t ld
 }
 
 // ------------------------------------------------ pipelined host-buffer path
-constexpr int kHostStreams = 3;
+// Three streams (H2D copy engine, compute, D2H copy engine) over a ring of
+// kRing device buffer pairs, ordered by events: chunk k's kernel waits for its
+// H2D, its D2H waits for its kernel, and slot reuse waits for the kernel / D2H
+// that last used the slot.  H2D of chunk k+1, compute of chunk k and D2H of
+// chunk k-1 run concurrently, so a call costs ~max(H2D, D2H) + one chunk.
+constexpr int kRing = 4;
 struct HostCtx {
   std::mutex mu;
   bool init = false;
-  cudaStream_t st[kHostStreams] = {};
-  float* dx[kHostStreams] = {};
-  float* dy[kHostStreams] = {};
+  cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_h2d[kRing] = {}, ev_k[kRing] = {}, ev_d2h[kRing] = {};
+  float* dx[kRing] = {};
+  float* dy[kRing] = {};
   unsigned long long* dbad = nullptr;  // one bad-row flag per chunk
   unsigned long long* hbad = nullptr;  // pinned mirror
   int64_t flag_cap = 0;
@@ -613,6 +619,7 @@ struct HostCtx {
 };
 std::mutex g_host_mu;
 std::map<int, HostCtx*> g_host;
+std::atomic<int> g_host_chunk_kb{0};  // 0: auto
 
 HostCtx* host_ctx(int dev) {
   std::lock_guard<std::mutex> g(g_host_mu);
@@ -676,6 +683,7 @@ int sk_set_tuning(const char* key, int value) {
   }
   else if (k == "chunk_occ_div") g_chunk_occ_div = value;
   else if (k == "claim_batch") g_claim_batch = value;
+  else if (k == "host_chunk_kb") g_host_chunk_kb = value;
   else if (k == "k3_impl") g_k3_impl = value;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;
@@ -733,26 +741,33 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
   HostCtx* c = host_ctx(device);
   std::lock_guard<std::mutex> g(c->mu);
   if (!c->init) {
-    for (int i = 0; i < kHostStreams; ++i)
-      SK_CUDA(cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking));
+    SK_CUDA(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+    SK_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
+    SK_CUDA(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+    for (int i = 0; i < kRing; ++i) {
+      SK_CUDA(cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming));
+      SK_CUDA(cudaEventCreateWithFlags(&c->ev_k[i], cudaEventDisableTiming));
+      SK_CUDA(cudaEventCreateWithFlags(&c->ev_d2h[i], cudaEventDisableTiming));
+    }
     c->init = true;
   }
   const int64_t row_bytes = cols * 4;
   const int64_t total = rows * row_bytes;
-  // chunk: ~1/8 of the job, 2..32 MiB, whole rows
-  int64_t chunk_bytes = std::min<int64_t>(std::max<int64_t>(total / 8, 2 << 20), 32 << 20);
+  // chunk: ~1/16 of the job, 1..16 MiB (tunable), whole rows
+  int64_t chunk_bytes = std::min<int64_t>(std::max<int64_t>(total / 16, 1 << 20), 16 << 20);
+  if (g_host_chunk_kb.load() > 0) chunk_bytes = int64_t(g_host_chunk_kb.load()) << 10;
   int64_t chunk_rows = std::max<int64_t>(1, chunk_bytes / row_bytes);
   chunk_rows = std::min(chunk_rows, rows);
   const size_t need = size_t(chunk_rows * row_bytes);
   if (c->cap_bytes < need) {
-    for (int i = 0; i < kHostStreams; ++i) SK_CUDA(cudaStreamSynchronize(c->st[i]));
-    for (int i = 0; i < kHostStreams; ++i) {
+    SK_CUDA(cudaDeviceSynchronize());
+    for (int i = 0; i < kRing; ++i) {
       if (c->dx[i]) cudaFree(c->dx[i]);
       if (c->dy[i]) cudaFree(c->dy[i]);
       c->dx[i] = c->dy[i] = nullptr;
     }
     c->cap_bytes = 0;
-    for (int i = 0; i < kHostStreams; ++i) {
+    for (int i = 0; i < kRing; ++i) {
       SK_CUDA(cudaMalloc(&c->dx[i], need));
       SK_CUDA(cudaMalloc(&c->dy[i], need));
     }
@@ -760,6 +775,7 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
   }
   const int64_t nchunks = (rows + chunk_rows - 1) / chunk_rows;
   if (c->flag_cap < nchunks) {
+    SK_CUDA(cudaDeviceSynchronize());
     if (c->dbad) cudaFree(c->dbad);
     if (c->hbad) cudaFreeHost(c->hbad);
     c->dbad = nullptr;
@@ -771,25 +787,31 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
     SK_CUDA(cudaMallocHost(&c->hbad, cap * sizeof(unsigned long long)));
     c->flag_cap = cap;
   }
-  // chunk k on stream k % kHostStreams: H2D -> fused kernel -> D2H -> its flag.
-  // In-order streams make buffer reuse safe; the copy engines overlap H2D of one
-  // chunk with D2H of another.
   for (int64_t k = 0; k < nchunks; ++k) {
-    const int i = static_cast<int>(k % kHostStreams);
+    const int i = static_cast<int>(k % kRing);
     const int64_t r0 = k * chunk_rows;
     const int64_t nr = std::min(chunk_rows, rows - r0);
     const size_t bytes = size_t(nr * row_bytes);
+    // input slot free once the kernel that last read it is done
+    if (k >= kRing) SK_CUDA(cudaStreamWaitEvent(c->s_h2d, c->ev_k[i], 0));
     SK_CUDA(cudaMemcpyAsync(c->dx[i], x_host + r0 * cols, bytes, cudaMemcpyHostToDevice,
-                            c->st[i]));
+                            c->s_h2d));
+    SK_CUDA(cudaEventRecord(c->ev_h2d[i], c->s_h2d));
+    SK_CUDA(cudaStreamWaitEvent(c->s_comp, c->ev_h2d[i], 0));
+    // output slot free once the D2H that last read it is done
+    if (k >= kRing) SK_CUDA(cudaStreamWaitEvent(c->s_comp, c->ev_d2h[i], 0));
     st = softmax_dev(c->dx[i], c->dy[i], nr, cols, cols, cols, mode, c->dbad + k, nullptr, 0,
-                     c->st[i]);
+                     c->s_comp);
     if (st) return st;
+    SK_CUDA(cudaEventRecord(c->ev_k[i], c->s_comp));
+    SK_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_k[i], 0));
     SK_CUDA(cudaMemcpyAsync(y_host + r0 * cols, c->dy[i], bytes, cudaMemcpyDeviceToHost,
-                            c->st[i]));
+                            c->s_d2h));
     SK_CUDA(cudaMemcpyAsync(c->hbad + k, c->dbad + k, sizeof(unsigned long long),
-                            cudaMemcpyDeviceToHost, c->st[i]));
+                            cudaMemcpyDeviceToHost, c->s_d2h));
+    SK_CUDA(cudaEventRecord(c->ev_d2h[i], c->s_d2h));
   }
-  for (int i = 0; i < kHostStreams; ++i) SK_CUDA(cudaStreamSynchronize(c->st[i]));
+  SK_CUDA(cudaStreamSynchronize(c->s_d2h));
   for (int64_t k = 0; k < nchunks; ++k) {
     if (c->hbad[k] != SK_NO_BAD_ROW) {
       const int64_t row = k * chunk_rows + static_cast<int64_t>(c->hbad[k]);

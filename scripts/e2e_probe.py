@@ -1,0 +1,71 @@
+#!/usr/bin/env python
+"""PCIe ceilings and the host-buffer softmax (sk_softmax_f32_host) by chunk size."""
+
+import json
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+import paper_1904_12380_b200 as sk  # noqa: E402
+from paper_1904_12380_b200 import _native, configs  # noqa: E402
+
+
+def gbs(nbytes, sec):
+    return nbytes / sec / 1e9
+
+
+def main():
+    n = 64 << 20  # 64 MiB
+    h = torch.empty(n // 4, dtype=torch.float32, pin_memory=True)
+    h2 = torch.empty_like(h, pin_memory=True)
+    d = torch.empty(n // 4, dtype=torch.float32, device="cuda")
+    d2 = torch.empty_like(d)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        d.copy_(h, non_blocking=True)
+        h2.copy_(d2, non_blocking=True)
+    torch.cuda.synchronize()
+    res = {}
+    t = time.perf_counter()
+    for _ in range(10):
+        d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    res["h2d_GBps"] = gbs(10 * n, time.perf_counter() - t)
+    t = time.perf_counter()
+    for _ in range(10):
+        h2.copy_(d2, non_blocking=True)
+    torch.cuda.synchronize()
+    res["d2h_GBps"] = gbs(10 * n, time.perf_counter() - t)
+    t = time.perf_counter()
+    for _ in range(10):
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+    torch.cuda.synchronize()
+    res["bidir_GBps_total"] = gbs(20 * n, time.perf_counter() - t)
+    print(json.dumps(res), flush=True)
+    for name in ("c2", "c3", "c4"):
+        spec = configs.get(name)
+        m = sk.Matrix2D.from_array(configs.generate(spec), pinned=True)
+        out = sk.alloc_matrix(spec.rows, spec.cols, pinned=True)
+        for kb in (0, 1024, 2048, 4096, 8192, 16384):
+            _native.set_tuning("host_chunk_kb", kb)
+            sk.softmax(m, sk.KernelVariant.REFERENCE_CLIPPED, out=out)
+            reps = 10
+            t = time.perf_counter()
+            for _ in range(reps):
+                sk.softmax(m, sk.KernelVariant.REFERENCE_CLIPPED, out=out)
+            dt = (time.perf_counter() - t) / reps
+            print(json.dumps({"config": name, "chunk_kb": kb, "ms": dt * 1e3,
+                              "e2e_GBps": gbs(8 * spec.rows * spec.cols, dt)}), flush=True)
+    _native.set_tuning("host_chunk_kb", 0)
+
+
+if __name__ == "__main__":
+    main()
