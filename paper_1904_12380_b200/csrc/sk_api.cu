@@ -753,12 +753,33 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
   }
   const int64_t row_bytes = cols * 4;
   const int64_t total = rows * row_bytes;
-  // chunk: ~1/16 of the job, 1..16 MiB (tunable), whole rows
-  int64_t chunk_bytes = std::min<int64_t>(std::max<int64_t>(total / 16, 1 << 20), 16 << 20);
+  // Chunk schedule: a ramp 1/8, 1/4, 1/2 of the steady chunk at both ends (the
+  // pipeline fills and drains on small copies), steady chunks of ~1/6 of the
+  // job (4..16 MiB; tunable) in the middle.  Whole rows.
+  int64_t chunk_bytes = std::min<int64_t>(std::max<int64_t>(total / 6, 4 << 20), 16 << 20);
   if (g_host_chunk_kb.load() > 0) chunk_bytes = int64_t(g_host_chunk_kb.load()) << 10;
-  int64_t chunk_rows = std::max<int64_t>(1, chunk_bytes / row_bytes);
-  chunk_rows = std::min(chunk_rows, rows);
-  const size_t need = size_t(chunk_rows * row_bytes);
+  const int64_t big = std::min(rows, std::max<int64_t>(1, chunk_bytes / row_bytes));
+  std::vector<int64_t> sched;  // rows per chunk
+  {
+    std::vector<int64_t> head;
+    for (int64_t r = big / 8; r >= 1 && r < big; r *= 2) head.push_back(r);
+    int64_t left = rows;
+    std::vector<int64_t> tail;
+    for (int64_t r : head) {  // ramp up at the start and down at the end
+      if (left >= 2 * r + big) {
+        sched.push_back(r);
+        tail.push_back(r);
+        left -= 2 * r;
+      }
+    }
+    while (left > 0) {
+      const int64_t r = std::min(big, left);
+      sched.push_back(r);
+      left -= r;
+    }
+    for (auto it = tail.rbegin(); it != tail.rend(); ++it) sched.push_back(*it);
+  }
+  const size_t need = size_t(big * row_bytes);
   if (c->cap_bytes < need) {
     SK_CUDA(cudaDeviceSynchronize());
     for (int i = 0; i < kRing; ++i) {
@@ -773,7 +794,7 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
     }
     c->cap_bytes = need;
   }
-  const int64_t nchunks = (rows + chunk_rows - 1) / chunk_rows;
+  const int64_t nchunks = static_cast<int64_t>(sched.size());
   if (c->flag_cap < nchunks) {
     SK_CUDA(cudaDeviceSynchronize());
     if (c->dbad) cudaFree(c->dbad);
@@ -787,10 +808,12 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
     SK_CUDA(cudaMallocHost(&c->hbad, cap * sizeof(unsigned long long)));
     c->flag_cap = cap;
   }
+  std::vector<int64_t> start(nchunks + 1, 0);
+  for (int64_t k = 0; k < nchunks; ++k) start[k + 1] = start[k] + sched[k];
   for (int64_t k = 0; k < nchunks; ++k) {
     const int i = static_cast<int>(k % kRing);
-    const int64_t r0 = k * chunk_rows;
-    const int64_t nr = std::min(chunk_rows, rows - r0);
+    const int64_t r0 = start[k];
+    const int64_t nr = sched[k];
     const size_t bytes = size_t(nr * row_bytes);
     // input slot free once the kernel that last read it is done
     if (k >= kRing) SK_CUDA(cudaStreamWaitEvent(c->s_h2d, c->ev_k[i], 0));
@@ -814,7 +837,7 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
   SK_CUDA(cudaStreamSynchronize(c->s_d2h));
   for (int64_t k = 0; k < nchunks; ++k) {
     if (c->hbad[k] != SK_NO_BAD_ROW) {
-      const int64_t row = k * chunk_rows + static_cast<int64_t>(c->hbad[k]);
+      const int64_t row = start[k] + static_cast<int64_t>(c->hbad[k]);
       SK_CUDA(cudaMemset(c->dbad, 0xFF, nchunks * sizeof(unsigned long long)));
       if (bad_row_out) *bad_row_out = row;
       g_last_error = "non-finite logits in row " + std::to_string(row);
