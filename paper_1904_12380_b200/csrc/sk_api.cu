@@ -620,6 +620,19 @@ struct HostCtx {
 std::mutex g_host_mu;
 std::map<int, HostCtx*> g_host;
 std::atomic<int> g_host_chunk_kb{0};  // 0: auto
+std::atomic<int> g_host_zero_copy{1};  // K1/K2 rows read/write pinned host memory directly
+
+// Device-visible address of a page-locked (cudaHostAlloc / registered) host
+// buffer, or nullptr for pageable memory.
+const void* mapped_device_ptr(const void* h) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
+  return a.devicePointer;
+}
 
 HostCtx* host_ctx(int dev) {
   std::lock_guard<std::mutex> g(g_host_mu);
@@ -684,6 +697,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "chunk_occ_div") g_chunk_occ_div = value;
   else if (k == "claim_batch") g_claim_batch = value;
   else if (k == "host_chunk_kb") g_host_chunk_kb = value;
+  else if (k == "host_zero_copy") g_host_zero_copy = value;
   else if (k == "k3_impl") g_k3_impl = value;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;
@@ -750,6 +764,35 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
       SK_CUDA(cudaEventCreateWithFlags(&c->ev_d2h[i], cudaEventDisableTiming));
     }
     c->init = true;
+  }
+  // Zero-copy: a row that fits one CTA (K1/K2) is read from and written to
+  // pinned host memory directly by the kernel -- PCIe reads and (posted) writes
+  // proceed concurrently inside one launch, with no staging copies, events or
+  // chunk pipeline.  Long rows (K3/K4 re-read segments) keep the staged path.
+  if (g_host_zero_copy.load() && cols <= kSegCap) {
+    const float* xd = static_cast<const float*>(mapped_device_ptr(x_host));
+    float* yd = static_cast<float*>(const_cast<void*>(mapped_device_ptr(y_host)));
+    if (xd && yd) {
+      if (c->flag_cap < 1) {
+        SK_CUDA(cudaMalloc(&c->dbad, 64 * sizeof(unsigned long long)));
+        SK_CUDA(cudaMemset(c->dbad, 0xFF, 64 * sizeof(unsigned long long)));
+        SK_CUDA(cudaMallocHost(&c->hbad, 64 * sizeof(unsigned long long)));
+        c->flag_cap = 64;
+      }
+      st = softmax_dev(xd, yd, rows, cols, cols, cols, mode, c->dbad, nullptr, 0, c->s_comp);
+      if (st) return st;
+      SK_CUDA(cudaMemcpyAsync(c->hbad, c->dbad, sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, c->s_comp));
+      SK_CUDA(cudaStreamSynchronize(c->s_comp));
+      if (c->hbad[0] != SK_NO_BAD_ROW) {
+        const int64_t row = static_cast<int64_t>(c->hbad[0]);
+        SK_CUDA(cudaMemset(c->dbad, 0xFF, sizeof(unsigned long long)));
+        if (bad_row_out) *bad_row_out = row;
+        g_last_error = "non-finite logits in row " + std::to_string(row);
+        return SK_ERR_NONFINITE;
+      }
+      return SK_OK;
+    }
   }
   const int64_t row_bytes = cols * 4;
   const int64_t total = rows * row_bytes;

@@ -54,7 +54,8 @@ def main():
         spec = configs.get(name)
         m = sk.Matrix2D.from_array(configs.generate(spec), pinned=True)
         out = sk.alloc_matrix(spec.rows, spec.cols, pinned=True)
-        for kb in (0, 1024, 2048, 4096, 8192, 16384):
+        for zc, kb in ((1, 0), (0, 0), (0, 4096), (0, 8192), (0, 16384)):
+            _native.set_tuning("host_zero_copy", zc)
             _native.set_tuning("host_chunk_kb", kb)
             sk.softmax(m, sk.KernelVariant.REFERENCE_CLIPPED, out=out)
             reps = 10
@@ -62,9 +63,13 @@ def main():
             for _ in range(reps):
                 sk.softmax(m, sk.KernelVariant.REFERENCE_CLIPPED, out=out)
             dt = (time.perf_counter() - t) / reps
-            print(json.dumps({"config": name, "chunk_kb": kb, "ms": dt * 1e3,
+            ok = bool((out.view2d == sk.softmax(torch.from_numpy(m.view2d).cuda(),
+                       sk.KernelVariant.REFERENCE_CLIPPED).cpu().numpy()).all())
+            print(json.dumps({"config": name, "zero_copy": zc, "chunk_kb": kb, "ms": dt * 1e3,
+                              "bitwise_equal_device": ok,
                               "e2e_GBps": gbs(8 * spec.rows * spec.cols, dt)}), flush=True)
     _native.set_tuning("host_chunk_kb", 0)
+    _native.set_tuning("host_zero_copy", 1)
 
 
 if __name__ == "__main__":
