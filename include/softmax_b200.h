@@ -84,11 +84,11 @@ size_t sk_softmax_workspace_bytes(int64_t rows, int64_t cols);
 
 /*
  * Host-buffer softmax: the compat path behind softmax(Matrix2D, ...).
- * Pinned (page-locked) buffers with rows of <= 8192 floats: one kernel reads
- * x_host and writes y_host directly over PCIe (zero-copy).  Otherwise x_host is
- * copied to the device in row chunks, each chunk is computed and copied back,
- * pipelined over H2D / compute / D2H streams and a ring of device buffers;
- * pageable buffers work, slower.  Returns after y_host is complete.
+ * x_host is copied to the device in row chunks, each chunk is computed and
+ * copied back, pipelined over H2D / compute / D2H streams and a ring of device
+ * buffers (or, with the "host_zero_copy" tuning, one kernel reads and writes
+ * pinned host memory directly).  Pinned (page-locked) host buffers give full
+ * PCIe bandwidth; pageable ones work, slower.  Returns after y_host is complete.
  * On non-finite input returns SK_ERR_NONFINITE and stores the first bad row
  * in *bad_row_out (y_host contents then unspecified).
  */
@@ -154,9 +154,10 @@ void sk_free_pinned(void* p);
  *   "k1_pf", "pdl"   K1 register prefetch (-1 table default), PDL on launches (1)
  *   "seg_align"      1 (default): K3 grid is a whole multiple of the row's
  *                    segment count, so row groups never straddle CTAs
- *   "host_chunk_kb"  sk_softmax_f32_host chunk size in KiB (0 = auto, ~1/6 of the job)
- *   "host_zero_copy" 1 (default): pinned host buffers with rows <= 8192 are read and
- *                    written by the kernel directly over PCIe (no staging copies)
+ *   "host_chunk_kb"  sk_softmax_f32_host chunk size in KiB (0 = auto, ~1/4 of the job)
+ *   "host_zero_copy" 1: pinned host buffers with rows <= 8192 are read and written
+ *                    by the kernel directly over PCIe (measured no faster than
+ *                    staging on this box, so 0 by default)
  *   "skip_max_shift" 1: shift by 0 instead of the row max -- the reference's
  *                    _SKIP_MAX_SHIFT fault hook (kernels.py:103-105, :309-311);
  *                    large logits then overflow and verification must fail.

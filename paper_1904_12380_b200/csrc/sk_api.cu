@@ -620,7 +620,7 @@ struct HostCtx {
 std::mutex g_host_mu;
 std::map<int, HostCtx*> g_host;
 std::atomic<int> g_host_chunk_kb{0};  // 0: auto
-std::atomic<int> g_host_zero_copy{1};  // K1/K2 rows read/write pinned host memory directly
+std::atomic<int> g_host_zero_copy{0};  // K1/K2 rows read/write pinned host memory directly
 
 // Device-visible address of a page-locked (cudaHostAlloc / registered) host
 // buffer, or nullptr for pageable memory.
@@ -796,10 +796,10 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
   }
   const int64_t row_bytes = cols * 4;
   const int64_t total = rows * row_bytes;
-  // Chunk schedule: a ramp 1/8, 1/4, 1/2 of the steady chunk at both ends (the
-  // pipeline fills and drains on small copies), steady chunks of ~1/6 of the
-  // job (4..16 MiB; tunable) in the middle.  Whole rows.
-  int64_t chunk_bytes = std::min<int64_t>(std::max<int64_t>(total / 6, 4 << 20), 16 << 20);
+  // Chunk schedule: steady chunks of ~1/4 of the job (4..16 MiB; tunable),
+  // ramped 1/8, 1/4, 1/2 at both ends when the job is long enough for the
+  // ramp to pay for its extra per-copy latency.  Whole rows.
+  int64_t chunk_bytes = std::min<int64_t>(std::max<int64_t>(total / 4, 4 << 20), 16 << 20);
   if (g_host_chunk_kb.load() > 0) chunk_bytes = int64_t(g_host_chunk_kb.load()) << 10;
   const int64_t big = std::min(rows, std::max<int64_t>(1, chunk_bytes / row_bytes));
   std::vector<int64_t> sched;  // rows per chunk
@@ -809,7 +809,7 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
     int64_t left = rows;
     std::vector<int64_t> tail;
     for (int64_t r : head) {  // ramp up at the start and down at the end
-      if (left >= 2 * r + big) {
+      if (left >= 2 * r + 8 * big) {
         sched.push_back(r);
         tail.push_back(r);
         left -= 2 * r;

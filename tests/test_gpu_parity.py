@@ -273,6 +273,19 @@ def test_host_path_equals_device_path():
     assert np.array_equal(pageable.view2d.view(np.uint32), dev.view(np.uint32))
     arr = sk.softmax(x, sk.KernelVariant.REFERENCE_CLIPPED)
     assert np.array_equal(arr.view(np.uint32), dev.view(np.uint32))
+    _native.set_tuning("host_zero_copy", 1)
+    try:
+        zc = sk.softmax(m, sk.KernelVariant.REFERENCE_CLIPPED)
+        assert np.array_equal(zc.view2d.view(np.uint32), dev.view(np.uint32))
+    finally:
+        _native.set_tuning("host_zero_copy", 0)
+    for kb in (256, 1024):  # many chunks: ring reuse, ramp
+        _native.set_tuning("host_chunk_kb", kb)
+        try:
+            ck = sk.softmax(m, sk.KernelVariant.REFERENCE_CLIPPED)
+            assert np.array_equal(ck.view2d.view(np.uint32), dev.view(np.uint32))
+        finally:
+            _native.set_tuning("host_chunk_kb", 0)
 
 
 def test_every_variant_through_public_api(oracle):
