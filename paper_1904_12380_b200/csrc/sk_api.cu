@@ -20,6 +20,7 @@
 #include "sk_dyn.cuh"
 #include "sk_warp3.cuh"
 #include "sk_reg3.cuh"
+#include "sk_cluster.cuh"
 
 namespace sk {
 namespace {
@@ -76,7 +77,8 @@ std::atomic<int> g_pdl{1};        // programmatic dependent launch on every kern
 std::atomic<int> g_chunk_mb{24};  // K3 row-chunk size (MB of input) kept L2 resident
 std::atomic<int> g_chunk_mb_set{0};  // chunk_mb explicitly tuned (overrides the K3 warp lag)
 std::atomic<int> g_chunk_occ_div{2};
-std::atomic<int> g_claim_batch{0};   // K3 warp queue: tasks per atomic claim (0 = static)  // K3 grid = SMs*occupancy/div: two launches co-reside
+std::atomic<int> g_claim_batch{0};
+std::atomic<int> g_cluster_k3{1};    // use the cluster-resident K3 when a row fits   // K3 warp queue: tasks per atomic claim (0 = static)  // K3 grid = SMs*occupancy/div: two launches co-reside
 std::atomic<int> g_k3_impl{3};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
 
 // Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.
@@ -176,6 +178,50 @@ SegFn seg_fn(int mode) {
     default: return &k_seg<kApprox, NV>;
   }
 }
+const void* cluster_fn(int mode) {
+  switch (mode) {
+    case kClipAccurate: return reinterpret_cast<const void*>(&k3_cluster<kClipAccurate>);
+    case kAccurate: return reinterpret_cast<const void*>(&k3_cluster<kAccurate>);
+    default: return reinterpret_cast<const void*>(&k3_cluster<kApprox>);
+  }
+}
+constexpr int64_t kClusterSliceMax = 16384;  // floats per CTA slice (64 KB x 3 stages)
+
+// Clusters of `cs` CTAs that can be co-resident (0 if the shape cannot launch).
+int max_active_clusters(const void* fn, int cs, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(fn, cs, smem, dev);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs * 148);
+  cfg.blockDim = dim3(kClusterThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = cs;
+  a[0].val.clusterDim.y = 1;
+  a[0].val.clusterDim.z = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
+    (void)cudaGetLastError();
+    n = 0;
+  }
+  std::lock_guard<std::mutex> g(mu);
+  cache[key] = n;
+  return n;
+}
+
 template <int NV>
 const void* reg3_fn(int mode) {
   switch (mode) {
@@ -327,6 +373,27 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
   }
   if (kind == kPathSeg) {
     const int impl0 = g_k3_impl.load();
+    // K3c: the row resident in one thread-block cluster (default when it fits)
+    if (cols > kSegCap && (impl0 == 5 || impl0 == 3) && g_cluster_k3.load() &&
+        cols <= 16 * kClusterSliceMax) {
+      int cs = 2;
+      while (cs < 16 && (cols + cs - 1) / cs > kClusterSliceMax) cs *= 2;
+      const int64_t slice = align_up((cols + cs - 1) / cs, 4);
+      const size_t smem = size_t(kClusterStages) * slice * sizeof(float);
+      const void* fn = cluster_fn(mode);
+      const int ncl = max_active_clusters(fn, cs, smem);
+      if (ncl > 0) {
+        p.kind = kPathSeg;
+        p.k3 = 6;
+        p.nseg = cs;
+        p.seglen = static_cast<int>(slice);
+        p.threads = kClusterThreads;
+        p.smem = smem;
+        p.grid = int64_t(ncl) * cs;
+        return SK_OK;
+      }
+      if (impl0 == 5) return arg_fail("cluster K3 cannot launch on this device");
+    }
     const bool chunked = cols > kSegCap && impl0 != 1;
     const bool warp3 = cols > kSegCap && (impl0 == 3 || impl0 == 4);
     int64_t target = g_seg_len.load() > 0 ? g_seg_len.load() : (chunked ? kChunkSeg : kSegCap);
@@ -413,6 +480,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
 }
 
 size_t plan_ws_bytes(const Plan& p, int64_t rows) {
+  if (p.kind == kPathSeg && p.k3 == 6) return ws_layout(0, 0).total;
   if (p.kind == kPathSeg && p.nseg > 1) return ws_layout(rows, p.nseg).total;
   if (p.kind == kPathSplit) return ws_layout(rows, p.nch).total;
   return ws_layout(0, 0).total;
@@ -510,7 +578,7 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
     const int nseg = p.nseg, seglen = p.seglen;
     // K3 row counters start at zero every launch (the workspace is shared by
     // launches of different shapes, so no state is assumed across launches).
-    if (nseg > 1 && p.k3 != 1 && p.k3 != 4 && p.k3 != 5) SK_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(unsigned), s));
+    if (nseg > 1 && p.k3 != 1 && p.k3 != 4 && p.k3 != 5 && p.k3 != 6) SK_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(unsigned), s));
     if (p.k3 == 3) {
       const void* fn = p.seglen <= kChunkThreads * 16 ? chunk_fn<4>(mode) : chunk_fn<8>(mode);
       float* rmax = reinterpret_cast<float*>(ws + l.rmax);
@@ -526,6 +594,30 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
                          y, cols, ldx, ldy, nseg, seglen, s0, sr, std::max<int64_t>(n0, 0), nr,
                          wait_first, cnt, part, rmax, rsum, bad, sh));
       }
+    } else if (p.k3 == 6) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>(p.grid));
+      cfg.blockDim = dim3(p.threads);
+      cfg.dynamicSmemBytes = p.smem;
+      cfg.stream = s;
+      cudaLaunchAttribute a[2];
+      a[0].id = cudaLaunchAttributeClusterDimension;
+      a[0].val.clusterDim.x = static_cast<unsigned>(p.nseg);
+      a[0].val.clusterDim.y = 1;
+      a[0].val.clusterDim.z = 1;
+      int na = 1;
+      if (g_pdl.load()) {
+        a[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        a[1].val.programmaticStreamSerializationAllowed = 1;
+        na = 2;
+      }
+      cfg.attrs = a;
+      cfg.numAttrs = na;
+      int slice = p.seglen;
+      float shv = sh;
+      void* args[] = {(void*)&x, (void*)&y, (void*)&rows, (void*)&cols, (void*)&ldx,
+                      (void*)&ldy, (void*)&slice, (void*)&bad, (void*)&shv};
+      SK_CUDA(cudaLaunchKernelExC(&cfg, cluster_fn(mode), args));
     } else if (p.k3 == 5) {
       const void* fn = p.seglen == 2048 ? reg3_fn<16>(mode)
                        : p.seglen == 512 ? reg3_fn<4>(mode) : reg3_fn<8>(mode);
@@ -698,6 +790,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "claim_batch") g_claim_batch = value;
   else if (k == "host_chunk_kb") g_host_chunk_kb = value;
   else if (k == "host_zero_copy") g_host_zero_copy = value;
+  else if (k == "cluster_k3") g_cluster_k3 = value;
   else if (k == "k3_impl") g_k3_impl = value;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;
@@ -736,6 +829,7 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
                             : p.k3 == 3 ? "k3_chunk"
                             : p.k3 == 4 ? "k3_warp"
                             : p.k3 == 5 ? "k3_reg"
+                            : p.k3 == 6 ? "k3_cluster"
                                         : "k3_smem"),
              p.nseg, p.seglen,
              p.threads, p.smem, (long long)p.chunk_rows, (long long)p.grid);

@@ -1,0 +1,185 @@
+// sk_cluster.cuh -- K3c: a long row resident in one thread-block CLUSTER.
+//
+// A cluster of CS CTAs (CS = 16, one CTA per SM) owns a row at a time; CTA
+// `rank` holds columns [rank*L, (rank+1)*L) of it in shared memory.  Per row:
+//
+//   1. the slice lands in smem by cp.async.bulk (1-D TMA) on an mbarrier; the
+//      ring has NS stages, so the slices of the next NS-1 rows are in flight
+//      while this one is computed (HBM keeps streaming)
+//   2. local max -> this CTA's smem slot; cluster barrier; every CTA reads all
+//      CS slots over DSMEM (ld.shared::cluster) -> the row max M, identical in
+//      every CTA (fixed rank order)
+//   3. e = exp(clip(x - M)) computed against the GLOBAL max -- the reference's
+//      exact operation order, kernels.py:144-174 -- written back in place;
+//      local f64 sum -> slot; cluster barrier; S = sum of the CS slots (rank order)
+//   4. y = e * (1/(float)S) (flush as the reference, kernels.py:184-188),
+//      streaming 128-bit stores; the stage is then re-armed with the slice of
+//      the row NS steps ahead
+//
+// The row never leaves the chip between its passes, so HBM *and* L2 each see
+// one read and one write per element (8 B/element) -- unlike two-pass schemes
+// whose re-read costs L2 bandwidth -- and the row exchange is two cluster
+// barriers plus CS DSMEM loads, not a global-memory handshake.
+#pragma once
+#include "sk_common.cuh"
+
+namespace sk {
+
+constexpr int kClusterThreads = 512;
+constexpr int kClusterStages = 3;
+
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_nrank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_id_x() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned ncluster_x() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t dsmem_addr(const void* local, unsigned rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
+  return ra;
+}
+__device__ __forceinline__ float ld_dsmem_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ double ld_dsmem_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kClusterThreads, 1)
+    k3_cluster(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
+               int64_t ldx, int64_t ldy, int slice, unsigned long long* __restrict__ bad_row,
+               float shift_scale) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stage_buf = reinterpret_cast<float*>(smem_raw);
+  __shared__ uint64_t bars[kClusterStages];
+  __shared__ float red_f[kClusterThreads / 32];
+  __shared__ double red_d[kClusterThreads / 32];
+  __shared__ float slot_max;   // read by peers over DSMEM
+  __shared__ double slot_sum;  // read by peers over DSMEM
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kClusterThreads / 32;
+  const unsigned rank = cluster_rank(), cs = cluster_nrank();
+  const int64_t cid = cluster_id_x(), ncl = ncluster_x();
+  const int64_t c0 = int64_t(rank) * slice;
+  const int64_t rem = cols - c0;
+  const int len = rem <= 0 ? 0 : static_cast<int>(rem < slice ? rem : slice);  // floats, % 4 == 0
+  const int nvec = len >> 2;
+
+  auto issue = [&](int64_t row, int stage) {
+    mbar_arrive_expect_tx(&bars[stage], static_cast<uint32_t>(len) * 4u);
+    if (len > 0)
+      tma_load_1d(stage_buf + size_t(stage) * slice, x + row * ldx + c0,
+                  static_cast<uint32_t>(len) * 4u, &bars[stage]);
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < kClusterStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_launch_dependents();
+  if (tid == 0)
+    for (int s = 0; s < kClusterStages; ++s) {
+      const int64_t row = cid + int64_t(s) * ncl;
+      if (row < rows) issue(row, s);
+    }
+
+  int k = 0;
+  for (int64_t row = cid; row < rows; row += ncl, ++k) {
+    const int stage = k % kClusterStages;
+    mbar_wait(&bars[stage], (k / kClusterStages) & 1);
+    float4* sb = reinterpret_cast<float4*>(stage_buf + size_t(stage) * slice);
+
+    // ---- local max + finite check -> DSMEM exchange -> row max
+    float mt = kPadLogit;
+    u64 z = f2pk(0.0f, 0.0f);
+    for (int q = tid; q < nvec; q += kClusterThreads) {
+      const float4 v = sb[q];
+      mt = fmaxf(mt, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+      z = nf_acc2(nf_acc2(z, v.x, v.y), v.z, v.w);
+    }
+    if (nf_bad(z)) atomicMin(bad_row, static_cast<unsigned long long>(row));
+    mt = group_max<32>(mt);
+    if (lane == 0) red_f[warp] = mt;
+    __syncthreads();
+    if (tid == 0) {
+      float m = red_f[0];
+      for (int w = 1; w < NW; ++w) m = fmaxf(m, red_f[w]);
+      slot_max = m;
+    }
+    cluster_sync_all();  // (A) every slice's max is published
+    float M = kPadLogit;
+    for (unsigned j = 0; j < cs; ++j) M = fmaxf(M, ld_dsmem_f32(dsmem_addr(&slot_max, j)));
+    M *= shift_scale;  // shift_scale = 0: fault hook
+
+    // ---- e = exp(clip(x - M)) in place (reference order), local sum -> exchange
+    u64 acc = f2pk(0.0f, 0.0f);
+    for (int q = tid; q < nvec; q += kClusterThreads) {
+      const float4 v = sb[q];
+      const float2 a = sexp2<MODE>(v.x, v.y, M);
+      const float2 b = sexp2<MODE>(v.z, v.w, M);
+      sb[q] = make_float4(a.x, a.y, b.x, b.y);
+      acc = f2add(f2add(acc, f2pk(a.x, a.y)), f2pk(b.x, b.y));
+    }
+    const float2 acc2 = f2up(acc);
+    const double sd = group_sum<32>(static_cast<double>(acc2.x + acc2.y));
+    if (lane == 0) red_d[warp] = sd;
+    __syncthreads();
+    if (tid == 0) {
+      double s = red_d[0];
+      for (int w = 1; w < NW; ++w) s += red_d[w];
+      slot_sum = s;
+    }
+    cluster_sync_all();  // (B) every slice's sum is published; all maxes were read
+    double S = 0.0;
+    for (unsigned j = 0; j < cs; ++j) S += ld_dsmem_f64(dsmem_addr(&slot_sum, j));
+    const float rcp = recip_of_sum(S);
+
+    // ---- y = e * r, streaming stores
+    float* yr = y + row * ldy + c0;
+    for (int q = tid; q < nvec; q += kClusterThreads) {
+      const float4 e = sb[q];
+      const float2 a = scale2<MODE>(make_float2(e.x, e.y), rcp);
+      const float2 b = scale2<MODE>(make_float2(e.z, e.w), rcp);
+      st_stream4(yr + 4 * q, make_float4(a.x, a.y, b.x, b.y));
+    }
+    __syncthreads();  // stage fully consumed
+    if (tid == 0) {
+      const int64_t rn = row + int64_t(kClusterStages) * ncl;
+      if (rn < rows) {
+        fence_proxy_async_smem();
+        issue(rn, stage);
+      }
+    }
+  }
+  // peers may still read our slots (loop (B) of the last row): keep the CTA alive
+  cluster_sync_all();
+}
+
+}  // namespace sk

@@ -111,9 +111,15 @@ def main():
         _native.set_tuning("pdl", 0)
         record("default pdl=0", bench_once(xs, ys, rows, cols, args.reps, s))
         _native.set_tuning("pdl", 1)
-        for impl, mbs, sls, bs in ((4, (0,), (512, 1024, 2048), (0,)),
-                                   (3, (0,), (2048,), (0, 4))):
+        _native.set_tuning("cluster_k3", 0)
+        record("k3_warp (cluster off)", bench_once(xs, ys, rows, cols, args.reps, s))
+        _native.set_tuning("pdl", 0)
+        _native.set_tuning("cluster_k3", 1)
+        record("cluster pdl=0", bench_once(xs, ys, rows, cols, args.reps, s))
+        _native.set_tuning("pdl", 1)
+        for impl, mbs, sls, bs in ((3, (0,), (2048,), (0, 4)),):
             _native.set_tuning("k3_impl", impl)
+            _native.set_tuning("cluster_k3", 0)
             for b in bs:
                 _native.set_tuning("claim_batch", b)
                 for mb in mbs:
@@ -124,12 +130,12 @@ def main():
                                bench_once(xs, ys, rows, cols, args.reps, s))
         _native.set_tuning("claim_batch", 0)
         _native.set_tuning("chunk_mb", 0)
-        _native.set_tuning("k3_impl", 0)
-        _native.set_tuning("chunk_mb", 0)
-        _native.set_tuning("seg_len", 0)
+        _native.set_tuning("cluster_k3", 1)
         _native.set_tuning("k3_impl", 1)
+        _native.set_tuning("cluster_k3", 0)
         record("k3_smem", bench_once(xs, ys, rows, cols, args.reps, s))
-        _native.set_tuning("k3_impl", 0)
+        _native.set_tuning("k3_impl", 3)
+        _native.set_tuning("cluster_k3", 1)
         _native.set_tuning("path", 2)
         record("split(k4)", bench_once(xs, ys, rows, cols, max(10, args.reps // 4), s))
         _native.set_tuning("path", -1)

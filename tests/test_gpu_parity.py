@@ -30,7 +30,7 @@ def assert_parity(oracle, y, ref, approx=False, what=""):
 def _reset_tuning():
     yield
     for k, v in (("path", -1), ("k1_lpr", 0), ("grid_mult", 0), ("seg_len", 0),
-                 ("skip_max_shift", 0)):
+                 ("skip_max_shift", 0), ("k3_impl", 3), ("cluster_k3", 1), ("chunk_mb", 0)):
         _native.set_tuning(k, v)
 
 
@@ -159,7 +159,7 @@ def test_k1_instantiations_all_agree(oracle):
         assert_parity(oracle, y, ref, what=(lpr, nv, u))
 
 
-@pytest.mark.parametrize("impl", [0, 1, 2, 3, "3b", 4])
+@pytest.mark.parametrize("impl", [0, 1, 2, 3, "3b", 4, 5])
 def test_every_k3_implementation(impl, oracle):
     """Long-row kernels: ordered CTA queue (0), smem-resident cooperative (1),
     per-chunk launches (2), ordered warp queue (3) -- all against the oracle,
@@ -170,6 +170,7 @@ def test_every_k3_implementation(impl, oracle):
     if impl == "3b":  # warp queue with batched atomic claims instead of static tasks
         impl = 3
         _native.set_tuning("claim_batch", 4)
+    _native.set_tuning("cluster_k3", 1 if impl == 5 else 0)
     _native.set_tuning("k3_impl", impl)
     try:
         for mb in (1, 3, 0):
@@ -179,7 +180,8 @@ def test_every_k3_implementation(impl, oracle):
             assert_parity(oracle, y, ref, what=(impl, mb, gu.plan(*x.shape)))
     finally:
         _native.set_tuning("claim_batch", 0)
-        _native.set_tuning("k3_impl", 0)
+        _native.set_tuning("cluster_k3", 1)
+        _native.set_tuning("k3_impl", 3)
         _native.set_tuning("chunk_mb", 0)
 
 
