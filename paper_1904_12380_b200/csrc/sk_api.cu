@@ -70,6 +70,21 @@ std::atomic<int> g_force_path{-1};  // -1 auto, 0 k1, 1 seg, 2 split
 // kernels shift by 0 instead of the row max, so large logits overflow exp.
 std::atomic<int> g_skip_max_shift{0};
 float shift_scale() { return g_skip_max_shift.load() ? 0.0f : 1.0f; }
+
+// Raise (never lower) a kernel's dynamic shared-memory limit.
+void ensure_smem_attr(const void* fn, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> set;
+  if (smem <= 48 * 1024) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  size_t& cur = set[{fn, dev}];
+  if (smem > cur) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cur = smem;
+  }
+}
 std::atomic<int> g_k1_lpr{0}, g_k1_nv{0}, g_k1_u{0}, g_grid_mult{0}, g_seg_len{0};
 std::atomic<int> g_seg_align{0};  // K3 grid = whole multiple of nseg (row groups never straddle)
 std::atomic<int> g_k1_pf{-1};     // -1: table default, 0/1 force register prefetch
@@ -200,7 +215,7 @@ int max_active_clusters(const void* fn, int cs, size_t smem) {
     if (it != cache.end()) return it->second;
   }
   cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  ensure_smem_attr(fn, smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs * 148);
   cfg.blockDim = dim3(kClusterThreads);
@@ -262,6 +277,7 @@ constexpr int64_t kSegCap = int64_t(kSegMaxThreads) * kSegNV * 4;  // 8192 float
 
 // Occupancy per (kernel, block, smem, device), cached: the query is not free
 // and sk_softmax_f32 is called once per softmax.
+
 int occupancy(const void* fn, int threads, size_t smem) {
   static std::mutex mu;
   static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
@@ -273,15 +289,7 @@ int occupancy(const void* fn, int threads, size_t smem) {
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
   }
-  static std::map<std::pair<const void*, int>, size_t> smem_set;  // only ever raised
-  if (smem > 48 * 1024) {
-    std::lock_guard<std::mutex> g(mu);
-    size_t& cur = smem_set[{fn, dev}];
-    if (smem > cur) {
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      cur = smem;
-    }
-  }
+  ensure_smem_attr(fn, smem);
   int nb = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem) != cudaSuccess) {
     (void)cudaGetLastError();

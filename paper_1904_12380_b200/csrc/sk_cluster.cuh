@@ -134,9 +134,9 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
       slot_max = m;
     }
     cluster_sync_all();  // (A) every slice's max is published
-    float M = kPadLogit;
-    for (unsigned j = 0; j < cs; ++j) M = fmaxf(M, ld_dsmem_f32(dsmem_addr(&slot_max, j)));
-    M *= shift_scale;  // shift_scale = 0: fault hook
+    // lane j of every warp reads rank j's slot: one DSMEM round trip, then shuffles
+    float M = lane < static_cast<int>(cs) ? ld_dsmem_f32(dsmem_addr(&slot_max, lane)) : kPadLogit;
+    M = group_max<32>(M) * shift_scale;  // shift_scale = 0: fault hook
 
     // ---- e = exp(clip(x - M)) in place (reference order), local sum -> exchange
     u64 acc = f2pk(0.0f, 0.0f);
@@ -157,8 +157,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
       slot_sum = s;
     }
     cluster_sync_all();  // (B) every slice's sum is published; all maxes were read
-    double S = 0.0;
-    for (unsigned j = 0; j < cs; ++j) S += ld_dsmem_f64(dsmem_addr(&slot_sum, j));
+    double S = lane < static_cast<int>(cs) ? ld_dsmem_f64(dsmem_addr(&slot_sum, lane)) : 0.0;
+    S = group_sum<32>(S);  // same butterfly in every CTA: identical S cluster-wide
     const float rcp = recip_of_sum(S);
 
     // ---- y = e * r, streaming stores
