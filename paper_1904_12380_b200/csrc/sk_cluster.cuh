@@ -6,12 +6,16 @@
 //   1. the slice lands in smem by cp.async.bulk (1-D TMA) on an mbarrier; the
 //      ring has NS stages, so the slices of the next NS-1 rows are in flight
 //      while this one is computed (HBM keeps streaming)
-//   2. local max -> this CTA's smem slot; cluster barrier; every CTA reads all
-//      CS slots over DSMEM (ld.shared::cluster) -> the row max M, identical in
-//      every CTA (fixed rank order)
+//   2. local max -> pushed into slot [rank] of every peer's smem with
+//      st.async (DSMEM store that completes a transaction count on the peer's
+//      mbarrier); each CTA waits on its own mbarrier for all CS slots, then
+//      reduces them -> the row max M, identical in every CTA (fixed order).
+//      No cluster barrier and no fence: nothing waits for the previous row's
+//      global stores to drain.  Slots/barriers alternate by row parity (a
+//      peer can be at most one exchange ahead).
 //   3. e = exp(clip(x - M)) computed against the GLOBAL max -- the reference's
 //      exact operation order, kernels.py:144-174 -- written back in place;
-//      local f64 sum -> slot; cluster barrier; S = sum of the CS slots (rank order)
+//      local f64 sum -> pushed the same way; S = sum of the CS slots (fixed order)
 //   4. y = e * (1/(float)S) (flush as the reference, kernels.py:184-188),
 //      streaming 128-bit stores; the stage is then re-armed with the slice of
 //      the row NS steps ahead
@@ -19,7 +23,7 @@
 // The row never leaves the chip between its passes, so HBM *and* L2 each see
 // one read and one write per element (8 B/element) -- unlike two-pass schemes
 // whose re-read costs L2 bandwidth -- and the row exchange is two cluster
-// barriers plus CS DSMEM loads, not a global-memory handshake.
+// DSMEM pushes per row, not a global-memory handshake.
 #pragma once
 #include "sk_common.cuh"
 
@@ -67,6 +71,15 @@ __device__ __forceinline__ double ld_dsmem_f64(uint32_t a) {
   asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
   return v;
 }
+// remote smem store that completes `bytes` of transaction on the peer's mbarrier
+__device__ __forceinline__ void st_async_f32(uint32_t raddr, float v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];"
+               ::"r"(raddr), "f"(v), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];"
+               ::"r"(raddr), "d"(v), "r"(rbar) : "memory");
+}
 
 template <int MODE>
 __global__ void __launch_bounds__(kClusterThreads, 1)
@@ -78,8 +91,9 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   __shared__ uint64_t bars[kClusterStages];
   __shared__ float red_f[kClusterThreads / 32];
   __shared__ double red_d[kClusterThreads / 32];
-  __shared__ float slot_max;   // read by peers over DSMEM
-  __shared__ double slot_sum;  // read by peers over DSMEM
+  __shared__ float slot_max[2][16];   // [row parity][sender rank], pushed by peers
+  __shared__ double slot_sum[2][16];
+  __shared__ uint64_t xbar_max[2], xbar_sum[2];  // exchange barriers per row parity
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = kClusterThreads / 32;
@@ -99,9 +113,14 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
 
   if (tid == 0) {
     for (int s = 0; s < kClusterStages; ++s) mbar_init(&bars[s], 1);
+    for (int p = 0; p < 2; ++p) {
+      mbar_init(&xbar_max[p], 1);
+      mbar_init(&xbar_sum[p], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
+  cluster_sync_all();  // peers' exchange barriers are initialised before any push
   pdl_wait();
   pdl_launch_dependents();
   if (tid == 0)
@@ -128,14 +147,18 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     mt = group_max<32>(mt);
     if (lane == 0) red_f[warp] = mt;
     __syncthreads();
-    if (tid == 0) {
-      float m = red_f[0];
-      for (int w = 1; w < NW; ++w) m = fmaxf(m, red_f[w]);
-      slot_max = m;
+    const int par = k & 1;
+    const uint32_t xpar = (k >> 1) & 1;  // phase of this parity's barrier
+    if (tid == 0) mbar_arrive_expect_tx(&xbar_max[par], cs * 4u);
+    if (warp == 0) {
+      float m = lane < NW ? red_f[lane] : kPadLogit;
+      m = group_max<32>(m);
+      if (lane < static_cast<int>(cs))  // push to rank `lane`
+        st_async_f32(dsmem_addr(&slot_max[par][rank], lane), m,
+                     dsmem_addr(&xbar_max[par], lane));
     }
-    cluster_sync_all();  // (A) every slice's max is published
-    // lane j of every warp reads rank j's slot: one DSMEM round trip, then shuffles
-    float M = lane < static_cast<int>(cs) ? ld_dsmem_f32(dsmem_addr(&slot_max, lane)) : kPadLogit;
+    mbar_wait(&xbar_max[par], xpar);
+    float M = lane < static_cast<int>(cs) ? slot_max[par][lane] : kPadLogit;
     M = group_max<32>(M) * shift_scale;  // shift_scale = 0: fault hook
 
     // ---- e = exp(clip(x - M)) in place (reference order), local sum -> exchange
@@ -151,13 +174,16 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     const double sd = group_sum<32>(static_cast<double>(acc2.x + acc2.y));
     if (lane == 0) red_d[warp] = sd;
     __syncthreads();
-    if (tid == 0) {
-      double s = red_d[0];
-      for (int w = 1; w < NW; ++w) s += red_d[w];
-      slot_sum = s;
+    if (tid == 0) mbar_arrive_expect_tx(&xbar_sum[par], cs * 8u);
+    if (warp == 0) {
+      double t = lane < NW ? red_d[lane] : 0.0;
+      t = group_sum<32>(t);
+      if (lane < static_cast<int>(cs))
+        st_async_f64(dsmem_addr(&slot_sum[par][rank], lane), t,
+                     dsmem_addr(&xbar_sum[par], lane));
     }
-    cluster_sync_all();  // (B) every slice's sum is published; all maxes were read
-    double S = lane < static_cast<int>(cs) ? ld_dsmem_f64(dsmem_addr(&slot_sum, lane)) : 0.0;
+    mbar_wait(&xbar_sum[par], xpar);
+    double S = lane < static_cast<int>(cs) ? slot_sum[par][lane] : 0.0;
     S = group_sum<32>(S);  // same butterfly in every CTA: identical S cluster-wide
     const float rcp = recip_of_sum(S);
 
@@ -178,7 +204,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
       }
     }
   }
-  // peers may still read our slots (loop (B) of the last row): keep the CTA alive
+  // no CTA leaves while a peer's push into it may still be in flight
   cluster_sync_all();
 }
 
