@@ -149,9 +149,10 @@ void sk_free_pinned(void* p);
  *   "k3_impl"        long rows: 3 (default) warp-task queue with L2 re-read,
  *                    0 CTA-task queue, 1 smem-resident cooperative, 2 one launch
  *                    per L2-sized row chunk, 4 register-resident warp tasks
- *   "cluster_k3"     1 (default): rows of 8193..262144 floats are held in one
- *                    thread-block cluster (<= 16 CTAs x 64 KB slices, DSMEM exchange);
- *                    0: use "k3_impl"
+ *   "cluster_k3"     1 (default): rows of 8193..~450K floats are held in one
+ *                    thread-block cluster (2..16 CTAs, 2-3 stage smem ring per CTA,
+ *                    DSMEM push exchange); 0: use "k3_impl"
+ *   "cluster_size"   force the K3c cluster size (0 = auto: most SMs covered)
  *   "claim_batch"    K3 warp queue: 0 (default) static round-robin tasks on a
  *                    cooperative grid, n > 0 tasks claimed n per atomic
  *   "k1_pf", "pdl"   K1 register prefetch (-1 table default), PDL on launches (1)

@@ -93,7 +93,8 @@ std::atomic<int> g_chunk_mb{24};  // K3 row-chunk size (MB of input) kept L2 res
 std::atomic<int> g_chunk_mb_set{0};  // chunk_mb explicitly tuned (overrides the K3 warp lag)
 std::atomic<int> g_chunk_occ_div{2};
 std::atomic<int> g_claim_batch{0};
-std::atomic<int> g_cluster_k3{1};    // use the cluster-resident K3 when a row fits   // K3 warp queue: tasks per atomic claim (0 = static)  // K3 grid = SMs*occupancy/div: two launches co-reside
+std::atomic<int> g_cluster_k3{1};    // use the cluster-resident K3 when a row fits
+std::atomic<int> g_cluster_size{0};  // force a K3c cluster size (0 = auto)   // K3 warp queue: tasks per atomic claim (0 = static)  // K3 grid = SMs*occupancy/div: two launches co-reside
 std::atomic<int> g_k3_impl{3};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
 
 // Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.
@@ -200,7 +201,8 @@ const void* cluster_fn(int mode) {
     default: return reinterpret_cast<const void*>(&k3_cluster<kApprox>);
   }
 }
-constexpr int64_t kClusterSliceMax = 16384;  // floats per CTA slice (64 KB x 3 stages)
+constexpr int64_t kClusterSmemMax = 220 * 1024;  // ring bytes per CTA (227 KB minus statics)
+constexpr int64_t kClusterSliceMaxAny = kClusterSmemMax / (2 * 4);  // 2-stage ring
 
 // Clusters of `cs` CTAs that can be co-resident (0 if the shape cannot launch).
 int max_active_clusters(const void* fn, int cs, size_t smem) {
@@ -308,7 +310,7 @@ struct Plan {
   // K1
   const K1Entry* k1 = nullptr;
   // seg (K2: nseg == 1; K3: nseg > 1)
-  int nseg = 1, seglen = 0, threads = 0;
+  int nseg = 1, seglen = 0, threads = 0, lag = 0;
   int k3 = 0;  // 0 none/K2, 1 dyn, 2 smem, 3 chunk
   int64_t chunk_rows = 0;
   size_t smem = 0;
@@ -383,21 +385,37 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     const int impl0 = g_k3_impl.load();
     // K3c: the row resident in one thread-block cluster (default when it fits)
     if (cols > kSegCap && (impl0 == 5 || impl0 == 3) && g_cluster_k3.load() &&
-        cols <= 16 * kClusterSliceMax) {
-      int cs = 2;
-      while (cs < 16 && (cols + cs - 1) / cs > kClusterSliceMax) cs *= 2;
-      const int64_t slice = align_up((cols + cs - 1) / cs, 4);
-      const size_t smem = size_t(kClusterStages) * slice * sizeof(float);
+        cols <= 16 * kClusterSliceMaxAny) {
+      // pick the cluster size that keeps the most SMs busy (GPC packing), with a
+      // ring of >= 2 stages of the row slice in shared memory
       const void* fn = cluster_fn(mode);
-      const int ncl = max_active_clusters(fn, cs, smem);
-      if (ncl > 0) {
+      int best_cs = 0, best_st = 0, best_n = 0;
+      int64_t best_slice = 0;
+      for (int cs = 16; cs >= 2; --cs) {
+        if (g_cluster_size.load() > 0 && cs != g_cluster_size.load()) continue;
+        const int64_t slice = align_up((cols + cs - 1) / cs, 4);
+        if ((cs - 1) * slice >= cols) continue;  // every rank needs a non-empty slice
+        const int st = static_cast<int>(std::min<int64_t>(
+            kClusterStages, kClusterSmemMax / (slice * int64_t(sizeof(float)))));
+        if (st < 2) continue;
+        const size_t smem = size_t(st) * slice * sizeof(float);
+        const int n = max_active_clusters(fn, cs, smem);
+        if (n * cs > best_n * best_cs || (n * cs == best_n * best_cs && st > best_st)) {
+          best_cs = cs;
+          best_st = st;
+          best_n = n;
+          best_slice = slice;
+        }
+      }
+      if (best_n > 0) {
         p.kind = kPathSeg;
         p.k3 = 6;
-        p.nseg = cs;
-        p.seglen = static_cast<int>(slice);
+        p.nseg = best_cs;
+        p.seglen = static_cast<int>(best_slice);
+        p.lag = best_st;
         p.threads = kClusterThreads;
-        p.smem = smem;
-        p.grid = int64_t(ncl) * cs;
+        p.smem = size_t(best_st) * best_slice * sizeof(float);
+        p.grid = int64_t(best_n) * best_cs;
         return SK_OK;
       }
       if (impl0 == 5) return arg_fail("cluster K3 cannot launch on this device");
@@ -621,10 +639,10 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
       }
       cfg.attrs = a;
       cfg.numAttrs = na;
-      int slice = p.seglen;
+      int slice = p.seglen, nst = p.lag;
       float shv = sh;
       void* args[] = {(void*)&x, (void*)&y, (void*)&rows, (void*)&cols, (void*)&ldx,
-                      (void*)&ldy, (void*)&slice, (void*)&bad, (void*)&shv};
+                      (void*)&ldy, (void*)&slice, (void*)&nst, (void*)&bad, (void*)&shv};
       SK_CUDA(cudaLaunchKernelExC(&cfg, cluster_fn(mode), args));
     } else if (p.k3 == 5) {
       const void* fn = p.seglen == 2048 ? reg3_fn<16>(mode)
@@ -799,6 +817,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "host_chunk_kb") g_host_chunk_kb = value;
   else if (k == "host_zero_copy") g_host_zero_copy = value;
   else if (k == "cluster_k3") g_cluster_k3 = value;
+  else if (k == "cluster_size") g_cluster_size = value;
   else if (k == "k3_impl") g_k3_impl = value;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;
@@ -831,7 +850,7 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
     snprintf(buf, buflen, "k1 vec=%d lpr=%d nv=%d u=%d pf=%d threads=%d grid=%lld", p.k1->vec,
              p.k1->lpr, p.k1->nv, p.k1->u, p.k1->pf, kRowsThreads, (long long)p.grid);
   else if (p.kind == kPathSeg)
-    snprintf(buf, buflen, "%s nseg=%d seglen=%d threads=%d smem=%zu chunk_rows=%lld grid=%lld",
+    snprintf(buf, buflen, "%s nseg=%d seglen=%d threads=%d smem=%zu chunk_rows=%lld stages=%d grid=%lld",
              p.nseg == 1 ? "k2_tma"
                          : (p.k3 == 1   ? "k3_dyn"
                             : p.k3 == 3 ? "k3_chunk"
@@ -840,7 +859,7 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
                             : p.k3 == 6 ? "k3_cluster"
                                         : "k3_smem"),
              p.nseg, p.seglen,
-             p.threads, p.smem, (long long)p.chunk_rows, (long long)p.grid);
+             p.threads, p.smem, (long long)p.chunk_rows, p.lag, (long long)p.grid);
   else
     snprintf(buf, buflen, "k4_split vec=%d nch=%d grid=%lld", p.vec ? 4 : 1, p.nch,
              (long long)p.grid);

@@ -1,6 +1,7 @@
 // sk_cluster.cuh -- K3c: a long row resident in one thread-block CLUSTER.
 //
-// A cluster of CS CTAs (CS = 16, one CTA per SM) owns a row at a time; CTA
+// A cluster of CS CTAs (one per SM; CS chosen by the launcher to cover the most
+// SMs given the GPC layout) owns a row at a time; CTA
 // `rank` holds columns [rank*L, (rank+1)*L) of it in shared memory.  Per row:
 //
 //   1. the slice lands in smem by cp.async.bulk (1-D TMA) on an mbarrier; the
@@ -30,7 +31,7 @@
 namespace sk {
 
 constexpr int kClusterThreads = 512;
-constexpr int kClusterStages = 3;
+constexpr int kClusterStages = 3;  // maximum ring depth (runtime nstages <= this)
 
 __device__ __forceinline__ unsigned cluster_rank() {
   unsigned r;
@@ -84,8 +85,8 @@ __device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t 
 template <int MODE>
 __global__ void __launch_bounds__(kClusterThreads, 1)
     k3_cluster(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
-               int64_t ldx, int64_t ldy, int slice, unsigned long long* __restrict__ bad_row,
-               float shift_scale) {
+               int64_t ldx, int64_t ldy, int slice, int nstages,
+               unsigned long long* __restrict__ bad_row, float shift_scale) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage_buf = reinterpret_cast<float*>(smem_raw);
   __shared__ uint64_t bars[kClusterStages];
@@ -112,7 +113,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   };
 
   if (tid == 0) {
-    for (int s = 0; s < kClusterStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < nstages; ++s) mbar_init(&bars[s], 1);
     for (int p = 0; p < 2; ++p) {
       mbar_init(&xbar_max[p], 1);
       mbar_init(&xbar_sum[p], 1);
@@ -124,15 +125,15 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   pdl_wait();
   pdl_launch_dependents();
   if (tid == 0)
-    for (int s = 0; s < kClusterStages; ++s) {
+    for (int s = 0; s < nstages; ++s) {
       const int64_t row = cid + int64_t(s) * ncl;
       if (row < rows) issue(row, s);
     }
 
   int k = 0;
   for (int64_t row = cid; row < rows; row += ncl, ++k) {
-    const int stage = k % kClusterStages;
-    mbar_wait(&bars[stage], (k / kClusterStages) & 1);
+    const int stage = k % nstages;
+    mbar_wait(&bars[stage], (k / nstages) & 1);
     float4* sb = reinterpret_cast<float4*>(stage_buf + size_t(stage) * slice);
 
     // ---- local max + finite check -> DSMEM exchange -> row max
@@ -197,7 +198,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     }
     __syncthreads();  // stage fully consumed
     if (tid == 0) {
-      const int64_t rn = row + int64_t(kClusterStages) * ncl;
+      const int64_t rn = row + int64_t(nstages) * ncl;
       if (rn < rows) {
         fence_proxy_async_smem();
         issue(rn, stage);

@@ -111,6 +111,13 @@ def main():
         _native.set_tuning("pdl", 0)
         record("default pdl=0", bench_once(xs, ys, rows, cols, args.reps, s))
         _native.set_tuning("pdl", 1)
+        for csz in (16, 14, 12, 10, 9, 8):
+            _native.set_tuning("cluster_size", csz)
+            try:
+                record(f"cluster size {csz}", bench_once(xs, ys, rows, cols, args.reps, s))
+            except Exception as e:  # noqa: BLE001
+                print(json.dumps({"variant": f"cluster {csz}", "error": str(e)}))
+        _native.set_tuning("cluster_size", 0)
         _native.set_tuning("cluster_k3", 0)
         record("k3_warp (cluster off)", bench_once(xs, ys, rows, cols, args.reps, s))
         _native.set_tuning("pdl", 0)
