@@ -400,7 +400,13 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
         if (st < 2) continue;
         const size_t smem = size_t(st) * slice * sizeof(float);
         const int n = max_active_clusters(fn, cs, smem);
-        if (n * cs > best_n * best_cs || (n * cs == best_n * best_cs && st > best_st)) {
+        // throughput model: SMs covered x per-row efficiency, where each row
+        // step costs ~8192 floats' worth of time in its two exchanges
+        const double score = double(n) * cs * double(slice) / double(slice + 8192);
+        const double best = best_n > 0 ? double(best_n) * best_cs * double(best_slice) /
+                                             double(best_slice + 8192)
+                                       : 0.0;
+        if (n > 0 && score > best) {
           best_cs = cs;
           best_st = st;
           best_n = n;
