@@ -65,8 +65,13 @@ def main():
     p.add_argument("--reps", type=int, default=200)
     p.add_argument("--seg-lens", default="1024,2048,4096")
     p.add_argument("--grid-mults", default="1,2")
+    p.add_argument("--shape", default="", help="RxC: synthetic N(0,4^2) matrix instead of a config")
     args = p.parse_args()
-    spec = configs.get(args.config)
+    if args.shape:
+        r, c = map(int, args.shape.lower().split("x"))
+        spec = configs.InputSpec(f"shape{r}x{c}", r, c, "normal", 11, sigma=4.0)
+    else:
+        spec = configs.get(args.config)
     x_host = configs.generate(spec)
     dev = torch.device("cuda", 0)
     pair = 8 * spec.rows * spec.cols
@@ -88,7 +93,12 @@ def main():
         out.append(d)
 
     record("default", bench_once(xs, ys, rows, cols, args.reps, s))
-    if cols <= 1024:
+    if 1024 < cols <= 8192:
+        for path in (2,):
+            _native.set_tuning("path", path)
+            record(f"path={path}", bench_once(xs, ys, rows, cols, args.reps, s))
+        _native.set_tuning("path", -1)
+    elif cols <= 1024:
         _native.set_tuning("pdl", 0)
         record("default pdl=0", bench_once(xs, ys, rows, cols, args.reps, s))
         _native.set_tuning("pdl", 1)
