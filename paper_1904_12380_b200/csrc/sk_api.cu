@@ -391,7 +391,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
       const void* fn = cluster_fn(mode);
       int best_cs = 0, best_st = 0, best_n = 0;
       int64_t best_slice = 0;
-      for (int cs = 16; cs >= 2; --cs) {
+      for (int cs = 16; cs >= 1; --cs) {
         if (g_cluster_size.load() > 0 && cs != g_cluster_size.load()) continue;
         const int64_t slice = align_up((cols + cs - 1) / cs, 4);
         if ((cs - 1) * slice >= cols) continue;  // every rank needs a non-empty slice
