@@ -857,7 +857,8 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
              p.k1->lpr, p.k1->nv, p.k1->u, p.k1->pf, kRowsThreads, (long long)p.grid);
   else if (p.kind == kPathSeg)
     snprintf(buf, buflen, "%s nseg=%d seglen=%d threads=%d smem=%zu chunk_rows=%lld stages=%d grid=%lld",
-             p.nseg == 1 ? "k2_tma"
+             p.k3 == 6 ? "k3_cluster"
+             : p.nseg == 1 ? "k2_tma"
                          : (p.k3 == 1   ? "k3_dyn"
                             : p.k3 == 3 ? "k3_chunk"
                             : p.k3 == 4 ? "k3_warp"
