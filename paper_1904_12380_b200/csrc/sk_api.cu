@@ -94,7 +94,8 @@ std::atomic<int> g_chunk_mb_set{0};  // chunk_mb explicitly tuned (overrides the
 std::atomic<int> g_chunk_occ_div{2};
 std::atomic<int> g_claim_batch{0};
 std::atomic<int> g_cluster_k3{1};    // use the cluster-resident K3 when a row fits
-std::atomic<int> g_cluster_size{0};  // force a K3c cluster size (0 = auto)   // K3 warp queue: tasks per atomic claim (0 = static)  // K3 grid = SMs*occupancy/div: two launches co-reside
+std::atomic<int> g_cluster_size{0};  // force a K3c cluster size (0 = auto)
+std::atomic<int> g_vec8{1};          // 256-bit K1 path when rows are 32-B aligned   // K3 warp queue: tasks per atomic claim (0 = static)  // K3 grid = SMs*occupancy/div: two launches co-reside
 std::atomic<int> g_k3_impl{3};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
 
 // Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.
@@ -145,6 +146,10 @@ const K1Entry kK1Table[] = {
     SK_K1(4, 32, 4, 1, 0), SK_K1(4, 32, 8, 1, 0), SK_K1(4, 32, 1, 2, 0), SK_K1(4, 32, 2, 1, 0),
     SK_K1(4, 8, 4, 1, 1), SK_K1(4, 16, 2, 1, 1), SK_K1(4, 16, 4, 1, 1), SK_K1(4, 32, 2, 1, 1),
     SK_K1(4, 32, 4, 1, 1), SK_K1(4, 32, 8, 1, 1), SK_K1(4, 16, 1, 4, 1), SK_K1(4, 8, 1, 4, 1),
+    // 256-bit path (cols % 8 == 0, 32-B aligned rows)
+    SK_K1(8, 8, 1, 4, 0), SK_K1(8, 16, 1, 2, 0), SK_K1(8, 16, 1, 4, 0), SK_K1(8, 8, 2, 1, 0),
+    SK_K1(8, 8, 2, 2, 0), SK_K1(8, 16, 2, 1, 0), SK_K1(8, 32, 1, 1, 0), SK_K1(8, 32, 1, 2, 0),
+    SK_K1(8, 32, 2, 1, 0), SK_K1(8, 32, 4, 1, 0), SK_K1(8, 16, 1, 1, 0),
     // 32-bit path (any pitch / alignment)
     SK_K1(1, 8, 1, 4, 0), SK_K1(1, 16, 1, 4, 0), SK_K1(1, 32, 1, 4, 0), SK_K1(1, 16, 4, 2, 0),
     SK_K1(1, 32, 2, 2, 0), SK_K1(1, 32, 4, 1, 0), SK_K1(1, 32, 8, 1, 0), SK_K1(1, 32, 16, 1, 0),
@@ -163,7 +168,13 @@ const K1Entry* k1_find(int vec, int lpr, int nv, int u, int pf) {
 void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u, int& pf, int& gm) {
   pf = 0;
   gm = 1;
-  if (vec == 4) {
+  if (vec == 8) {
+    if (cols <= 64) { lpr = 8; nv = 1; u = 4; }
+    else if (cols <= 128) { lpr = 16; nv = 1; u = 2; gm = 2; }
+    else if (cols <= 256) { lpr = 16; nv = 2; u = 1; gm = 4; }
+    else if (cols <= 512) { lpr = 32; nv = 2; u = 1; gm = 2; }
+    else { lpr = 32; nv = 4; u = 1; gm = 2; }
+  } else if (vec == 4) {
     if (cols <= 16) { lpr = 4; nv = 1; u = 4; }
     else if (cols <= 32) { lpr = 8; nv = 1; u = 4; }
     else if (cols <= 64) { lpr = 16; nv = 1; u = 4; }
@@ -353,6 +364,8 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
   const DevInfo di = dev_info(dev);
   const bool vec = (cols % 4 == 0) && (ldx % 4 == 0) && (ldy % 4 == 0) && (xa % 16 == 0) &&
                    (ya % 16 == 0);
+  const bool vec8 = vec && (cols % 8 == 0) && (ldx % 8 == 0) && (ldy % 8 == 0) &&
+                    (xa % 32 == 0) && (ya % 32 == 0) && g_vec8.load();
   p.vec = vec;
   const int force = g_force_path.load();
   PathKind kind;
@@ -365,11 +378,12 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
 
   if (kind == kPathK1) {
     int lpr, nv, u, pf, gm;
-    k1_default(vec ? 4 : 1, cols, lpr, nv, u, pf, gm);
+    const int vw = vec8 ? 8 : vec ? 4 : 1;
+    k1_default(vw, cols, lpr, nv, u, pf, gm);
     if (g_k1_lpr.load() > 0) { lpr = g_k1_lpr; nv = g_k1_nv; u = g_k1_u; }
     if (g_k1_pf.load() >= 0) pf = g_k1_pf.load();
     if (g_grid_mult.load() > 0) gm = g_grid_mult.load();
-    const K1Entry* e = k1_find(vec ? 4 : 1, lpr, nv, u, pf);
+    const K1Entry* e = k1_find(vw, lpr, nv, u, pf);
     if (!e) return arg_fail("no K1 instantiation for the requested shape");
     if (int64_t(lpr) * nv * e->vec < cols) return arg_fail("K1 shape does not cover cols");
     p.kind = kPathK1;
@@ -824,6 +838,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "host_zero_copy") g_host_zero_copy = value;
   else if (k == "cluster_k3") g_cluster_k3 = value;
   else if (k == "cluster_size") g_cluster_size = value;
+  else if (k == "vec8") g_vec8 = value;
   else if (k == "k3_impl") g_k3_impl = value;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;

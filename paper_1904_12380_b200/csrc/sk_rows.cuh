@@ -42,7 +42,12 @@ __device__ __forceinline__ void k1_load(RowBatch<VEC, LPR, NV, U>& B, const floa
     for (int j = 0; j < NV; ++j) {
       const int c = (j * LPR + sl) * VEC;
       if (rv && c < cols) {
-        if constexpr (VEC == 4) {
+        if constexpr (VEC == 8) {
+          float t[8];
+          ld_stream8(xr + c, t);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) B.v[u][8 * j + k] = t[k];
+        } else if constexpr (VEC == 4) {
           const float4 t = ld_stream4(xr + c);
           B.v[u][4 * j] = t.x; B.v[u][4 * j + 1] = t.y;
           B.v[u][4 * j + 2] = t.z; B.v[u][4 * j + 3] = t.w;
@@ -125,7 +130,17 @@ __device__ __forceinline__ void k1_process(RowBatch<VEC, LPR, NV, U>& B, float* 
     for (int j = 0; j < NV; ++j) {
       const int c = (j * LPR + sl) * VEC;
       if (FULL || c < cols) {
-        if constexpr (VEC == 4) {
+        if constexpr (VEC == 8) {
+          float o[8];
+#pragma unroll
+          for (int k = 0; k < 8; k += 2) {
+            const float2 a = scale2<MODE>(make_float2(B.v[u][8 * j + k], B.v[u][8 * j + k + 1]),
+                                          rcp[u]);
+            o[k] = a.x;
+            o[k + 1] = a.y;
+          }
+          st_stream8(yr + c, o);
+        } else if constexpr (VEC == 4) {
           const float2 a = scale2<MODE>(make_float2(B.v[u][4 * j], B.v[u][4 * j + 1]), rcp[u]);
           const float2 b =
               scale2<MODE>(make_float2(B.v[u][4 * j + 2], B.v[u][4 * j + 3]), rcp[u]);
@@ -168,7 +183,7 @@ __global__ void __launch_bounds__(kRowsThreads, (k1_min_blocks<VEC, NV, U, PF>()
     k1_rows(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int cols,
             int64_t ldx, int64_t ldy, unsigned long long* __restrict__ bad_row,
             float shift_scale) {
-  static_assert(VEC == 1 || VEC == 4, "VEC");
+  static_assert(VEC == 1 || VEC == 4 || VEC == 8, "VEC");
   static_assert(LPR >= 1 && LPR <= 32 && (LPR & (LPR - 1)) == 0, "LPR");
   constexpr int ROWS_ITER = U * (32 / LPR);
   const int lane = threadIdx.x & 31;

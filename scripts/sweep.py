@@ -22,10 +22,12 @@ import torch  # noqa: E402
 from paper_1904_12380_b200 import _native, configs  # noqa: E402
 
 K1_SHAPES = {
-    # (lpr, nv, u, pf) -- vec=4 entries instantiated in sk_api.cu
-    "c2": [(8, 4, 1, 0), (16, 2, 1, 0), (8, 4, 1, 1), (16, 2, 1, 1), (16, 1, 4, 1), (8, 1, 4, 1)],
-    "c5a": [(16, 4, 1, 0), (16, 4, 1, 1), (32, 2, 1, 1), (32, 2, 2, 0)],
-    "c3": [(32, 8, 1, 0), (32, 8, 1, 1)],
+    # (vec, lpr, nv, u, pf) -- entries instantiated in sk_api.cu
+    "c2": [(4, 8, 4, 1, 0), (4, 16, 2, 1, 0), (8, 16, 1, 2, 0), (8, 16, 1, 4, 0), (8, 8, 2, 1, 0),
+           (8, 8, 2, 2, 0), (8, 16, 1, 1, 0)],
+    "c5a": [(4, 16, 4, 1, 0), (4, 16, 4, 1, 1), (8, 16, 2, 1, 0), (8, 32, 1, 1, 0),
+            (8, 32, 1, 2, 0)],
+    "c3": [(4, 32, 8, 1, 0), (8, 32, 4, 1, 0)],
 }
 
 
@@ -102,7 +104,8 @@ def main():
         _native.set_tuning("pdl", 0)
         record("default pdl=0", bench_once(xs, ys, rows, cols, args.reps, s))
         _native.set_tuning("pdl", 1)
-        for lpr, nv, u, pf in K1_SHAPES.get(spec.name, []):
+        for vw, lpr, nv, u, pf in K1_SHAPES.get(spec.name, []):
+            _native.set_tuning("vec8", 1 if vw == 8 else 0)
             for gm in map(int, args.grid_mults.split(",")):
                 _native.set_tuning("k1_lpr", lpr)
                 _native.set_tuning("k1_nv", nv)
@@ -110,10 +113,11 @@ def main():
                 _native.set_tuning("k1_pf", pf)
                 _native.set_tuning("grid_mult", gm)
                 try:
-                    record(f"k1 lpr={lpr} nv={nv} u={u} pf={pf} gm={gm}",
+                    record(f"k1 vec={vw} lpr={lpr} nv={nv} u={u} pf={pf} gm={gm}",
                            bench_once(xs, ys, rows, cols, args.reps, s))
                 except Exception as e:  # noqa: BLE001
                     print(json.dumps({"variant": f"{lpr},{nv},{u},{pf}", "error": str(e)}))
+        _native.set_tuning("vec8", 1)
         _native.set_tuning("k1_lpr", 0)
         _native.set_tuning("k1_pf", -1)
         _native.set_tuning("grid_mult", 0)
