@@ -141,8 +141,8 @@ void sk_free_pinned(void* p);
  *                    segments (K2/K3), 2 force split (K4)
  *   "k1_lpr","k1_nv","k1_u"  force a K1 instantiation (lanes per row,
  *                    float4s per lane, rows per lane-group batch)
- *   "vec8"           1 (default): K1 uses 256-bit loads/stores when cols % 8 == 0
- *                    and rows are 32-B aligned; 0: 128-bit
+ *   "vec8"           1: K1 uses 256-bit loads/stores when cols % 8 == 0 and rows
+ *                    are 32-B aligned (measured no faster than 128-bit; default 0)
  *   "grid_mult"      K1 grid = SMs * occupancy * grid_mult (default 1)
  *   "seg_len"        target segment length (floats) for K2/K3
  *   "chunk_mb"       K3 re-read distance / row-chunk size in MB (default 24)

@@ -95,7 +95,7 @@ std::atomic<int> g_chunk_occ_div{2};
 std::atomic<int> g_claim_batch{0};
 std::atomic<int> g_cluster_k3{1};    // use the cluster-resident K3 when a row fits
 std::atomic<int> g_cluster_size{0};  // force a K3c cluster size (0 = auto)
-std::atomic<int> g_vec8{1};          // 256-bit K1 path when rows are 32-B aligned   // K3 warp queue: tasks per atomic claim (0 = static)  // K3 grid = SMs*occupancy/div: two launches co-reside
+std::atomic<int> g_vec8{0};          // 256-bit K1 path (measured no faster: off by default)   // K3 warp queue: tasks per atomic claim (0 = static)  // K3 grid = SMs*occupancy/div: two launches co-reside
 std::atomic<int> g_k3_impl{3};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
 
 // Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.
@@ -178,8 +178,8 @@ void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u, int& pf, int& 
     if (cols <= 16) { lpr = 4; nv = 1; u = 4; }
     else if (cols <= 32) { lpr = 8; nv = 1; u = 4; }
     else if (cols <= 64) { lpr = 16; nv = 1; u = 4; }
-    else if (cols <= 128) { lpr = 8; nv = 4; u = 1; gm = 2; }
-    else if (cols <= 256) { lpr = 16; nv = 4; u = 1; gm = 4; }
+    else if (cols <= 128) { lpr = 8; nv = 4; u = 1; gm = 4; }
+    else if (cols <= 256) { lpr = 16; nv = 4; u = 1; pf = 1; }
     else if (cols <= 512) { lpr = 32; nv = 4; u = 1; gm = 2; }
     else { lpr = 32; nv = 8; u = 1; gm = 2; }
   } else {

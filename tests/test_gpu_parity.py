@@ -151,12 +151,21 @@ def test_every_path_on_same_input(path, oracle):
 def test_k1_instantiations_all_agree(oracle):
     x = configs.generate("c2", 0, 999)
     ref = oracle.softmax_ref(x)
-    for lpr, nv, u in ((8, 4, 1), (8, 4, 2), (16, 2, 2), (16, 4, 1), (32, 1, 4), (32, 4, 1)):
-        _native.set_tuning("k1_lpr", lpr)
-        _native.set_tuning("k1_nv", nv)
-        _native.set_tuning("k1_u", u)
-        y, _ = gu.softmax_abi(x, 0)
-        assert_parity(oracle, y, ref, what=(lpr, nv, u))
+    shapes = ((4, 8, 4, 1), (4, 8, 4, 2), (4, 16, 2, 2), (4, 16, 4, 1), (4, 32, 1, 4),
+              (4, 32, 4, 1), (8, 16, 1, 2), (8, 8, 2, 1), (8, 32, 1, 1))
+    try:
+        for vec, lpr, nv, u in shapes:
+            _native.set_tuning("vec8", 1 if vec == 8 else 0)
+            _native.set_tuning("k1_lpr", lpr)
+            _native.set_tuning("k1_nv", nv)
+            _native.set_tuning("k1_u", u)
+            for pf in (0, 1) if (vec, lpr, nv, u) == (4, 8, 4, 1) else (0,):
+                _native.set_tuning("k1_pf", pf)
+                y, _ = gu.softmax_abi(x, 0)
+                assert_parity(oracle, y, ref, what=(vec, lpr, nv, u, pf))
+    finally:
+        _native.set_tuning("vec8", 0)
+        _native.set_tuning("k1_pf", -1)
 
 
 @pytest.mark.parametrize("impl", [0, 1, 2, 3, "3b", 4, 5])
