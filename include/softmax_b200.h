@@ -180,6 +180,13 @@ int sk_set_tuning(const char* key, int value);
 int sk_exp_accuracy(int mode, float lo, float hi, double* max_ulp, double* max_rel, int device);
 
 /*
+ * Diagnostic streaming copy y[0, n) = x[0, n) (n % 4 == 0, 16-B aligned) with
+ * the softmax kernels' load/store hints and PDL: the same-run floor for a kernel
+ * that moves 8 B/element (bound_probe.py:67-87 analogue).  blocks <= 0: auto.
+ */
+int sk_copy_f32(const float* x, float* y, int64_t n, int blocks, void* stream);
+
+/*
  * Launch plan that sk_softmax_f32 would use for this shape/alignment, as a
  * short text ("k1_vec lpr=8 nv=4 u=2 grid=..." ...), for tests and bench logs.
  * Writes at most buflen bytes (NUL-terminated); returns SK_OK.

@@ -64,6 +64,7 @@ SIGNATURES: dict[str, tuple] = {
     "sk_alloc_pinned": (c_void_p, [c_size_t]),
     "sk_free_pinned": (None, [c_void_p]),
     "sk_set_tuning": (c_int, [c_char_p, c_int]),
+    "sk_copy_f32": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p]),
     "sk_exp_accuracy": (c_int, [c_int, c_float, c_float, POINTER(c_double), POINTER(c_double), c_int]),
     "sk_describe_plan": (
         c_int, [c_int64, c_int64, c_int64, c_int64, c_uint64, c_uint64, c_int, c_char_p, c_int]

@@ -85,3 +85,52 @@ extern "C" int sk_exp_accuracy(int mode, float lo, float hi, double* max_ulp, do
   std::memcpy(max_rel, &h2[1], 8);
   return SK_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Diagnostic streaming copy with the softmax kernels' access pattern
+// (128-bit no-allocate loads, streaming stores, PDL): the same-run floor for a
+// kernel that moves 8 B/element, used by scripts/sweep.py and the bound probe.
+namespace sk {
+namespace {
+__global__ void __launch_bounds__(256) k_copy4(const float4* __restrict__ x, float4* __restrict__ y,
+                                               int64_t n4) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n4; i += 4 * stride) {
+    const float4 a = ld_stream4(reinterpret_cast<const float*>(x + i));
+    const float4 b = ld_stream4(reinterpret_cast<const float*>(x + i + stride));
+    const float4 c = ld_stream4(reinterpret_cast<const float*>(x + i + 2 * stride));
+    const float4 d = ld_stream4(reinterpret_cast<const float*>(x + i + 3 * stride));
+    st_stream4(reinterpret_cast<float*>(y + i), a);
+    st_stream4(reinterpret_cast<float*>(y + i + stride), b);
+    st_stream4(reinterpret_cast<float*>(y + i + 2 * stride), c);
+    st_stream4(reinterpret_cast<float*>(y + i + 3 * stride), d);
+  }
+  for (; i < n4; i += stride)
+    st_stream4(reinterpret_cast<float*>(y + i), ld_stream4(reinterpret_cast<const float*>(x + i)));
+}
+}  // namespace
+}  // namespace sk
+
+extern "C" int sk_copy_f32(const float* x, float* y, int64_t n, int blocks, void* stream) {
+  if (n < 0 || (n % 4) || (n > 0 && (!x || !y)) ||
+      (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) % 16)
+    return SK_ERR_ARGUMENT;
+  if (n == 0) return SK_OK;
+  const int64_t n4 = n / 4;
+  int64_t g = blocks > 0 ? blocks : (n4 + 1023) / 1024;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(g < 1 ? 1 : g));
+  cfg.blockDim = dim3(256);
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = 1;
+  const float4* xs = reinterpret_cast<const float4*>(x);
+  float4* ys = reinterpret_cast<float4*>(y);
+  return cudaLaunchKernelEx(&cfg, sk::k_copy4, xs, ys, n4) == cudaSuccess ? SK_OK : SK_ERR_CUDA;
+}

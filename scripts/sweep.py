@@ -160,6 +160,33 @@ def main():
         _native.set_tuning("path", 2)
         record("split(k4)", bench_once(xs, ys, rows, cols, max(10, args.reps // 4), s))
         _native.set_tuning("path", -1)
+    # our own streaming copy kernel of the same bytes, several grid sizes
+    L = _native.lib()
+    for blocks in (0, 592, 1184, 2368, 4736):
+        def launch_copy(i, blocks=blocks):
+            _native.check(L.sk_copy_f32(xs[i % R].data_ptr(), ys[i % R].data_ptr(), rows * cols,
+                                        blocks, s.cuda_stream))
+        with torch.cuda.stream(s):
+            for i in range(10):
+                launch_copy(i)
+            g = torch.cuda.CUDAGraph()
+            G = R * max(1, 32 // R)
+            with torch.cuda.graph(g, stream=s):
+                for i in range(G):
+                    launch_copy(i)
+            g.replay()
+            s.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            n = max(1, args.reps // G)
+            e0.record(s)
+            for _ in range(n):
+                g.replay()
+            e1.record(s)
+        s.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / (n * G)
+        print(json.dumps({"config": spec.name, "variant": f"sk_copy blocks={blocks}", "us": us,
+                          "gbs": 8.0 * rows * cols / us / 1e3}), flush=True)
     # copy roofline in the same run: D2D copy of the same bytes (bound_probe analog)
     a = xs[0]
     b = ys[0]
