@@ -143,7 +143,8 @@ void sk_free_pinned(void* p);
  *                    float4s per lane, rows per lane-group batch)
  *   "vec8"           1: K1 uses 256-bit loads/stores when cols % 8 == 0 and rows
  *                    are 32-B aligned (measured no faster than 128-bit; default 0)
- *   "grid_mult"      K1 grid = SMs * occupancy * grid_mult (default 1)
+ *   "grid_mult"      K1 grid = SMs * occupancy * grid_mult (default: one row batch
+ *                    per warp, i.e. no grid-stride loop)
  *   "seg_len"        target segment length (floats) for K2/K3
  *   "chunk_mb"       K3 re-read distance / row-chunk size in MB (default 24)
  *   "chunk_occ_div"  K3 grid = SMs * occupancy / div (default 2: consecutive

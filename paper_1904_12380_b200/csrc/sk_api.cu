@@ -163,25 +163,26 @@ const K1Entry* k1_find(int vec, int lpr, int nv, int u, int pf) {
   return nullptr;
 }
 
-// default K1 shape per row length (covers cols <= 1024); grid multiplier:
-// 0 = persistent (SMs x occupancy), m > 0 = m x that many CTAs (waves).
+// default K1 shape per row length (covers cols <= 1024).  gm: grid multiplier
+// over SMs x occupancy; 0 = non-persistent (one row batch per warp, grid = rows /
+// rows-per-CTA), which measured fastest for every shape (c5a: 7.0 TB/s).
 void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u, int& pf, int& gm) {
   pf = 0;
-  gm = 1;
+  gm = 0;
   if (vec == 8) {
     if (cols <= 64) { lpr = 8; nv = 1; u = 4; }
-    else if (cols <= 128) { lpr = 16; nv = 1; u = 2; gm = 2; }
-    else if (cols <= 256) { lpr = 16; nv = 2; u = 1; gm = 4; }
-    else if (cols <= 512) { lpr = 32; nv = 2; u = 1; gm = 2; }
-    else { lpr = 32; nv = 4; u = 1; gm = 2; }
+    else if (cols <= 128) { lpr = 16; nv = 1; u = 2; }
+    else if (cols <= 256) { lpr = 16; nv = 2; u = 1; }
+    else if (cols <= 512) { lpr = 32; nv = 2; u = 1; }
+    else { lpr = 32; nv = 4; u = 1; }
   } else if (vec == 4) {
     if (cols <= 16) { lpr = 4; nv = 1; u = 4; }
     else if (cols <= 32) { lpr = 8; nv = 1; u = 4; }
     else if (cols <= 64) { lpr = 16; nv = 1; u = 4; }
-    else if (cols <= 128) { lpr = 8; nv = 4; u = 1; gm = 4; }
-    else if (cols <= 256) { lpr = 16; nv = 4; u = 1; pf = 1; }
-    else if (cols <= 512) { lpr = 32; nv = 4; u = 1; gm = 2; }
-    else { lpr = 32; nv = 8; u = 1; gm = 2; }
+    else if (cols <= 128) { lpr = 8; nv = 4; u = 1; }
+    else if (cols <= 256) { lpr = 16; nv = 4; u = 2; }
+    else if (cols <= 512) { lpr = 32; nv = 4; u = 1; }
+    else { lpr = 32; nv = 8; u = 1; }
   } else {
     if (cols <= 8) { lpr = 8; nv = 1; u = 4; }
     else if (cols <= 16) { lpr = 16; nv = 1; u = 4; }
@@ -391,8 +392,8 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     const int64_t rows_per_cta = int64_t(kRowsThreads / 32) * u * (32 / lpr);
     const int64_t need = (rows + rows_per_cta - 1) / rows_per_cta;
     const int occ = occupancy(reinterpret_cast<const void*>(e->fn[mode]), kRowsThreads, 0);
-    const int64_t cap = int64_t(di.sms) * std::max(occ, 1) * gm;
-    p.grid = std::max<int64_t>(1, std::min(need, cap));
+    const int64_t cap = gm > 0 ? int64_t(di.sms) * std::max(occ, 1) * gm : need;
+    p.grid = std::max<int64_t>(1, std::min({need, cap, int64_t(INT32_MAX)}));
     return SK_OK;
   }
   if (kind == kPathSeg) {

@@ -23,11 +23,11 @@ from paper_1904_12380_b200 import _native, configs  # noqa: E402
 
 K1_SHAPES = {
     # (vec, lpr, nv, u, pf) -- entries instantiated in sk_api.cu
-    "c2": [(4, 8, 4, 1, 0), (4, 16, 2, 1, 0), (8, 16, 1, 2, 0), (8, 16, 1, 4, 0), (8, 8, 2, 1, 0),
-           (8, 8, 2, 2, 0), (8, 16, 1, 1, 0)],
+    "c2": [(4, 8, 4, 1, 0), (4, 16, 2, 1, 0), (4, 8, 4, 2, 0), (4, 16, 2, 2, 0), (8, 8, 2, 1, 0)],
     "c5a": [(4, 16, 4, 1, 0), (4, 16, 4, 1, 1), (4, 16, 4, 2, 0), (4, 32, 2, 1, 0),
             (4, 32, 2, 2, 0), (8, 16, 2, 1, 0)],
     "c3": [(4, 32, 8, 1, 0), (8, 32, 4, 1, 0)],
+    "c1": [(1, 16, 4, 2, 0), (1, 16, 4, 1, 1), (1, 32, 2, 2, 0)],
 }
 
 
