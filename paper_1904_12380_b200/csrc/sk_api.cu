@@ -187,7 +187,7 @@ void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u, int& pf, int& 
     if (cols <= 8) { lpr = 8; nv = 1; u = 4; }
     else if (cols <= 16) { lpr = 16; nv = 1; u = 4; }
     else if (cols <= 32) { lpr = 32; nv = 1; u = 4; }
-    else if (cols <= 64) { lpr = 16; nv = 4; u = 2; }
+    else if (cols <= 64) { lpr = 16; nv = 4; u = 1; pf = 1; }
     else if (cols <= 128) { lpr = 32; nv = 4; u = 1; }
     else if (cols <= 256) { lpr = 32; nv = 8; u = 1; }
     else if (cols <= 512) { lpr = 32; nv = 16; u = 1; }
