@@ -206,11 +206,19 @@ SegFn seg_fn(int mode) {
     default: return &k_seg<kApprox, NV>;
   }
 }
+std::atomic<int> g_cluster_onex{1};  // K3c: one (m, s) exchange per row
 const void* cluster_fn(int mode) {
+  const bool one = g_cluster_onex.load() != 0;
   switch (mode) {
-    case kClipAccurate: return reinterpret_cast<const void*>(&k3_cluster<kClipAccurate>);
-    case kAccurate: return reinterpret_cast<const void*>(&k3_cluster<kAccurate>);
-    default: return reinterpret_cast<const void*>(&k3_cluster<kApprox>);
+    case kClipAccurate:
+      return one ? reinterpret_cast<const void*>(&k3_cluster<kClipAccurate, true>)
+                 : reinterpret_cast<const void*>(&k3_cluster<kClipAccurate, false>);
+    case kAccurate:
+      return one ? reinterpret_cast<const void*>(&k3_cluster<kAccurate, true>)
+                 : reinterpret_cast<const void*>(&k3_cluster<kAccurate, false>);
+    default:
+      return one ? reinterpret_cast<const void*>(&k3_cluster<kApprox, true>)
+                 : reinterpret_cast<const void*>(&k3_cluster<kApprox, false>);
   }
 }
 constexpr int64_t kClusterSmemMax = 220 * 1024;  // ring bytes per CTA (227 KB minus statics)
@@ -840,6 +848,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "cluster_k3") g_cluster_k3 = value;
   else if (k == "cluster_size") g_cluster_size = value;
   else if (k == "vec8") g_vec8 = value;
+  else if (k == "cluster_onex") g_cluster_onex = value;
   else if (k == "k3_impl") g_k3_impl = value;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;

@@ -82,7 +82,12 @@ __device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t 
                ::"r"(raddr), "d"(v), "r"(rbar) : "memory");
 }
 
-template <int MODE>
+// ONEX = true: one exchange per row -- each CTA reduces its slice to
+// (m_l, s_l = sum exp(clip(x - m_l))) locally and pushes the pair once; every
+// CTA merges M = max m_j, S = sum s_j exp(m_j - M) (fixed order) and the output
+// pass recomputes exp(clip(x - M)) from the untouched slice (reference order).
+// Trades one exp per element for one fewer cluster round trip per row.
+template <int MODE, bool ONEX>
 __global__ void __launch_bounds__(kClusterThreads, 1)
     k3_cluster(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
                int64_t ldx, int64_t ldy, int slice, int nstages,
@@ -94,6 +99,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   __shared__ double red_d[kClusterThreads / 32];
   __shared__ float slot_max[2][16];   // [row parity][sender rank], pushed by peers
   __shared__ double slot_sum[2][16];
+  __shared__ float bc_m;
   __shared__ uint64_t xbar_max[2], xbar_sum[2];  // exchange barriers per row parity
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -150,50 +156,85 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     __syncthreads();
     const int par = k & 1;
     const uint32_t xpar = (k >> 1) & 1;  // phase of this parity's barrier
-    if (tid == 0) mbar_arrive_expect_tx(&xbar_max[par], cs * 4u);
-    if (warp == 0) {
-      float m = lane < NW ? red_f[lane] : kPadLogit;
-      m = group_max<32>(m);
-      if (lane < static_cast<int>(cs))  // push to rank `lane`
-        st_async_f32(dsmem_addr(&slot_max[par][rank], lane), m,
-                     dsmem_addr(&xbar_max[par], lane));
+    float M;
+    if constexpr (ONEX) {
+      if (tid == 0) {
+        float m = red_f[0];
+        for (int w = 1; w < NW; ++w) m = fmaxf(m, red_f[w]);
+        bc_m = m * shift_scale;  // shift_scale = 0: fault hook
+      }
+      __syncthreads();
+      M = bc_m;  // local max of this slice for now
+    } else {
+      if (tid == 0) mbar_arrive_expect_tx(&xbar_max[par], cs * 4u);
+      if (warp == 0) {
+        float m = lane < NW ? red_f[lane] : kPadLogit;
+        m = group_max<32>(m);
+        if (lane < static_cast<int>(cs))  // push to rank `lane`
+          st_async_f32(dsmem_addr(&slot_max[par][rank], lane), m,
+                       dsmem_addr(&xbar_max[par], lane));
+      }
+      mbar_wait(&xbar_max[par], xpar);
+      M = lane < static_cast<int>(cs) ? slot_max[par][lane] : kPadLogit;
+      M = group_max<32>(M) * shift_scale;  // shift_scale = 0: fault hook
     }
-    mbar_wait(&xbar_max[par], xpar);
-    float M = lane < static_cast<int>(cs) ? slot_max[par][lane] : kPadLogit;
-    M = group_max<32>(M) * shift_scale;  // shift_scale = 0: fault hook
 
-    // ---- e = exp(clip(x - M)) in place (reference order), local sum -> exchange
+    // ---- e = exp(clip(x - M)) (in place unless ONEX), local sum -> exchange
     u64 acc = f2pk(0.0f, 0.0f);
     for (int q = tid; q < nvec; q += kClusterThreads) {
       const float4 v = sb[q];
       const float2 a = sexp2<MODE>(v.x, v.y, M);
       const float2 b = sexp2<MODE>(v.z, v.w, M);
-      sb[q] = make_float4(a.x, a.y, b.x, b.y);
+      if constexpr (!ONEX) sb[q] = make_float4(a.x, a.y, b.x, b.y);
       acc = f2add(f2add(acc, f2pk(a.x, a.y)), f2pk(b.x, b.y));
     }
     const float2 acc2 = f2up(acc);
     const double sd = group_sum<32>(static_cast<double>(acc2.x + acc2.y));
     if (lane == 0) red_d[warp] = sd;
     __syncthreads();
-    if (tid == 0) mbar_arrive_expect_tx(&xbar_sum[par], cs * 8u);
+    if (tid == 0) {
+      if (ONEX) mbar_arrive_expect_tx(&xbar_max[par], cs * 4u);
+      mbar_arrive_expect_tx(&xbar_sum[par], cs * 8u);
+    }
     if (warp == 0) {
       double t = lane < NW ? red_d[lane] : 0.0;
       t = group_sum<32>(t);
-      if (lane < static_cast<int>(cs))
+      if (lane < static_cast<int>(cs)) {
+        if (ONEX)
+          st_async_f32(dsmem_addr(&slot_max[par][rank], lane), M,
+                       dsmem_addr(&xbar_max[par], lane));
         st_async_f64(dsmem_addr(&slot_sum[par][rank], lane), t,
                      dsmem_addr(&xbar_sum[par], lane));
+      }
     }
+    if (ONEX) mbar_wait(&xbar_max[par], xpar);
     mbar_wait(&xbar_sum[par], xpar);
-    double S = lane < static_cast<int>(cs) ? slot_sum[par][lane] : 0.0;
-    S = group_sum<32>(S);  // same butterfly in every CTA: identical S cluster-wide
+    double S;
+    if constexpr (ONEX) {
+      const float mj = lane < static_cast<int>(cs) ? slot_max[par][lane] : kPadLogit;
+      const float Mg = group_max<32>(mj);
+      double sj = lane < static_cast<int>(cs) ? slot_sum[par][lane] : 0.0;
+      if (lane < static_cast<int>(cs) && mj != Mg) sj *= static_cast<double>(expf(mj - Mg));
+      S = group_sum<32>(sj);  // same butterfly in every CTA: identical S cluster-wide
+      M = Mg;
+    } else {
+      S = lane < static_cast<int>(cs) ? slot_sum[par][lane] : 0.0;
+      S = group_sum<32>(S);  // same butterfly in every CTA: identical S cluster-wide
+    }
     const float rcp = recip_of_sum(S);
 
     // ---- y = e * r, streaming stores
     float* yr = y + row * ldy + c0;
     for (int q = tid; q < nvec; q += kClusterThreads) {
       const float4 e = sb[q];
-      const float2 a = scale2<MODE>(make_float2(e.x, e.y), rcp);
-      const float2 b = scale2<MODE>(make_float2(e.z, e.w), rcp);
+      float2 a, b;
+      if constexpr (ONEX) {
+        a = scale2<MODE>(sexp2<MODE>(e.x, e.y, M), rcp);
+        b = scale2<MODE>(sexp2<MODE>(e.z, e.w, M), rcp);
+      } else {
+        a = scale2<MODE>(make_float2(e.x, e.y), rcp);
+        b = scale2<MODE>(make_float2(e.z, e.w), rcp);
+      }
       st_stream4(yr + 4 * q, make_float4(a.x, a.y, b.x, b.y));
     }
     __syncthreads();  // stage fully consumed

@@ -168,7 +168,7 @@ def test_k1_instantiations_all_agree(oracle):
         _native.set_tuning("k1_pf", -1)
 
 
-@pytest.mark.parametrize("impl", [0, 1, 2, 3, "3b", 4, 5])
+@pytest.mark.parametrize("impl", [0, 1, 2, 3, "3b", 4, 5, "5x2"])
 def test_every_k3_implementation(impl, oracle):
     """Long-row kernels: ordered CTA queue (0), smem-resident cooperative (1),
     per-chunk launches (2), ordered warp queue (3) -- all against the oracle,
@@ -179,6 +179,9 @@ def test_every_k3_implementation(impl, oracle):
     if impl == "3b":  # warp queue with batched atomic claims instead of static tasks
         impl = 3
         _native.set_tuning("claim_batch", 4)
+    if impl == "5x2":  # cluster kernel with the two-exchange schedule
+        impl = 5
+        _native.set_tuning("cluster_onex", 0)
     _native.set_tuning("cluster_k3", 1 if impl == 5 else 0)
     _native.set_tuning("k3_impl", impl)
     try:
@@ -189,6 +192,7 @@ def test_every_k3_implementation(impl, oracle):
             assert_parity(oracle, y, ref, what=(impl, mb, gu.plan(*x.shape)))
     finally:
         _native.set_tuning("claim_batch", 0)
+        _native.set_tuning("cluster_onex", 1)
         _native.set_tuning("cluster_k3", 1)
         _native.set_tuning("k3_impl", 3)
         _native.set_tuning("chunk_mb", 0)
