@@ -156,8 +156,8 @@ void sk_free_pinned(void* p);
  *                    thread-block cluster (2..16 CTAs, 2-3 stage smem ring per CTA,
  *                    DSMEM push exchange); 0: use "k3_impl"
  *   "cluster_size"   force the K3c cluster size (0 = auto: most SMs covered)
- *   "cluster_onex"   1 (default): K3c exchanges one (max, sum) pair per row and
- *                    recomputes exp; 0: two exchanges (max, then sum), exp kept in smem
+ *   "cluster_onex"   1: K3c exchanges one (max, sum) pair per row and recomputes
+ *                    exp; 0 (default): two exchanges (max, then sum), exp kept in smem
  *   "claim_batch"    K3 warp queue: 0 (default) static round-robin tasks on a
  *                    cooperative grid, n > 0 tasks claimed n per atomic
  *   "k1_pf", "pdl"   K1 register prefetch (-1 table default), PDL on launches (1)

@@ -206,7 +206,7 @@ SegFn seg_fn(int mode) {
     default: return &k_seg<kApprox, NV>;
   }
 }
-std::atomic<int> g_cluster_onex{1};  // K3c: one (m, s) exchange per row
+std::atomic<int> g_cluster_onex{0};  // K3c: one (m, s) exchange per row (measured slower)
 const void* cluster_fn(int mode) {
   const bool one = g_cluster_onex.load() != 0;
   switch (mode) {

@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     // ---- local max + finite check -> DSMEM exchange -> row max
     float mt = kPadLogit;
     u64 z = f2pk(0.0f, 0.0f);
+#pragma unroll 4
     for (int q = tid; q < nvec; q += kClusterThreads) {
       const float4 v = sb[q];
       mt = fmaxf(mt, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
@@ -181,6 +182,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
 
     // ---- e = exp(clip(x - M)) (in place unless ONEX), local sum -> exchange
     u64 acc = f2pk(0.0f, 0.0f);
+#pragma unroll 4
     for (int q = tid; q < nvec; q += kClusterThreads) {
       const float4 v = sb[q];
       const float2 a = sexp2<MODE>(v.x, v.y, M);
@@ -225,6 +227,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
 
     // ---- y = e * r, streaming stores
     float* yr = y + row * ldy + c0;
+#pragma unroll 4
     for (int q = tid; q < nvec; q += kClusterThreads) {
       const float4 e = sb[q];
       float2 a, b;
