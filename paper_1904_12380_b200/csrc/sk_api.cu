@@ -207,20 +207,27 @@ SegFn seg_fn(int mode) {
   }
 }
 std::atomic<int> g_cluster_onex{0};  // K3c: one (m, s) exchange per row (measured slower)
-const void* cluster_fn(int mode) {
-  const bool one = g_cluster_onex.load() != 0;
+std::atomic<int> g_cluster_tpb{512};  // K3c threads per CTA (512 or 1024)
+template <int TPB>
+const void* cluster_fn_t(int mode, bool one) {
   switch (mode) {
     case kClipAccurate:
-      return one ? reinterpret_cast<const void*>(&k3_cluster<kClipAccurate, true>)
-                 : reinterpret_cast<const void*>(&k3_cluster<kClipAccurate, false>);
+      return one ? reinterpret_cast<const void*>(&k3_cluster<kClipAccurate, true, TPB>)
+                 : reinterpret_cast<const void*>(&k3_cluster<kClipAccurate, false, TPB>);
     case kAccurate:
-      return one ? reinterpret_cast<const void*>(&k3_cluster<kAccurate, true>)
-                 : reinterpret_cast<const void*>(&k3_cluster<kAccurate, false>);
+      return one ? reinterpret_cast<const void*>(&k3_cluster<kAccurate, true, TPB>)
+                 : reinterpret_cast<const void*>(&k3_cluster<kAccurate, false, TPB>);
     default:
-      return one ? reinterpret_cast<const void*>(&k3_cluster<kApprox, true>)
-                 : reinterpret_cast<const void*>(&k3_cluster<kApprox, false>);
+      return one ? reinterpret_cast<const void*>(&k3_cluster<kApprox, true, TPB>)
+                 : reinterpret_cast<const void*>(&k3_cluster<kApprox, false, TPB>);
   }
 }
+const void* cluster_fn(int mode) {
+  const bool one = g_cluster_onex.load() != 0;
+  return g_cluster_tpb.load() == 1024 ? cluster_fn_t<1024>(mode, one)
+                                      : cluster_fn_t<512>(mode, one);
+}
+int cluster_tpb() { return g_cluster_tpb.load() == 1024 ? 1024 : 512; }
 constexpr int64_t kClusterSmemMax = 220 * 1024;  // ring bytes per CTA (227 KB minus statics)
 constexpr int64_t kClusterSliceMaxAny = kClusterSmemMax / (2 * 4);  // 2-stage ring
 
@@ -240,7 +247,7 @@ int max_active_clusters(const void* fn, int cs, size_t smem) {
   ensure_smem_attr(fn, smem);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs * 148);
-  cfg.blockDim = dim3(kClusterThreads);
+  cfg.blockDim = dim3(cluster_tpb());
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute a[1];
   a[0].id = cudaLaunchAttributeClusterDimension;
@@ -442,7 +449,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
         p.nseg = best_cs;
         p.seglen = static_cast<int>(best_slice);
         p.lag = best_st;
-        p.threads = kClusterThreads;
+        p.threads = cluster_tpb();
         p.smem = size_t(best_st) * best_slice * sizeof(float);
         p.grid = int64_t(best_n) * best_cs;
         return SK_OK;
@@ -849,6 +856,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "cluster_size") g_cluster_size = value;
   else if (k == "vec8") g_vec8 = value;
   else if (k == "cluster_onex") g_cluster_onex = value;
+  else if (k == "cluster_tpb") g_cluster_tpb = value;
   else if (k == "k3_impl") g_k3_impl = value;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;

@@ -87,23 +87,23 @@ __device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t 
 // CTA merges M = max m_j, S = sum s_j exp(m_j - M) (fixed order) and the output
 // pass recomputes exp(clip(x - M)) from the untouched slice (reference order).
 // Trades one exp per element for one fewer cluster round trip per row.
-template <int MODE, bool ONEX>
-__global__ void __launch_bounds__(kClusterThreads, 1)
+template <int MODE, bool ONEX, int TPB = kClusterThreads>
+__global__ void __launch_bounds__(TPB, 1)
     k3_cluster(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
                int64_t ldx, int64_t ldy, int slice, int nstages,
                unsigned long long* __restrict__ bad_row, float shift_scale) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage_buf = reinterpret_cast<float*>(smem_raw);
   __shared__ uint64_t bars[kClusterStages];
-  __shared__ float red_f[kClusterThreads / 32];
-  __shared__ double red_d[kClusterThreads / 32];
+  __shared__ float red_f[TPB / 32];
+  __shared__ double red_d[TPB / 32];
   __shared__ float slot_max[2][16];   // [row parity][sender rank], pushed by peers
   __shared__ double slot_sum[2][16];
   __shared__ float bc_m;
   __shared__ uint64_t xbar_max[2], xbar_sum[2];  // exchange barriers per row parity
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = kClusterThreads / 32;
+  constexpr int NW = TPB / 32;
   const unsigned rank = cluster_rank(), cs = cluster_nrank();
   const int64_t cid = cluster_id_x(), ncl = ncluster_x();
   const int64_t c0 = int64_t(rank) * slice;
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     float mt = kPadLogit;
     u64 z = f2pk(0.0f, 0.0f);
 #pragma unroll 4
-    for (int q = tid; q < nvec; q += kClusterThreads) {
+    for (int q = tid; q < nvec; q += TPB) {
       const float4 v = sb[q];
       mt = fmaxf(mt, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
       z = nf_acc2(nf_acc2(z, v.x, v.y), v.z, v.w);
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     // ---- e = exp(clip(x - M)) (in place unless ONEX), local sum -> exchange
     u64 acc = f2pk(0.0f, 0.0f);
 #pragma unroll 4
-    for (int q = tid; q < nvec; q += kClusterThreads) {
+    for (int q = tid; q < nvec; q += TPB) {
       const float4 v = sb[q];
       const float2 a = sexp2<MODE>(v.x, v.y, M);
       const float2 b = sexp2<MODE>(v.z, v.w, M);
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     // ---- y = e * r, streaming stores
     float* yr = y + row * ldy + c0;
 #pragma unroll 4
-    for (int q = tid; q < nvec; q += kClusterThreads) {
+    for (int q = tid; q < nvec; q += TPB) {
       const float4 e = sb[q];
       float2 a, b;
       if constexpr (ONEX) {

@@ -125,9 +125,12 @@ def main():
         _native.set_tuning("pdl", 0)
         record("default pdl=0", bench_once(xs, ys, rows, cols, args.reps, s))
         _native.set_tuning("pdl", 1)
-        _native.set_tuning("cluster_onex", 0)
-        record("cluster two exchanges", bench_once(xs, ys, rows, cols, args.reps, s))
         _native.set_tuning("cluster_onex", 1)
+        record("cluster one exchange", bench_once(xs, ys, rows, cols, args.reps, s))
+        _native.set_tuning("cluster_onex", 0)
+        _native.set_tuning("cluster_tpb", 1024)
+        record("cluster 1024 threads", bench_once(xs, ys, rows, cols, args.reps, s))
+        _native.set_tuning("cluster_tpb", 512)
         for csz in (16, 14, 12, 10, 9, 8):
             _native.set_tuning("cluster_size", csz)
             try:
