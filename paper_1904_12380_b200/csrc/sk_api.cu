@@ -595,9 +595,15 @@ int launch_split(const float* x, float* y, int64_t rows, int64_t cols, int64_t l
   double* rsum = rsum_out ? rsum_out : reinterpret_cast<double*>(ws + l.rsum);
   const dim3 g(static_cast<unsigned>(rows * nch));
   const float sh = shift_scale();
-  const void* stats = mode == kClipAccurate ? reinterpret_cast<const void*>(&k4_stats<kClipAccurate>)
-                      : mode == kAccurate   ? reinterpret_cast<const void*>(&k4_stats<kAccurate>)
-                                            : reinterpret_cast<const void*>(&k4_stats<kApprox>);
+  const bool sv4 = (cols % 4 == 0) && (ldx % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+  const void* stats =
+      mode == kClipAccurate
+          ? (sv4 ? reinterpret_cast<const void*>(&k4_stats<kClipAccurate, 4>)
+                 : reinterpret_cast<const void*>(&k4_stats<kClipAccurate, 1>))
+      : mode == kAccurate ? (sv4 ? reinterpret_cast<const void*>(&k4_stats<kAccurate, 4>)
+                                 : reinterpret_cast<const void*>(&k4_stats<kAccurate, 1>))
+                          : (sv4 ? reinterpret_cast<const void*>(&k4_stats<kApprox, 4>)
+                                 : reinterpret_cast<const void*>(&k4_stats<kApprox, 1>));
   SK_CUDA(launch_k(stats, g, dim3(kSplitThreads), 0, s, false, x, rows, cols, ldx, nch, part,
                    bad, sh));
   SK_CUDA(launch_k(reinterpret_cast<const void*>(&k4_combine),

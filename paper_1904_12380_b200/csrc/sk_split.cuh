@@ -52,7 +52,7 @@ __device__ __forceinline__ double block_sum_256(double v, double* red) {
   return r;
 }
 
-template <int MODE>
+template <int MODE, int VEC>
 __global__ void __launch_bounds__(kSplitThreads)
     k4_stats(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx, int nch,
              RowPartial* __restrict__ partials, unsigned long long* __restrict__ bad_row,
@@ -69,13 +69,32 @@ __global__ void __launch_bounds__(kSplitThreads)
   const int64_t rem = cols - c0;
   const int len = static_cast<int>(rem < kSplitChunk ? rem : kSplitChunk);
   float v[kSplitPerThread];
+  // element i of this thread sits at column col(i): strided scalars, or
+  // 128-bit vectors (thread-strided) when VEC == 4
+  auto col = [&](int i) {
+    return VEC == 4 ? 4 * (static_cast<int>(threadIdx.x) + (i / 4) * kSplitThreads) + (i % 4)
+                    : static_cast<int>(threadIdx.x) + i * kSplitThreads;
+  };
+  if constexpr (VEC == 4) {
+#pragma unroll
+    for (int i = 0; i < kSplitPerThread; i += 4) {
+      const int c = col(i);
+      if (c < len) {
+        const float4 t = ld_stream4(xr + c);
+        v[i] = t.x; v[i + 1] = t.y; v[i + 2] = t.z; v[i + 3] = t.w;
+      } else {
+        v[i] = v[i + 1] = v[i + 2] = v[i + 3] = kPadLogit;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kSplitPerThread; ++i) {
+      const int c = col(i);
+      v[i] = c < len ? ld_stream1(xr + c) : kPadLogit;
+    }
+  }
   float mt = kPadLogit;
   u64 z = f2pk(0.0f, 0.0f);
-#pragma unroll
-  for (int i = 0; i < kSplitPerThread; ++i) {
-    const int c = threadIdx.x + i * kSplitThreads;
-    v[i] = c < len ? ld_stream1(xr + c) : kPadLogit;
-  }
 #pragma unroll
   for (int i = 0; i < kSplitPerThread; i += 2) {
     mt = fmaxf(mt, fmaxf(v[i], v[i + 1]));
@@ -87,8 +106,8 @@ __global__ void __launch_bounds__(kSplitThreads)
 #pragma unroll
   for (int i = 0; i < kSplitPerThread; i += 2) {
     float2 e = sexp2<MODE>(v[i], v[i + 1], m);
-    if (!(static_cast<int>(threadIdx.x) + i * kSplitThreads < len)) e.x = 0.0f;
-    if (!(static_cast<int>(threadIdx.x) + (i + 1) * kSplitThreads < len)) e.y = 0.0f;
+    if (!(col(i) < len)) e.x = 0.0f;
+    if (!(col(i + 1) < len)) e.y = 0.0f;
     acc = f2add(acc, f2pk(e.x, e.y));
   }
   const float2 acc2 = f2up(acc);
