@@ -21,6 +21,7 @@
 #include "sk_warp3.cuh"
 #include "sk_reg3.cuh"
 #include "sk_cluster.cuh"
+#include "sk_gres.cuh"
 
 namespace sk {
 namespace {
@@ -96,6 +97,9 @@ std::atomic<int> g_claim_batch{0};
 std::atomic<int> g_cluster_k3{1};    // use the cluster-resident K3 when a row fits
 std::atomic<int> g_cluster_size{0};  // force a K3c cluster size (0 = auto)
 std::atomic<int> g_vec8{0};          // 256-bit K1 path (measured no faster: off by default)   // K3 warp queue: tasks per atomic claim (0 = static)  // K3 grid = SMs*occupancy/div: two launches co-reside
+std::atomic<int> g_gres{1};       // K3g grid-resident rows: 0 off, 1 when it out-scores K3c, 2 force
+std::atomic<int> g_gres_p{0};     // force K3g CTAs per row (0 = auto)
+std::atomic<int> g_gres_x{12288}; // K3g per-row exchange cost model, in floats of streaming time
 std::atomic<int> g_k3_impl{3};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
 
 // Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.
@@ -266,6 +270,14 @@ int max_active_clusters(const void* fn, int cs, size_t smem) {
   return n;
 }
 
+const void* gres_fn(int mode) {
+  switch (mode) {
+    case kClipAccurate: return reinterpret_cast<const void*>(&k3_gres<kClipAccurate>);
+    case kAccurate: return reinterpret_cast<const void*>(&k3_gres<kAccurate>);
+    default: return reinterpret_cast<const void*>(&k3_gres<kApprox>);
+  }
+}
+
 template <int NV>
 const void* reg3_fn(int mode) {
   switch (mode) {
@@ -413,48 +425,93 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
   }
   if (kind == kPathSeg) {
     const int impl0 = g_k3_impl.load();
-    // K3c: the row resident in one thread-block cluster (default when it fits)
-    if (cols > kSegCap && (impl0 == 5 || impl0 == 3) && g_cluster_k3.load() &&
-        cols <= 16 * kClusterSliceMaxAny) {
-      // pick the cluster size that keeps the most SMs busy (GPC packing), with a
-      // ring of >= 2 stages of the row slice in shared memory
-      const void* fn = cluster_fn(mode);
-      int best_cs = 0, best_st = 0, best_n = 0;
-      int64_t best_slice = 0;
-      for (int cs = 16; cs >= 1; --cs) {
-        if (g_cluster_size.load() > 0 && cs != g_cluster_size.load()) continue;
-        const int64_t slice = align_up((cols + cs - 1) / cs, 4);
-        if ((cs - 1) * slice >= cols) continue;  // every rank needs a non-empty slice
-        const int st = static_cast<int>(std::min<int64_t>(
-            kClusterStages, kClusterSmemMax / (slice * int64_t(sizeof(float)))));
-        if (st < 2) continue;
-        const size_t smem = size_t(st) * slice * sizeof(float);
-        const int n = max_active_clusters(fn, cs, smem);
-        // throughput model: SMs covered x per-row efficiency, where each row
-        // step costs ~8192 floats' worth of time in its two exchanges
-        const double score = double(n) * cs * double(slice) / double(slice + 8192);
-        const double best = best_n > 0 ? double(best_n) * best_cs * double(best_slice) /
-                                             double(best_slice + 8192)
-                                       : 0.0;
-        if (n > 0 && score > best) {
-          best_cs = cs;
-          best_st = st;
-          best_n = n;
-          best_slice = slice;
+    // Resident rows: K3c (one thread-block cluster per row) or K3g (P CTAs
+    // anywhere on the chip, global-memory exchange).  Each candidate is scored
+    // as SMs covered x per-row efficiency slice / (slice + exchange cost).
+    const int gres = g_gres.load();
+    if (cols > kSegCap && (impl0 == 5 || impl0 == 3)) {
+      double best_c = 0.0, best_g = 0.0;
+      int c_cs = 0, c_st = 0, c_n = 0;
+      int64_t c_slice = 0;
+      if (g_cluster_k3.load() && gres != 2 && cols <= 16 * kClusterSliceMaxAny) {
+        // K3c: the cluster size that keeps the most SMs busy (GPC packing), with
+        // a ring of >= 2 stages of the row slice in shared memory
+        const void* fn = cluster_fn(mode);
+        for (int cs = 16; cs >= 1; --cs) {
+          if (g_cluster_size.load() > 0 && cs != g_cluster_size.load()) continue;
+          const int64_t slice = align_up((cols + cs - 1) / cs, 4);
+          if ((cs - 1) * slice >= cols) continue;  // every rank needs a non-empty slice
+          const int st = static_cast<int>(std::min<int64_t>(
+              kClusterStages, kClusterSmemMax / (slice * int64_t(sizeof(float)))));
+          if (st < 2) continue;
+          const size_t smem = size_t(st) * slice * sizeof(float);
+          const int n = max_active_clusters(fn, cs, smem);
+          // each row step costs ~8192 floats' worth of time in its two exchanges
+          const double score = double(std::min<int64_t>(n, rows)) * cs * double(slice) /
+                               double(slice + 8192);
+          if (n > 0 && score > best_c) {
+            best_c = score;
+            c_cs = cs;
+            c_st = st;
+            c_n = n;
+            c_slice = slice;
+          }
         }
       }
-      if (best_n > 0) {
+      int g_p = 0, g_st = 0, g_groups = 0;
+      int64_t g_slice = 0;
+      if (gres != 0 && di.coop) {
+        const void* fn = gres_fn(mode);
+        const double xg = std::max(0, g_gres_x.load());
+        for (int P = 2; P <= di.sms; ++P) {
+          if (g_gres_p.load() > 0 && P != g_gres_p.load()) continue;
+          const int64_t slice = align_up((cols + P - 1) / P, 4);
+          if ((P - 1) * slice >= cols) continue;
+          const int st = static_cast<int>(std::min<int64_t>(
+              kGresStages, kClusterSmemMax / (slice * int64_t(sizeof(float)))));
+          if (st < 2) continue;
+          const size_t smem = size_t(st) * slice * sizeof(float);
+          const int occ = occupancy(fn, kGresThreads, smem);
+          if (occ < 1) continue;
+          const int groups = di.sms * occ / P;
+          if (groups < 1) continue;
+          const int64_t rows_g = (rows + groups - 1) / groups;  // exchange counter range
+          if (2 * rows_g * P >= (int64_t(1) << 31)) continue;
+          const double score = double(std::min<int64_t>(groups, rows)) * P / occ *
+                               double(slice) / (double(slice) + xg);
+          if (score > best_g) {
+            best_g = score;
+            g_p = P;
+            g_st = st;
+            g_groups = groups;
+            g_slice = slice;
+          }
+        }
+      }
+      if (g_p > 0 && (gres == 2 || best_g > best_c)) {
+        p.kind = kPathSeg;
+        p.k3 = 7;
+        p.nseg = g_p;
+        p.seglen = static_cast<int>(g_slice);
+        p.lag = g_st;
+        p.threads = kGresThreads;
+        p.smem = size_t(g_st) * g_slice * sizeof(float);
+        p.grid = int64_t(g_groups) * g_p;
+        return SK_OK;
+      }
+      if (c_n > 0) {
         p.kind = kPathSeg;
         p.k3 = 6;
-        p.nseg = best_cs;
-        p.seglen = static_cast<int>(best_slice);
-        p.lag = best_st;
+        p.nseg = c_cs;
+        p.seglen = static_cast<int>(c_slice);
+        p.lag = c_st;
         p.threads = cluster_tpb();
-        p.smem = size_t(best_st) * best_slice * sizeof(float);
-        p.grid = int64_t(best_n) * best_cs;
+        p.smem = size_t(c_st) * c_slice * sizeof(float);
+        p.grid = int64_t(c_n) * c_cs;
         return SK_OK;
       }
       if (impl0 == 5) return arg_fail("cluster K3 cannot launch on this device");
+      if (gres == 2) return arg_fail("K3g cannot launch this row length on this device");
     }
     const bool chunked = cols > kSegCap && impl0 != 1;
     const bool warp3 = cols > kSegCap && (impl0 == 3 || impl0 == 4);
@@ -541,8 +598,23 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
   return plan_split(rows, cols, p);
 }
 
+// K3g control block: abort flag | one 128-B counter line per group | max slots
+// [group][parity][P] | sum slots [group][parity][P]; [0, pmax) zeroed per launch.
+struct GresWs {
+  size_t abort = 256, cnt = 384, pmax = 0, psum = 0, total = 0;
+};
+GresWs gres_ws(const Plan& p) {
+  GresWs w;
+  const size_t groups = size_t(p.grid / p.nseg);
+  w.pmax = align_up(w.cnt + groups * 128, 256);
+  w.psum = align_up(w.pmax + groups * 2 * p.nseg * sizeof(float), 256);
+  w.total = align_up(w.psum + groups * 2 * p.nseg * sizeof(double), 256);
+  return w;
+}
+
 size_t plan_ws_bytes(const Plan& p, int64_t rows) {
   if (p.kind == kPathSeg && p.k3 == 6) return ws_layout(0, 0).total;
+  if (p.kind == kPathSeg && p.k3 == 7) return gres_ws(p).total;
   if (p.kind == kPathSeg && p.nseg > 1) return ws_layout(rows, p.nseg).total;
   if (p.kind == kPathSplit) return ws_layout(rows, p.nch).total;
   return ws_layout(0, 0).total;
@@ -646,7 +718,7 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
     const int nseg = p.nseg, seglen = p.seglen;
     // K3 row counters start at zero every launch (the workspace is shared by
     // launches of different shapes, so no state is assumed across launches).
-    if (nseg > 1 && p.k3 != 1 && p.k3 != 4 && p.k3 != 5 && p.k3 != 6) SK_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(unsigned), s));
+    if (nseg > 1 && p.k3 != 1 && p.k3 != 4 && p.k3 != 5 && p.k3 != 6 && p.k3 != 7) SK_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(unsigned), s));
     if (p.k3 == 3) {
       const void* fn = p.seglen <= kChunkThreads * 16 ? chunk_fn<4>(mode) : chunk_fn<8>(mode);
       float* rmax = reinterpret_cast<float*>(ws + l.rmax);
@@ -686,6 +758,15 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
       void* args[] = {(void*)&x, (void*)&y, (void*)&rows, (void*)&cols, (void*)&ldx,
                       (void*)&ldy, (void*)&slice, (void*)&nst, (void*)&bad, (void*)&shv};
       SK_CUDA(cudaLaunchKernelExC(&cfg, cluster_fn(mode), args));
+    } else if (p.k3 == 7) {
+      const GresWs w = gres_ws(p);
+      SK_CUDA(cudaMemsetAsync(ws + w.abort, 0, w.pmax - w.abort, s));
+      int P = p.nseg, slice = p.seglen, nst = p.lag;
+      SK_CUDA(launch_k(gres_fn(mode), dim3(static_cast<unsigned>(p.grid)), dim3(p.threads),
+                       p.smem, s, true, x, y, rows, cols, ldx, ldy, P, slice, nst,
+                       reinterpret_cast<unsigned*>(ws + w.cnt), reinterpret_cast<float*>(ws + w.pmax),
+                       reinterpret_cast<double*>(ws + w.psum), reinterpret_cast<unsigned*>(ws + w.abort),
+                       bad, sh));
     } else if (p.k3 == 5) {
       const void* fn = p.seglen == 2048 ? reg3_fn<16>(mode)
                        : p.seglen == 512 ? reg3_fn<4>(mode) : reg3_fn<8>(mode);
@@ -864,6 +945,9 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "cluster_onex") g_cluster_onex = value;
   else if (k == "cluster_tpb") g_cluster_tpb = value;
   else if (k == "k3_impl") g_k3_impl = value;
+  else if (k == "gres") g_gres = value;
+  else if (k == "gres_p") g_gres_p = value;
+  else if (k == "gres_x") g_gres_x = value;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;
 }
@@ -872,7 +956,8 @@ size_t sk_softmax_workspace_bytes(int64_t rows, int64_t cols) {
   if (rows <= 0 || cols <= 0) return ws_layout(0, 0).total;
   const int64_t nseg = (cols + 512 - 1) / 512;  // smallest K3 segment
   const int64_t nch = (cols + kSplitChunk - 1) / kSplitChunk;
-  return std::max(ws_layout(rows, nseg).total, ws_layout(rows, nch).total);
+  const size_t gres_max = size_t(128) << 10;  // K3g control block (<= 3 CTAs/SM x 148 SMs)
+  return std::max({ws_layout(rows, nseg).total, ws_layout(rows, nch).total, gres_max});
 }
 
 int sk_softmax_f32(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
@@ -897,6 +982,7 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
   else if (p.kind == kPathSeg)
     snprintf(buf, buflen, "%s nseg=%d seglen=%d threads=%d smem=%zu chunk_rows=%lld stages=%d grid=%lld",
              p.k3 == 6 ? "k3_cluster"
+             : p.k3 == 7 ? "k3_gres"
              : p.nseg == 1 ? "k2_tma"
                          : (p.k3 == 1   ? "k3_dyn"
                             : p.k3 == 3 ? "k3_chunk"

@@ -68,6 +68,10 @@ def main():
     p.add_argument("--seg-lens", default="1024,2048,4096")
     p.add_argument("--grid-mults", default="1,2")
     p.add_argument("--shape", default="", help="RxC: synthetic N(0,4^2) matrix instead of a config")
+    p.add_argument("--gres-ps", default="0,10,12,16,24,37,48,74",
+                   help="K3g CTAs per row to try (0 = planner's choice)")
+    p.add_argument("--only-resident", action="store_true",
+                   help="long rows: only the resident-row kernels (K3c / K3g) and split")
     args = p.parse_args()
     if args.shape:
         r, c = map(int, args.shape.lower().split("x"))
@@ -121,6 +125,24 @@ def main():
         _native.set_tuning("k1_lpr", 0)
         _native.set_tuning("k1_pf", -1)
         _native.set_tuning("grid_mult", 0)
+    elif args.only_resident:
+        _native.set_tuning("gres", 0)
+        try:
+            record("k3_cluster (gres off)", bench_once(xs, ys, rows, cols, args.reps, s))
+        except Exception as e:  # noqa: BLE001
+            print(json.dumps({"variant": "k3_cluster", "error": str(e)}))
+        _native.set_tuning("gres", 2)
+        for gp in map(int, args.gres_ps.split(",")):
+            _native.set_tuning("gres_p", gp)
+            try:
+                record(f"k3_gres P={gp or 'auto'}", bench_once(xs, ys, rows, cols, args.reps, s))
+            except Exception as e:  # noqa: BLE001
+                print(json.dumps({"variant": f"gres {gp}", "error": str(e)}))
+        _native.set_tuning("gres_p", 0)
+        _native.set_tuning("gres", 1)
+        _native.set_tuning("path", 2)
+        record("split(k4)", bench_once(xs, ys, rows, cols, max(10, args.reps // 4), s))
+        _native.set_tuning("path", -1)
     else:
         _native.set_tuning("pdl", 0)
         record("default pdl=0", bench_once(xs, ys, rows, cols, args.reps, s))

@@ -30,7 +30,8 @@ def assert_parity(oracle, y, ref, approx=False, what=""):
 def _reset_tuning():
     yield
     for k, v in (("path", -1), ("k1_lpr", 0), ("grid_mult", 0), ("seg_len", 0),
-                 ("skip_max_shift", 0), ("k3_impl", 3), ("cluster_k3", 1), ("chunk_mb", 0)):
+                 ("skip_max_shift", 0), ("k3_impl", 3), ("cluster_k3", 1), ("chunk_mb", 0),
+                 ("gres", 1), ("gres_p", 0), ("cluster_onex", 0)):
         _native.set_tuning(k, v)
 
 
@@ -168,7 +169,7 @@ def test_k1_instantiations_all_agree(oracle):
         _native.set_tuning("k1_pf", -1)
 
 
-@pytest.mark.parametrize("impl", [0, 1, 2, 3, "3b", 4, 5, "5x2"])
+@pytest.mark.parametrize("impl", [0, 1, 2, 3, "3b", 4, 5, "5x2", "g"])
 def test_every_k3_implementation(impl, oracle):
     """Long-row kernels: ordered CTA queue (0), smem-resident cooperative (1),
     per-chunk launches (2), ordered warp queue (3) -- all against the oracle,
@@ -179,9 +180,14 @@ def test_every_k3_implementation(impl, oracle):
     if impl == "3b":  # warp queue with batched atomic claims instead of static tasks
         impl = 3
         _native.set_tuning("claim_batch", 4)
-    if impl == "5x2":  # cluster kernel with the two-exchange schedule
+    if impl == "5x2":  # cluster kernel with the one-exchange schedule
         impl = 5
-        _native.set_tuning("cluster_onex", 0)
+        _native.set_tuning("cluster_onex", 1)
+    if impl == "g":  # grid-resident rows, global-memory exchange
+        impl = 3
+        _native.set_tuning("gres", 2)
+    else:
+        _native.set_tuning("gres", 0)
     _native.set_tuning("cluster_k3", 1 if impl == 5 else 0)
     _native.set_tuning("k3_impl", impl)
     try:
@@ -192,10 +198,54 @@ def test_every_k3_implementation(impl, oracle):
             assert_parity(oracle, y, ref, what=(impl, mb, gu.plan(*x.shape)))
     finally:
         _native.set_tuning("claim_batch", 0)
-        _native.set_tuning("cluster_onex", 1)
+        _native.set_tuning("cluster_onex", 0)
+        _native.set_tuning("gres", 1)
         _native.set_tuning("cluster_k3", 1)
         _native.set_tuning("k3_impl", 3)
         _native.set_tuning("chunk_mb", 0)
+
+
+@pytest.mark.parametrize("P", [2, 3, 10, 37, 74, 148])
+def test_k3_gres_group_sizes(P, oracle):
+    """K3g with P CTAs per row (ragged last slice, one- to many-group grids,
+    more groups than rows, clip firing, a large negative row), every mode."""
+    C = 200_004 if P >= 10 else 30_004
+    rows = 13
+    x = configs.generate("c4", 0, rows)[:, :C].copy()
+    x[3, 777] = -500.0
+    x[5, :] -= 400.0
+    _native.set_tuning("gres", 2)
+    _native.set_tuning("gres_p", P)
+    try:
+        assert gu.plan(rows, C).startswith("k3_gres nseg=%d " % P), gu.plan(rows, C)
+        for mode in (0, 1, 2):
+            ref = oracle.softmax_ref(x, clip=(mode == 0))
+            y, bad = gu.softmax_abi(x, mode)
+            assert bad == gu.NO_BAD
+            assert_parity(oracle, y, ref, approx=(mode == 2), what=(P, mode, gu.plan(rows, C)))
+        x2 = x.copy()
+        x2[9, C - 1] = np.inf
+        x2[7, 0] = np.nan
+        assert gu.softmax_abi(x2, 0)[1] == 7
+    finally:
+        _native.set_tuning("gres", 1)
+        _native.set_tuning("gres_p", 0)
+
+
+def test_k3_gres_full_c4_rowsums():
+    """K3g over all of c4 (1024 x 262144): every row sums to 1, determinism."""
+    t = gu.torch()
+    xd = t.from_numpy(configs.generate("c4")).cuda()
+    _native.set_tuning("gres", 2)
+    try:
+        y1 = sk.softmax(xd, sk.KernelVariant.REFERENCE_CLIPPED)
+        y2 = sk.softmax(xd, sk.KernelVariant.REFERENCE_CLIPPED)
+        t.cuda.synchronize()
+    finally:
+        _native.set_tuning("gres", 1)
+    assert bool(t.equal(y1, y2))
+    rs = y1.double().sum(dim=1)
+    assert float((rs - 1).abs().max()) <= 1e-5
 
 
 def test_seg_lengths_all_agree(oracle):
