@@ -99,6 +99,7 @@ std::atomic<int> g_cluster_size{0};  // force a K3c cluster size (0 = auto)
 std::atomic<int> g_vec8{0};          // 256-bit K1 path (measured no faster: off by default)   // K3 warp queue: tasks per atomic claim (0 = static)  // K3 grid = SMs*occupancy/div: two launches co-reside
 std::atomic<int> g_gres{1};       // K3g grid-resident rows: 0 off, 1 when it out-scores K3c, 2 force
 std::atomic<int> g_gres_p{0};     // force K3g CTAs per row (0 = auto)
+std::atomic<int> g_gres_st{0};    // force K3g ring depth (0 = as deep as smem allows)
 std::atomic<int> g_gres_x{12288}; // K3g per-row exchange cost model, in floats of streaming time
 std::atomic<int> g_k3_impl{3};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
 
@@ -467,8 +468,12 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
           if (g_gres_p.load() > 0 && P != g_gres_p.load()) continue;
           const int64_t slice = align_up((cols + P - 1) / P, 4);
           if ((P - 1) * slice >= cols) continue;
-          const int st = static_cast<int>(std::min<int64_t>(
+          int st = static_cast<int>(std::min<int64_t>(
               kGresStages, kClusterSmemMax / (slice * int64_t(sizeof(float)))));
+          if (g_gres_st.load() >= 2) {
+            if (st < g_gres_st.load()) continue;
+            st = g_gres_st.load();
+          }
           if (st < 2) continue;
           const size_t smem = size_t(st) * slice * sizeof(float);
           const int occ = occupancy(fn, kGresThreads, smem);
@@ -948,6 +953,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "gres") g_gres = value;
   else if (k == "gres_p") g_gres_p = value;
   else if (k == "gres_x") g_gres_x = value;
+  else if (k == "gres_st") g_gres_st = value;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;
 }

@@ -8,24 +8,29 @@
 // CTA `rank` of the group holds columns [rank*L, (rank+1)*L) of the row in
 // shared memory (TMA ring of NS stages, like K3c).
 //
-// The two row statistics are exchanged through global memory: every CTA
-// publishes its partial (max, then f64 sum of exp) into a per-group slot array
-// and bumps the group's monotonic counter with red.release.gpu; the group
-// waits for counter == (exchange+1) * P with ld.acquire.gpu and reduces the P
-// slots in fixed order, so M and S are bit-identical in every CTA of the row.
-// Slots alternate by row parity: a CTA can be at most one exchange ahead.
+// One exchange per row, overlapped with the next row.  Each compute warp
+// reduces its share of the slice to a pair (m_w, s_w = sum exp(clip(x - m_w)))
+// without any CTA barrier; the exchange warp merges the 16 pairs into the CTA
+// pair (fixed order, s_w scaled by exp(m_w - m)), publishes it into the
+// group's slot array and bumps the group's monotonic counter with
+// red.release.gpu, then waits for counter == (k+1) * P with ld.acquire.gpu and
+// merges the P pairs in rank order -- so M and S are bit-identical in every CTA
+// of the row.  Meanwhile the compute warps already run row k+1's local pass;
+// only then do they write row k: y = exp(clip(x - M)) * (1/(float)S), the exp
+// recomputed against the GLOBAL max from the untouched slice (reference order,
+// kernels.py:144-188).  The group round trip (~1.5 us through L2) therefore
+// hides behind a full row step instead of stalling it.  Slots alternate by
+// row parity (a CTA can run at most one exchange ahead of its group).
 //
-// Warp specialisation keeps the handshake off the data path: warps 0..15
-// compute (max pass, exp pass in place, normalise + streaming stores); warp
-// 16 only issues the TMA loads and does the exchanges.  Its release fence thus
-// never waits for the compute warps' output stores to drain (the stall that a
-// single-role CTA pays at every global handshake), and named barriers hand the
-// statistics between the roles:
-//   bar 1  compute -> exchange  "CTA partials of this exchange are in smem"
-//   bar 2  exchange -> compute  "row statistic broadcast in smem"
-//   bar 3  compute -> exchange  "ring stage consumed (proxy-fenced): refill it"
-// Traffic is 8 B/element in both HBM and L2 (the row never leaves the chip
-// between its passes); kernels.py:144-188 is the operation order followed.
+// Warp specialisation keeps the handshake off the data path: warp 16 only
+// issues the TMA loads and does the exchanges, so its release fence never
+// waits for the compute warps' output stores to drain.  Named barriers:
+//   bar 1/4  compute -> exchange  "warp pairs of row k in smem" (by row parity)
+//   bar 2    exchange -> compute  "(M, S) of row k in smem"
+//   bar 3    compute -> exchange  "row k's stage consumed (proxy-fenced): refill"
+// HBM and L2 each see 8 B/element: the row never leaves the chip between its
+// three shared-memory passes (ring depth NS >= 3 keeps one row loading, one
+// in its local pass and one awaiting its statistics).
 #pragma once
 #include "sk_common.cuh"
 
@@ -33,7 +38,7 @@ namespace sk {
 
 constexpr int kGresCompute = 512;                   // 16 compute warps
 constexpr int kGresThreads = kGresCompute + 32;     // + 1 exchange/TMA warp
-constexpr int kGresStages = 3;                      // maximum ring depth
+constexpr int kGresStages = 4;                      // maximum ring depth
 constexpr unsigned kGresSpinLimit = 1u << 24;       // ~10 s of polling: abort, never hang
 
 __device__ __forceinline__ void bar_sync_n(int id, int n) {
@@ -88,11 +93,12 @@ __global__ void __launch_bounds__(kGresThreads, 1)
             unsigned long long* __restrict__ bad_row, float shift_scale) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage_buf = reinterpret_cast<float*>(smem_raw);
+  constexpr int NW = kGresCompute / 32;
   __shared__ uint64_t bars[kGresStages];
-  __shared__ float red_f[kGresCompute / 32];
-  __shared__ double red_d[kGresCompute / 32];
-  __shared__ float bc_m;
-  __shared__ double bc_s;
+  __shared__ float red_f[2][NW];   // [row parity][warp]: warp-local max
+  __shared__ double red_d[2][NW];  //                     warp-local sum vs that max
+  __shared__ float bc_m[2];        // [row parity] merged row max / sum
+  __shared__ double bc_s[2];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = static_cast<int>(gridDim.x) / P;
@@ -110,7 +116,7 @@ __global__ void __launch_bounds__(kGresThreads, 1)
   __syncthreads();
   pdl_wait();
 
-  if (warp == kGresCompute / 32) {
+  if (warp == NW) {
     // ------------------------------------------------ exchange + TMA warp
     unsigned* cnt = cnt_base + size_t(g) * 32;  // own 128-B line per group
     auto issue = [&](int64_t row, int stage) {
@@ -127,50 +133,75 @@ __global__ void __launch_bounds__(kGresThreads, 1)
     unsigned k = 0;
     for (int64_t row = g; row < rows; row += G, ++k) {
       const int par = k & 1;
+      // CTA pair (m, s) of row k from the 16 warp pairs, fixed order
+      bar_sync_n(1 + 3 * par, kGresThreads);
+      const float mw = lane < NW ? red_f[par][lane] : kPadLogit;
+      const float mc = group_max<32>(mw);
+      double sw = lane < NW ? red_d[par][lane] : 0.0;
+      if (lane < NW && mw != mc) sw *= static_cast<double>(expf(mw - mc));
+      const double sc = group_sum<32>(sw);
       float* pm = pmax + (size_t(g) * 2 + par) * P;
       double* ps = psum + (size_t(g) * 2 + par) * P;
-      // max exchange
-      bar_sync_n(1, kGresThreads);
-      float m = lane < kGresCompute / 32 ? red_f[lane] : kPadLogit;
-      m = group_max<32>(m);
       if (lane == 0) {
-        st_relaxed_f32(pm + rank, m);
+        st_relaxed_f32(pm + rank, mc);
+        st_relaxed_f64(ps + rank, sc);
         red_release_add_gpu(cnt, 1u);
       }
-      gres_wait(cnt, (2u * k + 1u) * unsigned(P), abort_flag);
-      float M = kPadLogit;
-      for (int j = lane; j < P; j += 32) M = fmaxf(M, ld_relaxed_f32(pm + j));
-      M = group_max<32>(M);
-      if (lane == 0) bc_m = M * shift_scale;  // shift_scale = 0: fault hook
-      bar_arrive_n(2, kGresThreads);
-      // sum exchange
-      bar_sync_n(1, kGresThreads);
-      double t = lane < kGresCompute / 32 ? red_d[lane] : 0.0;
-      t = group_sum<32>(t);
-      if (lane == 0) {
-        st_relaxed_f64(ps + rank, t);
-        red_release_add_gpu(cnt, 1u);
+      // while the group's pairs arrive: refill the stage row k-1 released
+      if (k > 0) {
+        bar_sync_n(3, kGresThreads);
+        const int64_t rn = row - G + int64_t(nstages) * G;
+        if (lane == 0 && rn < rows) issue(rn, static_cast<int>((k - 1) % unsigned(nstages)));
       }
-      gres_wait(cnt, (2u * k + 2u) * unsigned(P), abort_flag);
+      gres_wait(cnt, (k + 1u) * unsigned(P), abort_flag);
+      // merge the P pairs in rank order: identical (M, S) in every CTA of the row
+      float Mg = kPadLogit;
+      for (int j = lane; j < P; j += 32) Mg = fmaxf(Mg, ld_relaxed_f32(pm + j));
+      Mg = group_max<32>(Mg);
       double S = 0.0;
-      for (int j = lane; j < P; j += 32) S += ld_relaxed_f64(ps + j);  // fixed order
-      S = group_sum<32>(S);  // same butterfly in every CTA: identical S group-wide
-      if (lane == 0) bc_s = S;
+      for (int j = lane; j < P; j += 32) {
+        const float mj = ld_relaxed_f32(pm + j);
+        double sj = ld_relaxed_f64(ps + j);
+        if (mj != Mg) sj *= static_cast<double>(expf(mj - Mg));
+        S += sj;
+      }
+      S = group_sum<32>(S);
+      if (lane == 0) {
+        bc_m[par] = Mg * shift_scale;  // shift_scale = 0: fault hook
+        bc_s[par] = S;
+      }
       bar_arrive_n(2, kGresThreads);
-      // refill the consumed stage with the row NS steps ahead
-      bar_sync_n(3, kGresThreads);
-      const int64_t rn = row + int64_t(nstages) * G;
-      if (lane == 0 && rn < rows) issue(rn, static_cast<int>(k % unsigned(nstages)));
     }
+    if (k > 0) bar_sync_n(3, kGresThreads);  // last row's output pass done
     return;
   }
 
   // ---------------------------------------------------------- compute warps
+  // row k's output pass runs after row k+1's local pass, so the group
+  // exchange of row k overlaps a full row of streaming work.
+  auto output = [&](unsigned j, int64_t orow) {
+    bar_sync_n(2, kGresThreads);
+    const float M = bc_m[j & 1];
+    const float rcp = recip_of_sum(bc_s[j & 1]);
+    const float4* sb = reinterpret_cast<const float4*>(stage_buf + size_t(j % unsigned(nstages)) * slice);
+    float* yr = y + orow * ldy + c0;
+#pragma unroll 4
+    for (int q = tid; q < nvec; q += kGresCompute) {
+      const float4 v = sb[q];
+      const float2 a = scale2<MODE>(sexp2<MODE>(v.x, v.y, M), rcp);
+      const float2 b = scale2<MODE>(sexp2<MODE>(v.z, v.w, M), rcp);
+      st_stream4(yr + 4 * q, make_float4(a.x, a.y, b.x, b.y));
+    }
+    fence_proxy_async_smem();  // generic smem reads before the TMA refill
+    bar_arrive_n(3, kGresThreads);
+  };
+
   unsigned k = 0;
+  int64_t prow = 0;
   for (int64_t row = g; row < rows; row += G, ++k) {
     const int stage = static_cast<int>(k % unsigned(nstages));
     mbar_wait(&bars[stage], (k / unsigned(nstages)) & 1u);
-    float4* sb = reinterpret_cast<float4*>(stage_buf + size_t(stage) * slice);
+    const float4* sb = reinterpret_cast<const float4*>(stage_buf + size_t(stage) * slice);
 
     float mt = kPadLogit;
     u64 z = f2pk(0.0f, 0.0f);
@@ -181,39 +212,26 @@ __global__ void __launch_bounds__(kGresThreads, 1)
       z = nf_acc2(nf_acc2(z, v.x, v.y), v.z, v.w);
     }
     if (nf_bad(z)) atomicMin(bad_row, static_cast<unsigned long long>(row));
-    mt = group_max<32>(mt);
-    if (lane == 0) red_f[warp] = mt;
-    bar_arrive_n(1, kGresThreads);
-    bar_sync_n(2, kGresThreads);
-    const float M = bc_m;
-
+    const float mw = group_max<32>(mt);  // warp-local max: no CTA barrier
     u64 acc = f2pk(0.0f, 0.0f);
 #pragma unroll 4
     for (int q = tid; q < nvec; q += kGresCompute) {
       const float4 v = sb[q];
-      const float2 a = sexp2<MODE>(v.x, v.y, M);
-      const float2 b = sexp2<MODE>(v.z, v.w, M);
-      sb[q] = make_float4(a.x, a.y, b.x, b.y);
+      const float2 a = sexp2<MODE>(v.x, v.y, mw);
+      const float2 b = sexp2<MODE>(v.z, v.w, mw);
       acc = f2add(f2add(acc, f2pk(a.x, a.y)), f2pk(b.x, b.y));
     }
     const float2 acc2 = f2up(acc);
-    const double sd = group_sum<32>(static_cast<double>(acc2.x + acc2.y));
-    if (lane == 0) red_d[warp] = sd;
-    bar_arrive_n(1, kGresThreads);
-    bar_sync_n(2, kGresThreads);
-    const float rcp = recip_of_sum(bc_s);
-
-    float* yr = y + row * ldy + c0;
-#pragma unroll 4
-    for (int q = tid; q < nvec; q += kGresCompute) {
-      const float4 e = sb[q];
-      const float2 a = scale2<MODE>(make_float2(e.x, e.y), rcp);
-      const float2 b = scale2<MODE>(make_float2(e.z, e.w), rcp);
-      st_stream4(yr + 4 * q, make_float4(a.x, a.y, b.x, b.y));
+    const double sw = group_sum<32>(static_cast<double>(acc2.x + acc2.y));
+    if (lane == 0) {
+      red_f[k & 1][warp] = mw;
+      red_d[k & 1][warp] = sw;
     }
-    fence_proxy_async_smem();  // generic smem accesses before the TMA refill
-    bar_arrive_n(3, kGresThreads);
+    bar_arrive_n(1 + 3 * (k & 1), kGresThreads);
+    if (k > 0) output(k - 1, prow);
+    prow = row;
   }
+  if (k > 0) output(k - 1, prow);
 }
 
 }  // namespace sk

@@ -70,6 +70,7 @@ def main():
     p.add_argument("--shape", default="", help="RxC: synthetic N(0,4^2) matrix instead of a config")
     p.add_argument("--gres-ps", default="0,10,12,16,24,37,48,74",
                    help="K3g CTAs per row to try (0 = planner's choice)")
+    p.add_argument("--gres-st", default="0", help="K3g ring depths to try (0 = planner's)")
     p.add_argument("--only-resident", action="store_true",
                    help="long rows: only the resident-row kernels (K3c / K3g) and split")
     args = p.parse_args()
@@ -133,12 +134,16 @@ def main():
             print(json.dumps({"variant": "k3_cluster", "error": str(e)}))
         _native.set_tuning("gres", 2)
         for gp in map(int, args.gres_ps.split(",")):
-            _native.set_tuning("gres_p", gp)
-            try:
-                record(f"k3_gres P={gp or 'auto'}", bench_once(xs, ys, rows, cols, args.reps, s))
-            except Exception as e:  # noqa: BLE001
-                print(json.dumps({"variant": f"gres {gp}", "error": str(e)}))
+            for gs in map(int, args.gres_st.split(",")):
+                _native.set_tuning("gres_p", gp)
+                _native.set_tuning("gres_st", gs)
+                try:
+                    record(f"k3_gres P={gp or 'auto'} st={gs or 'auto'}",
+                           bench_once(xs, ys, rows, cols, args.reps, s))
+                except Exception as e:  # noqa: BLE001
+                    print(json.dumps({"variant": f"gres {gp} st {gs}", "error": str(e)}))
         _native.set_tuning("gres_p", 0)
+        _native.set_tuning("gres_st", 0)
         _native.set_tuning("gres", 1)
         _native.set_tuning("path", 2)
         record("split(k4)", bench_once(xs, ys, rows, cols, max(10, args.reps // 4), s))
