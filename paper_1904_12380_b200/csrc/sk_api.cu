@@ -99,6 +99,7 @@ std::atomic<int> g_cluster_size{0};  // force a K3c cluster size (0 = auto)
 std::atomic<int> g_vec8{0};          // 256-bit K1 path (measured no faster: off by default)   // K3 warp queue: tasks per atomic claim (0 = static)  // K3 grid = SMs*occupancy/div: two launches co-reside
 std::atomic<int> g_gres{1};       // K3g grid-resident rows: 0 off, 1 when it out-scores K3c, 2 force
 std::atomic<int> g_gres_p{0};     // force K3g CTAs per row (0 = auto)
+std::atomic<int> g_gres_diag{0};  // K3g timing diagnostics (1: skip the group exchange -- wrong results)
 std::atomic<int> g_gres_st{0};    // force K3g ring depth (0 = as deep as smem allows)
 std::atomic<int> g_gres_x{12288}; // K3g per-row exchange cost model, in floats of streaming time
 std::atomic<int> g_k3_impl{3};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
@@ -464,7 +465,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
       if (gres != 0 && di.coop) {
         const void* fn = gres_fn(mode);
         const double xg = std::max(0, g_gres_x.load());
-        for (int P = 2; P <= di.sms; ++P) {
+        for (int P = 2; P <= std::min(di.sms, kGresMaxP); ++P) {
           if (g_gres_p.load() > 0 && P != g_gres_p.load()) continue;
           const int64_t slice = align_up((cols + P - 1) / P, 4);
           if ((P - 1) * slice >= cols) continue;
@@ -481,7 +482,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
           const int groups = di.sms * occ / P;
           if (groups < 1) continue;
           const int64_t rows_g = (rows + groups - 1) / groups;  // exchange counter range
-          if (2 * rows_g * P >= (int64_t(1) << 31)) continue;
+          if (rows_g >= (int64_t(1) << 31)) continue;  // 32-bit slot tags
           const double score = double(std::min<int64_t>(groups, rows)) * P / occ *
                                double(slice) / (double(slice) + xg);
           if (score > best_g) {
@@ -603,17 +604,15 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
   return plan_split(rows, cols, p);
 }
 
-// K3g control block: abort flag | one 128-B counter line per group | max slots
-// [group][parity][P] | sum slots [group][parity][P]; [0, pmax) zeroed per launch.
+// K3g control block: abort flag | slots [group][row parity][P] x 16 B, all
+// zeroed per launch (a zero slot never carries a valid tag).
 struct GresWs {
-  size_t abort = 256, cnt = 384, pmax = 0, psum = 0, total = 0;
+  size_t abort = 256, slots = 512, total = 0;
 };
 GresWs gres_ws(const Plan& p) {
   GresWs w;
   const size_t groups = size_t(p.grid / p.nseg);
-  w.pmax = align_up(w.cnt + groups * 128, 256);
-  w.psum = align_up(w.pmax + groups * 2 * p.nseg * sizeof(float), 256);
-  w.total = align_up(w.psum + groups * 2 * p.nseg * sizeof(double), 256);
+  w.total = align_up(w.slots + groups * 2 * p.nseg * 16, 256);
   return w;
 }
 
@@ -765,13 +764,13 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
       SK_CUDA(cudaLaunchKernelExC(&cfg, cluster_fn(mode), args));
     } else if (p.k3 == 7) {
       const GresWs w = gres_ws(p);
-      SK_CUDA(cudaMemsetAsync(ws + w.abort, 0, w.pmax - w.abort, s));
+      SK_CUDA(cudaMemsetAsync(ws + w.abort, 0, w.total - w.abort, s));
       int P = p.nseg, slice = p.seglen, nst = p.lag;
       SK_CUDA(launch_k(gres_fn(mode), dim3(static_cast<unsigned>(p.grid)), dim3(p.threads),
                        p.smem, s, true, x, y, rows, cols, ldx, ldy, P, slice, nst,
-                       reinterpret_cast<unsigned*>(ws + w.cnt), reinterpret_cast<float*>(ws + w.pmax),
-                       reinterpret_cast<double*>(ws + w.psum), reinterpret_cast<unsigned*>(ws + w.abort),
-                       bad, sh));
+                       reinterpret_cast<unsigned long long*>(ws + w.slots),
+                       reinterpret_cast<unsigned*>(ws + w.abort),
+                       bad, sh, g_gres_diag.load()));
     } else if (p.k3 == 5) {
       const void* fn = p.seglen == 2048 ? reg3_fn<16>(mode)
                        : p.seglen == 512 ? reg3_fn<4>(mode) : reg3_fn<8>(mode);
@@ -954,6 +953,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "gres_p") g_gres_p = value;
   else if (k == "gres_x") g_gres_x = value;
   else if (k == "gres_st") g_gres_st = value;
+  else if (k == "gres_diag") g_gres_diag = value;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;
 }

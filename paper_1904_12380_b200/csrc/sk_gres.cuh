@@ -11,15 +11,15 @@
 // One exchange per row, overlapped with the next row.  Each compute warp
 // reduces its share of the slice to a pair (m_w, s_w = sum exp(clip(x - m_w)))
 // without any CTA barrier; the exchange warp merges the 16 pairs into the CTA
-// pair (fixed order, s_w scaled by exp(m_w - m)), publishes it into the
-// group's slot array and bumps the group's monotonic counter with
-// red.release.gpu, then waits for counter == (k+1) * P with ld.acquire.gpu and
-// merges the P pairs in rank order -- so M and S are bit-identical in every CTA
-// of the row.  Meanwhile the compute warps already run row k+1's local pass;
+// pair (fixed order, s_w scaled by exp(m_w - m)) and publishes it as one
+// sequence-tagged 16-B slot of the group's slot array (one relaxed store: no
+// counter, no release fence); it then polls the P slots -- the poll returns
+// the data itself -- and merges the pairs in rank order, so M and S are
+// bit-identical in every CTA of the row.  Meanwhile the compute warps already run row k+1's local pass;
 // only then do they write row k: y = exp(clip(x - M)) * (1/(float)S), the exp
 // recomputed against the GLOBAL max from the untouched slice (reference order,
-// kernels.py:144-188).  The group round trip (~1.5 us through L2) therefore
-// hides behind a full row step instead of stalling it.  Slots alternate by
+// kernels.py:144-188).  The group round trip (store to L2 + one polling
+// load) therefore hides behind a full row step instead of stalling it.  Slots alternate by
 // row parity (a CTA can run at most one exchange ahead of its group).
 //
 // Warp specialisation keeps the handshake off the data path: warp 16 only
@@ -69,28 +69,37 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
   return v;
 }
 
-// Exchange warp: all lanes poll the group counter (one broadcast load).  A
-// stuck peer (impossible under a cooperative launch, but a hung GPU costs more
-// than a wrong answer) raises the kernel-wide abort flag instead of spinning.
-__device__ __forceinline__ void gres_wait(const unsigned* cnt, unsigned target, unsigned* abort_flag) {
-  unsigned spins = 0;
-  while (ld_acquire_gpu(cnt) < target) {
-    if ((++spins & 0xFFFu) == 0) {
-      if (ld_relaxed_u32(abort_flag)) return;
-      if (spins >= kGresSpinLimit) {
-        atomicExch(abort_flag, 1u);
-        return;
-      }
-    }
-  }
+__device__ __forceinline__ void st_relaxed_v2u64(unsigned long long* p, unsigned long long a,
+                                                 unsigned long long b) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_relaxed_v2u64(const unsigned long long* p, unsigned long long& a,
+                                                 unsigned long long& b) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+
+constexpr int kGresMaxP = 160;  // slots per lane: 5
+
+// A CTA's row pair as one 16-B slot of two independently tagged 64-bit words
+// (each 64-bit access is single-copy atomic): word 0 = tag << 32 | bits(m),
+// word 1 = bits(s) with its 8 low mantissa bits replaced by the tag (2^-44
+// relative: far below the f64 sum's own rounding).  A reader accepts a slot
+// when both tags match, so the data IS the flag: no counter, no fence.
+__device__ __forceinline__ void gres_pack(float m, double s, unsigned tag, unsigned long long& w0,
+                                          unsigned long long& w1) {
+  w0 = (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(m);
+  w1 = (static_cast<unsigned long long>(__double_as_longlong(s)) & ~0xFFull) | (tag & 0xFFu);
+}
+__device__ __forceinline__ bool gres_valid(unsigned long long w0, unsigned long long w1, unsigned tag) {
+  return static_cast<unsigned>(w0 >> 32) == tag && static_cast<unsigned>(w1 & 0xFFu) == (tag & 0xFFu);
 }
 
 template <int MODE>
 __global__ void __launch_bounds__(kGresThreads, 1)
     k3_gres(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
-            int64_t ldx, int64_t ldy, int P, int slice, int nstages, unsigned* __restrict__ cnt_base,
-            float* __restrict__ pmax, double* __restrict__ psum, unsigned* __restrict__ abort_flag,
-            unsigned long long* __restrict__ bad_row, float shift_scale) {
+            int64_t ldx, int64_t ldy, int P, int slice, int nstages,
+            unsigned long long* __restrict__ slots, unsigned* __restrict__ abort_flag,
+            unsigned long long* __restrict__ bad_row, float shift_scale, int diag) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage_buf = reinterpret_cast<float*>(smem_raw);
   constexpr int NW = kGresCompute / 32;
@@ -118,7 +127,6 @@ __global__ void __launch_bounds__(kGresThreads, 1)
 
   if (warp == NW) {
     // ------------------------------------------------ exchange + TMA warp
-    unsigned* cnt = cnt_base + size_t(g) * 32;  // own 128-B line per group
     auto issue = [&](int64_t row, int stage) {
       mbar_arrive_expect_tx(&bars[stage], static_cast<uint32_t>(len) * 4u);
       if (len > 0)
@@ -140,12 +148,13 @@ __global__ void __launch_bounds__(kGresThreads, 1)
       double sw = lane < NW ? red_d[par][lane] : 0.0;
       if (lane < NW && mw != mc) sw *= static_cast<double>(expf(mw - mc));
       const double sc = group_sum<32>(sw);
-      float* pm = pmax + (size_t(g) * 2 + par) * P;
-      double* ps = psum + (size_t(g) * 2 + par) * P;
-      if (lane == 0) {
-        st_relaxed_f32(pm + rank, mc);
-        st_relaxed_f64(ps + rank, sc);
-        red_release_add_gpu(cnt, 1u);
+      // slot array of this group and row parity: [P] x 16 B
+      unsigned long long* sl = slots + (size_t(g) * 2 + par) * size_t(P) * 2;
+      const unsigned tag = k + 1u;  // never 0: the per-launch memset reads as "not yet"
+      if (lane == 0 && !(diag & 1)) {
+        unsigned long long w0, w1;
+        gres_pack(mc, sc, tag, w0, w1);
+        st_relaxed_v2u64(sl + 2 * rank, w0, w1);
       }
       // while the group's pairs arrive: refill the stage row k-1 released
       if (k > 0) {
@@ -153,18 +162,50 @@ __global__ void __launch_bounds__(kGresThreads, 1)
         const int64_t rn = row - G + int64_t(nstages) * G;
         if (lane == 0 && rn < rows) issue(rn, static_cast<int>((k - 1) % unsigned(nstages)));
       }
-      gres_wait(cnt, (k + 1u) * unsigned(P), abort_flag);
+      if (diag & 1) {  // timing diagnostic only: CTA-local statistics, no exchange
+        if (lane == 0) {
+          bc_m[par] = mc;
+          bc_s[par] = sc;
+        }
+        bar_arrive_n(2, kGresThreads);
+        continue;
+      }
+      // poll the P slots (lane j reads slots j, j+32, ...) until all carry the tag
+      unsigned long long w0[kGresMaxP / 32], w1[kGresMaxP / 32];
+      unsigned spins = 0;
+      while (true) {
+        bool ok = true;
+#pragma unroll
+        for (int i = 0; i < kGresMaxP / 32; ++i) {
+          const int j = lane + 32 * i;
+          if (j < P) {
+            ld_relaxed_v2u64(sl + 2 * j, w0[i], w1[i]);
+            ok = ok && gres_valid(w0[i], w1[i], tag);
+          }
+        }
+        if (__all_sync(0xffffffffu, ok)) break;
+        if ((++spins & 0xFFFu) == 0) {  // a stuck peer raises abort: never hang the GPU
+          if (ld_relaxed_u32(abort_flag) || spins >= kGresSpinLimit) {
+            if (lane == 0) atomicExch(abort_flag, 1u);
+            break;
+          }
+        }
+      }
       // merge the P pairs in rank order: identical (M, S) in every CTA of the row
       float Mg = kPadLogit;
-      for (int j = lane; j < P; j += 32) Mg = fmaxf(Mg, ld_relaxed_f32(pm + j));
+#pragma unroll
+      for (int i = 0; i < kGresMaxP / 32; ++i)
+        if (lane + 32 * i < P) Mg = fmaxf(Mg, __uint_as_float(static_cast<unsigned>(w0[i])));
       Mg = group_max<32>(Mg);
       double S = 0.0;
-      for (int j = lane; j < P; j += 32) {
-        const float mj = ld_relaxed_f32(pm + j);
-        double sj = ld_relaxed_f64(ps + j);
-        if (mj != Mg) sj *= static_cast<double>(expf(mj - Mg));
-        S += sj;
-      }
+#pragma unroll
+      for (int i = 0; i < kGresMaxP / 32; ++i)
+        if (lane + 32 * i < P) {
+          const float mj = __uint_as_float(static_cast<unsigned>(w0[i]));
+          double sj = __longlong_as_double(static_cast<long long>(w1[i]));
+          if (mj != Mg) sj *= static_cast<double>(expf(mj - Mg));
+          S += sj;
+        }
       S = group_sum<32>(S);
       if (lane == 0) {
         bc_m[par] = Mg * shift_scale;  // shift_scale = 0: fault hook

@@ -1,0 +1,49 @@
+#!/usr/bin/env python
+"""K3g diagnostics: time the grid-resident kernel with and without its group
+exchange (gres_diag=1 skips it: results wrong, timing = the pipeline's own
+bound) over a list of group sizes / ring depths.  One JSON line per point."""
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "scripts"))
+
+import torch  # noqa: E402
+
+from paper_1904_12380_b200 import _native, configs  # noqa: E402
+from sweep import bench_once  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--points", default="14:3,16:3,20:4,24:4", help="P:stages,...")
+    ap.add_argument("--reps", type=int, default=60)
+    ap.add_argument("--diags", default="0,1")
+    args = ap.parse_args()
+    spec = configs.get(args.config)
+    x0 = torch.from_numpy(configs.generate(spec)).cuda()
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    R = max(2, -(-3 * l2 // (8 * spec.rows * spec.cols)))
+    xs = [x0] + [x0.clone() for _ in range(R - 1)]
+    ys = [torch.empty_like(x0) for _ in range(R)]
+    s = torch.cuda.Stream()
+    _native.set_tuning("gres", 2)
+    for pt in args.points.split(","):
+        P, st = map(int, pt.split(":"))
+        _native.set_tuning("gres_p", P)
+        _native.set_tuning("gres_st", st)
+        for d in map(int, args.diags.split(",")):
+            _native.set_tuning("gres_diag", d)
+            us = bench_once(xs, ys, spec.rows, spec.cols, args.reps, s)
+            print(json.dumps({"config": spec.name, "P": P, "stages": st, "diag": d, "us": us,
+                              "gbs": 8.0 * spec.rows * spec.cols / us / 1e3}), flush=True)
+    _native.set_tuning("gres_diag", 0)
+
+
+if __name__ == "__main__":
+    main()
