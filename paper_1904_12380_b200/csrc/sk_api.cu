@@ -272,6 +272,7 @@ int max_active_clusters(const void* fn, int cs, size_t smem) {
   return n;
 }
 
+constexpr int64_t kGresSmemMax = 225 * 1024;  // ring bytes per K3g CTA (227 KB opt-in minus statics)
 const void* gres_fn(int mode) {
   switch (mode) {
     case kClipAccurate: return reinterpret_cast<const void*>(&k3_gres<kClipAccurate>);
@@ -470,7 +471,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
           const int64_t slice = align_up((cols + P - 1) / P, 4);
           if ((P - 1) * slice >= cols) continue;
           int st = static_cast<int>(std::min<int64_t>(
-              kGresStages, kClusterSmemMax / (slice * int64_t(sizeof(float)))));
+              kGresStages, kGresSmemMax / (slice * int64_t(sizeof(float)))));
           if (g_gres_st.load() >= 2) {
             if (st < g_gres_st.load()) continue;
             st = g_gres_st.load();

@@ -25,12 +25,13 @@
 // Warp specialisation keeps the handshake off the data path: warp 16 only
 // issues the TMA loads and does the exchanges, so its release fence never
 // waits for the compute warps' output stores to drain.  Named barriers:
-//   bar 1/4  compute -> exchange  "warp pairs of row k in smem" (by row parity)
-//   bar 2    exchange -> compute  "(M, S) of row k in smem"
-//   bar 3    compute -> exchange  "row k's stage consumed (proxy-fenced): refill"
-// HBM and L2 each see 8 B/element: the row never leaves the chip between its
-// three shared-memory passes (ring depth NS >= 3 keeps one row loading, one
-// in its local pass and one awaiting its statistics).
+//   bar1  compute -> exchange  "warp pairs of row k in smem"
+//   bar2  exchange -> compute  "(M, S) of row k in smem"
+//   bar3  compute -> exchange  "row k's stage consumed (proxy-fenced): refill"
+// With a ring of NS stages the output pass of row k runs after the local pass
+// of row k+L, L = NS-2 (one row loading, L+1 resident awaiting statistics);
+// the group round trip hides behind L row steps.  HBM and L2 each see
+// 8 B/element: the row never leaves the chip between its three smem passes.
 #pragma once
 #include "sk_common.cuh"
 
@@ -38,7 +39,7 @@ namespace sk {
 
 constexpr int kGresCompute = 512;                   // 16 compute warps
 constexpr int kGresThreads = kGresCompute + 32;     // + 1 exchange/TMA warp
-constexpr int kGresStages = 4;                      // maximum ring depth
+constexpr int kGresStages = 5;                      // maximum ring depth (lag <= 3)
 constexpr unsigned kGresSpinLimit = 1u << 24;       // ~10 s of polling: abort, never hang
 
 __device__ __forceinline__ void bar_sync_n(int id, int n) {
@@ -94,6 +95,13 @@ __device__ __forceinline__ bool gres_valid(unsigned long long w0, unsigned long 
   return static_cast<unsigned>(w0 >> 32) == tag && static_cast<unsigned>(w1 & 0xFFu) == (tag & 0xFFu);
 }
 
+// Named barrier ids for lag L (stages - 2, 1..3): a hand-off can have at most
+// L+1 (bar 1) or L (bars 2 and 3) phases outstanding, so each rotates over
+// that many ids.  Id 0 is __syncthreads.
+__device__ __forceinline__ int gres_bar1(unsigned k, int L) { return 1 + int(k % unsigned(L + 1)); }
+__device__ __forceinline__ int gres_bar2(unsigned k, int L) { return 2 + L + int(k % unsigned(L)); }
+__device__ __forceinline__ int gres_bar3(unsigned k, int L) { return 2 + 2 * L + int(k % unsigned(L)); }
+
 template <int MODE>
 __global__ void __launch_bounds__(kGresThreads, 1)
     k3_gres(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
@@ -103,16 +111,18 @@ __global__ void __launch_bounds__(kGresThreads, 1)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage_buf = reinterpret_cast<float*>(smem_raw);
   constexpr int NW = kGresCompute / 32;
+  constexpr int NB = kGresStages - 1;  // L + 1 <= NB broadcast slots
   __shared__ uint64_t bars[kGresStages];
-  __shared__ float red_f[2][NW];   // [row parity][warp]: warp-local max
-  __shared__ double red_d[2][NW];  //                     warp-local sum vs that max
-  __shared__ float bc_m[2];        // [row parity] merged row max / sum
-  __shared__ double bc_s[2];
+  __shared__ float red_f[NB][NW];   // [row % (L+1)][warp]: warp-local max
+  __shared__ double red_d[NB][NW];  //                      warp-local sum vs that max
+  __shared__ float bc_m[NB];        // [row % (L+1)] merged row max / sum
+  __shared__ double bc_s[NB];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = static_cast<int>(gridDim.x) / P;
   const int g = static_cast<int>(blockIdx.x) / P, rank = static_cast<int>(blockIdx.x) % P;
   if (g >= G) return;  // whole CTA: no barrier below is shared with it
+  const int L = nstages > 2 ? nstages - 2 : 1;  // rows between local pass and output pass
   const int64_t c0 = int64_t(rank) * slice;
   const int64_t rem = cols - c0;
   const int len = rem <= 0 ? 0 : static_cast<int>(rem < slice ? rem : slice);  // % 4 == 0
@@ -140,105 +150,108 @@ __global__ void __launch_bounds__(kGresThreads, 1)
       }
     unsigned k = 0;
     for (int64_t row = g; row < rows; row += G, ++k) {
-      const int par = k & 1;
+      const int b = static_cast<int>(k % unsigned(L + 1));
       // CTA pair (m, s) of row k from the 16 warp pairs, fixed order
-      bar_sync_n(1 + 3 * par, kGresThreads);
-      const float mw = lane < NW ? red_f[par][lane] : kPadLogit;
+      bar_sync_n(gres_bar1(k, L), kGresThreads);
+      const float mw = lane < NW ? red_f[b][lane] : kPadLogit;
       const float mc = group_max<32>(mw);
-      double sw = lane < NW ? red_d[par][lane] : 0.0;
+      double sw = lane < NW ? red_d[b][lane] : 0.0;
       if (lane < NW && mw != mc) sw *= static_cast<double>(expf(mw - mc));
       const double sc = group_sum<32>(sw);
-      // slot array of this group and row parity: [P] x 16 B
-      unsigned long long* sl = slots + (size_t(g) * 2 + par) * size_t(P) * 2;
+      // slot array of this group and row parity: [P] x 16 B.  Parity suffices:
+      // a CTA publishes row k+1 only after merging row k.
+      unsigned long long* sl = slots + (size_t(g) * 2 + (k & 1)) * size_t(P) * 2;
       const unsigned tag = k + 1u;  // never 0: the per-launch memset reads as "not yet"
       if (lane == 0 && !(diag & 1)) {
         unsigned long long w0, w1;
         gres_pack(mc, sc, tag, w0, w1);
         st_relaxed_v2u64(sl + 2 * rank, w0, w1);
       }
-      // while the group's pairs arrive: refill the stage row k-1 released
-      if (k > 0) {
-        bar_sync_n(3, kGresThreads);
-        const int64_t rn = row - G + int64_t(nstages) * G;
-        if (lane == 0 && rn < rows) issue(rn, static_cast<int>((k - 1) % unsigned(nstages)));
+      // while the group's pairs arrive: refill the stage row k-L released
+      if (k >= unsigned(L)) {
+        const unsigned j = k - unsigned(L);
+        bar_sync_n(gres_bar3(j, L), kGresThreads);
+        const int64_t rn = row - int64_t(L) * G + int64_t(nstages) * G;
+        if (lane == 0 && rn < rows) issue(rn, static_cast<int>(j % unsigned(nstages)));
       }
+      float Mg;
+      double S;
       if (diag & 1) {  // timing diagnostic only: CTA-local statistics, no exchange
-        if (lane == 0) {
-          bc_m[par] = mc;
-          bc_s[par] = sc;
-        }
-        bar_arrive_n(2, kGresThreads);
-        continue;
-      }
-      // poll the P slots (lane j reads slots j, j+32, ...) until all carry the tag
-      unsigned long long w0[kGresMaxP / 32], w1[kGresMaxP / 32];
-      unsigned spins = 0;
-      while (true) {
-        bool ok = true;
+        Mg = mc;
+        S = sc;
+      } else {
+        // poll the P slots (lane j reads slots j, j+32, ...) until all carry the tag
+        unsigned long long w0[kGresMaxP / 32], w1[kGresMaxP / 32];
+        unsigned spins = 0;
+        while (true) {
+          bool ok = true;
 #pragma unroll
-        for (int i = 0; i < kGresMaxP / 32; ++i) {
-          const int j = lane + 32 * i;
-          if (j < P) {
-            ld_relaxed_v2u64(sl + 2 * j, w0[i], w1[i]);
-            ok = ok && gres_valid(w0[i], w1[i], tag);
+          for (int i = 0; i < kGresMaxP / 32; ++i) {
+            const int j = lane + 32 * i;
+            if (j < P) {
+              ld_relaxed_v2u64(sl + 2 * j, w0[i], w1[i]);
+              ok = ok && gres_valid(w0[i], w1[i], tag);
+            }
+          }
+          if (__all_sync(0xffffffffu, ok)) break;
+          if ((++spins & 0xFFFu) == 0) {  // a stuck peer raises abort: never hang the GPU
+            if (ld_relaxed_u32(abort_flag) || spins >= kGresSpinLimit) {
+              if (lane == 0) atomicExch(abort_flag, 1u);
+              break;
+            }
           }
         }
-        if (__all_sync(0xffffffffu, ok)) break;
-        if ((++spins & 0xFFFu) == 0) {  // a stuck peer raises abort: never hang the GPU
-          if (ld_relaxed_u32(abort_flag) || spins >= kGresSpinLimit) {
-            if (lane == 0) atomicExch(abort_flag, 1u);
-            break;
+        // merge the P pairs in rank order: identical (M, S) in every CTA of the row
+        Mg = kPadLogit;
+#pragma unroll
+        for (int i = 0; i < kGresMaxP / 32; ++i)
+          if (lane + 32 * i < P) Mg = fmaxf(Mg, __uint_as_float(static_cast<unsigned>(w0[i])));
+        Mg = group_max<32>(Mg);
+        S = 0.0;
+#pragma unroll
+        for (int i = 0; i < kGresMaxP / 32; ++i)
+          if (lane + 32 * i < P) {
+            const float mj = __uint_as_float(static_cast<unsigned>(w0[i]));
+            double sj = __longlong_as_double(static_cast<long long>(w1[i]));
+            if (mj != Mg) sj *= static_cast<double>(expf(mj - Mg));
+            S += sj;
           }
-        }
+        S = group_sum<32>(S);
       }
-      // merge the P pairs in rank order: identical (M, S) in every CTA of the row
-      float Mg = kPadLogit;
-#pragma unroll
-      for (int i = 0; i < kGresMaxP / 32; ++i)
-        if (lane + 32 * i < P) Mg = fmaxf(Mg, __uint_as_float(static_cast<unsigned>(w0[i])));
-      Mg = group_max<32>(Mg);
-      double S = 0.0;
-#pragma unroll
-      for (int i = 0; i < kGresMaxP / 32; ++i)
-        if (lane + 32 * i < P) {
-          const float mj = __uint_as_float(static_cast<unsigned>(w0[i]));
-          double sj = __longlong_as_double(static_cast<long long>(w1[i]));
-          if (mj != Mg) sj *= static_cast<double>(expf(mj - Mg));
-          S += sj;
-        }
-      S = group_sum<32>(S);
       if (lane == 0) {
-        bc_m[par] = Mg * shift_scale;  // shift_scale = 0: fault hook
-        bc_s[par] = S;
+        bc_m[b] = Mg * shift_scale;  // shift_scale = 0: fault hook
+        bc_s[b] = S;
       }
-      bar_arrive_n(2, kGresThreads);
+      bar_arrive_n(gres_bar2(k, L), kGresThreads);
     }
-    if (k > 0) bar_sync_n(3, kGresThreads);  // last row's output pass done
+    // the last L rows' output passes
+    for (unsigned j = k >= unsigned(L) ? k - unsigned(L) : 0u; j < k; ++j)
+      bar_sync_n(gres_bar3(j, L), kGresThreads);
     return;
   }
 
   // ---------------------------------------------------------- compute warps
-  // row k's output pass runs after row k+1's local pass, so the group
-  // exchange of row k overlaps a full row of streaming work.
-  auto output = [&](unsigned j, int64_t orow) {
-    bar_sync_n(2, kGresThreads);
-    const float M = bc_m[j & 1];
-    const float rcp = recip_of_sum(bc_s[j & 1]);
+  // row k's output pass runs after row k+L's local pass, so the group
+  // exchange of row k overlaps L full rows of streaming work.
+  auto output = [&](unsigned j) {
+    bar_sync_n(gres_bar2(j, L), kGresThreads);
+    const int b = static_cast<int>(j % unsigned(L + 1));
+    const float M = bc_m[b];
+    const float rcp = recip_of_sum(bc_s[b]);
     const float4* sb = reinterpret_cast<const float4*>(stage_buf + size_t(j % unsigned(nstages)) * slice);
-    float* yr = y + orow * ldy + c0;
+    float* yr = y + (g + int64_t(j) * G) * ldy + c0;
 #pragma unroll 4
     for (int q = tid; q < nvec; q += kGresCompute) {
       const float4 v = sb[q];
       const float2 a = scale2<MODE>(sexp2<MODE>(v.x, v.y, M), rcp);
-      const float2 b = scale2<MODE>(sexp2<MODE>(v.z, v.w, M), rcp);
-      st_stream4(yr + 4 * q, make_float4(a.x, a.y, b.x, b.y));
+      const float2 c = scale2<MODE>(sexp2<MODE>(v.z, v.w, M), rcp);
+      st_stream4(yr + 4 * q, make_float4(a.x, a.y, c.x, c.y));
     }
     fence_proxy_async_smem();  // generic smem reads before the TMA refill
-    bar_arrive_n(3, kGresThreads);
+    bar_arrive_n(gres_bar3(j, L), kGresThreads);
   };
 
   unsigned k = 0;
-  int64_t prow = 0;
   for (int64_t row = g; row < rows; row += G, ++k) {
     const int stage = static_cast<int>(k % unsigned(nstages));
     mbar_wait(&bars[stage], (k / unsigned(nstages)) & 1u);
@@ -259,20 +272,20 @@ __global__ void __launch_bounds__(kGresThreads, 1)
     for (int q = tid; q < nvec; q += kGresCompute) {
       const float4 v = sb[q];
       const float2 a = sexp2<MODE>(v.x, v.y, mw);
-      const float2 b = sexp2<MODE>(v.z, v.w, mw);
-      acc = f2add(f2add(acc, f2pk(a.x, a.y)), f2pk(b.x, b.y));
+      const float2 c = sexp2<MODE>(v.z, v.w, mw);
+      acc = f2add(f2add(acc, f2pk(a.x, a.y)), f2pk(c.x, c.y));
     }
     const float2 acc2 = f2up(acc);
     const double sw = group_sum<32>(static_cast<double>(acc2.x + acc2.y));
     if (lane == 0) {
-      red_f[k & 1][warp] = mw;
-      red_d[k & 1][warp] = sw;
+      const int b = static_cast<int>(k % unsigned(L + 1));
+      red_f[b][warp] = mw;
+      red_d[b][warp] = sw;
     }
-    bar_arrive_n(1 + 3 * (k & 1), kGresThreads);
-    if (k > 0) output(k - 1, prow);
-    prow = row;
+    bar_arrive_n(gres_bar1(k, L), kGresThreads);
+    if (k >= unsigned(L)) output(k - unsigned(L));
   }
-  if (k > 0) output(k - 1, prow);
+  for (unsigned j = k >= unsigned(L) ? k - unsigned(L) : 0u; j < k; ++j) output(j);
 }
 
 }  // namespace sk

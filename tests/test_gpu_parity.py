@@ -31,7 +31,7 @@ def _reset_tuning():
     yield
     for k, v in (("path", -1), ("k1_lpr", 0), ("grid_mult", 0), ("seg_len", 0),
                  ("skip_max_shift", 0), ("k3_impl", 3), ("cluster_k3", 1), ("chunk_mb", 0),
-                 ("gres", 1), ("gres_p", 0), ("cluster_onex", 0)):
+                 ("gres", 1), ("gres_p", 0), ("gres_st", 0), ("cluster_onex", 0)):
         _native.set_tuning(k, v)
 
 
@@ -205,10 +205,11 @@ def test_every_k3_implementation(impl, oracle):
         _native.set_tuning("chunk_mb", 0)
 
 
-@pytest.mark.parametrize("P", [2, 3, 10, 37, 74, 148])
-def test_k3_gres_group_sizes(P, oracle):
-    """K3g with P CTAs per row (ragged last slice, one- to many-group grids,
-    more groups than rows, clip firing, a large negative row), every mode."""
+@pytest.mark.parametrize("P,st", [(2, 0), (3, 2), (10, 0), (14, 3), (37, 4), (74, 5), (148, 0)])
+def test_k3_gres_group_sizes(P, st, oracle):
+    """K3g with P CTAs per row and ring depth st (lag st-2: 1..3) -- ragged last
+    slice, one- to many-group grids, more groups than rows, clip firing, a large
+    negative row -- every mode."""
     C = 200_004 if P >= 10 else 30_004
     rows = 13
     x = configs.generate("c4", 0, rows)[:, :C].copy()
@@ -216,8 +217,11 @@ def test_k3_gres_group_sizes(P, oracle):
     x[5, :] -= 400.0
     _native.set_tuning("gres", 2)
     _native.set_tuning("gres_p", P)
+    _native.set_tuning("gres_st", st)
     try:
         assert gu.plan(rows, C).startswith("k3_gres nseg=%d " % P), gu.plan(rows, C)
+        if st:
+            assert "stages=%d " % st in gu.plan(rows, C)
         for mode in (0, 1, 2):
             ref = oracle.softmax_ref(x, clip=(mode == 0))
             y, bad = gu.softmax_abi(x, mode)
@@ -230,6 +234,7 @@ def test_k3_gres_group_sizes(P, oracle):
     finally:
         _native.set_tuning("gres", 1)
         _native.set_tuning("gres_p", 0)
+        _native.set_tuning("gres_st", 0)
 
 
 def test_k3_gres_full_c4_rowsums():
