@@ -273,12 +273,17 @@ int max_active_clusters(const void* fn, int cs, size_t smem) {
 }
 
 constexpr int64_t kGresSmemMax = 225 * 1024;  // ring bytes per K3g CTA (227 KB opt-in minus statics)
-const void* gres_fn(int mode) {
+template <int L>
+const void* gres_fn_l(int mode) {
   switch (mode) {
-    case kClipAccurate: return reinterpret_cast<const void*>(&k3_gres<kClipAccurate>);
-    case kAccurate: return reinterpret_cast<const void*>(&k3_gres<kAccurate>);
-    default: return reinterpret_cast<const void*>(&k3_gres<kApprox>);
+    case kClipAccurate: return reinterpret_cast<const void*>(&k3_gres<kClipAccurate, L>);
+    case kAccurate: return reinterpret_cast<const void*>(&k3_gres<kAccurate, L>);
+    default: return reinterpret_cast<const void*>(&k3_gres<kApprox, L>);
   }
+}
+// ring depth 2 and 3 run lag 1; 4 -> lag 2; 5 -> lag 3
+const void* gres_fn(int mode, int nstages) {
+  return nstages >= 5 ? gres_fn_l<3>(mode) : nstages == 4 ? gres_fn_l<2>(mode) : gres_fn_l<1>(mode);
 }
 
 template <int NV>
@@ -464,7 +469,6 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
       int g_p = 0, g_st = 0, g_groups = 0;
       int64_t g_slice = 0;
       if (gres != 0 && di.coop) {
-        const void* fn = gres_fn(mode);
         const double xg = std::max(0, g_gres_x.load());
         for (int P = 2; P <= std::min(di.sms, kGresMaxP); ++P) {
           if (g_gres_p.load() > 0 && P != g_gres_p.load()) continue;
@@ -478,7 +482,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
           }
           if (st < 2) continue;
           const size_t smem = size_t(st) * slice * sizeof(float);
-          const int occ = occupancy(fn, kGresThreads, smem);
+          const int occ = occupancy(gres_fn(mode, st), kGresThreads, smem);
           if (occ < 1) continue;
           const int groups = di.sms * occ / P;
           if (groups < 1) continue;
@@ -767,7 +771,7 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
       const GresWs w = gres_ws(p);
       SK_CUDA(cudaMemsetAsync(ws + w.abort, 0, w.total - w.abort, s));
       int P = p.nseg, slice = p.seglen, nst = p.lag;
-      SK_CUDA(launch_k(gres_fn(mode), dim3(static_cast<unsigned>(p.grid)), dim3(p.threads),
+      SK_CUDA(launch_k(gres_fn(mode, p.lag), dim3(static_cast<unsigned>(p.grid)), dim3(p.threads),
                        p.smem, s, true, x, y, rows, cols, ldx, ldy, P, slice, nst,
                        reinterpret_cast<unsigned long long*>(ws + w.slots),
                        reinterpret_cast<unsigned*>(ws + w.abort),

@@ -5,7 +5,7 @@
 // row needs (10-12 CTAs at 2 ring stages) pack only ~110 of the 148 SMs.  K3g
 // drops the GPC constraint: a cooperative, persistent grid of one CTA per SM
 // is cut into G = SMs / P groups of P CTAs; group g owns rows g, g+G, ... and
-// CTA `rank` of the group holds columns [rank*L, (rank+1)*L) of the row in
+// CTA `rank` of the group holds columns [rank*W, (rank+1)*W) of the row in
 // shared memory (TMA ring of NS stages, like K3c).
 //
 // One exchange per row, overlapped with the next row.  Each compute warp
@@ -98,11 +98,15 @@ __device__ __forceinline__ bool gres_valid(unsigned long long w0, unsigned long 
 // Named barrier ids for lag L (stages - 2, 1..3): a hand-off can have at most
 // L+1 (bar 1) or L (bars 2 and 3) phases outstanding, so each rotates over
 // that many ids.  Id 0 is __syncthreads.
-__device__ __forceinline__ int gres_bar1(unsigned k, int L) { return 1 + int(k % unsigned(L + 1)); }
-__device__ __forceinline__ int gres_bar2(unsigned k, int L) { return 2 + L + int(k % unsigned(L)); }
-__device__ __forceinline__ int gres_bar3(unsigned k, int L) { return 2 + 2 * L + int(k % unsigned(L)); }
+template <int L>
+__device__ __forceinline__ int gres_bar1(unsigned k) { return 1 + int(k % unsigned(L + 1)); }
+template <int L>
+__device__ __forceinline__ int gres_bar2(unsigned k) { return 2 + L + int(k % unsigned(L)); }
+template <int L>
+__device__ __forceinline__ int gres_bar3(unsigned k) { return 2 + 2 * L + int(k % unsigned(L)); }
 
-template <int MODE>
+// L: rows between a row's local pass and its output pass (ring depth L + 2)
+template <int MODE, int L>
 __global__ void __launch_bounds__(kGresThreads, 1)
     k3_gres(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
             int64_t ldx, int64_t ldy, int P, int slice, int nstages,
@@ -111,7 +115,7 @@ __global__ void __launch_bounds__(kGresThreads, 1)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage_buf = reinterpret_cast<float*>(smem_raw);
   constexpr int NW = kGresCompute / 32;
-  constexpr int NB = kGresStages - 1;  // L + 1 <= NB broadcast slots
+  constexpr int NB = L + 1;  // broadcast slots
   __shared__ uint64_t bars[kGresStages];
   __shared__ float red_f[NB][NW];   // [row % (L+1)][warp]: warp-local max
   __shared__ double red_d[NB][NW];  //                      warp-local sum vs that max
@@ -122,7 +126,6 @@ __global__ void __launch_bounds__(kGresThreads, 1)
   const int G = static_cast<int>(gridDim.x) / P;
   const int g = static_cast<int>(blockIdx.x) / P, rank = static_cast<int>(blockIdx.x) % P;
   if (g >= G) return;  // whole CTA: no barrier below is shared with it
-  const int L = nstages > 2 ? nstages - 2 : 1;  // rows between local pass and output pass
   const int64_t c0 = int64_t(rank) * slice;
   const int64_t rem = cols - c0;
   const int len = rem <= 0 ? 0 : static_cast<int>(rem < slice ? rem : slice);  // % 4 == 0
@@ -152,7 +155,7 @@ __global__ void __launch_bounds__(kGresThreads, 1)
     for (int64_t row = g; row < rows; row += G, ++k) {
       const int b = static_cast<int>(k % unsigned(L + 1));
       // CTA pair (m, s) of row k from the 16 warp pairs, fixed order
-      bar_sync_n(gres_bar1(k, L), kGresThreads);
+      bar_sync_n(gres_bar1<L>(k), kGresThreads);
       const float mw = lane < NW ? red_f[b][lane] : kPadLogit;
       const float mc = group_max<32>(mw);
       double sw = lane < NW ? red_d[b][lane] : 0.0;
@@ -170,7 +173,7 @@ __global__ void __launch_bounds__(kGresThreads, 1)
       // while the group's pairs arrive: refill the stage row k-L released
       if (k >= unsigned(L)) {
         const unsigned j = k - unsigned(L);
-        bar_sync_n(gres_bar3(j, L), kGresThreads);
+        bar_sync_n(gres_bar3<L>(j), kGresThreads);
         const int64_t rn = row - int64_t(L) * G + int64_t(nstages) * G;
         if (lane == 0 && rn < rows) issue(rn, static_cast<int>(j % unsigned(nstages)));
       }
@@ -222,11 +225,11 @@ __global__ void __launch_bounds__(kGresThreads, 1)
         bc_m[b] = Mg * shift_scale;  // shift_scale = 0: fault hook
         bc_s[b] = S;
       }
-      bar_arrive_n(gres_bar2(k, L), kGresThreads);
+      bar_arrive_n(gres_bar2<L>(k), kGresThreads);
     }
     // the last L rows' output passes
     for (unsigned j = k >= unsigned(L) ? k - unsigned(L) : 0u; j < k; ++j)
-      bar_sync_n(gres_bar3(j, L), kGresThreads);
+      bar_sync_n(gres_bar3<L>(j), kGresThreads);
     return;
   }
 
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(kGresThreads, 1)
   // row k's output pass runs after row k+L's local pass, so the group
   // exchange of row k overlaps L full rows of streaming work.
   auto output = [&](unsigned j) {
-    bar_sync_n(gres_bar2(j, L), kGresThreads);
+    bar_sync_n(gres_bar2<L>(j), kGresThreads);
     const int b = static_cast<int>(j % unsigned(L + 1));
     const float M = bc_m[b];
     const float rcp = recip_of_sum(bc_s[b]);
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(kGresThreads, 1)
       st_stream4(yr + 4 * q, make_float4(a.x, a.y, c.x, c.y));
     }
     fence_proxy_async_smem();  // generic smem reads before the TMA refill
-    bar_arrive_n(gres_bar3(j, L), kGresThreads);
+    bar_arrive_n(gres_bar3<L>(j), kGresThreads);
   };
 
   unsigned k = 0;
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(kGresThreads, 1)
       red_f[b][warp] = mw;
       red_d[b][warp] = sw;
     }
-    bar_arrive_n(gres_bar1(k, L), kGresThreads);
+    bar_arrive_n(gres_bar1<L>(k), kGresThreads);
     if (k >= unsigned(L)) output(k - unsigned(L));
   }
   for (unsigned j = k >= unsigned(L) ? k - unsigned(L) : 0u; j < k; ++j) output(j);
