@@ -39,7 +39,11 @@ def main():
         _native.set_tuning("gres_st", st)
         for d in map(int, args.diags.split(",")):
             _native.set_tuning("gres_diag", d)
-            us = bench_once(xs, ys, spec.rows, spec.cols, args.reps, s)
+            try:
+                us = bench_once(xs, ys, spec.rows, spec.cols, args.reps, s)
+            except Exception as e:  # noqa: BLE001
+                print(json.dumps({"P": P, "stages": st, "error": str(e)}), flush=True)
+                continue
             print(json.dumps({"config": spec.name, "P": P, "stages": st, "diag": d, "us": us,
                               "gbs": 8.0 * spec.rows * spec.cols / us / 1e3}), flush=True)
     _native.set_tuning("gres_diag", 0)
