@@ -482,7 +482,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
           }
           if (st < 2) continue;
           const size_t smem = size_t(st) * slice * sizeof(float);
-          const int occ = occupancy(gres_fn(mode, st), kGresThreads, smem);
+          const int occ = occupancy(gres_fn(mode, st), kGresBlock, smem);
           if (occ < 1) continue;
           const int groups = di.sms * occ / P;
           if (groups < 1) continue;
@@ -505,7 +505,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
         p.nseg = g_p;
         p.seglen = static_cast<int>(g_slice);
         p.lag = g_st;
-        p.threads = kGresThreads;
+        p.threads = kGresBlock;
         p.smem = size_t(g_st) * g_slice * sizeof(float);
         p.grid = int64_t(g_groups) * g_p;
         return SK_OK;
@@ -617,7 +617,8 @@ struct GresWs {
 GresWs gres_ws(const Plan& p) {
   GresWs w;
   const size_t groups = size_t(p.grid / p.nseg);
-  w.total = align_up(w.slots + groups * 2 * p.nseg * 16, 256);
+  const int lag = p.lag >= 5 ? 3 : p.lag == 4 ? 2 : 1;
+  w.total = align_up(w.slots + groups * gres_slot_sets(lag) * p.nseg * 16, 256);
   return w;
 }
 

@@ -22,12 +22,14 @@
 // load) therefore hides behind a full row step instead of stalling it.  Slots alternate by
 // row parity (a CTA can run at most one exchange ahead of its group).
 //
-// Warp specialisation keeps the handshake off the data path: warp 16 only
-// issues the TMA loads and does the exchanges, so its release fence never
-// waits for the compute warps' output stores to drain.  Named barriers:
-//   bar1  compute -> exchange  "warp pairs of row k in smem"
-//   bar2  exchange -> compute  "(M, S) of row k in smem"
-//   bar3  compute -> exchange  "row k's stage consumed (proxy-fenced): refill"
+// Warp specialisation keeps the handshake off the data path: warp 16 merges
+// and publishes each row's CTA pair and issues the TMA refills, warp 17 polls
+// and merges the group's pairs -- so a slow poll never delays this CTA's next
+// publication (which would chain the group into a per-row convoy), and no
+// fence ever waits on the compute warps' output stores.  Named barriers:
+//   bar1  compute -> publisher  "warp pairs of row k in smem"
+//   bar2  poller -> compute     "(M, S) of row k in smem"
+//   bar3  compute -> publisher  "row k's stage consumed (proxy-fenced): refill"
 // With a ring of NS stages the output pass of row k runs after the local pass
 // of row k+L, L = NS-2 (one row loading, L+1 resident awaiting statistics);
 // the group round trip hides behind L row steps.  HBM and L2 each see
@@ -38,7 +40,8 @@
 namespace sk {
 
 constexpr int kGresCompute = 512;                   // 16 compute warps
-constexpr int kGresThreads = kGresCompute + 32;     // + 1 exchange/TMA warp
+constexpr int kGresThreads = kGresCompute + 32;     // compute + one hand-off warp per barrier
+constexpr int kGresBlock = kGresCompute + 64;       // + publisher/TMA warp + poller warp
 constexpr int kGresStages = 5;                      // maximum ring depth (lag <= 3)
 constexpr unsigned kGresSpinLimit = 1u << 24;       // ~10 s of polling: abort, never hang
 
@@ -81,6 +84,13 @@ __device__ __forceinline__ void ld_relaxed_v2u64(const unsigned long long* p, un
 
 constexpr int kGresMaxP = 160;  // slots per lane: 5
 
+// Global slot sets per group.  A publisher can run ahead of a REMOTE poller:
+// CTA A publishing row k needs its own row k-1-L merged (all of the group
+// published k-1-L), so every CTA B has finished its local pass of k-1-L and
+// hence its output -- and its poller's read -- of row k-2-2L.  Rows
+// k-1-2L .. k may be live: 2L+2 sets.
+__host__ __device__ constexpr int gres_slot_sets(int L) { return 2 * L + 2; }
+
 // A CTA's row pair as one 16-B slot of two independently tagged 64-bit words
 // (each 64-bit access is single-copy atomic): word 0 = tag << 32 | bits(m),
 // word 1 = bits(s) with its 8 low mantissa bits replaced by the tag (2^-44
@@ -101,13 +111,13 @@ __device__ __forceinline__ bool gres_valid(unsigned long long w0, unsigned long 
 template <int L>
 __device__ __forceinline__ int gres_bar1(unsigned k) { return 1 + int(k % unsigned(L + 1)); }
 template <int L>
-__device__ __forceinline__ int gres_bar2(unsigned k) { return 2 + L + int(k % unsigned(L)); }
+__device__ __forceinline__ int gres_bar2(unsigned k) { return 2 + L + int(k % unsigned(L + 1)); }
 template <int L>
-__device__ __forceinline__ int gres_bar3(unsigned k) { return 2 + 2 * L + int(k % unsigned(L)); }
+__device__ __forceinline__ int gres_bar3(unsigned k) { return 3 + 2 * L + int(k % unsigned(L)); }
 
 // L: rows between a row's local pass and its output pass (ring depth L + 2)
 template <int MODE, int L>
-__global__ void __launch_bounds__(kGresThreads, 1)
+__global__ void __launch_bounds__(kGresBlock, 1)
     k3_gres(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
             int64_t ldx, int64_t ldy, int P, int slice, int nstages,
             unsigned long long* __restrict__ slots, unsigned* __restrict__ abort_flag,
@@ -115,7 +125,8 @@ __global__ void __launch_bounds__(kGresThreads, 1)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage_buf = reinterpret_cast<float*>(smem_raw);
   constexpr int NW = kGresCompute / 32;
-  constexpr int NB = L + 1;  // broadcast slots
+  constexpr int NB = L + 1;            // smem broadcast slots
+  constexpr int NS = gres_slot_sets(L);  // global slot sets
   __shared__ uint64_t bars[kGresStages];
   __shared__ float red_f[NB][NW];   // [row % (L+1)][warp]: warp-local max
   __shared__ double red_d[NB][NW];  //                      warp-local sum vs that max
@@ -130,6 +141,9 @@ __global__ void __launch_bounds__(kGresThreads, 1)
   const int64_t rem = cols - c0;
   const int len = rem <= 0 ? 0 : static_cast<int>(rem < slice ? rem : slice);  // % 4 == 0
   const int nvec = len >> 2;
+  auto slot_set = [&](unsigned k) {  // [P] x 16 B for row k of this group
+    return slots + (size_t(g) * NS + k % unsigned(NS)) * size_t(P) * 2;
+  };
 
   if (tid == 0) {
     for (int s = 0; s < nstages; ++s) mbar_init(&bars[s], 1);
@@ -139,7 +153,7 @@ __global__ void __launch_bounds__(kGresThreads, 1)
   pdl_wait();
 
   if (warp == NW) {
-    // ------------------------------------------------ exchange + TMA warp
+    // ------------------------------------------------ publisher + TMA warp
     auto issue = [&](int64_t row, int stage) {
       mbar_arrive_expect_tx(&bars[stage], static_cast<uint32_t>(len) * 4u);
       if (len > 0)
@@ -153,7 +167,7 @@ __global__ void __launch_bounds__(kGresThreads, 1)
       }
     unsigned k = 0;
     for (int64_t row = g; row < rows; row += G, ++k) {
-      const int b = static_cast<int>(k % unsigned(L + 1));
+      const int b = static_cast<int>(k % unsigned(NB));
       // CTA pair (m, s) of row k from the 16 warp pairs, fixed order
       bar_sync_n(gres_bar1<L>(k), kGresThreads);
       const float mw = lane < NW ? red_f[b][lane] : kPadLogit;
@@ -161,75 +175,75 @@ __global__ void __launch_bounds__(kGresThreads, 1)
       double sw = lane < NW ? red_d[b][lane] : 0.0;
       if (lane < NW && mw != mc) sw *= static_cast<double>(expf(mw - mc));
       const double sc = group_sum<32>(sw);
-      // slot array of this group and row parity: [P] x 16 B.  Parity suffices:
-      // a CTA publishes row k+1 only after merging row k.
-      unsigned long long* sl = slots + (size_t(g) * 2 + (k & 1)) * size_t(P) * 2;
-      const unsigned tag = k + 1u;  // never 0: the per-launch memset reads as "not yet"
-      if (lane == 0 && !(diag & 1)) {
+      if (lane == 0) {
         unsigned long long w0, w1;
-        gres_pack(mc, sc, tag, w0, w1);
-        st_relaxed_v2u64(sl + 2 * rank, w0, w1);
+        gres_pack(mc, sc, k + 1u, w0, w1);
+        st_relaxed_v2u64(slot_set(k) + 2 * rank, w0, w1);
       }
-      // while the group's pairs arrive: refill the stage row k-L released
+      // refill the stage row k-L released
       if (k >= unsigned(L)) {
         const unsigned j = k - unsigned(L);
         bar_sync_n(gres_bar3<L>(j), kGresThreads);
         const int64_t rn = row - int64_t(L) * G + int64_t(nstages) * G;
         if (lane == 0 && rn < rows) issue(rn, static_cast<int>(j % unsigned(nstages)));
       }
-      float Mg;
-      double S;
-      if (diag & 1) {  // timing diagnostic only: CTA-local statistics, no exchange
-        Mg = mc;
-        S = sc;
-      } else {
-        // poll the P slots (lane j reads slots j, j+32, ...) until all carry the tag
-        unsigned long long w0[kGresMaxP / 32], w1[kGresMaxP / 32];
-        unsigned spins = 0;
-        while (true) {
-          bool ok = true;
+    }
+    for (unsigned j = k >= unsigned(L) ? k - unsigned(L) : 0u; j < k; ++j)
+      bar_sync_n(gres_bar3<L>(j), kGresThreads);  // the last L output passes
+    return;
+  }
+
+  if (warp == NW + 1) {
+    // ------------------------------------------------ poller warp
+    // diag & 1 (timing only): wait for this CTA's own slot, not the group's
+    const int pp = (diag & 1) ? 1 : P;
+    unsigned k = 0;
+    for (int64_t row = g; row < rows; row += G, ++k) {
+      const unsigned long long* sl = slot_set(k);
+      const unsigned tag = k + 1u;  // never 0: the per-launch memset reads as "not yet"
+      unsigned long long w0[kGresMaxP / 32], w1[kGresMaxP / 32];
+      unsigned spins = 0;
+      while (true) {  // lane l reads slots l, l+32, ... until all carry the tag
+        bool ok = true;
 #pragma unroll
-          for (int i = 0; i < kGresMaxP / 32; ++i) {
-            const int j = lane + 32 * i;
-            if (j < P) {
-              ld_relaxed_v2u64(sl + 2 * j, w0[i], w1[i]);
-              ok = ok && gres_valid(w0[i], w1[i], tag);
-            }
-          }
-          if (__all_sync(0xffffffffu, ok)) break;
-          if ((++spins & 0xFFFu) == 0) {  // a stuck peer raises abort: never hang the GPU
-            if (ld_relaxed_u32(abort_flag) || spins >= kGresSpinLimit) {
-              if (lane == 0) atomicExch(abort_flag, 1u);
-              break;
-            }
+        for (int i = 0; i < kGresMaxP / 32; ++i) {
+          const int j = lane + 32 * i;
+          if (j < pp) {
+            ld_relaxed_v2u64(sl + 2 * ((diag & 1) ? rank : j), w0[i], w1[i]);
+            ok = ok && gres_valid(w0[i], w1[i], tag);
           }
         }
-        // merge the P pairs in rank order: identical (M, S) in every CTA of the row
-        Mg = kPadLogit;
-#pragma unroll
-        for (int i = 0; i < kGresMaxP / 32; ++i)
-          if (lane + 32 * i < P) Mg = fmaxf(Mg, __uint_as_float(static_cast<unsigned>(w0[i])));
-        Mg = group_max<32>(Mg);
-        S = 0.0;
-#pragma unroll
-        for (int i = 0; i < kGresMaxP / 32; ++i)
-          if (lane + 32 * i < P) {
-            const float mj = __uint_as_float(static_cast<unsigned>(w0[i]));
-            double sj = __longlong_as_double(static_cast<long long>(w1[i]));
-            if (mj != Mg) sj *= static_cast<double>(expf(mj - Mg));
-            S += sj;
+        if (__all_sync(0xffffffffu, ok)) break;
+        if ((++spins & 0xFFFu) == 0) {  // a stuck peer raises abort: never hang the GPU
+          if (ld_relaxed_u32(abort_flag) || spins >= kGresSpinLimit) {
+            if (lane == 0) atomicExch(abort_flag, 1u);
+            break;
           }
-        S = group_sum<32>(S);
+        }
       }
+      // merge the P pairs in rank order: identical (M, S) in every CTA of the row
+      float Mg = kPadLogit;
+#pragma unroll
+      for (int i = 0; i < kGresMaxP / 32; ++i)
+        if (lane + 32 * i < pp) Mg = fmaxf(Mg, __uint_as_float(static_cast<unsigned>(w0[i])));
+      Mg = group_max<32>(Mg);
+      double S = 0.0;
+#pragma unroll
+      for (int i = 0; i < kGresMaxP / 32; ++i)
+        if (lane + 32 * i < pp) {
+          const float mj = __uint_as_float(static_cast<unsigned>(w0[i]));
+          double sj = __longlong_as_double(static_cast<long long>(w1[i]));
+          if (mj != Mg) sj *= static_cast<double>(expf(mj - Mg));
+          S += sj;
+        }
+      S = group_sum<32>(S);
       if (lane == 0) {
+        const int b = static_cast<int>(k % unsigned(NB));
         bc_m[b] = Mg * shift_scale;  // shift_scale = 0: fault hook
         bc_s[b] = S;
       }
       bar_arrive_n(gres_bar2<L>(k), kGresThreads);
     }
-    // the last L rows' output passes
-    for (unsigned j = k >= unsigned(L) ? k - unsigned(L) : 0u; j < k; ++j)
-      bar_sync_n(gres_bar3<L>(j), kGresThreads);
     return;
   }
 
@@ -238,7 +252,7 @@ __global__ void __launch_bounds__(kGresThreads, 1)
   // exchange of row k overlaps L full rows of streaming work.
   auto output = [&](unsigned j) {
     bar_sync_n(gres_bar2<L>(j), kGresThreads);
-    const int b = static_cast<int>(j % unsigned(L + 1));
+    const int b = static_cast<int>(j % unsigned(NB));
     const float M = bc_m[b];
     const float rcp = recip_of_sum(bc_s[b]);
     const float4* sb = reinterpret_cast<const float4*>(stage_buf + size_t(j % unsigned(nstages)) * slice);
@@ -281,7 +295,7 @@ __global__ void __launch_bounds__(kGresThreads, 1)
     const float2 acc2 = f2up(acc);
     const double sw = group_sum<32>(static_cast<double>(acc2.x + acc2.y));
     if (lane == 0) {
-      const int b = static_cast<int>(k % unsigned(L + 1));
+      const int b = static_cast<int>(k % unsigned(NB));
       red_f[b][warp] = mw;
       red_d[b][warp] = sw;
     }

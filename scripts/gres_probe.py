@@ -23,7 +23,8 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--points", default="14:3,16:3,20:4,24:4", help="P:stages,...")
     ap.add_argument("--reps", type=int, default=60)
-    ap.add_argument("--diags", default="0,1")
+    ap.add_argument("--diags", default="0,1",
+                    help="gres_diag values: bit 0 skips the exchange, bits 8+ = poll back-off ns")
     args = ap.parse_args()
     spec = configs.get(args.config)
     x0 = torch.from_numpy(configs.generate(spec)).cuda()
