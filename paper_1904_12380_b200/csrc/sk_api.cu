@@ -100,7 +100,8 @@ std::atomic<int> g_vec8{0};          // 256-bit K1 path (measured no faster: off
 std::atomic<int> g_gres{1};       // K3g grid-resident rows: 0 off, 1 when it out-scores K3c, 2 force
 std::atomic<int> g_gres_p{0};     // force K3g CTAs per row (0 = auto)
 std::atomic<int> g_gres_diag{0};  // K3g timing diagnostics (1: skip the group exchange -- wrong results)
-std::atomic<int> g_gres_st{0};    // force K3g ring depth (0 = as deep as smem allows)
+std::atomic<int> g_gres_st{0};
+std::atomic<int> g_gres_sleep{128};  // K3g poller back-off between polls (ns)    // force K3g ring depth (0 = as deep as smem allows)
 std::atomic<int> g_gres_x{12288}; // K3g per-row exchange cost model, in floats of streaming time
 std::atomic<int> g_k3_impl{3};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
 
@@ -776,7 +777,7 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
                        p.smem, s, true, x, y, rows, cols, ldx, ldy, P, slice, nst,
                        reinterpret_cast<unsigned long long*>(ws + w.slots),
                        reinterpret_cast<unsigned*>(ws + w.abort),
-                       bad, sh, g_gres_diag.load()));
+                       bad, sh, g_gres_sleep.load(), g_gres_diag.load()));
     } else if (p.k3 == 5) {
       const void* fn = p.seglen == 2048 ? reg3_fn<16>(mode)
                        : p.seglen == 512 ? reg3_fn<4>(mode) : reg3_fn<8>(mode);
@@ -960,6 +961,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "gres_x") g_gres_x = value;
   else if (k == "gres_st") g_gres_st = value;
   else if (k == "gres_diag") g_gres_diag = value;
+  else if (k == "gres_sleep") g_gres_sleep = value;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;
 }

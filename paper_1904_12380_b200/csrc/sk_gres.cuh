@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kGresBlock, 1)
     k3_gres(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
             int64_t ldx, int64_t ldy, int P, int slice, int nstages,
             unsigned long long* __restrict__ slots, unsigned* __restrict__ abort_flag,
-            unsigned long long* __restrict__ bad_row, float shift_scale, int diag) {
+            unsigned long long* __restrict__ bad_row, float shift_scale, int poll_ns, int diag) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage_buf = reinterpret_cast<float*>(smem_raw);
   constexpr int NW = kGresCompute / 32;
@@ -214,6 +214,8 @@ __global__ void __launch_bounds__(kGresBlock, 1)
           }
         }
         if (__all_sync(0xffffffffu, ok)) break;
+        // back off: a spinning poller steals issue slots from its sub-partition's compute warps
+        if (poll_ns > 0) __nanosleep(static_cast<unsigned>(poll_ns));
         if ((++spins & 0xFFFu) == 0) {  // a stuck peer raises abort: never hang the GPU
           if (ld_relaxed_u32(abort_flag) || spins >= kGresSpinLimit) {
             if (lane == 0) atomicExch(abort_flag, 1u);
