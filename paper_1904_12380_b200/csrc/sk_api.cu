@@ -101,7 +101,12 @@ std::atomic<int> g_gres{1};       // K3g grid-resident rows: 0 off, 1 when it ou
 std::atomic<int> g_gres_p{0};     // force K3g CTAs per row (0 = auto)
 std::atomic<int> g_gres_diag{0};  // K3g timing diagnostics (1: skip the group exchange -- wrong results)
 std::atomic<int> g_gres_st{0};
-std::atomic<int> g_gres_sleep{128};  // K3g poller back-off between polls (ns)    // force K3g ring depth (0 = as deep as smem allows)
+std::atomic<int> g_gres_sleep{128};
+std::atomic<int> g_gres_split{-1};   // K3g poller warp: -1 auto (lag >= 2), 0 off, 1 on
+bool gres_split(int nstages) {
+  const int v = g_gres_split.load();
+  return v < 0 ? nstages >= 4 : v != 0;
+}  // K3g poller back-off between polls (ns)    // force K3g ring depth (0 = as deep as smem allows)
 std::atomic<int> g_gres_x{12288}; // K3g per-row exchange cost model, in floats of streaming time
 std::atomic<int> g_k3_impl{3};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
 
@@ -273,18 +278,23 @@ int max_active_clusters(const void* fn, int cs, size_t smem) {
   return n;
 }
 
+bool gres_split(int nstages);
 constexpr int64_t kGresSmemMax = 225 * 1024;  // ring bytes per K3g CTA (227 KB opt-in minus statics)
-template <int L>
+template <int L, bool SPLIT>
 const void* gres_fn_l(int mode) {
   switch (mode) {
-    case kClipAccurate: return reinterpret_cast<const void*>(&k3_gres<kClipAccurate, L>);
-    case kAccurate: return reinterpret_cast<const void*>(&k3_gres<kAccurate, L>);
-    default: return reinterpret_cast<const void*>(&k3_gres<kApprox, L>);
+    case kClipAccurate: return reinterpret_cast<const void*>(&k3_gres<kClipAccurate, L, SPLIT>);
+    case kAccurate: return reinterpret_cast<const void*>(&k3_gres<kAccurate, L, SPLIT>);
+    default: return reinterpret_cast<const void*>(&k3_gres<kApprox, L, SPLIT>);
   }
 }
 // ring depth 2 and 3 run lag 1; 4 -> lag 2; 5 -> lag 3
-const void* gres_fn(int mode, int nstages) {
-  return nstages >= 5 ? gres_fn_l<3>(mode) : nstages == 4 ? gres_fn_l<2>(mode) : gres_fn_l<1>(mode);
+const void* gres_fn(int mode, int nstages, bool split) {
+  if (split)
+    return nstages >= 5 ? gres_fn_l<3, true>(mode)
+           : nstages == 4 ? gres_fn_l<2, true>(mode) : gres_fn_l<1, true>(mode);
+  return nstages >= 5 ? gres_fn_l<3, false>(mode)
+         : nstages == 4 ? gres_fn_l<2, false>(mode) : gres_fn_l<1, false>(mode);
 }
 
 template <int NV>
@@ -483,7 +493,8 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
           }
           if (st < 2) continue;
           const size_t smem = size_t(st) * slice * sizeof(float);
-          const int occ = occupancy(gres_fn(mode, st), kGresBlock, smem);
+          const bool split = gres_split(st);
+          const int occ = occupancy(gres_fn(mode, st, split), split ? kGresBlock : kGresThreads, smem);
           if (occ < 1) continue;
           const int groups = di.sms * occ / P;
           if (groups < 1) continue;
@@ -506,7 +517,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
         p.nseg = g_p;
         p.seglen = static_cast<int>(g_slice);
         p.lag = g_st;
-        p.threads = kGresBlock;
+        p.threads = gres_split(g_st) ? kGresBlock : kGresThreads;
         p.smem = size_t(g_st) * g_slice * sizeof(float);
         p.grid = int64_t(g_groups) * g_p;
         return SK_OK;
@@ -773,7 +784,7 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
       const GresWs w = gres_ws(p);
       SK_CUDA(cudaMemsetAsync(ws + w.abort, 0, w.total - w.abort, s));
       int P = p.nseg, slice = p.seglen, nst = p.lag;
-      SK_CUDA(launch_k(gres_fn(mode, p.lag), dim3(static_cast<unsigned>(p.grid)), dim3(p.threads),
+      SK_CUDA(launch_k(gres_fn(mode, p.lag, p.threads == kGresBlock), dim3(static_cast<unsigned>(p.grid)), dim3(p.threads),
                        p.smem, s, true, x, y, rows, cols, ldx, ldy, P, slice, nst,
                        reinterpret_cast<unsigned long long*>(ws + w.slots),
                        reinterpret_cast<unsigned*>(ws + w.abort),
@@ -962,6 +973,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "gres_st") g_gres_st = value;
   else if (k == "gres_diag") g_gres_diag = value;
   else if (k == "gres_sleep") g_gres_sleep = value;
+  else if (k == "gres_split") g_gres_split = value;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;
 }

@@ -115,8 +115,10 @@ __device__ __forceinline__ int gres_bar2(unsigned k) { return 2 + L + int(k % un
 template <int L>
 __device__ __forceinline__ int gres_bar3(unsigned k) { return 3 + 2 * L + int(k % unsigned(L)); }
 
-// L: rows between a row's local pass and its output pass (ring depth L + 2)
-template <int MODE, int L>
+// L: rows between a row's local pass and its output pass (ring depth L + 2).
+// SPLIT: a separate poller warp (block 576) vs the publisher warp polling
+// after each publication (block 544).
+template <int MODE, int L, bool SPLIT>
 __global__ void __launch_bounds__(kGresBlock, 1)
     k3_gres(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
             int64_t ldx, int64_t ldy, int P, int slice, int nstages,
@@ -151,6 +153,57 @@ __global__ void __launch_bounds__(kGresBlock, 1)
   }
   __syncthreads();
   pdl_wait();
+
+  // wait for the group's pairs of row k, merge them in rank order (identical
+  // (M, S) in every CTA of the row) and broadcast through smem slot k % NB.
+  // diag & 1 (timing only): wait for this CTA's own slot, not the group's.
+  auto poll_merge = [&](unsigned k) {
+    const int pp = (diag & 1) ? 1 : P;
+    const unsigned long long* sl = slot_set(k);
+    const unsigned tag = k + 1u;  // never 0: the per-launch memset reads as "not yet"
+    unsigned long long w0[kGresMaxP / 32], w1[kGresMaxP / 32];
+    unsigned spins = 0;
+    while (true) {  // lane l reads slots l, l+32, ... until all carry the tag
+      bool ok = true;
+#pragma unroll
+      for (int i = 0; i < kGresMaxP / 32; ++i) {
+        const int j = lane + 32 * i;
+        if (j < pp) {
+          ld_relaxed_v2u64(sl + 2 * ((diag & 1) ? rank : j), w0[i], w1[i]);
+          ok = ok && gres_valid(w0[i], w1[i], tag);
+        }
+      }
+      if (__all_sync(0xffffffffu, ok)) break;
+      // back off: a spinning poller steals issue slots from its sub-partition's compute warps
+      if (SPLIT && poll_ns > 0) __nanosleep(static_cast<unsigned>(poll_ns));
+      if ((++spins & 0xFFFu) == 0) {  // a stuck peer raises abort: never hang the GPU
+        if (ld_relaxed_u32(abort_flag) || spins >= kGresSpinLimit) {
+          if (lane == 0) atomicExch(abort_flag, 1u);
+          break;
+        }
+      }
+    }
+    float Mg = kPadLogit;
+#pragma unroll
+    for (int i = 0; i < kGresMaxP / 32; ++i)
+      if (lane + 32 * i < pp) Mg = fmaxf(Mg, __uint_as_float(static_cast<unsigned>(w0[i])));
+    Mg = group_max<32>(Mg);
+    double S = 0.0;
+#pragma unroll
+    for (int i = 0; i < kGresMaxP / 32; ++i)
+      if (lane + 32 * i < pp) {
+        const float mj = __uint_as_float(static_cast<unsigned>(w0[i]));
+        double sj = __longlong_as_double(static_cast<long long>(w1[i]));
+        if (mj != Mg) sj *= static_cast<double>(expf(mj - Mg));
+        S += sj;
+      }
+    S = group_sum<32>(S);
+    if (lane == 0) {
+      const int b = static_cast<int>(k % unsigned(NB));
+      bc_m[b] = Mg * shift_scale;  // shift_scale = 0: fault hook
+      bc_s[b] = S;
+    }
+  };
 
   if (warp == NW) {
     // ------------------------------------------------ publisher + TMA warp
@@ -187,63 +240,21 @@ __global__ void __launch_bounds__(kGresBlock, 1)
         const int64_t rn = row - int64_t(L) * G + int64_t(nstages) * G;
         if (lane == 0 && rn < rows) issue(rn, static_cast<int>(j % unsigned(nstages)));
       }
+      if (!SPLIT) {
+        poll_merge(k);
+        bar_arrive_n(gres_bar2<L>(k), kGresThreads);
+      }
     }
     for (unsigned j = k >= unsigned(L) ? k - unsigned(L) : 0u; j < k; ++j)
       bar_sync_n(gres_bar3<L>(j), kGresThreads);  // the last L output passes
     return;
   }
 
-  if (warp == NW + 1) {
+  if (SPLIT && warp == NW + 1) {
     // ------------------------------------------------ poller warp
-    // diag & 1 (timing only): wait for this CTA's own slot, not the group's
-    const int pp = (diag & 1) ? 1 : P;
     unsigned k = 0;
     for (int64_t row = g; row < rows; row += G, ++k) {
-      const unsigned long long* sl = slot_set(k);
-      const unsigned tag = k + 1u;  // never 0: the per-launch memset reads as "not yet"
-      unsigned long long w0[kGresMaxP / 32], w1[kGresMaxP / 32];
-      unsigned spins = 0;
-      while (true) {  // lane l reads slots l, l+32, ... until all carry the tag
-        bool ok = true;
-#pragma unroll
-        for (int i = 0; i < kGresMaxP / 32; ++i) {
-          const int j = lane + 32 * i;
-          if (j < pp) {
-            ld_relaxed_v2u64(sl + 2 * ((diag & 1) ? rank : j), w0[i], w1[i]);
-            ok = ok && gres_valid(w0[i], w1[i], tag);
-          }
-        }
-        if (__all_sync(0xffffffffu, ok)) break;
-        // back off: a spinning poller steals issue slots from its sub-partition's compute warps
-        if (poll_ns > 0) __nanosleep(static_cast<unsigned>(poll_ns));
-        if ((++spins & 0xFFFu) == 0) {  // a stuck peer raises abort: never hang the GPU
-          if (ld_relaxed_u32(abort_flag) || spins >= kGresSpinLimit) {
-            if (lane == 0) atomicExch(abort_flag, 1u);
-            break;
-          }
-        }
-      }
-      // merge the P pairs in rank order: identical (M, S) in every CTA of the row
-      float Mg = kPadLogit;
-#pragma unroll
-      for (int i = 0; i < kGresMaxP / 32; ++i)
-        if (lane + 32 * i < pp) Mg = fmaxf(Mg, __uint_as_float(static_cast<unsigned>(w0[i])));
-      Mg = group_max<32>(Mg);
-      double S = 0.0;
-#pragma unroll
-      for (int i = 0; i < kGresMaxP / 32; ++i)
-        if (lane + 32 * i < pp) {
-          const float mj = __uint_as_float(static_cast<unsigned>(w0[i]));
-          double sj = __longlong_as_double(static_cast<long long>(w1[i]));
-          if (mj != Mg) sj *= static_cast<double>(expf(mj - Mg));
-          S += sj;
-        }
-      S = group_sum<32>(S);
-      if (lane == 0) {
-        const int b = static_cast<int>(k % unsigned(NB));
-        bc_m[b] = Mg * shift_scale;  // shift_scale = 0: fault hook
-        bc_s[b] = S;
-      }
+      poll_merge(k);
       bar_arrive_n(gres_bar2<L>(k), kGresThreads);
     }
     return;

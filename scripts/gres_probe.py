@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--reps", type=int, default=60)
     ap.add_argument("--diags", default="0,1", help="gres_diag values: 1 skips the group exchange")
     ap.add_argument("--sleeps", default="128", help="poller back-off values (ns)")
+    ap.add_argument("--splits", default="-1", help="poller warp: -1 auto, 0 off, 1 on")
     args = ap.parse_args()
     spec = configs.get(args.config)
     x0 = torch.from_numpy(configs.generate(spec)).cuda()
@@ -38,16 +39,18 @@ def main():
         P, st = map(int, pt.split(":"))
         _native.set_tuning("gres_p", P)
         _native.set_tuning("gres_st", st)
-        for d, sl in [(d, sl) for d in map(int, args.diags.split(","))
-                      for sl in map(int, args.sleeps.split(","))]:
+        for d, sl, sp in [(d, sl, sp) for d in map(int, args.diags.split(","))
+                          for sl in map(int, args.sleeps.split(","))
+                          for sp in map(int, args.splits.split(","))]:
             _native.set_tuning("gres_diag", d)
             _native.set_tuning("gres_sleep", sl)
+            _native.set_tuning("gres_split", sp)
             try:
                 us = bench_once(xs, ys, spec.rows, spec.cols, args.reps, s)
             except Exception as e:  # noqa: BLE001
                 print(json.dumps({"P": P, "stages": st, "error": str(e)}), flush=True)
                 continue
-            print(json.dumps({"config": spec.name, "P": P, "stages": st, "diag": d, "sleep": sl, "us": us,
+            print(json.dumps({"config": spec.name, "P": P, "stages": st, "diag": d, "sleep": sl, "split": sp, "us": us,
                               "gbs": 8.0 * spec.rows * spec.cols / us / 1e3}), flush=True)
     _native.set_tuning("gres_diag", 0)
 

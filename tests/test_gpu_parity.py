@@ -31,7 +31,7 @@ def _reset_tuning():
     yield
     for k, v in (("path", -1), ("k1_lpr", 0), ("grid_mult", 0), ("seg_len", 0),
                  ("skip_max_shift", 0), ("k3_impl", 3), ("cluster_k3", 1), ("chunk_mb", 0),
-                 ("gres", 1), ("gres_p", 0), ("gres_st", 0), ("cluster_onex", 0)):
+                 ("gres", 1), ("gres_p", 0), ("gres_st", 0), ("gres_split", -1), ("cluster_onex", 0)):
         _native.set_tuning(k, v)
 
 
@@ -205,8 +205,10 @@ def test_every_k3_implementation(impl, oracle):
         _native.set_tuning("chunk_mb", 0)
 
 
-@pytest.mark.parametrize("P,st", [(2, 0), (3, 2), (10, 0), (14, 3), (37, 4), (74, 5), (148, 0)])
-def test_k3_gres_group_sizes(P, st, oracle):
+@pytest.mark.parametrize("P,st,split", [(2, 0, -1), (3, 2, 1), (10, 0, 1), (14, 3, -1), (14, 3, 1),
+                                        (37, 4, -1), (37, 4, 0), (74, 5, -1), (74, 5, 0),
+                                        (148, 0, -1)])
+def test_k3_gres_group_sizes(P, st, split, oracle):
     """K3g with P CTAs per row and ring depth st (lag st-2: 1..3) -- ragged last
     slice, one- to many-group grids, more groups than rows, clip firing, a large
     negative row -- every mode."""
@@ -218,6 +220,7 @@ def test_k3_gres_group_sizes(P, st, oracle):
     _native.set_tuning("gres", 2)
     _native.set_tuning("gres_p", P)
     _native.set_tuning("gres_st", st)
+    _native.set_tuning("gres_split", split)
     try:
         assert gu.plan(rows, C).startswith("k3_gres nseg=%d " % P), gu.plan(rows, C)
         if st:
@@ -235,6 +238,7 @@ def test_k3_gres_group_sizes(P, st, oracle):
         _native.set_tuning("gres", 1)
         _native.set_tuning("gres_p", 0)
         _native.set_tuning("gres_st", 0)
+        _native.set_tuning("gres_split", -1)
 
 
 def test_k3_gres_full_c4_rowsums():
