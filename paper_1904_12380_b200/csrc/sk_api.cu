@@ -107,7 +107,7 @@ bool gres_split(int nstages) {
   const int v = g_gres_split.load();
   return v < 0 ? nstages >= 4 : v != 0;
 }  // K3g poller back-off between polls (ns)    // force K3g ring depth (0 = as deep as smem allows)
-std::atomic<int> g_gres_x{12288}; // K3g per-row exchange cost model, in floats of streaming time
+std::atomic<int> g_gres_x{8192};  // K3g per-row exchange cost model, in floats of streaming time
 std::atomic<int> g_k3_impl{3};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
 
 // Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.
@@ -500,8 +500,13 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
           if (groups < 1) continue;
           const int64_t rows_g = (rows + groups - 1) / groups;  // exchange counter range
           if (rows_g >= (int64_t(1) << 31)) continue;  // 32-bit slot tags
+          // SMs covered x per-step efficiency (the exchange costs ~xg floats of
+          // streaming per row step when it is not hidden); a 2-stage ring
+          // cannot overlap it at all, deeper rings hide more (measured c4 /
+          // c5b: 14x3 170 us, 20x4 187, 10x2 229; 74x4 1530, 74x3 1690, 48x2 1775)
           const double score = double(std::min<int64_t>(groups, rows)) * P / occ *
-                               double(slice) / (double(slice) + xg);
+                               double(slice) / (double(slice) + xg) *
+                               (st == 2 ? 0.8 : 1.0) * (1.0 + 0.01 * st);
           if (score > best_g) {
             best_g = score;
             g_p = P;
