@@ -448,7 +448,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     // anywhere on the chip, global-memory exchange).  Each candidate is scored
     // as SMs covered x per-row efficiency slice / (slice + exchange cost).
     const int gres = g_gres.load();
-    if (cols > kSegCap && (impl0 == 5 || impl0 == 3)) {
+    if ((cols > kSegCap || gres == 2) && (impl0 == 5 || impl0 == 3)) {
       double best_c = 0.0, best_g = 0.0;
       int c_cs = 0, c_st = 0, c_n = 0;
       int64_t c_slice = 0;
@@ -481,7 +481,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
       int64_t g_slice = 0;
       if (gres != 0 && di.coop) {
         const double xg = std::max(0, g_gres_x.load());
-        for (int P = 2; P <= std::min(di.sms, kGresMaxP); ++P) {
+        for (int P = 1; P <= std::min(di.sms, kGresMaxP); ++P) {
           if (g_gres_p.load() > 0 && P != g_gres_p.load()) continue;
           const int64_t slice = align_up((cols + P - 1) / P, 4);
           if ((P - 1) * slice >= cols) continue;

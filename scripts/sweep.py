@@ -61,6 +61,31 @@ def bench_once(x, ys, rows, cols, reps, stream):
     return e0.elapsed_time(e1) * 1e3 / (n * G)
 
 
+def resident(record, xs, ys, rows, cols, args, s):
+    """K3c vs K3g (group sizes x ring depths) vs split, on the same buffers."""
+    _native.set_tuning("gres", 0)
+    try:
+        record("k3_cluster (gres off)", bench_once(xs, ys, rows, cols, args.reps, s))
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"variant": "k3_cluster", "error": str(e)}))
+    _native.set_tuning("gres", 2)
+    for gp in map(int, args.gres_ps.split(",")):
+        for gs in map(int, args.gres_st.split(",")):
+            _native.set_tuning("gres_p", gp)
+            _native.set_tuning("gres_st", gs)
+            try:
+                record(f"k3_gres P={gp or 'auto'} st={gs or 'auto'}",
+                       bench_once(xs, ys, rows, cols, args.reps, s))
+            except Exception as e:  # noqa: BLE001
+                print(json.dumps({"variant": f"gres {gp} st {gs}", "error": str(e)}))
+    _native.set_tuning("gres_p", 0)
+    _native.set_tuning("gres_st", 0)
+    _native.set_tuning("gres", 1)
+    _native.set_tuning("path", 2)
+    record("split(k4)", bench_once(xs, ys, rows, cols, max(10, args.reps // 4), s))
+    _native.set_tuning("path", -1)
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--config", default="c2")
@@ -100,7 +125,9 @@ def main():
         out.append(d)
 
     record("default", bench_once(xs, ys, rows, cols, args.reps, s))
-    if 1024 < cols <= 8192:
+    if cols > 1024 and args.only_resident:
+        resident(record, xs, ys, rows, cols, args, s)
+    elif 1024 < cols <= 8192:
         for path in (2,):
             _native.set_tuning("path", path)
             record(f"path={path}", bench_once(xs, ys, rows, cols, args.reps, s))
@@ -126,28 +153,6 @@ def main():
         _native.set_tuning("k1_lpr", 0)
         _native.set_tuning("k1_pf", -1)
         _native.set_tuning("grid_mult", 0)
-    elif args.only_resident:
-        _native.set_tuning("gres", 0)
-        try:
-            record("k3_cluster (gres off)", bench_once(xs, ys, rows, cols, args.reps, s))
-        except Exception as e:  # noqa: BLE001
-            print(json.dumps({"variant": "k3_cluster", "error": str(e)}))
-        _native.set_tuning("gres", 2)
-        for gp in map(int, args.gres_ps.split(",")):
-            for gs in map(int, args.gres_st.split(",")):
-                _native.set_tuning("gres_p", gp)
-                _native.set_tuning("gres_st", gs)
-                try:
-                    record(f"k3_gres P={gp or 'auto'} st={gs or 'auto'}",
-                           bench_once(xs, ys, rows, cols, args.reps, s))
-                except Exception as e:  # noqa: BLE001
-                    print(json.dumps({"variant": f"gres {gp} st {gs}", "error": str(e)}))
-        _native.set_tuning("gres_p", 0)
-        _native.set_tuning("gres_st", 0)
-        _native.set_tuning("gres", 1)
-        _native.set_tuning("path", 2)
-        record("split(k4)", bench_once(xs, ys, rows, cols, max(10, args.reps // 4), s))
-        _native.set_tuning("path", -1)
     else:
         _native.set_tuning("pdl", 0)
         record("default pdl=0", bench_once(xs, ys, rows, cols, args.reps, s))
