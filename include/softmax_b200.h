@@ -54,6 +54,9 @@ enum sk_mode { SK_MODE_CLIPPED = 0, SK_MODE_EXACT = 1, SK_MODE_APPROX = 2 };
 
 /* Sentinel stored in *bad_row when no non-finite input was seen. */
 #define SK_NO_BAD_ROW 0xFFFFFFFFFFFFFFFFull
+/* written into *bad_row when a cross-CTA / cross-GPU row-statistics exchange
+ * timed out (a peer never arrived); the output is then undefined. */
+#define SK_EXCHANGE_ABORTED 0xFFFFFFFFFFFFFFFEull
 
 int sk_abi_version(void);
 const char* sk_status_string(int status);

@@ -481,7 +481,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
       int64_t g_slice = 0;
       if (gres != 0 && di.coop) {
         const double xg = std::max(0, g_gres_x.load());
-        for (int P = 1; P <= std::min(di.sms, kGresMaxP); ++P) {
+        for (int P = 1; P <= std::min(di.sms, kGresMaxSlots); ++P) {
           if (g_gres_p.load() > 0 && P != g_gres_p.load()) continue;
           const int64_t slice = align_up((cols + P - 1) / P, 4);
           if ((P - 1) * slice >= cols) continue;
@@ -626,22 +626,40 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
   return plan_split(rows, cols, p);
 }
 
-// K3g control block: abort flag | slots [group][row parity][P] x 16 B, all
-// zeroed per launch (a zero slot never carries a valid tag).
+// K3g control block: ctl words (epoch, finished CTAs, abort) | slot sets
+// [group][2L+2][P] x 32 B.  Slots are epoch-tagged, so a block that persists
+// across launches (the library's, below) is never cleared; a caller-supplied
+// workspace is cleared before every launch instead (epoch restarts at 0).
 struct GresWs {
-  size_t abort = 256, slots = 512, total = 0;
+  size_t ctl = 0, slots = 256, total = 0;
 };
 GresWs gres_ws(const Plan& p) {
   GresWs w;
   const size_t groups = size_t(p.grid / p.nseg);
   const int lag = p.lag >= 5 ? 3 : p.lag == 4 ? 2 : 1;
-  w.total = align_up(w.slots + groups * gres_slot_sets(lag) * p.nseg * 16, 256);
+  w.total = align_up(w.slots + groups * gres_slot_sets(lag) * p.nseg * 32, 256);
   return w;
+}
+constexpr size_t kGresWsMax = size_t(1) << 20;  // >= any single-device plan (<= 444 CTAs x 8 sets x 32 B)
+
+// Library-owned K3g control block per (device, stream): zeroed once, then
+// only ever advanced by the kernels themselves (other paths never touch it).
+std::mutex g_gres_mu;
+std::map<std::pair<int, cudaStream_t>, void*> g_gres_blk;
+int get_gres_block(int dev, cudaStream_t s, char** out) {
+  std::lock_guard<std::mutex> g(g_gres_mu);
+  void*& b = g_gres_blk[{dev, s}];
+  if (!b) {
+    SK_CUDA(cudaMallocAsync(&b, kGresWsMax, s));
+    SK_CUDA(cudaMemsetAsync(b, 0, kGresWsMax, s));
+  }
+  *out = static_cast<char*>(b);
+  return SK_OK;
 }
 
 size_t plan_ws_bytes(const Plan& p, int64_t rows) {
   if (p.kind == kPathSeg && p.k3 == 6) return ws_layout(0, 0).total;
-  if (p.kind == kPathSeg && p.k3 == 7) return gres_ws(p).total;
+  if (p.kind == kPathSeg && p.k3 == 7) return 256 + gres_ws(p).total;  // at ws + 256
   if (p.kind == kPathSeg && p.nseg > 1) return ws_layout(rows, p.nseg).total;
   if (p.kind == kPathSplit) return ws_layout(rows, p.nch).total;
   return ws_layout(0, 0).total;
@@ -730,7 +748,7 @@ int launch_split(const float* x, float* y, int64_t rows, int64_t cols, int64_t l
 
 int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t cols,
                 int64_t ldx, int64_t ldy, int mode, unsigned long long* bad, char* ws,
-                cudaStream_t s) {
+                cudaStream_t s, bool user_ws) {
   const float sh = shift_scale();
   if (p.kind == kPathK1) {
     SK_CUDA(launch_k(reinterpret_cast<const void*>(p.k1->fn[mode]),
@@ -787,12 +805,27 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
       SK_CUDA(cudaLaunchKernelExC(&cfg, cluster_fn(mode), args));
     } else if (p.k3 == 7) {
       const GresWs w = gres_ws(p);
-      SK_CUDA(cudaMemsetAsync(ws + w.abort, 0, w.total - w.abort, s));
+      char* blk = nullptr;
+      if (user_ws) {
+        blk = ws + 256;
+        SK_CUDA(cudaMemsetAsync(blk, 0, w.total, s));
+      } else {
+        int dev = 0;
+        SK_CUDA(cudaGetDevice(&dev));
+        const int st = get_gres_block(dev, s, &blk);
+        if (st) return st;
+      }
+      GresComm comm = {};
+      comm.dst[0] = reinterpret_cast<unsigned long long*>(blk + w.slots);
+      comm.ctl = reinterpret_cast<unsigned*>(blk + w.ctl);
+      comm.shard_stride = 0;
+      comm.world = 1;
+      comm.rank0 = 0;
+      comm.nvr = 1;
+      comm.sys = 0;
       int P = p.nseg, slice = p.seglen, nst = p.lag;
-      SK_CUDA(launch_k(gres_fn(mode, p.lag, p.threads == kGresBlock), dim3(static_cast<unsigned>(p.grid)), dim3(p.threads),
-                       p.smem, s, true, x, y, rows, cols, ldx, ldy, P, slice, nst,
-                       reinterpret_cast<unsigned long long*>(ws + w.slots),
-                       reinterpret_cast<unsigned*>(ws + w.abort),
+      SK_CUDA(launch_k(gres_fn(mode, p.lag, p.threads == kGresBlock), dim3(static_cast<unsigned>(p.grid)),
+                       dim3(p.threads), p.smem, s, true, x, y, rows, cols, ldx, ldy, P, slice, nst, comm,
                        bad, sh, g_gres_sleep.load(), g_gres_diag.load()));
     } else if (p.k3 == 5) {
       const void* fn = p.seglen == 2048 ? reg3_fn<16>(mode)
@@ -863,7 +896,7 @@ int softmax_dev(const float* x, float* y, int64_t rows, int64_t cols, int64_t ld
     ws = static_cast<char*>(w);
   }
   if (!bad) bad = reinterpret_cast<unsigned long long*>(ws);  // library flag at offset 0
-  return launch_plan(p, x, y, rows, cols, ldx, ldy, mode, bad, ws, s);
+  return launch_plan(p, x, y, rows, cols, ldx, ldy, mode, bad, ws, s, workspace != nullptr);
 }
 
 // ------------------------------------------------ pipelined host-buffer path
@@ -987,7 +1020,7 @@ size_t sk_softmax_workspace_bytes(int64_t rows, int64_t cols) {
   if (rows <= 0 || cols <= 0) return ws_layout(0, 0).total;
   const int64_t nseg = (cols + 512 - 1) / 512;  // smallest K3 segment
   const int64_t nch = (cols + kSplitChunk - 1) / kSplitChunk;
-  const size_t gres_max = size_t(128) << 10;  // K3g control block (<= 3 CTAs/SM x 148 SMs)
+  const size_t gres_max = 256 + kGresWsMax;  // K3g control block at ws + 256
   return std::max({ws_layout(rows, nseg).total, ws_layout(rows, nch).total, gres_max});
 }
 
@@ -1068,6 +1101,11 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
       SK_CUDA(cudaMemcpyAsync(c->hbad, c->dbad, sizeof(unsigned long long),
                               cudaMemcpyDeviceToHost, c->s_comp));
       SK_CUDA(cudaStreamSynchronize(c->s_comp));
+      if (c->hbad[0] == SK_EXCHANGE_ABORTED) {
+        SK_CUDA(cudaMemset(c->dbad, 0xFF, sizeof(unsigned long long)));
+        g_last_error = "row-statistics exchange timed out";
+        return SK_ERR_CUDA;
+      }
       if (c->hbad[0] != SK_NO_BAD_ROW) {
         const int64_t row = static_cast<int64_t>(c->hbad[0]);
         SK_CUDA(cudaMemset(c->dbad, 0xFF, sizeof(unsigned long long)));
@@ -1163,6 +1201,11 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
   }
   SK_CUDA(cudaStreamSynchronize(c->s_d2h));
   for (int64_t k = 0; k < nchunks; ++k) {
+    if (c->hbad[k] == SK_EXCHANGE_ABORTED) {
+      SK_CUDA(cudaMemset(c->dbad, 0xFF, nchunks * sizeof(unsigned long long)));
+      g_last_error = "row-statistics exchange timed out";
+      return SK_ERR_CUDA;
+    }
     if (c->hbad[k] != SK_NO_BAD_ROW) {
       const int64_t row = start[k] + static_cast<int64_t>(c->hbad[k]);
       SK_CUDA(cudaMemset(c->dbad, 0xFF, nchunks * sizeof(unsigned long long)));

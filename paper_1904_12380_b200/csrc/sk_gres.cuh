@@ -51,38 +51,62 @@ __device__ __forceinline__ void bar_sync_n(int id, int n) {
 __device__ __forceinline__ void bar_arrive_n(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-__device__ __forceinline__ float ld_relaxed_f32(const float* p) {
-  float v;
-  asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
-  double v;
-  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_f32(float* p, float v) {
-  asm volatile("st.relaxed.gpu.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
-__device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
-  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
-}
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-
-__device__ __forceinline__ void st_relaxed_v2u64(unsigned long long* p, unsigned long long a,
-                                                 unsigned long long b) {
-  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+// Slot stores/loads: .gpu scope on one device, .sys scope when the slot arrays
+// are peer memory (column shards across GPUs).  Each 64-bit element is
+// single-copy atomic; the pair is not, hence a tag in every word.
+__device__ __forceinline__ void st_slot2(unsigned long long* p, unsigned long long a,
+                                         unsigned long long b, bool sys) {
+  if (sys)
+    asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+  else
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
-__device__ __forceinline__ void ld_relaxed_v2u64(const unsigned long long* p, unsigned long long& a,
-                                                 unsigned long long& b) {
-  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+__device__ __forceinline__ void ld_slot2(const unsigned long long* p, unsigned long long& a,
+                                         unsigned long long& b, bool sys) {
+  if (sys)
+    asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+  else
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 
-constexpr int kGresMaxP = 160;  // slots per lane: 5
+constexpr int kGresMaxSlots = 160;  // pairs merged per row (world x P), 5 per poller lane
+constexpr int kGresMaxWorld = 8;
+
+// Where a group's pairs go.  dst[r] is rank r's slot array -- a peer pointer
+// for a real column shard on another GPU, or one of `world` arrays on this GPU
+// when the launch emulates all ranks (one cooperative kernel over every
+// rank's data).  This launch covers ranks rank0 .. rank0+nvr-1; virtual rank
+// v reads x + v*shard_stride.  ctl: [0] launch epoch, [1] finished-CTA count,
+// [2] abort flag -- in the LOCAL workspace, advanced by the launch's last CTA.
+struct GresComm {
+  unsigned long long* dst[kGresMaxWorld];
+  unsigned* ctl;
+  int64_t shard_stride;
+  int world, rank0, nvr, sys;
+};
+
+// A CTA's row pair as one 32-B slot of three independently tagged 64-bit
+// words: tag << 32 | bits(m), tag << 32 | bits(hi), tag << 32 | bits(lo) with
+// s = hi + lo (two floats: 48 significant bits).  tag = epoch << 16 | 0x8000 |
+// (k & 0x7fff): never 0 (zeroed memory is "not yet"), unique against the
+// slot's previous row (k - NS) and previous launches (epoch), so the data IS
+// the flag -- no counter, no fence, no per-launch memset for a peer to race.
+__device__ __forceinline__ unsigned gres_tag(unsigned epoch, unsigned k) {
+  return (epoch << 16) | 0x8000u | (k & 0x7fffu);
+}
+__device__ __forceinline__ void gres_publish(unsigned long long* slot, float m, double s,
+                                             unsigned tag, bool sys) {
+  const float hi = static_cast<float>(s);
+  const float lo = static_cast<float>(s - static_cast<double>(hi));
+  const unsigned long long t = static_cast<unsigned long long>(tag) << 32;
+  st_slot2(slot, t | __float_as_uint(m), t | __float_as_uint(hi), sys);
+  st_slot2(slot + 2, t | __float_as_uint(lo), 0ull, sys);
+}
 
 // Global slot sets per group.  A publisher can run ahead of a REMOTE poller:
 // CTA A publishing row k needs its own row k-1-L merged (all of the group
@@ -90,23 +114,10 @@ constexpr int kGresMaxP = 160;  // slots per lane: 5
 // hence its output -- and its poller's read -- of row k-2-2L.  Rows
 // k-1-2L .. k may be live: 2L+2 sets.
 __host__ __device__ constexpr int gres_slot_sets(int L) { return 2 * L + 2; }
-
-// A CTA's row pair as one 16-B slot of two independently tagged 64-bit words
-// (each 64-bit access is single-copy atomic): word 0 = tag << 32 | bits(m),
-// word 1 = bits(s) with its 8 low mantissa bits replaced by the tag (2^-44
-// relative: far below the f64 sum's own rounding).  A reader accepts a slot
-// when both tags match, so the data IS the flag: no counter, no fence.
-__device__ __forceinline__ void gres_pack(float m, double s, unsigned tag, unsigned long long& w0,
-                                          unsigned long long& w1) {
-  w0 = (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(m);
-  w1 = (static_cast<unsigned long long>(__double_as_longlong(s)) & ~0xFFull) | (tag & 0xFFu);
-}
-__device__ __forceinline__ bool gres_valid(unsigned long long w0, unsigned long long w1, unsigned tag) {
-  return static_cast<unsigned>(w0 >> 32) == tag && static_cast<unsigned>(w1 & 0xFFu) == (tag & 0xFFu);
-}
+constexpr unsigned long long kExchangeAborted = 0xFFFFFFFFFFFFFFFEull;  // in *bad_row
 
 // Named barrier ids for lag L (stages - 2, 1..3): a hand-off can have at most
-// L+1 (bar 1) or L (bars 2 and 3) phases outstanding, so each rotates over
+// L+1 (bars 1 and 2) or L (bar 3) phases outstanding, so each rotates over
 // that many ids.  Id 0 is __syncthreads.
 template <int L>
 __device__ __forceinline__ int gres_bar1(unsigned k) { return 1 + int(k % unsigned(L + 1)); }
@@ -121,79 +132,95 @@ __device__ __forceinline__ int gres_bar3(unsigned k) { return 3 + 2 * L + int(k 
 template <int MODE, int L, bool SPLIT>
 __global__ void __launch_bounds__(kGresBlock, 1)
     k3_gres(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
-            int64_t ldx, int64_t ldy, int P, int slice, int nstages,
-            unsigned long long* __restrict__ slots, unsigned* __restrict__ abort_flag,
+            int64_t ldx, int64_t ldy, int P, int slice, int nstages, const GresComm comm,
             unsigned long long* __restrict__ bad_row, float shift_scale, int poll_ns, int diag) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage_buf = reinterpret_cast<float*>(smem_raw);
   constexpr int NW = kGresCompute / 32;
-  constexpr int NB = L + 1;            // smem broadcast slots
+  constexpr int NB = L + 1;              // smem broadcast slots
   constexpr int NS = gres_slot_sets(L);  // global slot sets
   __shared__ uint64_t bars[kGresStages];
   __shared__ float red_f[NB][NW];   // [row % (L+1)][warp]: warp-local max
   __shared__ double red_d[NB][NW];  //                      warp-local sum vs that max
   __shared__ float bc_m[NB];        // [row % (L+1)] merged row max / sum
   __shared__ double bc_s[NB];
+  __shared__ unsigned epoch_s;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = static_cast<int>(gridDim.x) / P;
-  const int g = static_cast<int>(blockIdx.x) / P, rank = static_cast<int>(blockIdx.x) % P;
-  if (g >= G) return;  // whole CTA: no barrier below is shared with it
-  const int64_t c0 = int64_t(rank) * slice;
+  const int per_rank = static_cast<int>(gridDim.x) / comm.nvr;  // CTAs of one rank's shard
+  const int G = per_rank / P;
+  const int v = static_cast<int>(blockIdx.x) / per_rank;        // virtual rank in this launch
+  const int cta = static_cast<int>(blockIdx.x) % per_rank;
+  const int g = cta / P, prank = cta % P;
+  const int myr = comm.rank0 + v;                                // global rank of this shard
+  const int WP = comm.world * P;                                 // pairs per row
+  const int gi = myr * P + prank;                                // this CTA's slot index
+  const bool sys = comm.sys != 0;
+  x += v * comm.shard_stride;
+  y += v * comm.shard_stride;
+  const int64_t c0 = int64_t(prank) * slice;
   const int64_t rem = cols - c0;
   const int len = rem <= 0 ? 0 : static_cast<int>(rem < slice ? rem : slice);  // % 4 == 0
   const int nvec = len >> 2;
-  auto slot_set = [&](unsigned k) {  // [P] x 16 B for row k of this group
-    return slots + (size_t(g) * NS + k % unsigned(NS)) * size_t(P) * 2;
+  auto slot_set = [&](unsigned long long* base, unsigned k) {  // [WP] x 32 B, row k of group g
+    return base + (size_t(g) * NS + k % unsigned(NS)) * size_t(WP) * 4;
   };
 
   if (tid == 0) {
     for (int s = 0; s < nstages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
+    epoch_s = ld_relaxed_u32(comm.ctl);
   }
   __syncthreads();
   pdl_wait();
+  const unsigned epoch = epoch_s;
 
-  // wait for the group's pairs of row k, merge them in rank order (identical
-  // (M, S) in every CTA of the row) and broadcast through smem slot k % NB.
-  // diag & 1 (timing only): wait for this CTA's own slot, not the group's.
+  // wait for the group's pairs of row k in this rank's slot array, merge them
+  // in slot order (identical (M, S) on every CTA of the row, on every rank)
+  // and broadcast through smem slot k % NB.  diag & 1 (timing only): wait for
+  // this CTA's own slot, not the group's.
   auto poll_merge = [&](unsigned k) {
-    const int pp = (diag & 1) ? 1 : P;
-    const unsigned long long* sl = slot_set(k);
-    const unsigned tag = k + 1u;  // never 0: the per-launch memset reads as "not yet"
-    unsigned long long w0[kGresMaxP / 32], w1[kGresMaxP / 32];
+    const int pp = (diag & 1) ? 1 : WP;
+    const unsigned long long* sl = slot_set(comm.dst[myr], k);
+    const unsigned tag = gres_tag(epoch, k);
+    unsigned long long wa[kGresMaxSlots / 32], wb[kGresMaxSlots / 32], wc[kGresMaxSlots / 32];
     unsigned spins = 0;
-    while (true) {  // lane l reads slots l, l+32, ... until all carry the tag
+    while (true) {  // lane l reads slots l, l+32, ... until every word carries the tag
       bool ok = true;
 #pragma unroll
-      for (int i = 0; i < kGresMaxP / 32; ++i) {
+      for (int i = 0; i < kGresMaxSlots / 32; ++i) {
         const int j = lane + 32 * i;
         if (j < pp) {
-          ld_relaxed_v2u64(sl + 2 * ((diag & 1) ? rank : j), w0[i], w1[i]);
-          ok = ok && gres_valid(w0[i], w1[i], tag);
+          const unsigned long long* q = sl + 4 * ((diag & 1) ? gi : j);
+          unsigned long long wd;
+          ld_slot2(q, wa[i], wb[i], sys);
+          ld_slot2(q + 2, wc[i], wd, sys);
+          ok = ok && static_cast<unsigned>(wa[i] >> 32) == tag &&
+               static_cast<unsigned>(wb[i] >> 32) == tag && static_cast<unsigned>(wc[i] >> 32) == tag;
         }
       }
       if (__all_sync(0xffffffffu, ok)) break;
       // back off: a spinning poller steals issue slots from its sub-partition's compute warps
       if (SPLIT && poll_ns > 0) __nanosleep(static_cast<unsigned>(poll_ns));
       if ((++spins & 0xFFFu) == 0) {  // a stuck peer raises abort: never hang the GPU
-        if (ld_relaxed_u32(abort_flag) || spins >= kGresSpinLimit) {
-          if (lane == 0) atomicExch(abort_flag, 1u);
+        if (ld_relaxed_u32(comm.ctl + 2) || spins >= kGresSpinLimit) {
+          if (lane == 0) atomicExch(comm.ctl + 2, 1u);
           break;
         }
       }
     }
     float Mg = kPadLogit;
 #pragma unroll
-    for (int i = 0; i < kGresMaxP / 32; ++i)
-      if (lane + 32 * i < pp) Mg = fmaxf(Mg, __uint_as_float(static_cast<unsigned>(w0[i])));
+    for (int i = 0; i < kGresMaxSlots / 32; ++i)
+      if (lane + 32 * i < pp) Mg = fmaxf(Mg, __uint_as_float(static_cast<unsigned>(wa[i])));
     Mg = group_max<32>(Mg);
     double S = 0.0;
 #pragma unroll
-    for (int i = 0; i < kGresMaxP / 32; ++i)
+    for (int i = 0; i < kGresMaxSlots / 32; ++i)
       if (lane + 32 * i < pp) {
-        const float mj = __uint_as_float(static_cast<unsigned>(w0[i]));
-        double sj = __longlong_as_double(static_cast<long long>(w1[i]));
+        const float mj = __uint_as_float(static_cast<unsigned>(wa[i]));
+        double sj = static_cast<double>(__uint_as_float(static_cast<unsigned>(wb[i]))) +
+                    static_cast<double>(__uint_as_float(static_cast<unsigned>(wc[i])));
         if (mj != Mg) sj *= static_cast<double>(expf(mj - Mg));
         S += sj;
       }
@@ -205,7 +232,9 @@ __global__ void __launch_bounds__(kGresBlock, 1)
     }
   };
 
-  if (warp == NW) {
+  if (g >= G) {
+    // idle CTA (the grid is a whole multiple of neither P nor ranks): tail only
+  } else if (warp == NW) {
     // ------------------------------------------------ publisher + TMA warp
     auto issue = [&](int64_t row, int stage) {
       mbar_arrive_expect_tx(&bars[stage], static_cast<uint32_t>(len) * 4u);
@@ -228,11 +257,9 @@ __global__ void __launch_bounds__(kGresBlock, 1)
       double sw = lane < NW ? red_d[b][lane] : 0.0;
       if (lane < NW && mw != mc) sw *= static_cast<double>(expf(mw - mc));
       const double sc = group_sum<32>(sw);
-      if (lane == 0) {
-        unsigned long long w0, w1;
-        gres_pack(mc, sc, k + 1u, w0, w1);
-        st_relaxed_v2u64(slot_set(k) + 2 * rank, w0, w1);
-      }
+      // lane r stores the pair into rank r's slot array (a peer's, over NVLink)
+      if (lane < comm.world)
+        gres_publish(slot_set(comm.dst[lane], k) + 4 * gi, mc, sc, gres_tag(epoch, k), sys);
       // refill the stage row k-L released
       if (k >= unsigned(L)) {
         const unsigned j = k - unsigned(L);
@@ -247,75 +274,87 @@ __global__ void __launch_bounds__(kGresBlock, 1)
     }
     for (unsigned j = k >= unsigned(L) ? k - unsigned(L) : 0u; j < k; ++j)
       bar_sync_n(gres_bar3<L>(j), kGresThreads);  // the last L output passes
-    return;
-  }
-
-  if (SPLIT && warp == NW + 1) {
+  } else if (warp == NW + 1) {
     // ------------------------------------------------ poller warp
+    if (SPLIT) {
+      unsigned k = 0;
+      for (int64_t row = g; row < rows; row += G, ++k) {
+        poll_merge(k);
+        bar_arrive_n(gres_bar2<L>(k), kGresThreads);
+      }
+    }
+  } else {
+    // ------------------------------------------------ compute warps
+    // row k's output pass runs after row k+L's local pass, so the group
+    // exchange of row k overlaps L full rows of streaming work.
+    auto output = [&](unsigned j) {
+      bar_sync_n(gres_bar2<L>(j), kGresThreads);
+      const int b = static_cast<int>(j % unsigned(NB));
+      const float M = bc_m[b];
+      const float rcp = recip_of_sum(bc_s[b]);
+      const float4* sb =
+          reinterpret_cast<const float4*>(stage_buf + size_t(j % unsigned(nstages)) * slice);
+      float* yr = y + (g + int64_t(j) * G) * ldy + c0;
+#pragma unroll 4
+      for (int q = tid; q < nvec; q += kGresCompute) {
+        const float4 v4 = sb[q];
+        const float2 a = scale2<MODE>(sexp2<MODE>(v4.x, v4.y, M), rcp);
+        const float2 c = scale2<MODE>(sexp2<MODE>(v4.z, v4.w, M), rcp);
+        st_stream4(yr + 4 * q, make_float4(a.x, a.y, c.x, c.y));
+      }
+      fence_proxy_async_smem();  // generic smem reads before the TMA refill
+      bar_arrive_n(gres_bar3<L>(j), kGresThreads);
+    };
+
     unsigned k = 0;
     for (int64_t row = g; row < rows; row += G, ++k) {
-      poll_merge(k);
-      bar_arrive_n(gres_bar2<L>(k), kGresThreads);
+      const int stage = static_cast<int>(k % unsigned(nstages));
+      mbar_wait(&bars[stage], (k / unsigned(nstages)) & 1u);
+      const float4* sb = reinterpret_cast<const float4*>(stage_buf + size_t(stage) * slice);
+
+      float mt = kPadLogit;
+      u64 z = f2pk(0.0f, 0.0f);
+#pragma unroll 4
+      for (int q = tid; q < nvec; q += kGresCompute) {
+        const float4 v4 = sb[q];
+        mt = fmaxf(mt, fmaxf(fmaxf(v4.x, v4.y), fmaxf(v4.z, v4.w)));
+        z = nf_acc2(nf_acc2(z, v4.x, v4.y), v4.z, v4.w);
+      }
+      if (nf_bad(z)) atomicMin(bad_row, static_cast<unsigned long long>(row));
+      const float mw = group_max<32>(mt);  // warp-local max: no CTA barrier
+      u64 acc = f2pk(0.0f, 0.0f);
+#pragma unroll 4
+      for (int q = tid; q < nvec; q += kGresCompute) {
+        const float4 v4 = sb[q];
+        const float2 a = sexp2<MODE>(v4.x, v4.y, mw);
+        const float2 c = sexp2<MODE>(v4.z, v4.w, mw);
+        acc = f2add(f2add(acc, f2pk(a.x, a.y)), f2pk(c.x, c.y));
+      }
+      const float2 acc2 = f2up(acc);
+      const double sw = group_sum<32>(static_cast<double>(acc2.x + acc2.y));
+      if (lane == 0) {
+        const int b = static_cast<int>(k % unsigned(NB));
+        red_f[b][warp] = mw;
+        red_d[b][warp] = sw;
+      }
+      bar_arrive_n(gres_bar1<L>(k), kGresThreads);
+      if (k >= unsigned(L)) output(k - unsigned(L));
     }
-    return;
+    for (unsigned j = k >= unsigned(L) ? k - unsigned(L) : 0u; j < k; ++j) output(j);
   }
 
-  // ---------------------------------------------------------- compute warps
-  // row k's output pass runs after row k+L's local pass, so the group
-  // exchange of row k overlaps L full rows of streaming work.
-  auto output = [&](unsigned j) {
-    bar_sync_n(gres_bar2<L>(j), kGresThreads);
-    const int b = static_cast<int>(j % unsigned(NB));
-    const float M = bc_m[b];
-    const float rcp = recip_of_sum(bc_s[b]);
-    const float4* sb = reinterpret_cast<const float4*>(stage_buf + size_t(j % unsigned(nstages)) * slice);
-    float* yr = y + (g + int64_t(j) * G) * ldy + c0;
-#pragma unroll 4
-    for (int q = tid; q < nvec; q += kGresCompute) {
-      const float4 v = sb[q];
-      const float2 a = scale2<MODE>(sexp2<MODE>(v.x, v.y, M), rcp);
-      const float2 c = scale2<MODE>(sexp2<MODE>(v.z, v.w, M), rcp);
-      st_stream4(yr + 4 * q, make_float4(a.x, a.y, c.x, c.y));
+  // ------------------------------------------------------------------ tail
+  // The launch's last CTA advances the epoch (every CTA has read it by now)
+  // and turns an exchange timeout into a status the host can see.
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(comm.ctl + 1, 1u) == gridDim.x - 1) {
+      if (atomicExch(comm.ctl + 2, 0u)) atomicMin(bad_row, kExchangeAborted);
+      comm.ctl[1] = 0;
+      comm.ctl[0] = epoch + 1u;
     }
-    fence_proxy_async_smem();  // generic smem reads before the TMA refill
-    bar_arrive_n(gres_bar3<L>(j), kGresThreads);
-  };
-
-  unsigned k = 0;
-  for (int64_t row = g; row < rows; row += G, ++k) {
-    const int stage = static_cast<int>(k % unsigned(nstages));
-    mbar_wait(&bars[stage], (k / unsigned(nstages)) & 1u);
-    const float4* sb = reinterpret_cast<const float4*>(stage_buf + size_t(stage) * slice);
-
-    float mt = kPadLogit;
-    u64 z = f2pk(0.0f, 0.0f);
-#pragma unroll 4
-    for (int q = tid; q < nvec; q += kGresCompute) {
-      const float4 v = sb[q];
-      mt = fmaxf(mt, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
-      z = nf_acc2(nf_acc2(z, v.x, v.y), v.z, v.w);
-    }
-    if (nf_bad(z)) atomicMin(bad_row, static_cast<unsigned long long>(row));
-    const float mw = group_max<32>(mt);  // warp-local max: no CTA barrier
-    u64 acc = f2pk(0.0f, 0.0f);
-#pragma unroll 4
-    for (int q = tid; q < nvec; q += kGresCompute) {
-      const float4 v = sb[q];
-      const float2 a = sexp2<MODE>(v.x, v.y, mw);
-      const float2 c = sexp2<MODE>(v.z, v.w, mw);
-      acc = f2add(f2add(acc, f2pk(a.x, a.y)), f2pk(c.x, c.y));
-    }
-    const float2 acc2 = f2up(acc);
-    const double sw = group_sum<32>(static_cast<double>(acc2.x + acc2.y));
-    if (lane == 0) {
-      const int b = static_cast<int>(k % unsigned(NB));
-      red_f[b][warp] = mw;
-      red_d[b][warp] = sw;
-    }
-    bar_arrive_n(gres_bar1<L>(k), kGresThreads);
-    if (k >= unsigned(L)) output(k - unsigned(L));
   }
-  for (unsigned j = k >= unsigned(L) ? k - unsigned(L) : 0u; j < k; ++j) output(j);
 }
 
 }  // namespace sk

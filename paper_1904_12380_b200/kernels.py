@@ -192,6 +192,7 @@ def softmax_into(x, out, variant: KernelVariant, cfg: LaneConfig = LaneConfig(),
         _native.check(st, "softmax")
         if check_finite:
             bad = int(flag.item())  # syncs the current stream
+            _raise_if_aborted(flag, bad)
             if bad != -1:
                 flag.fill_(-1)
                 raise NumericDomainError(f"non-finite logits in row {bad}")
@@ -273,12 +274,22 @@ def row_stats_device(x, variant: KernelVariant = KernelVariant.REFERENCE_CLIPPED
     return RowStats(max=rmax, sum=rsum)
 
 
+EXCHANGE_ABORTED = -2  # SK_EXCHANGE_ABORTED as int64
+
+
+def _raise_if_aborted(flag, bad: int) -> None:
+    if bad == EXCHANGE_ABORTED:
+        flag.fill_(-1)
+        raise SoftmaxKitError("row-statistics exchange timed out (a peer never arrived)")
+
+
 def check_device_flag(device=None) -> None:
     """Raise NumericDomainError if an unchecked call on ``device`` saw bad rows."""
     torch = _torch()
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
     flag = _bad_flag(torch, dev)
     bad = int(flag.item())
+    _raise_if_aborted(flag, bad)
     if bad != -1:
         flag.fill_(-1)
         raise NumericDomainError(f"non-finite logits in row {bad}")
