@@ -90,6 +90,16 @@ struct GresComm {
   int world, rank0, nvr, sys;
 };
 
+// comm.dst[i] without dynamic indexing of the parameter array (which would
+// copy the whole descriptor to local memory)
+__device__ __forceinline__ unsigned long long* gres_dst(const GresComm& c, int i) {
+  unsigned long long* d = c.dst[0];
+#pragma unroll
+  for (int r = 1; r < kGresMaxWorld; ++r)
+    if (i == r) d = c.dst[r];
+  return d;
+}
+
 // A CTA's row pair as one 32-B slot of three independently tagged 64-bit
 // words: tag << 32 | bits(m), tag << 32 | bits(hi), tag << 32 | bits(lo) with
 // s = hi + lo (two floats: 48 significant bits).  tag = epoch << 16 | 0x8000 |
@@ -181,7 +191,7 @@ __global__ void __launch_bounds__(kGresBlock, 1)
   // this CTA's own slot, not the group's.
   auto poll_merge = [&](unsigned k) {
     const int pp = (diag & 1) ? 1 : WP;
-    const unsigned long long* sl = slot_set(comm.dst[myr], k);
+    const unsigned long long* sl = slot_set(gres_dst(comm, myr), k);
     const unsigned tag = gres_tag(epoch, k);
     unsigned long long wa[kGresMaxSlots / 32], wb[kGresMaxSlots / 32], wc[kGresMaxSlots / 32];
     unsigned spins = 0;
@@ -259,7 +269,7 @@ __global__ void __launch_bounds__(kGresBlock, 1)
       const double sc = group_sum<32>(sw);
       // lane r stores the pair into rank r's slot array (a peer's, over NVLink)
       if (lane < comm.world)
-        gres_publish(slot_set(comm.dst[lane], k) + 4 * gi, mc, sc, gres_tag(epoch, k), sys);
+        gres_publish(slot_set(gres_dst(comm, lane), k) + 4 * gi, mc, sc, gres_tag(epoch, k), sys);
       // refill the stage row k-L released
       if (k >= unsigned(L)) {
         const unsigned j = k - unsigned(L);
