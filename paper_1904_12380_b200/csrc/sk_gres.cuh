@@ -23,14 +23,13 @@
 // row parity (a CTA can run at most one exchange ahead of its group).
 //
 // Warp specialisation keeps the handshake off the data path: warp 16 merges
-// and publishes each row's CTA pair, warp 17 polls and merges the group's
-// pairs -- so a slow poll never delays this CTA's next publication (which
-// would chain the group into a per-row convoy); at lag 1 warp 16 polls
-// right after publishing instead (no warp 17).  Compute thread 0 refills the
-// TMA ring as soon as the compute warps have consumed a stage.  Named barriers:
+// and publishes each row's CTA pair and issues the TMA refills, warp 17 polls
+// and merges the group's pairs -- so a slow poll never delays this CTA's next
+// publication (which would chain the group into a per-row convoy), and no
+// fence ever waits on the compute warps' output stores.  Named barriers:
 //   bar1  compute -> publisher  "warp pairs of row k in smem"
 //   bar2  poller -> compute     "(M, S) of row k in smem"
-//   barC  compute only          "stage consumed (proxy-fenced): refill it"
+//   bar3  compute -> publisher  "row k's stage consumed (proxy-fenced): refill"
 // With a ring of NS stages the output pass of row k runs after the local pass
 // of row k+L, L = NS-2 (one row loading, L+1 resident awaiting statistics);
 // the group round trip hides behind L row steps.  HBM and L2 each see
@@ -127,15 +126,15 @@ __device__ __forceinline__ void gres_publish(unsigned long long* slot, float m, 
 __host__ __device__ constexpr int gres_slot_sets(int L) { return 2 * L + 2; }
 constexpr unsigned long long kExchangeAborted = 0xFFFFFFFFFFFFFFFEull;  // in *bad_row
 
-// Named barrier ids for lag L (stages - 2, 1..3): each hand-off can have at
-// most L+1 phases outstanding, so each rotates over L+1 ids; the compute
-// warps' own "stage consumed" barrier comes last.  Id 0 is __syncthreads.
+// Named barrier ids for lag L (stages - 2, 1..3): a hand-off can have at most
+// L+1 (bars 1 and 2) or L (bar 3) phases outstanding, so each rotates over
+// that many ids.  Id 0 is __syncthreads.
 template <int L>
 __device__ __forceinline__ int gres_bar1(unsigned k) { return 1 + int(k % unsigned(L + 1)); }
 template <int L>
 __device__ __forceinline__ int gres_bar2(unsigned k) { return 2 + L + int(k % unsigned(L + 1)); }
 template <int L>
-__device__ __forceinline__ constexpr int gres_bar_compute() { return 3 + 2 * L; }
+__device__ __forceinline__ int gres_bar3(unsigned k) { return 3 + 2 * L + int(k % unsigned(L)); }
 
 // L: rows between a row's local pass and its output pass (ring depth L + 2).
 // SPLIT: a separate poller warp (block 576) vs the publisher warp polling
@@ -180,7 +179,7 @@ __global__ void __launch_bounds__(kGresBlock, 1)
   if (tid == 0) {
     for (int s = 0; s < nstages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
-    epoch_s = (diag & 4) ? 0u : ld_relaxed_u32(comm.ctl);  // diag 4: timing only
+    epoch_s = ld_relaxed_u32(comm.ctl);
   }
   __syncthreads();
   pdl_wait();
@@ -246,7 +245,18 @@ __global__ void __launch_bounds__(kGresBlock, 1)
   if (g >= G) {
     // idle CTA (the grid is a whole multiple of neither P nor ranks): tail only
   } else if (warp == NW) {
-    // ------------------------------------------------ publisher warp
+    // ------------------------------------------------ publisher + TMA warp
+    auto issue = [&](int64_t row, int stage) {
+      mbar_arrive_expect_tx(&bars[stage], static_cast<uint32_t>(len) * 4u);
+      if (len > 0)
+        tma_load_1d(stage_buf + size_t(stage) * slice, x + row * ldx + c0,
+                    static_cast<uint32_t>(len) * 4u, &bars[stage]);
+    };
+    if (lane == 0)
+      for (int s = 0; s < nstages; ++s) {
+        const int64_t row = g + int64_t(s) * G;
+        if (row < rows) issue(row, s);
+      }
     unsigned k = 0;
     for (int64_t row = g; row < rows; row += G, ++k) {
       const int b = static_cast<int>(k % unsigned(NB));
@@ -260,11 +270,20 @@ __global__ void __launch_bounds__(kGresBlock, 1)
       // lane r stores the pair into rank r's slot array (a peer's, over NVLink)
       if (lane < comm.world)
         gres_publish(slot_set(gres_dst(comm, lane), k) + 4 * gi, mc, sc, gres_tag(epoch, k), sys);
-      if (!SPLIT) {  // poll right after publishing: the round trip overlaps two passes
+      // refill the stage row k-L released
+      if (k >= unsigned(L)) {
+        const unsigned j = k - unsigned(L);
+        bar_sync_n(gres_bar3<L>(j), kGresThreads);
+        const int64_t rn = row - int64_t(L) * G + int64_t(nstages) * G;
+        if (lane == 0 && rn < rows) issue(rn, static_cast<int>(j % unsigned(nstages)));
+      }
+      if (!SPLIT) {
         poll_merge(k);
         bar_arrive_n(gres_bar2<L>(k), kGresThreads);
       }
     }
+    for (unsigned j = k >= unsigned(L) ? k - unsigned(L) : 0u; j < k; ++j)
+      bar_sync_n(gres_bar3<L>(j), kGresThreads);  // the last L output passes
   } else if (warp == NW + 1) {
     // ------------------------------------------------ poller warp
     if (SPLIT) {
@@ -277,20 +296,7 @@ __global__ void __launch_bounds__(kGresBlock, 1)
   } else {
     // ------------------------------------------------ compute warps
     // row k's output pass runs after row k+L's local pass, so the group
-    // exchange of row k overlaps L full rows of streaming work.  Thread 0
-    // keeps the TMA ring full: the ring is refilled as soon as the compute
-    // warps have consumed a stage, without a hand-off to another warp.
-    auto issue = [&](int64_t row, int stage) {
-      mbar_arrive_expect_tx(&bars[stage], static_cast<uint32_t>(len) * 4u);
-      if (len > 0)
-        tma_load_1d(stage_buf + size_t(stage) * slice, x + row * ldx + c0,
-                    static_cast<uint32_t>(len) * 4u, &bars[stage]);
-    };
-    if (tid == 0)
-      for (int s = 0; s < nstages; ++s) {
-        const int64_t row = g + int64_t(s) * G;
-        if (row < rows) issue(row, s);
-      }
+    // exchange of row k overlaps L full rows of streaming work.
     auto output = [&](unsigned j) {
       bar_sync_n(gres_bar2<L>(j), kGresThreads);
       const int b = static_cast<int>(j % unsigned(NB));
@@ -307,9 +313,7 @@ __global__ void __launch_bounds__(kGresBlock, 1)
         st_stream4(yr + 4 * q, make_float4(a.x, a.y, c.x, c.y));
       }
       fence_proxy_async_smem();  // generic smem reads before the TMA refill
-      bar_sync_n(gres_bar_compute<L>(), kGresCompute);
-      const int64_t rn = g + int64_t(j + unsigned(nstages)) * G;
-      if (tid == 0 && rn < rows) issue(rn, static_cast<int>(j % unsigned(nstages)));
+      bar_arrive_n(gres_bar3<L>(j), kGresThreads);
     };
 
     unsigned k = 0;
@@ -352,7 +356,6 @@ __global__ void __launch_bounds__(kGresBlock, 1)
   // ------------------------------------------------------------------ tail
   // The launch's last CTA advances the epoch (every CTA has read it by now)
   // and turns an exchange timeout into a status the host can see.
-  if (diag & 2) return;  // timing only: no epoch advance
   __syncthreads();
   if (tid == 0) {
     __threadfence();
