@@ -8,13 +8,16 @@ shared library is missing, importing the compute entry points raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_int64, c_size_t, c_uint64, c_void_p
 from pathlib import Path
 
 from .errors import ArgumentError, NumericDomainError, ResourceError, SoftmaxKitError
 
-LIB_PATH = Path(__file__).resolve().with_name("libsoftmax_b200.so")
+# SK_LIB_PATH: load another build of this library (A/B timing of two builds)
+LIB_PATH = Path(os.environ.get("SK_LIB_PATH") or
+                Path(__file__).resolve().with_name("libsoftmax_b200.so"))
 
 SK_OK = 0
 SK_ERR_ARGUMENT = 1

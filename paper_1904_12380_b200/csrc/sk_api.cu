@@ -627,7 +627,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
 }
 
 // K3g control block: ctl words (epoch, finished CTAs, abort) | slot sets
-// [group][2L+2][P] x 32 B.  Slots are epoch-tagged, so a block that persists
+// [group][2L+2][P] x 16 B.  Slots are epoch-tagged, so a block that persists
 // across launches (the library's, below) is never cleared; a caller-supplied
 // workspace is cleared before every launch instead (epoch restarts at 0).
 struct GresWs {
@@ -637,7 +637,7 @@ GresWs gres_ws(const Plan& p) {
   GresWs w;
   const size_t groups = size_t(p.grid / p.nseg);
   const int lag = p.lag >= 5 ? 3 : p.lag == 4 ? 2 : 1;
-  w.total = align_up(w.slots + groups * gres_slot_sets(lag) * p.nseg * 32, 256);
+  w.total = align_up(w.slots + groups * gres_slot_sets(lag) * p.nseg * 16, 256);
   return w;
 }
 constexpr size_t kGresWsMax = size_t(1) << 20;  // >= any single-device plan (<= 444 CTAs x 8 sets x 32 B)

@@ -100,22 +100,20 @@ __device__ __forceinline__ unsigned long long* gres_dst(const GresComm& c, int i
   return d;
 }
 
-// A CTA's row pair as one 32-B slot of three independently tagged 64-bit
-// words: tag << 32 | bits(m), tag << 32 | bits(hi), tag << 32 | bits(lo) with
-// s = hi + lo (two floats: 48 significant bits).  tag = epoch << 16 | 0x8000 |
-// (k & 0x7fff): never 0 (zeroed memory is "not yet"), unique against the
-// slot's previous row (k - NS) and previous launches (epoch), so the data IS
-// the flag -- no counter, no fence, no per-launch memset for a peer to race.
+// A CTA's row pair as one 16-B slot of two independently tagged 64-bit words:
+// tag << 32 | bits(m) and tag << 32 | bits(s) -- the CTA's partial sum rounded
+// to fp32 (2^-24 relative; the row sum S itself is still accumulated in f64
+// over the pairs).  tag = epoch << 16 | 0x8000 | (k & 0x7fff): never 0 (zeroed
+// memory is "not yet"), unique against the slot's previous row (k - 2L-2)
+// and previous launches (epoch), so the data IS the flag -- no counter, no
+// fence, no per-launch memset for a peer to race.  One store, one load.
 __device__ __forceinline__ unsigned gres_tag(unsigned epoch, unsigned k) {
   return (epoch << 16) | 0x8000u | (k & 0x7fffu);
 }
 __device__ __forceinline__ void gres_publish(unsigned long long* slot, float m, double s,
                                              unsigned tag, bool sys) {
-  const float hi = static_cast<float>(s);
-  const float lo = static_cast<float>(s - static_cast<double>(hi));
   const unsigned long long t = static_cast<unsigned long long>(tag) << 32;
-  st_slot2(slot, t | __float_as_uint(m), t | __float_as_uint(hi), sys);
-  st_slot2(slot + 2, t | __float_as_uint(lo), 0ull, sys);
+  st_slot2(slot, t | __float_as_uint(m), t | __float_as_uint(static_cast<float>(s)), sys);
 }
 
 // Global slot sets per group.  A publisher can run ahead of a REMOTE poller:
@@ -172,8 +170,8 @@ __global__ void __launch_bounds__(kGresBlock, 1)
   const int64_t rem = cols - c0;
   const int len = rem <= 0 ? 0 : static_cast<int>(rem < slice ? rem : slice);  // % 4 == 0
   const int nvec = len >> 2;
-  auto slot_set = [&](unsigned long long* base, unsigned k) {  // [WP] x 32 B, row k of group g
-    return base + (size_t(g) * NS + k % unsigned(NS)) * size_t(WP) * 4;
+  auto slot_set = [&](unsigned long long* base, unsigned k) {  // [WP] x 16 B, row k of group g
+    return base + (size_t(g) * NS + k % unsigned(NS)) * size_t(WP) * 2;
   };
 
   if (tid == 0) {
@@ -193,7 +191,7 @@ __global__ void __launch_bounds__(kGresBlock, 1)
     const int pp = (diag & 1) ? 1 : WP;
     const unsigned long long* sl = slot_set(gres_dst(comm, myr), k);
     const unsigned tag = gres_tag(epoch, k);
-    unsigned long long wa[kGresMaxSlots / 32], wb[kGresMaxSlots / 32], wc[kGresMaxSlots / 32];
+    unsigned long long wa[kGresMaxSlots / 32], wb[kGresMaxSlots / 32];
     unsigned spins = 0;
     while (true) {  // lane l reads slots l, l+32, ... until every word carries the tag
       bool ok = true;
@@ -201,12 +199,9 @@ __global__ void __launch_bounds__(kGresBlock, 1)
       for (int i = 0; i < kGresMaxSlots / 32; ++i) {
         const int j = lane + 32 * i;
         if (j < pp) {
-          const unsigned long long* q = sl + 4 * ((diag & 1) ? gi : j);
-          unsigned long long wd;
-          ld_slot2(q, wa[i], wb[i], sys);
-          ld_slot2(q + 2, wc[i], wd, sys);
+          ld_slot2(sl + 2 * ((diag & 1) ? gi : j), wa[i], wb[i], sys);
           ok = ok && static_cast<unsigned>(wa[i] >> 32) == tag &&
-               static_cast<unsigned>(wb[i] >> 32) == tag && static_cast<unsigned>(wc[i] >> 32) == tag;
+               static_cast<unsigned>(wb[i] >> 32) == tag;
         }
       }
       if (__all_sync(0xffffffffu, ok)) break;
@@ -229,8 +224,7 @@ __global__ void __launch_bounds__(kGresBlock, 1)
     for (int i = 0; i < kGresMaxSlots / 32; ++i)
       if (lane + 32 * i < pp) {
         const float mj = __uint_as_float(static_cast<unsigned>(wa[i]));
-        double sj = static_cast<double>(__uint_as_float(static_cast<unsigned>(wb[i]))) +
-                    static_cast<double>(__uint_as_float(static_cast<unsigned>(wc[i])));
+        double sj = static_cast<double>(__uint_as_float(static_cast<unsigned>(wb[i])));
         if (mj != Mg) sj *= static_cast<double>(expf(mj - Mg));
         S += sj;
       }
@@ -269,7 +263,7 @@ __global__ void __launch_bounds__(kGresBlock, 1)
       const double sc = group_sum<32>(sw);
       // lane r stores the pair into rank r's slot array (a peer's, over NVLink)
       if (lane < comm.world)
-        gres_publish(slot_set(gres_dst(comm, lane), k) + 4 * gi, mc, sc, gres_tag(epoch, k), sys);
+        gres_publish(slot_set(gres_dst(comm, lane), k) + 2 * gi, mc, sc, gres_tag(epoch, k), sys);
       // refill the stage row k-L released
       if (k >= unsigned(L)) {
         const unsigned j = k - unsigned(L);
