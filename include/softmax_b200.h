@@ -118,6 +118,48 @@ int sk_normalize_f32(const float* x, float* y, int64_t rows, int64_t cols, int64
                      void* stream);
 
 /*
+ * Fused column shard (north_star's column-sharded very-wide-row mode; replaces
+ * the row_stats -> all-reduce(MAX) -> rescale -> all-reduce(SUM) -> normalize
+ * chain above, RowStats kernels.py:108-112 / 272-276, with ONE kernel per rank).
+ * Every rank holds a [rows, cols] column shard (same rows, same cols on every
+ * rank; cols % 4 == 0, 16-B aligned rows) and one exchange block of
+ * sk_xchg_block_bytes() from sk_xchg_alloc (zeroed, IPC-exportable).  The
+ * kernel keeps each row slice resident in shared memory, stores its CTAs'
+ * (max, sum) pairs straight into every rank's block over NVLink, polls its own
+ * block and writes y -- the cross-GPU all-reduce of the row statistics runs
+ * inside the kernel, overlapped with streaming.  Results are identical on all
+ * ranks and equal to the single-GPU softmax of the full rows (within the fp32
+ * tolerance).  Calls must be issued in the same order on every rank.
+ *   sk_ipc_handle / sk_ipc_open / sk_ipc_close: cudaIpc{Get,Open,Close}MemHandle
+ *       on an exchange block (handle = SK_IPC_HANDLE_BYTES opaque bytes, sent to
+ *       the peers with any host collective).
+ *   sk_colshard_softmax_f32: blocks[r] = rank r's block as mapped in THIS
+ *       process (blocks[rank] = the local one); bad_row: device flag as in
+ *       sk_softmax_f32 (row index within the shard); SK_EXCHANGE_ABORTED if a
+ *       peer never arrived.
+ *   sk_colshard_emulate_f32: all `world` ranks of a [rows, cols] matrix
+ *       (cols % world == 0, shard r = columns [r*cols/world, (r+1)*cols/world))
+ *       as ONE cooperative kernel on this GPU with `world` local blocks -- the
+ *       same kernel and exchange code, for testing with fewer GPUs than ranks.
+ *   sk_describe_colshard_plan: the per-rank plan (cols = shard width).
+ */
+#define SK_IPC_HANDLE_BYTES 64
+size_t sk_xchg_block_bytes(void);
+int sk_xchg_alloc(int device, void** block);
+int sk_xchg_free(void* block);
+int sk_ipc_handle(const void* dev_ptr, void* handle);
+int sk_ipc_open(const void* handle, void** dev_ptr);
+int sk_ipc_close(void* dev_ptr);
+int sk_colshard_softmax_f32(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
+                            int64_t ldy, int mode, int rank, int world, void* const* blocks,
+                            unsigned long long* bad_row, void* stream);
+int sk_colshard_emulate_f32(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
+                            int64_t ldy, int mode, int world, void* const* blocks,
+                            unsigned long long* bad_row, void* stream);
+int sk_describe_colshard_plan(int64_t rows, int64_t cols, int world, int emulate, int device,
+                              char* buf, int buflen);
+
+/*
  * The reference's three phases as separate kernels (NOT the hot path; the
  * fused sk_softmax_f32 is).  They back variant_pipeline() / the GPU phase
  * profile (kernels.py:283-339, profiler.py:96-133):

@@ -75,7 +75,27 @@ SIGNATURES: dict[str, tuple] = {
     "sk_fill_uniform_f32": (c_int, [c_void_p, c_int64, c_uint64, c_double, c_double, c_uint64, c_int]),
     "sk_fill_normal_f32": (c_int, [c_void_p, c_int64, c_uint64, c_double, c_uint64, c_int]),
     "sk_plant_f32": (c_int, [c_void_p, c_int64, c_int64, c_uint64, c_float]),
+    "sk_xchg_block_bytes": (c_size_t, []),
+    "sk_xchg_alloc": (c_int, [c_int, POINTER(c_void_p)]),
+    "sk_xchg_free": (c_int, [c_void_p]),
+    "sk_ipc_handle": (c_int, [c_void_p, c_void_p]),
+    "sk_ipc_open": (c_int, [c_void_p, POINTER(c_void_p)]),
+    "sk_ipc_close": (c_int, [c_void_p]),
+    "sk_colshard_softmax_f32": (
+        c_int,
+        [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int, c_int, c_int, c_void_p,
+         c_void_p, c_void_p],
+    ),
+    "sk_colshard_emulate_f32": (
+        c_int,
+        [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int, c_int, c_void_p, c_void_p,
+         c_void_p],
+    ),
+    "sk_describe_colshard_plan": (c_int, [c_int64, c_int64, c_int, c_int, c_int, c_char_p, c_int]),
 }
+
+SK_IPC_HANDLE_BYTES = 64
+SK_EXCHANGE_ABORTED = 0xFFFFFFFFFFFFFFFE
 
 
 def lib() -> ctypes.CDLL:
@@ -122,6 +142,13 @@ def check(status: int, what: str = "") -> None:
 
 def set_tuning(key: str, value: int) -> None:
     check(lib().sk_set_tuning(key.encode(), int(value)), f"sk_set_tuning({key})")
+
+
+def describe_colshard_plan(rows: int, cols: int, world: int, emulate: bool = False,
+                           device: int = 0) -> str:
+    buf = ctypes.create_string_buffer(256)
+    check(lib().sk_describe_colshard_plan(rows, cols, world, 1 if emulate else 0, device, buf, 256))
+    return buf.value.decode()
 
 
 def describe_plan(rows: int, cols: int, ldx: int | None = None, ldy: int | None = None,

@@ -99,7 +99,8 @@ std::atomic<int> g_cluster_size{0};  // force a K3c cluster size (0 = auto)
 std::atomic<int> g_vec8{0};          // 256-bit K1 path (measured no faster: off by default)   // K3 warp queue: tasks per atomic claim (0 = static)  // K3 grid = SMs*occupancy/div: two launches co-reside
 std::atomic<int> g_gres{1};       // K3g grid-resident rows: 0 off, 1 when it out-scores K3c, 2 force
 std::atomic<int> g_gres_p{0};     // force K3g CTAs per row (0 = auto)
-std::atomic<int> g_gres_diag{0};  // K3g timing diagnostics (1: skip the group exchange -- wrong results)
+std::atomic<int> g_gres_diag{0};
+std::atomic<unsigned> g_gres_spins{kGresSpinLimit};  // exchange timeout (polls), tests shorten it  // K3g timing diagnostics (1: skip the group exchange -- wrong results)
 std::atomic<int> g_gres_st{0};
 std::atomic<int> g_gres_sleep{128};
 std::atomic<int> g_gres_split{-1};   // K3g poller warp: -1 auto (lag >= 2), 0 off, 1 on
@@ -406,6 +407,56 @@ int plan_split(int64_t rows, int64_t cols, Plan& p) {
   return SK_OK;
 }
 
+// K3g shape: P CTAs per row (per rank), ring depth st, `groups` row groups
+// per rank.  world ranks each hold a [rows, cols] column shard (world*P pairs
+// merged per row); nvr of them run in this launch (nvr = world when one GPU
+// emulates all ranks, 1 on a real rank).  Deterministic in its inputs, so
+// every rank of a column shard derives the same plan.
+struct GresChoice {
+  int P = 0, st = 0, groups = 0;
+  int64_t slice = 0;
+  double score = 0.0;
+};
+GresChoice plan_gres(int64_t rows, int64_t cols, int mode, const DevInfo& di, int world, int nvr) {
+  GresChoice best;
+  const double xg = std::max(0, g_gres_x.load());
+  for (int P = 1; P * world <= kGresMaxSlots && P <= di.sms; ++P) {
+    if (g_gres_p.load() > 0 && P != g_gres_p.load()) continue;
+    const int64_t slice = align_up((cols + P - 1) / P, 4);
+    if ((P - 1) * slice >= cols) continue;
+    int st = static_cast<int>(std::min<int64_t>(
+        kGresStages, kGresSmemMax / (slice * int64_t(sizeof(float)))));
+    if (g_gres_st.load() >= 2) {
+      if (st < g_gres_st.load()) continue;
+      st = g_gres_st.load();
+    }
+    if (st < 2) continue;
+    const size_t smem = size_t(st) * slice * sizeof(float);
+    const bool split = gres_split(st);
+    const int occ = occupancy(gres_fn(mode, st, split), split ? kGresBlock : kGresThreads, smem);
+    if (occ < 1) continue;
+    const int groups = di.sms * occ / (P * nvr);
+    if (groups < 1) continue;
+    const int64_t rows_g = (rows + groups - 1) / groups;
+    if (rows_g >= (int64_t(1) << 31)) continue;
+    // SMs covered x per-step efficiency (the exchange costs ~xg floats of
+    // streaming per row step when it is not hidden); a 2-stage ring cannot
+    // overlap it at all, deeper rings hide more (measured c4 / c5b: 14x3
+    // 170 us, 20x4 187, 10x2 229; 74x4 1530, 74x3 1690, 48x2 1775)
+    const double score = double(std::min<int64_t>(groups, rows)) * P * nvr / occ *
+                         double(slice) / (double(slice) + xg) * (st == 2 ? 0.8 : 1.0) *
+                         (1.0 + 0.01 * st);
+    if (score > best.score) {
+      best.score = score;
+      best.P = P;
+      best.st = st;
+      best.groups = groups;
+      best.slice = slice;
+    }
+  }
+  return best;
+}
+
 int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa, uint64_t ya,
               int mode, int dev, Plan& p) {
   const DevInfo di = dev_info(dev);
@@ -449,7 +500,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     // as SMs covered x per-row efficiency slice / (slice + exchange cost).
     const int gres = g_gres.load();
     if ((cols > kSegCap || gres == 2) && (impl0 == 5 || impl0 == 3)) {
-      double best_c = 0.0, best_g = 0.0;
+      double best_c = 0.0;
       int c_cs = 0, c_st = 0, c_n = 0;
       int64_t c_slice = 0;
       if (g_cluster_k3.load() && gres != 2 && cols <= 16 * kClusterSliceMaxAny) {
@@ -477,45 +528,11 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
           }
         }
       }
-      int g_p = 0, g_st = 0, g_groups = 0;
-      int64_t g_slice = 0;
-      if (gres != 0 && di.coop) {
-        const double xg = std::max(0, g_gres_x.load());
-        for (int P = 1; P <= std::min(di.sms, kGresMaxSlots); ++P) {
-          if (g_gres_p.load() > 0 && P != g_gres_p.load()) continue;
-          const int64_t slice = align_up((cols + P - 1) / P, 4);
-          if ((P - 1) * slice >= cols) continue;
-          int st = static_cast<int>(std::min<int64_t>(
-              kGresStages, kGresSmemMax / (slice * int64_t(sizeof(float)))));
-          if (g_gres_st.load() >= 2) {
-            if (st < g_gres_st.load()) continue;
-            st = g_gres_st.load();
-          }
-          if (st < 2) continue;
-          const size_t smem = size_t(st) * slice * sizeof(float);
-          const bool split = gres_split(st);
-          const int occ = occupancy(gres_fn(mode, st, split), split ? kGresBlock : kGresThreads, smem);
-          if (occ < 1) continue;
-          const int groups = di.sms * occ / P;
-          if (groups < 1) continue;
-          const int64_t rows_g = (rows + groups - 1) / groups;  // exchange counter range
-          if (rows_g >= (int64_t(1) << 31)) continue;  // 32-bit slot tags
-          // SMs covered x per-step efficiency (the exchange costs ~xg floats of
-          // streaming per row step when it is not hidden); a 2-stage ring
-          // cannot overlap it at all, deeper rings hide more (measured c4 /
-          // c5b: 14x3 170 us, 20x4 187, 10x2 229; 74x4 1530, 74x3 1690, 48x2 1775)
-          const double score = double(std::min<int64_t>(groups, rows)) * P / occ *
-                               double(slice) / (double(slice) + xg) *
-                               (st == 2 ? 0.8 : 1.0) * (1.0 + 0.01 * st);
-          if (score > best_g) {
-            best_g = score;
-            g_p = P;
-            g_st = st;
-            g_groups = groups;
-            g_slice = slice;
-          }
-        }
-      }
+      GresChoice gc;
+      if (gres != 0 && di.coop) gc = plan_gres(rows, cols, mode, di, 1, 1);
+      const double best_g = gc.score;
+      const int g_p = gc.P, g_st = gc.st, g_groups = gc.groups;
+      const int64_t g_slice = gc.slice;
       if (g_p > 0 && (gres == 2 || best_g > best_c)) {
         p.kind = kPathSeg;
         p.k3 = 7;
@@ -627,7 +644,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
 }
 
 // K3g control block: ctl words (epoch, finished CTAs, abort) | slot sets
-// [group][2L+2][P] x 16 B.  Slots are epoch-tagged, so a block that persists
+// [epoch parity][group][2L+2][P] x 16 B.  Slots are epoch-tagged, so a block that persists
 // across launches (the library's, below) is never cleared; a caller-supplied
 // workspace is cleared before every launch instead (epoch restarts at 0).
 struct GresWs {
@@ -637,7 +654,7 @@ GresWs gres_ws(const Plan& p) {
   GresWs w;
   const size_t groups = size_t(p.grid / p.nseg);
   const int lag = p.lag >= 5 ? 3 : p.lag == 4 ? 2 : 1;
-  w.total = align_up(w.slots + groups * gres_slot_sets(lag) * p.nseg * 16, 256);
+  w.total = align_up(w.slots + 2 * groups * gres_slot_sets(lag) * p.nseg * 16, 256);
   return w;
 }
 constexpr size_t kGresWsMax = size_t(1) << 20;  // >= any single-device plan (<= 444 CTAs x 8 sets x 32 B)
@@ -823,6 +840,7 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
       comm.rank0 = 0;
       comm.nvr = 1;
       comm.sys = 0;
+      comm.spin_limit = g_gres_spins.load();
       int P = p.nseg, slice = p.seglen, nst = p.lag;
       SK_CUDA(launch_k(gres_fn(mode, p.lag, p.threads == kGresBlock), dim3(static_cast<unsigned>(p.grid)),
                        dim3(p.threads), p.smem, s, true, x, y, rows, cols, ldx, ldy, P, slice, nst, comm,
@@ -942,6 +960,69 @@ HostCtx* host_ctx(int dev) {
   return c;
 }
 
+
+// ------------------------------------------------ fused column shard (K3g)
+// Every rank holds a [rows, cols] column shard and one exchange block:
+// [0, 256) ctl words (epoch, finished CTAs, abort) | [256, ...) slot arrays
+// [2][groups][2L+2][world*P] x 16 B.  Rank r's K3g CTAs store their row pairs
+// into EVERY rank's block (peer pointers over NVLink) and poll only their
+// own, so the per-row (max, sum) all-reduce of the column shard happens inside
+// the kernel, overlapped with the streaming -- no NCCL call on the data path.
+constexpr size_t kXBlockBytes = size_t(2) << 20;
+constexpr size_t kXSlots = 256;
+
+int colshard_launch(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
+                    int64_t ldy, int mode, int rank, int world, int nvr, void* const* blocks,
+                    unsigned long long* bad, cudaStream_t s, char* desc, int desc_len) {
+  if (world < 1 || world > kGresMaxWorld) return arg_fail("world must be 1..8");
+  if (nvr != 1 && nvr != world) return arg_fail("bad virtual rank count");
+  if (rank < 0 || rank >= world) return arg_fail("rank out of range");
+  if (rows < 0 || cols < 1 || ldx < cols || ldy < cols) return arg_fail("bad shard shape");
+  if (mode < 0 || mode > 2) return arg_fail("mode must be SK_MODE_CLIPPED/EXACT/APPROX");
+  if (!blocks) return arg_fail("null exchange blocks");
+  for (int r = 0; r < world; ++r)
+    if (!blocks[r]) return arg_fail("null exchange block");
+  const bool aligned = cols % 4 == 0 && ldx % 4 == 0 && ldy % 4 == 0 &&
+                       reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
+                       reinterpret_cast<uintptr_t>(y) % 16 == 0;
+  if (!desc && rows > 0 && (!x || !y)) return arg_fail("null buffer");
+  if (!desc && !aligned) return arg_fail("fused column shard needs cols % 4 == 0 and 16-B aligned rows");
+  int dev = 0;
+  SK_CUDA(cudaGetDevice(&dev));
+  const DevInfo di = dev_info(dev);
+  if (!di.coop) return arg_fail("device cannot co-schedule the fused column shard");
+  const GresChoice gc = plan_gres(rows > 0 ? rows : 1, cols, mode, di, world, nvr);
+  if (gc.P == 0) return arg_fail("shard row too long for the fused column shard (use the split path)");
+  const bool split = gres_split(gc.st);
+  const int lag = gc.st >= 5 ? 3 : gc.st == 4 ? 2 : 1;
+  const size_t need = kXSlots + 2 * size_t(gc.groups) * gres_slot_sets(lag) * world * gc.P * 16;
+  if (need > kXBlockBytes) return arg_fail("exchange block too small for this plan");
+  if (desc) {
+    snprintf(desc, desc_len, "k3_gres_colshard world=%d nvr=%d nseg=%d seglen=%lld stages=%d groups=%d threads=%d",
+             world, nvr, gc.P, (long long)gc.slice, gc.st, gc.groups, split ? kGresBlock : kGresThreads);
+    return SK_OK;
+  }
+  if (rows == 0) return SK_OK;
+  GresComm comm = {};
+  for (int r = 0; r < world; ++r)
+    comm.dst[r] = reinterpret_cast<unsigned long long*>(static_cast<char*>(blocks[r]) + kXSlots);
+  comm.ctl = reinterpret_cast<unsigned*>(blocks[nvr == 1 ? rank : 0]);
+  comm.shard_stride = nvr == 1 ? 0 : cols;
+  comm.world = world;
+  comm.rank0 = nvr == 1 ? rank : 0;
+  comm.nvr = nvr;
+  comm.sys = (world > 1 && nvr == 1) ? 1 : 0;  // peers are other GPUs
+  comm.spin_limit = g_gres_spins.load();
+  const size_t smem = size_t(gc.st) * gc.slice * sizeof(float);
+  int P = gc.P, slice = static_cast<int>(gc.slice), nst = gc.st;
+  const int grid = gc.groups * gc.P * nvr;
+  SK_CUDA(launch_k(gres_fn(mode, gc.st, split), dim3(static_cast<unsigned>(grid)),
+                   dim3(split ? kGresBlock : kGresThreads), smem, s, true, x, y, rows, cols, ldx,
+                   ldy, P, slice, nst, comm, bad, shift_scale(), g_gres_sleep.load(),
+                   g_gres_diag.load()));
+  return SK_OK;
+}
+
 }  // namespace
 }  // namespace sk
 
@@ -1012,6 +1093,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "gres_diag") g_gres_diag = value;
   else if (k == "gres_sleep") g_gres_sleep = value;
   else if (k == "gres_split") g_gres_split = value;
+  else if (k == "gres_timeout_spins") g_gres_spins = value > 0 ? unsigned(value) : kGresSpinLimit;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;
 }
@@ -1289,6 +1371,79 @@ int sk_normalize_f32(const float* x, float* y, int64_t rows, int64_t cols, int64
   SK_CUDA(launch_k(norm, dim3(g), dim3(kSplitThreads), 0, s, false, x, y, rows, cols, ldx, ldy,
                    nch, row_max, row_sum));
   return SK_OK;
+}
+
+size_t sk_xchg_block_bytes(void) { return kXBlockBytes; }
+
+int sk_xchg_alloc(int device, void** block) {
+  if (!block) return arg_fail("null output pointer");
+  int prev = 0;
+  SK_CUDA(cudaGetDevice(&prev));
+  SK_CUDA(cudaSetDevice(device));
+  void* b = nullptr;
+  cudaError_t e = cudaMalloc(&b, kXBlockBytes);  // plain cudaMalloc: IPC-exportable
+  if (e == cudaSuccess) e = cudaMemset(b, 0, kXBlockBytes);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_fail(e, "sk_xchg_alloc");
+  *block = b;
+  return SK_OK;
+}
+
+int sk_xchg_free(void* block) {
+  if (block) SK_CUDA(cudaFree(block));
+  return SK_OK;
+}
+
+int sk_ipc_handle(const void* dev_ptr, void* handle) {
+  if (!dev_ptr || !handle) return arg_fail("null pointer");
+  cudaIpcMemHandle_t h;
+  SK_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  std::memcpy(handle, &h, sizeof(h));
+  return SK_OK;
+}
+
+int sk_ipc_open(const void* handle, void** dev_ptr) {
+  if (!handle || !dev_ptr) return arg_fail("null pointer");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  SK_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return SK_OK;
+}
+
+int sk_ipc_close(void* dev_ptr) {
+  if (dev_ptr) SK_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return SK_OK;
+}
+
+int sk_colshard_softmax_f32(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
+                            int64_t ldy, int mode, int rank, int world, void* const* blocks,
+                            unsigned long long* bad_row, void* stream) {
+  if (!bad_row) return arg_fail("bad_row flag required");
+  return colshard_launch(x, y, rows, cols, ldx, ldy, mode, rank, world, 1, blocks, bad_row,
+                         static_cast<cudaStream_t>(stream), nullptr, 0);
+}
+
+int sk_colshard_emulate_f32(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
+                            int64_t ldy, int mode, int world, void* const* blocks,
+                            unsigned long long* bad_row, void* stream) {
+  if (!bad_row) return arg_fail("bad_row flag required");
+  if (world < 1 || cols % world) return arg_fail("cols must split evenly over world");
+  return colshard_launch(x, y, rows, cols / world, ldx, ldy, mode, 0, world, world, blocks,
+                         bad_row, static_cast<cudaStream_t>(stream), nullptr, 0);
+}
+
+int sk_describe_colshard_plan(int64_t rows, int64_t cols, int world, int emulate, int device,
+                              char* buf, int buflen) {
+  if (!buf || buflen < 1) return arg_fail("null buffer");
+  int prev = 0;
+  SK_CUDA(cudaGetDevice(&prev));
+  SK_CUDA(cudaSetDevice(device));
+  void* fake[kGresMaxWorld];
+  for (auto& f : fake) f = reinterpret_cast<void*>(256);
+  const int st = colshard_launch(nullptr, nullptr, rows, cols, cols, cols, 0, 0, world,
+                                 emulate ? world : 1, fake, nullptr, nullptr, buf, buflen);
+  cudaSetDevice(prev);
+  return st;
 }
 
 }  // extern "C"

@@ -88,6 +88,7 @@ struct GresComm {
   unsigned* ctl;
   int64_t shard_stride;
   int world, rank0, nvr, sys;
+  unsigned spin_limit;  // polls before a missing peer aborts the exchange
 };
 
 // comm.dst[i] without dynamic indexing of the parameter array (which would
@@ -170,10 +171,6 @@ __global__ void __launch_bounds__(kGresBlock, 1)
   const int64_t rem = cols - c0;
   const int len = rem <= 0 ? 0 : static_cast<int>(rem < slice ? rem : slice);  // % 4 == 0
   const int nvec = len >> 2;
-  auto slot_set = [&](unsigned long long* base, unsigned k) {  // [WP] x 16 B, row k of group g
-    return base + (size_t(g) * NS + k % unsigned(NS)) * size_t(WP) * 2;
-  };
-
   if (tid == 0) {
     for (int s = 0; s < nstages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -182,6 +179,15 @@ __global__ void __launch_bounds__(kGresBlock, 1)
   __syncthreads();
   pdl_wait();
   const unsigned epoch = epoch_s;
+
+  // slot array layout: [epoch parity][group][NS sets][WP] x 16 B.  The epoch
+  // parity matters across GPUs: a rank can start its next launch (and publish
+  // into its peers' arrays) while a peer still polls this launch's last rows;
+  // it cannot get two launches ahead (its next launch waits for that peer).
+  auto slot_set = [&](unsigned long long* base, unsigned k) {  // row k of group g
+    return base + ((size_t(epoch & 1u) * G + g) * NS + k % unsigned(NS)) * size_t(WP) * 2;
+  };
+
 
   // wait for the group's pairs of row k in this rank's slot array, merge them
   // in slot order (identical (M, S) on every CTA of the row, on every rank)
@@ -208,7 +214,7 @@ __global__ void __launch_bounds__(kGresBlock, 1)
       // back off: a spinning poller steals issue slots from its sub-partition's compute warps
       if (SPLIT && poll_ns > 0) __nanosleep(static_cast<unsigned>(poll_ns));
       if ((++spins & 0xFFFu) == 0) {  // a stuck peer raises abort: never hang the GPU
-        if (ld_relaxed_u32(comm.ctl + 2) || spins >= kGresSpinLimit) {
+        if (ld_relaxed_u32(comm.ctl + 2) || spins >= comm.spin_limit) {
           if (lane == 0) atomicExch(comm.ctl + 2, 1u);
           break;
         }

@@ -124,3 +124,182 @@ def column_sharded_softmax(x_local, variant: KernelVariant, group=None,
 
 def _clone(t):
     return t.clone() if hasattr(t, "clone") else t.copy()
+
+
+# --------------------------------------------------------------------------
+# Fused column shard: the collective inside the kernel
+# --------------------------------------------------------------------------
+class NativeExchange:
+    """The exchange-block / IPC entry points of libsoftmax_b200 (C ABI)."""
+
+    def __init__(self):
+        from . import _native
+
+        self._native = _native
+        self.L = _native.lib()
+
+    def alloc(self, device: int) -> int:
+        import ctypes
+
+        p = ctypes.c_void_p()
+        self._native.check(self.L.sk_xchg_alloc(device, ctypes.byref(p)), "xchg_alloc")
+        return int(p.value)
+
+    def free(self, block: int) -> None:
+        self._native.check(self.L.sk_xchg_free(block), "xchg_free")
+
+    def handle(self, block: int) -> bytes:
+        import ctypes
+
+        buf = ctypes.create_string_buffer(self._native.SK_IPC_HANDLE_BYTES)
+        self._native.check(self.L.sk_ipc_handle(block, buf), "ipc_handle")
+        return buf.raw
+
+    def open(self, handle: bytes) -> int:
+        import ctypes
+
+        p = ctypes.c_void_p()
+        self._native.check(self.L.sk_ipc_open(handle, ctypes.byref(p)), "ipc_open")
+        return int(p.value)
+
+    def close(self, block: int) -> None:
+        self._native.check(self.L.sk_ipc_close(block), "ipc_close")
+
+    def launch(self, x, y, mode: int, rank: int, world: int, blocks: list[int], flag) -> None:
+        import ctypes
+
+        import torch
+
+        rows, cols = x.shape
+        arr = (ctypes.c_void_p * world)(*blocks)
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+        self._native.check(self.L.sk_colshard_softmax_f32(
+            x.data_ptr(), y.data_ptr(), rows, cols, x.stride(0) if rows > 1 else cols,
+            y.stride(0) if rows > 1 else cols, mode, rank, world, arr, flag.data_ptr(), stream),
+            "colshard_softmax")
+
+
+class FusedColumnShard:
+    """Column-sharded softmax as ONE kernel per rank.
+
+    Each rank's K3g kernel (sk_gres.cuh) keeps its [N, C_r] row slices in
+    shared memory and stores every CTA's per-row (max, sum) pair straight
+    into all ranks' exchange blocks -- peer memory mapped over NVLink with
+    cudaIpc -- then polls its own block and writes y.  The row-statistics
+    all-reduce of ``column_sharded_softmax`` (two NCCL calls and 12 B/element
+    of HBM traffic through the split kernels) becomes in-kernel stores
+    overlapped with the streaming (8 B/element).
+
+    Create once per (group, device) -- the exchange handles are swapped with
+    one host all-gather -- then call for every softmax, in the same order on
+    every rank.  ``native`` / ``all_gather`` are injectable so the host logic
+    runs on CPU with gloo and a test double (tests/test_sharding_gloo.py).
+    """
+
+    def __init__(self, group=None, device: int | None = None, *, native=None, all_gather=None):
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            self.world = dist.get_world_size(group)
+            self.rank = dist.get_rank(group)
+        else:
+            self.world, self.rank = 1, 0
+        if self.world > 8:
+            raise ArgumentError("the fused column shard spans at most 8 GPUs (one NVLink domain)")
+        if all_gather is None:
+            def all_gather(obj):
+                if self.world == 1:
+                    return [obj]
+                out = [None] * self.world
+                dist.all_gather_object(out, obj, group=group)
+                return out
+        if device is None:
+            import torch
+
+            device = torch.cuda.current_device()
+        self.device = device
+        self._n = native if native is not None else NativeExchange()
+        self.block = self._n.alloc(device)
+        handles = all_gather(self._n.handle(self.block))
+        if len(handles) != self.world:
+            raise ArgumentError("exchange handle all-gather returned the wrong count")
+        self.blocks = [self.block if r == self.rank else self._n.open(h)
+                       for r, h in enumerate(handles)]
+        self._closed = False
+
+    def __call__(self, x_local, variant: KernelVariant, out=None, check_finite: bool = True):
+        import torch
+
+        from .kernels import _bad_flag, _raise_if_aborted
+        from .errors import NumericDomainError
+
+        mode = variant_mode(variant)
+        if self._closed:
+            raise ArgumentError("FusedColumnShard is closed")
+        if x_local.dim() != 2 or x_local.dtype != torch.float32 or not x_local.is_cuda:
+            raise ArgumentError("x_local must be a CUDA float32 [N, C_r] tensor")
+        y = torch.empty_like(x_local) if out is None else out
+        flag = _bad_flag(torch, x_local.device)
+        self._n.launch(x_local, y, mode, self.rank, self.world, self.blocks, flag)
+        if check_finite:
+            bad = int(flag.item())
+            _raise_if_aborted(flag, bad)
+            if bad != -1:
+                flag.fill_(-1)
+                raise NumericDomainError(f"non-finite logits in row {bad}")
+        return y
+
+    def close(self) -> None:
+        if self._closed:
+            return
+        for r, b in enumerate(self.blocks):
+            if r != self.rank:
+                self._n.close(b)
+        self._n.free(self.block)
+        self._closed = True
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+_emu_blocks: dict[tuple[int, int], list[int]] = {}
+
+
+def emulate_column_shards(x, variant: KernelVariant, world: int, out=None, check_finite=True):
+    """All ``world`` ranks of a column-sharded softmax of ``x`` [N, C] as ONE
+    cooperative kernel on this GPU (shard r = columns [r*C/world, (r+1)*C/world)),
+    with one exchange block per virtual rank -- the same kernel and exchange
+    code as ``FusedColumnShard``, for testing with fewer GPUs than ranks."""
+    import ctypes
+
+    import torch
+
+    from . import _native
+    from .errors import NumericDomainError
+    from .kernels import _bad_flag, _raise_if_aborted
+
+    mode = variant_mode(variant)
+    rows, cols = x.shape
+    dev = x.device.index if x.device.index is not None else torch.cuda.current_device()
+    key = (dev, world)
+    if key not in _emu_blocks:
+        nat = NativeExchange()
+        _emu_blocks[key] = [nat.alloc(dev) for _ in range(world)]
+    blocks = _emu_blocks[key]
+    y = torch.empty_like(x) if out is None else out
+    flag = _bad_flag(torch, x.device)
+    arr = (ctypes.c_void_p * world)(*blocks)
+    _native.check(_native.lib().sk_colshard_emulate_f32(
+        x.data_ptr(), y.data_ptr(), rows, cols, x.stride(0) if rows > 1 else cols,
+        y.stride(0) if rows > 1 else cols, mode, world, arr, flag.data_ptr(),
+        torch.cuda.current_stream(x.device).cuda_stream), "colshard_emulate")
+    if check_finite:
+        bad = int(flag.item())
+        _raise_if_aborted(flag, bad)
+        if bad != -1:
+            flag.fill_(-1)
+            raise NumericDomainError(f"non-finite logits in row {bad}")
+    return y

@@ -107,3 +107,76 @@ def test_column_merge_math_matches_full_row(oracle):
     y = np.concatenate([ops.normalize(torch.from_numpy(np.ascontiguousarray(p)), M, S, 0).numpy()
                         for p in parts], axis=1)
     assert oracle.parity(y, oracle.softmax_ref(x, True))["ok"]
+
+
+class _FakeExchange:
+    """Test double for sharding.NativeExchange: blocks are integers, handles
+    name the block, "opening" a handle maps it to a distinct address."""
+
+    MAP = 1 << 40
+
+    def __init__(self):
+        self.closed, self.freed = [], []
+
+    def alloc(self, device):
+        return 0x1000 * (1 + int(os.environ["RANK"]))
+
+    def handle(self, block):
+        return f"blk:{block}".encode().ljust(64, b"\0")
+
+    def open(self, handle):
+        return self.MAP + int(handle.rstrip(b"\0").split(b":")[1])
+
+    def close(self, block):
+        self.closed.append(block)
+
+    def free(self, block):
+        self.freed.append(block)
+
+
+def _fused_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["RANK"] = str(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nat = _FakeExchange()
+        fc = sharding.FusedColumnShard(device=0, native=nat)
+        blocks = list(fc.blocks)
+        fc.close()
+        fc.close()  # idempotent
+        out_q.put((rank, fc.world, fc.rank, blocks, nat.closed, nat.freed))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_fused_column_shard_handle_exchange_gloo(world):
+    """Every rank maps every peer's exchange block (opened from the handle the
+    peer published) and keeps its own at its rank index; close() unmaps the
+    peers and frees its own block exactly once."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, w, r, blocks, closed, freed in res:
+        assert (w, r) == (world, rank)
+        own = 0x1000 * (1 + rank)
+        expect = [own if j == rank else _FakeExchange.MAP + 0x1000 * (1 + j) for j in range(world)]
+        assert blocks == expect
+        assert sorted(closed) == sorted(b for j, b in enumerate(expect) if j != rank)
+        assert freed == [own]
+
+
+def test_fused_column_shard_rejects_more_than_eight_ranks(monkeypatch):
+    monkeypatch.setattr(dist, "is_initialized", lambda: True)
+    monkeypatch.setattr(dist, "get_world_size", lambda group=None: 16)
+    monkeypatch.setattr(dist, "get_rank", lambda group=None: 0)
+    with pytest.raises(Exception, match="at most 8"):
+        sharding.FusedColumnShard(device=0, native=_FakeExchange())
