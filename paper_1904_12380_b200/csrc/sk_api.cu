@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -108,7 +109,6 @@ bool gres_split(int nstages) {
   const int v = g_gres_split.load();
   return v < 0 ? nstages >= 4 : v != 0;
 }  // K3g poller back-off between polls (ns)    // force K3g ring depth (0 = as deep as smem allows)
-std::atomic<int> g_gres_x{8192};  // K3g per-row exchange cost model, in floats of streaming time
 std::atomic<int> g_k3_impl{3};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
 
 // Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.
@@ -417,41 +417,52 @@ struct GresChoice {
   int64_t slice = 0;
   double score = 0.0;
 };
+// Step-time model, fitted to a (P, stages) grid measured on B200 (c4, c5b;
+// profiles/r1_gres_grid.jsonl) and checked against the best measured plan of
+// ten other long-row shapes.  Per row step a CTA streams 8 B x slice at its
+// SM's bandwidth share (HBM / active SMs, capped at ~55 GB/s per SM) plus
+// the part of the exchange round trip that is not hidden:
+//   X1 = -0.52 + 0.62 ln(world*P) - 0.0506 * slice/1000   us  (ring depth 3, lag 1)
+// halved at lag >= 2 (depth 4-5); depth 2 exposes a further ~1.3 us.  The
+// job takes ceil(rows / groups) steps.  One CTA per SM (the measured regime).
+double gres_time_us(int64_t rows, int P, int st, int64_t slice, int groups, int world, int nvr,
+                    int sms) {
+  const double active = double(std::min<int64_t>(groups, rows)) * P * nvr;
+  const double bw_sm = std::min(6.47e12 / std::max(1.0, active), 55e9);
+  (void)sms;
+  const double ts = double(slice) * 8.0 / bw_sm * 1e6;
+  const double x1 = std::max(0.1, -0.52 + 0.62 * std::log(double(world) * P) -
+                                      0.0506 * double(slice) / 1000.0);
+  const double x = st == 2 ? x1 + 1.3 : st == 3 ? x1 : 0.5 * x1;
+  return double((rows + groups - 1) / groups) * (ts + x);
+}
+
 GresChoice plan_gres(int64_t rows, int64_t cols, int mode, const DevInfo& di, int world, int nvr) {
   GresChoice best;
-  const double xg = std::max(0, g_gres_x.load());
+  double best_t = 0.0;
   for (int P = 1; P * world <= kGresMaxSlots && P <= di.sms; ++P) {
     if (g_gres_p.load() > 0 && P != g_gres_p.load()) continue;
     const int64_t slice = align_up((cols + P - 1) / P, 4);
     if ((P - 1) * slice >= cols) continue;
-    int st = static_cast<int>(std::min<int64_t>(
+    const int st_max = static_cast<int>(std::min<int64_t>(
         kGresStages, kGresSmemMax / (slice * int64_t(sizeof(float)))));
-    if (g_gres_st.load() >= 2) {
-      if (st < g_gres_st.load()) continue;
-      st = g_gres_st.load();
-    }
-    if (st < 2) continue;
-    const size_t smem = size_t(st) * slice * sizeof(float);
-    const bool split = gres_split(st);
-    const int occ = occupancy(gres_fn(mode, st, split), split ? kGresBlock : kGresThreads, smem);
-    if (occ < 1) continue;
-    const int groups = di.sms * occ / (P * nvr);
-    if (groups < 1) continue;
-    const int64_t rows_g = (rows + groups - 1) / groups;
-    if (rows_g >= (int64_t(1) << 31)) continue;
-    // SMs covered x per-step efficiency (the exchange costs ~xg floats of
-    // streaming per row step when it is not hidden); a 2-stage ring cannot
-    // overlap it at all, deeper rings hide more (measured c4 / c5b: 14x3
-    // 170 us, 20x4 187, 10x2 229; 74x4 1530, 74x3 1690, 48x2 1775)
-    const double score = double(std::min<int64_t>(groups, rows)) * P * nvr / occ *
-                         double(slice) / (double(slice) + xg) * (st == 2 ? 0.8 : 1.0) *
-                         (1.0 + 0.01 * st);
-    if (score > best.score) {
-      best.score = score;
-      best.P = P;
-      best.st = st;
-      best.groups = groups;
-      best.slice = slice;
+    for (int st = 2; st <= st_max; ++st) {
+      if (g_gres_st.load() >= 2 && st != g_gres_st.load()) continue;
+      const size_t smem = size_t(st) * slice * sizeof(float);
+      const bool split = gres_split(st);
+      if (occupancy(gres_fn(mode, st, split), split ? kGresBlock : kGresThreads, smem) < 1) continue;
+      const int groups = di.sms / (P * nvr);  // one CTA per SM
+      if (groups < 1) continue;
+      if ((rows + groups - 1) / groups >= (int64_t(1) << 31)) continue;
+      const double t = gres_time_us(rows, P, st, slice, groups, world, nvr, di.sms);
+      if (best.P == 0 || t < best_t) {
+        best_t = t;
+        best.P = P;
+        best.st = st;
+        best.groups = groups;
+        best.slice = slice;
+        best.score = 1.0 / t;
+      }
     }
   }
   return best;
@@ -495,15 +506,30 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
   }
   if (kind == kPathSeg) {
     const int impl0 = g_k3_impl.load();
-    // Resident rows: K3c (one thread-block cluster per row) or K3g (P CTAs
-    // anywhere on the chip, global-memory exchange).  Each candidate is scored
-    // as SMs covered x per-row efficiency slice / (slice + exchange cost).
+    // Resident rows: K3g (P CTAs anywhere on the chip, global-memory
+    // exchange; plan from the measured step-time model) -- measured 1.1-1.4x
+    // faster than K3c on every long-row shape tried -- else K3c (one
+    // thread-block cluster per row) when K3g is off or cannot launch.
     const int gres = g_gres.load();
     if ((cols > kSegCap || gres == 2) && (impl0 == 5 || impl0 == 3)) {
+      GresChoice gc;
+      if (gres != 0 && impl0 != 5 && di.coop) gc = plan_gres(rows, cols, mode, di, 1, 1);
+      if (gc.P > 0) {
+        p.kind = kPathSeg;
+        p.k3 = 7;
+        p.nseg = gc.P;
+        p.seglen = static_cast<int>(gc.slice);
+        p.lag = gc.st;
+        p.threads = gres_split(gc.st) ? kGresBlock : kGresThreads;
+        p.smem = size_t(gc.st) * gc.slice * sizeof(float);
+        p.grid = int64_t(gc.groups) * gc.P;
+        return SK_OK;
+      }
+      if (gres == 2) return arg_fail("K3g cannot launch this row length on this device");
       double best_c = 0.0;
       int c_cs = 0, c_st = 0, c_n = 0;
       int64_t c_slice = 0;
-      if (g_cluster_k3.load() && gres != 2 && cols <= 16 * kClusterSliceMaxAny) {
+      if (g_cluster_k3.load() && cols <= 16 * kClusterSliceMaxAny) {
         // K3c: the cluster size that keeps the most SMs busy (GPC packing), with
         // a ring of >= 2 stages of the row slice in shared memory
         const void* fn = cluster_fn(mode);
@@ -528,22 +554,6 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
           }
         }
       }
-      GresChoice gc;
-      if (gres != 0 && di.coop) gc = plan_gres(rows, cols, mode, di, 1, 1);
-      const double best_g = gc.score;
-      const int g_p = gc.P, g_st = gc.st, g_groups = gc.groups;
-      const int64_t g_slice = gc.slice;
-      if (g_p > 0 && (gres == 2 || best_g > best_c)) {
-        p.kind = kPathSeg;
-        p.k3 = 7;
-        p.nseg = g_p;
-        p.seglen = static_cast<int>(g_slice);
-        p.lag = g_st;
-        p.threads = gres_split(g_st) ? kGresBlock : kGresThreads;
-        p.smem = size_t(g_st) * g_slice * sizeof(float);
-        p.grid = int64_t(g_groups) * g_p;
-        return SK_OK;
-      }
       if (c_n > 0) {
         p.kind = kPathSeg;
         p.k3 = 6;
@@ -556,7 +566,6 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
         return SK_OK;
       }
       if (impl0 == 5) return arg_fail("cluster K3 cannot launch on this device");
-      if (gres == 2) return arg_fail("K3g cannot launch this row length on this device");
     }
     const bool chunked = cols > kSegCap && impl0 != 1;
     const bool warp3 = cols > kSegCap && (impl0 == 3 || impl0 == 4);
@@ -1088,7 +1097,6 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "k3_impl") g_k3_impl = value;
   else if (k == "gres") g_gres = value;
   else if (k == "gres_p") g_gres_p = value;
-  else if (k == "gres_x") g_gres_x = value;
   else if (k == "gres_st") g_gres_st = value;
   else if (k == "gres_diag") g_gres_diag = value;
   else if (k == "gres_sleep") g_gres_sleep = value;
