@@ -417,24 +417,24 @@ struct GresChoice {
   int64_t slice = 0;
   double score = 0.0;
 };
-// Plan choice, from a (P, stages) grid measured on B200 (c4, c5b;
-// profiles/r1_gres_grid.jsonl) and the best measured plan of ten other
-// long-row shapes:
-//  * ring depth: 3 (lag 1, the publisher polls) while P <= 32; 4 (lag 2, a
-//    separate poller warp) above -- the poller warp costs ~0.4 us per row
-//    step, which only pays off when the group is large enough that the
-//    exchange cannot hide behind one row step; depth 2 exposes the whole
-//    round trip (penalised; used only when nothing deeper fits);
-//  * time ~ steps x (streamed floats per CTA x active/SMs + exchange cost)
-//    with steps = ceil(rows / groups), exchange ~ 550 + 40 * slots floats
-//    (slots = world * min(P, 32) merged pairs); one CTA per SM.
-double gres_time(int64_t rows, int P, int st, int64_t slice, int groups, int world, int nvr,
-                 int sms) {
-  const bool deep = P > 32;
-  const double fit = ((st == 3 && !deep) || (st >= 4 && deep)) ? 1.0 : st >= 3 ? 0.85 : 0.75;
+// Step-time model, fitted to a (P, stages) grid measured on B200 (c4, c5b;
+// profiles/r1_gres_grid.jsonl) and checked against the best measured plan of
+// ten other long-row shapes (it picks it, within ~5%, on all of them):
+//   step   = streaming of 8 B x slice at the SM's share of HBM (<= 55 GB/s)
+//          + X, the part of the exchange round trip the ring does not hide:
+//   RTT    = 1.6 us (+16 ns per merged pair beyond 32, at most 2.3 us)
+//   hide   = 0.0775 us per 1000 floats of slice per lag step
+//   X      = RTT (depth 2) | RTT - hide (depth 3, lag 1) |
+//            RTT - 2 hide + 0.3 us (depth 4, lag 2: the poller warp's cost)
+//   time   = (ceil(rows / groups) + 1) x step     (one CTA per SM)
+double gres_time_us(int64_t rows, int P, int st, int64_t slice, int groups, int world, int nvr) {
   const double active = double(std::min<int64_t>(groups, rows)) * P * nvr;
-  const double x = 550.0 + 40.0 * world * std::min(P, 32);
-  return double((rows + groups - 1) / groups) * (double(slice) * active / sms + x) / fit;
+  const double ts = double(slice) * 8.0 / std::min(6.47e12 / std::max(1.0, active), 55e9) * 1e6;
+  const double rtt = std::min(2.3, 1.6 + 0.016 * std::max(0, world * P - 32));
+  const double hide = 0.0775 * double(slice) / 1000.0;
+  const double x = st == 2 ? rtt : st == 3 ? std::max(0.1, rtt - hide)
+                                           : std::max(0.1, rtt - 2.0 * hide) + 0.3;
+  return double((rows + groups - 1) / groups + 1) * (ts + x);
 }
 
 GresChoice plan_gres(int64_t rows, int64_t cols, int mode, const DevInfo& di, int world, int nvr) {
@@ -444,28 +444,27 @@ GresChoice plan_gres(int64_t rows, int64_t cols, int mode, const DevInfo& di, in
     if (g_gres_p.load() > 0 && P != g_gres_p.load()) continue;
     const int64_t slice = align_up((cols + P - 1) / P, 4);
     if ((P - 1) * slice >= cols) continue;
+    // depth 5 (lag 3) measured no better than 4: only when forced
+    const int st_cap = g_gres_st.load() >= 2 ? kGresStages : 4;
     const int st_max = static_cast<int>(std::min<int64_t>(
-        kGresStages, kGresSmemMax / (slice * int64_t(sizeof(float)))));
-    if (st_max < 2) continue;
-    int st = (P <= 32 && st_max >= 3) ? 3 : st_max >= 4 ? 4 : st_max;
-    if (g_gres_st.load() >= 2) {
-      if (g_gres_st.load() > st_max) continue;
-      st = g_gres_st.load();
-    }
-    const size_t smem = size_t(st) * slice * sizeof(float);
-    const bool split = gres_split(st);
-    if (occupancy(gres_fn(mode, st, split), split ? kGresBlock : kGresThreads, smem) < 1) continue;
+        st_cap, kGresSmemMax / (slice * int64_t(sizeof(float)))));
     const int groups = di.sms / (P * nvr);  // one CTA per SM
-    if (groups < 1) continue;
-    if ((rows + groups - 1) / groups >= (int64_t(1) << 31)) continue;
-    const double t = gres_time(rows, P, st, slice, groups, world, nvr, di.sms);
-    if (best.P == 0 || t < best_t) {
-      best_t = t;
-      best.P = P;
-      best.st = st;
-      best.groups = groups;
-      best.slice = slice;
-      best.score = 1.0 / t;
+    if (groups < 1 || (rows + groups - 1) / groups >= (int64_t(1) << 31)) continue;
+    for (int st = 2; st <= st_max; ++st) {
+      if (g_gres_st.load() >= 2 && st != g_gres_st.load()) continue;
+      const size_t smem = size_t(st) * slice * sizeof(float);
+      const bool split = gres_split(st);
+      if (occupancy(gres_fn(mode, st, split), split ? kGresBlock : kGresThreads, smem) < 1)
+        continue;
+      const double t = gres_time_us(rows, P, st, slice, groups, world, nvr);
+      if (best.P == 0 || t < best_t) {
+        best_t = t;
+        best.P = P;
+        best.st = st;
+        best.groups = groups;
+        best.slice = slice;
+        best.score = 1.0 / t;
+      }
     }
   }
   return best;
