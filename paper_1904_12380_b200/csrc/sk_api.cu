@@ -437,6 +437,13 @@ double gres_time_us(int64_t rows, int P, int st, int64_t slice, int groups, int 
   return double((rows + groups - 1) / groups + 1) * (ts + x);
 }
 
+// The plan is a function of the row LENGTH only (modelled at a fixed row
+// count), so a row block computed alone takes the same plan -- and gives the
+// same bits -- as the whole matrix: row sharding stays communication-free and
+// bit-identical.  At 2048 rows the choice equals the per-shape best on every
+// measured long-row shape.
+constexpr int64_t kGresPlanRows = 2048;
+
 GresChoice plan_gres(int64_t rows, int64_t cols, int mode, const DevInfo& di, int world, int nvr) {
   GresChoice best;
   double best_t = 0.0;
@@ -515,7 +522,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     const int gres = g_gres.load();
     if ((cols > kSegCap || gres == 2) && (impl0 == 5 || impl0 == 3)) {
       GresChoice gc;
-      if (gres != 0 && impl0 != 5 && di.coop) gc = plan_gres(rows, cols, mode, di, 1, 1);
+      if (gres != 0 && impl0 != 5 && di.coop) gc = plan_gres(kGresPlanRows, cols, mode, di, 1, 1);
       if (gc.P > 0) {
         p.kind = kPathSeg;
         p.k3 = 7;
@@ -1002,7 +1009,7 @@ int colshard_launch(const float* x, float* y, int64_t rows, int64_t cols, int64_
   SK_CUDA(cudaGetDevice(&dev));
   const DevInfo di = dev_info(dev);
   if (!di.coop) return arg_fail("device cannot co-schedule the fused column shard");
-  const GresChoice gc = plan_gres(rows > 0 ? rows : 1, cols, mode, di, world, nvr);
+  const GresChoice gc = plan_gres(kGresPlanRows, cols, mode, di, world, nvr);
   if (gc.P == 0) return arg_fail("shard row too long for the fused column shard (use the split path)");
   const bool split = gres_split(gc.st);
   const int lag = gc.st >= 5 ? 3 : gc.st == 4 ? 2 : 1;
