@@ -1218,8 +1218,10 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
   const int64_t row_bytes = cols * 4;
   const int64_t total = rows * row_bytes;
   // Chunk schedule: steady chunks of ~1/4 of the job (4..16 MiB; tunable),
-  // ramped 1/8, 1/4, 1/2 at both ends when the job is long enough for the
-  // ramp to pay for its extra per-copy latency.  Whole rows.
+  // ramped 1/8, 1/4, 1/2 at both ends: the first H2D and the last D2H are
+  // the only transfers that cannot overlap the other direction, so they are
+  // made small (each ramp chunk costs ~10 us of issue + DMA setup, paid once).
+  // Whole rows.
   int64_t chunk_bytes = std::min<int64_t>(std::max<int64_t>(total / 4, 4 << 20), 16 << 20);
   if (g_host_chunk_kb.load() > 0) chunk_bytes = int64_t(g_host_chunk_kb.load()) << 10;
   const int64_t big = std::min(rows, std::max<int64_t>(1, chunk_bytes / row_bytes));
@@ -1230,7 +1232,7 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
     int64_t left = rows;
     std::vector<int64_t> tail;
     for (int64_t r : head) {  // ramp up at the start and down at the end
-      if (left >= 2 * r + 8 * big) {
+      if (left >= 2 * r + 2 * big && r * row_bytes >= (int64_t(512) << 10)) {
         sched.push_back(r);
         tail.push_back(r);
         left -= 2 * r;
@@ -1294,10 +1296,12 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
     SK_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_k[i], 0));
     SK_CUDA(cudaMemcpyAsync(y_host + r0 * cols, c->dy[i], bytes, cudaMemcpyDeviceToHost,
                             c->s_d2h));
-    SK_CUDA(cudaMemcpyAsync(c->hbad + k, c->dbad + k, sizeof(unsigned long long),
-                            cudaMemcpyDeviceToHost, c->s_d2h));
     SK_CUDA(cudaEventRecord(c->ev_d2h[i], c->s_d2h));
   }
+  // every chunk's non-finite flag in one small copy after the last kernel
+  // (one DMA instead of one per chunk between the bulk transfers)
+  SK_CUDA(cudaMemcpyAsync(c->hbad, c->dbad, size_t(nchunks) * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, c->s_d2h));
   SK_CUDA(cudaStreamSynchronize(c->s_d2h));
   for (int64_t k = 0; k < nchunks; ++k) {
     if (c->hbad[k] == SK_EXCHANGE_ABORTED) {
