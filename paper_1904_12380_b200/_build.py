@@ -89,6 +89,38 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+TORCH_OPS_SRC = PKG / "torch_ops" / "sk_torch_ops.cpp"
+TORCH_OPS_LIB = PKG / "libsoftmax_b200_torch.so"
+
+
+def build_torch_ops(force: bool = False) -> Path:
+    """torch.ops.softmax_b200.* (TORCH_LIBRARY launchers over the C ABI), g++
+    against torch's headers, linked to libsoftmax_b200.so via $ORIGIN."""
+    deps = [TORCH_OPS_SRC, ROOT / "include" / "softmax_b200.h", LIB]
+    if not force and not _stale(TORCH_OPS_LIB, deps):
+        return TORCH_OPS_LIB
+    import torch
+    from torch.utils import cpp_extension as ce
+
+    inc = [str(Path(torch.__file__).parent / "include"),
+           str(Path(torch.__file__).parent / "include" / "torch" / "csrc" / "api" / "include"),
+           "/usr/local/cuda/include", str(ROOT / "include")]
+    libdir = str(Path(torch.__file__).parent / "lib")
+    abi = int(torch._C._GLIBCXX_USE_CXX11_ABI)
+    tmp = TORCH_OPS_LIB.with_suffix(".so.tmp")
+    cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-shared", f"-D_GLIBCXX_USE_CXX11_ABI={abi}",
+           *[f"-I{i}" for i in inc], str(TORCH_OPS_SRC), "-o", str(tmp),
+           f"-L{libdir}", f"-L{PKG}", "-lsoftmax_b200", "-lc10", "-lc10_cuda", "-ltorch",
+           "-ltorch_cpu", "-ltorch_cuda", "-Wl,-rpath,$ORIGIN", f"-Wl,-rpath,{libdir}",
+           "-L/usr/local/cuda/lib64", "-lcudart"]
+    del ce
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"torch ops build failed: {' '.join(cmd)}\n{r.stdout}{r.stderr}")
+    os.replace(tmp, TORCH_OPS_LIB)
+    return TORCH_OPS_LIB
+
+
 def build_oracle(force: bool = False) -> Path:
     """Compile the C restatement of the reference (test infrastructure only)."""
     src = ORACLE_DIR / "sk_oracle.c"
@@ -106,5 +138,6 @@ def build_oracle(force: bool = False) -> Path:
 
 if __name__ == "__main__":
     build_native(force="--force" in sys.argv, verbose=True)
+    build_torch_ops(force="--force" in sys.argv)
     build_oracle(force="--force" in sys.argv)
     print(LIB, ORACLE_LIB)

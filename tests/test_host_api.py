@@ -175,3 +175,22 @@ def test_product_never_imports_oracle():
         assert "import oracle" not in src and "from oracle" not in src, p
     for p in (ROOT / "paper_1904_12380_b200" / "csrc").iterdir():
         assert "sk_oracle" not in p.read_text(), p
+
+
+def test_torch_ops_register_without_a_gpu():
+    """torch.ops.softmax_b200 loads on a CPU-only host; every op has a schema
+    and only a CUDA kernel (a CPU tensor raises: no CPU fallback)."""
+    import torch
+
+    from paper_1904_12380_b200 import torch_ops
+
+    ops = torch_ops.load()
+    for name, schema in (("softmax_fwd", "softmax_fwd(Tensor x, bool clip) -> Tensor"),
+                         ("softmax_fwd_out", "softmax_fwd_out(Tensor x, Tensor(a!) y, bool clip) -> ()"),
+                         ("row_max", "row_max(Tensor x) -> Tensor"),
+                         ("row_sumexp", "row_sumexp(Tensor x, Tensor gmax, bool clip) -> Tensor"),
+                         ("normalize_", "normalize_(Tensor x, Tensor gmax, Tensor gsum, Tensor(a!) y, bool clip) -> ()")):
+        op = getattr(ops, name)
+        assert str(op.default._schema) == "softmax_b200::" + schema
+    with pytest.raises((NotImplementedError, RuntimeError)):
+        ops.softmax_fwd(torch.zeros(2, 3), True)
