@@ -257,6 +257,23 @@ def test_k3_gres_full_c4_rowsums():
     assert float((rs - 1).abs().max()) <= 1e-5
 
 
+@pytest.mark.parametrize("C", [4_194_304, 4_400_000, 8_000_000])
+def test_rows_at_and_beyond_chip_capacity(C, oracle):
+    """4 M floats: K3g at its largest group (148 CTAs, 2-stage ring).  Longer
+    rows than the chip's shared memory holds (> 148 x 225 KB / 2 stages) fall
+    back to the warp queue / split path; all match the oracle."""
+    from paper_1904_12380_b200 import tensor
+
+    x = np.empty((3, C), np.float32)
+    tensor.fill_normal_array(x, 17, 3.0)
+    x[1, C // 3] = -400.0
+    plan = gu.plan(3, C)
+    assert ("k3_gres" in plan) == (C <= 148 * 28_800), plan
+    y, bad = gu.softmax_abi(x, 0)
+    assert bad == gu.NO_BAD
+    assert_parity(oracle, y, oracle.softmax_ref(x, True, nthreads=0), what=plan)
+
+
 def test_seg_lengths_all_agree(oracle):
     x = configs.generate("c4", 0, 4)[:, :100000].copy()
     ref = oracle.softmax_ref(x)
