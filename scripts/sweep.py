@@ -26,7 +26,7 @@ K1_SHAPES = {
     "c2": [(4, 8, 4, 1, 0), (4, 16, 2, 1, 0), (4, 8, 4, 2, 0), (4, 16, 2, 2, 0), (8, 8, 2, 1, 0)],
     "c5a": [(4, 16, 4, 1, 0), (4, 16, 4, 1, 1), (4, 16, 4, 2, 0), (4, 32, 2, 1, 0),
             (4, 32, 2, 2, 0), (8, 16, 2, 1, 0)],
-    "c3": [(4, 32, 8, 1, 0), (8, 32, 4, 1, 0)],
+    "c3": [(4, 32, 8, 1, 0), (4, 32, 8, 1, 1), (8, 32, 4, 1, 0)],
     "c1": [(1, 16, 4, 2, 0), (1, 16, 4, 1, 1), (1, 32, 2, 2, 0)],
 }
 
@@ -133,6 +133,13 @@ def main():
             record(f"path={path}", bench_once(xs, ys, rows, cols, args.reps, s))
         _native.set_tuning("path", -1)
     elif cols <= 1024:
+        for path in (1, 2):  # K2 TMA block-per-row, K4 split, on the same rows
+            _native.set_tuning("path", path)
+            try:
+                record(f"path={path}", bench_once(xs, ys, rows, cols, args.reps, s))
+            except Exception as e:  # noqa: BLE001
+                print(json.dumps({"variant": f"path={path}", "error": str(e)}))
+        _native.set_tuning("path", -1)
         _native.set_tuning("pdl", 0)
         record("default pdl=0", bench_once(xs, ys, rows, cols, args.reps, s))
         _native.set_tuning("pdl", 1)
