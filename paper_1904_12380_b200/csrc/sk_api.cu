@@ -159,6 +159,8 @@ const K1Entry kK1Table[] = {
     SK_K1(4, 32, 4, 1, 0), SK_K1(4, 32, 8, 1, 0), SK_K1(4, 32, 1, 2, 0), SK_K1(4, 32, 2, 1, 0),
     SK_K1(4, 8, 4, 1, 1), SK_K1(4, 16, 2, 1, 1), SK_K1(4, 16, 4, 1, 1), SK_K1(4, 32, 2, 1, 1),
     SK_K1(4, 32, 4, 1, 1), SK_K1(4, 32, 8, 1, 1), SK_K1(4, 16, 1, 4, 1), SK_K1(4, 8, 1, 4, 1),
+    // medium rows: a warp holds up to 2048 / 3072 floats in registers
+    SK_K1(4, 32, 16, 1, 0), SK_K1(4, 32, 24, 1, 0),
     // 256-bit path (cols % 8 == 0, 32-B aligned rows)
     SK_K1(8, 8, 1, 4, 0), SK_K1(8, 16, 1, 2, 0), SK_K1(8, 16, 1, 4, 0), SK_K1(8, 8, 2, 1, 0),
     SK_K1(8, 8, 2, 2, 0), SK_K1(8, 16, 2, 1, 0), SK_K1(8, 32, 1, 1, 0), SK_K1(8, 32, 1, 2, 0),
@@ -176,7 +178,9 @@ const K1Entry* k1_find(int vec, int lpr, int nv, int u, int pf) {
   return nullptr;
 }
 
-// default K1 shape per row length (covers cols <= 1024).  gm: grid multiplier
+constexpr int64_t kK1MaxCols = 3072;  // 128-bit rows up to here take K1
+
+// default K1 shape per row length (covers cols <= 1024; 128-bit rows <= 3072).  gm: grid multiplier
 // over SMs x occupancy; 0 = non-persistent (one row batch per warp, grid = rows /
 // rows-per-CTA), which measured fastest for every shape (c5a: 7.0 TB/s).
 void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u, int& pf, int& gm) {
@@ -195,7 +199,11 @@ void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u, int& pf, int& 
     else if (cols <= 128) { lpr = 8; nv = 4; u = 1; }
     else if (cols <= 256) { lpr = 16; nv = 4; u = 2; }
     else if (cols <= 512) { lpr = 32; nv = 4; u = 1; }
-    else { lpr = 32; nv = 8; u = 1; }
+    else if (cols <= 1024) { lpr = 32; nv = 8; u = 1; }
+    // medium rows: a whole warp holds the row in registers -- measured
+    // 1.1-1.3x faster than the TMA block-per-row K2 from 1536 to 3072 columns
+    else if (cols <= 2048) { lpr = 32; nv = 16; u = 1; }
+    else { lpr = 32; nv = 24; u = 1; }
   } else {
     if (cols <= 8) { lpr = 8; nv = 1; u = 4; }
     else if (cols <= 16) { lpr = 16; nv = 1; u = 4; }
@@ -488,10 +496,10 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
   const int force = g_force_path.load();
   PathKind kind;
   if (force >= 0) kind = static_cast<PathKind>(force);
-  else if (cols <= 1024) kind = kPathK1;
+  else if (cols <= 1024 || (vec && cols <= kK1MaxCols)) kind = kPathK1;
   else if (vec) kind = kPathSeg;
   else kind = kPathSplit;
-  if (kind == kPathK1 && cols > 1024) return arg_fail("k1 path needs cols <= 1024");
+  if (kind == kPathK1 && cols > kK1MaxCols) return arg_fail("k1 path needs cols <= 3072");
   if (kind == kPathSeg && !vec) return arg_fail("seg path needs 16-B aligned rows");
 
   if (kind == kPathK1) {
@@ -506,9 +514,16 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     if (int64_t(lpr) * nv * e->vec < cols) return arg_fail("K1 shape does not cover cols");
     p.kind = kPathK1;
     p.k1 = e;
-    const int64_t rows_per_cta = int64_t(kRowsThreads / 32) * u * (32 / lpr);
+    // block size: 256 threads, halved (to 64) while the job would occupy fewer
+    // CTAs than SMs -- a small job then spreads over the chip.  Each row is one
+    // warp's work whatever the block size, so the bits do not change.
+    int threads = kRowsThreads;
+    auto rows_per = [&](int t) { return int64_t(t / 32) * u * (32 / lpr); };
+    while (threads > 64 && (rows + rows_per(threads) - 1) / rows_per(threads) < di.sms) threads /= 2;
+    p.threads = threads;
+    const int64_t rows_per_cta = rows_per(threads);
     const int64_t need = (rows + rows_per_cta - 1) / rows_per_cta;
-    const int occ = occupancy(reinterpret_cast<const void*>(e->fn[mode]), kRowsThreads, 0);
+    const int occ = occupancy(reinterpret_cast<const void*>(e->fn[mode]), threads, 0);
     const int64_t cap = gm > 0 ? int64_t(di.sms) * std::max(occ, 1) * gm : need;
     p.grid = std::max<int64_t>(1, std::min({need, cap, int64_t(INT32_MAX)}));
     return SK_OK;
@@ -787,7 +802,7 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
   const float sh = shift_scale();
   if (p.kind == kPathK1) {
     SK_CUDA(launch_k(reinterpret_cast<const void*>(p.k1->fn[mode]),
-                     dim3(static_cast<unsigned>(p.grid)), dim3(kRowsThreads), 0, s, false, x, y,
+                     dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), 0, s, false, x, y,
                      rows, static_cast<int>(cols), ldx, ldy, bad, sh));
     return SK_OK;
   }
@@ -1141,7 +1156,7 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
   if (st) return st;
   if (p.kind == kPathK1)
     snprintf(buf, buflen, "k1 vec=%d lpr=%d nv=%d u=%d pf=%d threads=%d grid=%lld", p.k1->vec,
-             p.k1->lpr, p.k1->nv, p.k1->u, p.k1->pf, kRowsThreads, (long long)p.grid);
+             p.k1->lpr, p.k1->nv, p.k1->u, p.k1->pf, p.threads, (long long)p.grid);
   else if (p.kind == kPathSeg)
     snprintf(buf, buflen, "%s nseg=%d seglen=%d threads=%d smem=%zu chunk_rows=%lld stages=%d grid=%lld",
              p.k3 == 6 ? "k3_cluster"

@@ -175,7 +175,9 @@ __device__ __forceinline__ void k1_process_any(RowBatch<VEC, LPR, NV, U>& B,
 // >= 4 otherwise, so there are always enough warps to cover HBM latency.
 template <int VEC, int NV, int U, int PF>
 constexpr int k1_min_blocks() {
-  return NV * VEC * U * (PF ? 2 : 1) >= 32 ? 3 : 4;
+  return NV * VEC * U * (PF ? 2 : 1) >= 128 ? 1
+         : NV * VEC * U * (PF ? 2 : 1) >= 64 ? 2
+         : NV * VEC * U * (PF ? 2 : 1) >= 32 ? 3 : 4;
 }
 
 template <int MODE, int VEC, int LPR, int NV, int U, int PF>

@@ -169,6 +169,36 @@ def test_k1_instantiations_all_agree(oracle):
         _native.set_tuning("k1_pf", -1)
 
 
+@pytest.mark.parametrize("rows,C", [(300, 2048), (37, 1536), (4096, 3072), (5, 2052),
+                                    (2000, 1028), (1, 3072)])
+def test_k1_medium_rows(rows, C, oracle):
+    """128-bit rows of 1025..3072 floats: a whole warp holds the row in
+    registers (K1, 16/24 vectors per lane); small jobs shrink the block so
+    they spread over the SMs (same bits).  Clip firing, large negative row,
+    strided pitch, non-finite detection."""
+    from paper_1904_12380_b200 import tensor
+
+    x = np.empty((rows, C), np.float32)
+    tensor.fill_normal_array(x, C + rows, 5.0)
+    x[0, C // 2] = -300.0
+    x[rows // 2, :] -= 500.0
+    plan = gu.plan(rows, C)
+    assert plan.startswith("k1 vec=4 lpr=32"), plan
+    for mode in (0, 1):
+        ref = oracle.softmax_ref(x, clip=(mode == 0))
+        y, bad = gu.softmax_abi(x, mode)
+        assert bad == gu.NO_BAD
+        assert_parity(oracle, y, ref, what=(rows, C, mode, plan))
+    y, _ = gu.softmax_abi(x, 0, ldx=C + 8, ldy=C + 4)
+    assert_parity(oracle, y, oracle.softmax_ref(x), what=(rows, C, "strided"))
+    whole, _ = gu.softmax_abi(x, 0)
+    part, _ = gu.softmax_abi(x[rows // 3:], 0)   # a row block: same bits
+    assert np.array_equal(part.view(np.uint32), whole[rows // 3:].view(np.uint32))
+    x2 = x.copy()
+    x2[rows - 1, C - 1] = np.nan
+    assert gu.softmax_abi(x2, 0)[1] == rows - 1
+
+
 @pytest.mark.parametrize("impl", [0, 1, 2, 3, "3b", 4, 5, "5x2", "g"])
 def test_every_k3_implementation(impl, oracle):
     """Long-row kernels: ordered CTA queue (0), smem-resident cooperative (1),
