@@ -23,6 +23,7 @@
 #include "sk_reg3.cuh"
 #include "sk_cluster.cuh"
 #include "sk_gres.cuh"
+#include "sk_rows_mw.cuh"
 
 namespace sk {
 namespace {
@@ -67,7 +68,7 @@ DevInfo dev_info(int dev) {
 }
 
 // ------------------------------------------------------------ tuning overrides
-std::atomic<int> g_force_path{-1};  // -1 auto, 0 k1, 1 seg, 2 split
+std::atomic<int> g_force_path{-1};  // -1 auto, 0 k1, 1 seg, 2 split, 3 k1m
 // fault hook mirroring kernels._SKIP_MAX_SHIFT (kernels.py:103-105): when set the
 // kernels shift by 0 instead of the row max, so large logits overflow exp.
 std::atomic<int> g_skip_max_shift{0};
@@ -370,12 +371,42 @@ int occupancy(const void* fn, int threads, size_t smem) {
 }
 
 // --------------------------------------------------------------- planning
-enum PathKind { kPathK1 = 0, kPathSeg = 1, kPathSplit = 2 };
+enum PathKind { kPathK1 = 0, kPathSeg = 1, kPathSplit = 2, kPathK1m = 3 };
+
+// ------------------------------------------------------------ K1m table
+using K1mFn = K1Fn;
+struct K1mEntry {
+  int wpr, nv;
+  K1mFn fn[3];
+};
+#define SK_K1M(WPR, NV)                                                                  \
+  K1mEntry {                                                                             \
+    WPR, NV, {                                                                           \
+      &k1m_rows<kClipAccurate, WPR, NV>, &k1m_rows<kAccurate, WPR, NV>,                  \
+          &k1m_rows<kApprox, WPR, NV>                                                    \
+    }                                                                                    \
+  }
+const K1mEntry kK1mTable[] = {SK_K1M(2, 16), SK_K1M(4, 8), SK_K1M(4, 12), SK_K1M(4, 16),
+                              SK_K1M(8, 8)};
+#undef SK_K1M
+const K1mEntry* k1m_find(int wpr, int nv) {
+  for (const auto& e : kK1mTable)
+    if (e.wpr == wpr && e.nv == nv) return &e;
+  return nullptr;
+}
+constexpr int64_t kK1mMaxCols = 8192;
+std::atomic<int> g_k1m{1}, g_k1m_wpr{0}, g_k1m_nv{0};
+void k1m_default(int64_t cols, int& wpr, int& nv) {
+  if (cols <= 4096) { wpr = 4; nv = 8; }
+  else if (cols <= 6144) { wpr = 4; nv = 12; }
+  else { wpr = 4; nv = 16; }
+}
 
 struct Plan {
   PathKind kind = kPathK1;
   // K1
   const K1Entry* k1 = nullptr;
+  const K1mEntry* k1m = nullptr;
   // seg (K2: nseg == 1; K3: nseg > 1)
   int nseg = 1, seglen = 0, threads = 0, lag = 0;
   int k3 = 0;  // 0 none/K2, 1 dyn, 2 smem, 3 chunk
@@ -497,11 +528,27 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
   PathKind kind;
   if (force >= 0) kind = static_cast<PathKind>(force);
   else if (cols <= 1024 || (vec && cols <= kK1MaxCols)) kind = kPathK1;
+  else if (vec && cols <= kK1mMaxCols && g_k1m.load()) kind = kPathK1m;
   else if (vec) kind = kPathSeg;
   else kind = kPathSplit;
   if (kind == kPathK1 && cols > kK1MaxCols) return arg_fail("k1 path needs cols <= 3072");
   if (kind == kPathSeg && !vec) return arg_fail("seg path needs 16-B aligned rows");
 
+  if (kind == kPathK1m) {
+    if (!vec) return arg_fail("k1m path needs 16-B aligned rows");
+    int wpr, nv;
+    k1m_default(cols, wpr, nv);
+    if (g_k1m_wpr.load() > 0) { wpr = g_k1m_wpr; nv = g_k1m_nv; }
+    const K1mEntry* e = k1m_find(wpr, nv);
+    if (!e) return arg_fail("no K1m instantiation for the requested shape");
+    if (int64_t(wpr) * 32 * nv * 4 < cols) return arg_fail("K1m shape does not cover cols");
+    p.kind = kPathK1m;
+    p.k1m = e;
+    p.threads = kRowsThreads;
+    const int64_t rpc = kRowsThreads / 32 / wpr;
+    p.grid = std::max<int64_t>(1, std::min<int64_t>((rows + rpc - 1) / rpc, INT32_MAX));
+    return SK_OK;
+  }
   if (kind == kPathK1) {
     int lpr, nv, u, pf, gm;
     const int vw = vec8 ? 8 : vec ? 4 : 1;
@@ -800,6 +847,12 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
                 int64_t ldx, int64_t ldy, int mode, unsigned long long* bad, char* ws,
                 cudaStream_t s, bool user_ws) {
   const float sh = shift_scale();
+  if (p.kind == kPathK1m) {
+    SK_CUDA(launch_k(reinterpret_cast<const void*>(p.k1m->fn[mode]),
+                     dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), 0, s, false, x, y,
+                     rows, static_cast<int>(cols), ldx, ldy, bad, sh));
+    return SK_OK;
+  }
   if (p.kind == kPathK1) {
     SK_CUDA(launch_k(reinterpret_cast<const void*>(p.k1->fn[mode]),
                      dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), 0, s, false, x, y,
@@ -1125,6 +1178,9 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "gres_diag") g_gres_diag = value;
   else if (k == "gres_sleep") g_gres_sleep = value;
   else if (k == "gres_split") g_gres_split = value;
+  else if (k == "k1m") g_k1m = value;
+  else if (k == "k1m_wpr") g_k1m_wpr = value;
+  else if (k == "k1m_nv") g_k1m_nv = value;
   else if (k == "gres_timeout_spins") g_gres_spins = value > 0 ? unsigned(value) : kGresSpinLimit;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;
@@ -1154,7 +1210,10 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
   Plan p;
   st = make_plan(rows, cols, ldx, ldy, x_addr, y_addr, 0, device, p);
   if (st) return st;
-  if (p.kind == kPathK1)
+  if (p.kind == kPathK1m)
+    snprintf(buf, buflen, "k1m wpr=%d nv=%d threads=%d grid=%lld", p.k1m->wpr, p.k1m->nv,
+             p.threads, (long long)p.grid);
+  else if (p.kind == kPathK1)
     snprintf(buf, buflen, "k1 vec=%d lpr=%d nv=%d u=%d pf=%d threads=%d grid=%lld", p.k1->vec,
              p.k1->lpr, p.k1->nv, p.k1->u, p.k1->pf, p.threads, (long long)p.grid);
   else if (p.kind == kPathSeg)

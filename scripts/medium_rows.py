@@ -30,9 +30,16 @@ def main():
         ys = [torch.empty_like(x0) for _ in range(R)]
         s = torch.cuda.Stream()
         variants = [("default", {})]
-        for gm in (0, 1, 2):
-            variants.append((f"k1 lpr=32 nv={nv} gm={gm}",
-                             {"path": 0, "k1_lpr": 32, "k1_nv": nv, "k1_u": 1, "grid_mult": gm}))
+        if cols <= 3072:
+            for gm in (0, 2):
+                variants.append((f"k1 lpr=32 nv={nv} gm={gm}",
+                                 {"path": 0, "k1_lpr": 32, "k1_nv": nv, "k1_u": 1, "grid_mult": gm}))
+        else:
+            variants.append(("k2 (k1m off)", {"k1m": 0}))
+            for wpr, nv2 in ((2, 16), (4, 8), (4, 12), (4, 16), (8, 8)):
+                if wpr * 32 * nv2 * 4 >= cols:
+                    variants.append((f"k1m wpr={wpr} nv={nv2}",
+                                     {"path": 3, "k1m_wpr": wpr, "k1m_nv": nv2}))
         for tag, tun in variants:
             for k, v in tun.items():
                 _native.set_tuning(k, v)
@@ -44,7 +51,7 @@ def main():
             except Exception as e:  # noqa: BLE001
                 print(json.dumps({"shape": [rows, cols], "variant": tag, "error": str(e)}))
             for k in tun:
-                _native.set_tuning(k, {"path": -1}.get(k, 0))
+                _native.set_tuning(k, {"path": -1, "k1m": 1}.get(k, 0))
 
 
 if __name__ == "__main__":
