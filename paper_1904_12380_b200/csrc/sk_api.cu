@@ -78,7 +78,10 @@ float shift_scale() { return g_skip_max_shift.load() ? 0.0f : 1.0f; }
 void ensure_smem_attr(const void* fn, size_t smem) {
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, size_t> set;
-  if (smem <= 48 * 1024) return;
+  // any dynamic request: static + dynamic must fit the opt-in limit (the
+  // default 48 KB cap counts the static arrays too -- K2 at 6144 columns asks
+  // for exactly 48 KB of dynamic smem and failed to launch without this)
+  if (smem == 0) return;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> g(mu);
@@ -396,8 +399,10 @@ const K1mEntry* k1m_find(int wpr, int nv) {
 }
 constexpr int64_t kK1mMaxCols = 8192;
 std::atomic<int> g_k1m{1}, g_k1m_wpr{0}, g_k1m_nv{0};
+// measured (scripts/medium_rows.py): 16384x4096 80.5 us with (2,16) vs 101.5
+// for K2; 8192x6144 62.4 (4,12); 8192x8192 80.1 (4,16) vs 88.6 for K2
 void k1m_default(int64_t cols, int& wpr, int& nv) {
-  if (cols <= 4096) { wpr = 4; nv = 8; }
+  if (cols <= 4096) { wpr = 2; nv = 16; }
   else if (cols <= 6144) { wpr = 4; nv = 12; }
   else { wpr = 4; nv = 16; }
 }

@@ -31,7 +31,8 @@ def _reset_tuning():
     yield
     for k, v in (("path", -1), ("k1_lpr", 0), ("grid_mult", 0), ("seg_len", 0),
                  ("skip_max_shift", 0), ("k3_impl", 3), ("cluster_k3", 1), ("chunk_mb", 0),
-                 ("gres", 1), ("gres_p", 0), ("gres_st", 0), ("gres_split", -1), ("cluster_onex", 0)):
+                 ("gres", 1), ("gres_p", 0), ("gres_st", 0), ("gres_split", -1), ("cluster_onex", 0), ("k1m", 1),
+                 ("k1m_wpr", 0), ("k1m_nv", 0)):
         _native.set_tuning(k, v)
 
 
@@ -139,9 +140,9 @@ def test_unaligned_and_strided(C, oracle):
         assert_parity(oracle, y, ref, what=(C, xo, yo, ldx, ldy))
 
 
-@pytest.mark.parametrize("path", [0, 1, 2])
+@pytest.mark.parametrize("path", [0, 1, 2, 3])
 def test_every_path_on_same_input(path, oracle):
-    C = 1024 if path == 0 else 20000
+    C = 1024 if path == 0 else 8192 if path == 3 else 20000
     x = configs.generate("c4", 0, 3)[:, :C].copy()
     ref = oracle.softmax_ref(x)
     _native.set_tuning("path", path)
@@ -197,6 +198,64 @@ def test_k1_medium_rows(rows, C, oracle):
     x2 = x.copy()
     x2[rows - 1, C - 1] = np.nan
     assert gu.softmax_abi(x2, 0)[1] == rows - 1
+
+
+@pytest.mark.parametrize("rows,C", [(300, 8192), (4096, 4000), (2048, 5000), (64, 6144),
+                                    (3, 8192), (1000, 3076)])
+def test_k1m_medium_rows(rows, C, oracle):
+    """128-bit rows of 3073..8192 floats held in the registers of 2-8 warps
+    (K1m): every mode, clip firing, a large negative row, strided pitch, row
+    blocks bit-identical to the whole matrix, non-finite detection."""
+    from paper_1904_12380_b200 import tensor
+
+    x = np.empty((rows, C), np.float32)
+    tensor.fill_normal_array(x, 3 * C + rows, 5.0)
+    x[0, C - 1] = -300.0
+    x[rows // 2, :] -= 500.0
+    plan = gu.plan(rows, C)
+    assert plan.startswith("k1m "), plan
+    for mode in (0, 1, 2):
+        ref = oracle.softmax_ref(x, clip=(mode == 0))
+        y, bad = gu.softmax_abi(x, mode)
+        assert bad == gu.NO_BAD
+        assert_parity(oracle, y, ref, approx=(mode == 2), what=(rows, C, mode, plan))
+    y, _ = gu.softmax_abi(x, 0, ldx=C + 12, ldy=C + 4)
+    assert_parity(oracle, y, oracle.softmax_ref(x), what=(rows, C, "strided"))
+    whole, _ = gu.softmax_abi(x, 0)
+    part, _ = gu.softmax_abi(x[rows // 3:], 0)
+    assert np.array_equal(part.view(np.uint32), whole[rows // 3:].view(np.uint32))
+    x2 = x.copy()
+    x2[rows - 1, 5] = np.inf
+    assert gu.softmax_abi(x2, 0)[1] == rows - 1
+
+
+def test_k1m_instantiations_and_k2_fallback(oracle):
+    """Every K1m (warps per row, vectors per lane) shape that covers the row,
+    and the TMA block-per-row K2 (k1m off) on the same rows -- including 6144
+    columns, where K2 needs exactly 48 KB of dynamic shared memory."""
+    from paper_1904_12380_b200 import tensor
+
+    for C in (4096, 6144, 8192):
+        x = np.empty((40, C), np.float32)
+        tensor.fill_normal_array(x, C, 4.0)
+        ref = oracle.softmax_ref(x)
+        try:
+            for wpr, nv in ((2, 16), (4, 8), (4, 12), (4, 16), (8, 8)):
+                if wpr * 32 * nv * 4 < C:
+                    continue
+                _native.set_tuning("k1m_wpr", wpr)
+                _native.set_tuning("k1m_nv", nv)
+                y, _ = gu.softmax_abi(x, 0)
+                assert_parity(oracle, y, ref, what=(C, wpr, nv))
+            _native.set_tuning("k1m_wpr", 0)
+            _native.set_tuning("k1m", 0)
+            assert gu.plan(40, C).startswith("k2_tma"), gu.plan(40, C)
+            y, _ = gu.softmax_abi(x, 0)
+            assert_parity(oracle, y, ref, what=(C, "k2"))
+        finally:
+            _native.set_tuning("k1m", 1)
+            _native.set_tuning("k1m_wpr", 0)
+            _native.set_tuning("k1m_nv", 0)
 
 
 @pytest.mark.parametrize("impl", [0, 1, 2, 3, "3b", 4, 5, "5x2", "g"])
