@@ -49,7 +49,8 @@ def _sources() -> list[Path]:
 
 
 def _deps() -> list[Path]:
-    return _sources() + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "softmax_b200.h"]
+    return (_sources() + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h"))
+            + [ROOT / "include" / "softmax_b200.h"])
 
 
 def _stale(target: Path, deps: list[Path]) -> bool:

@@ -1,5 +1,7 @@
-// sk_api.cu -- C ABI (include/softmax_b200.h): launch planning, workspaces,
-// the pipelined host-buffer path, and the column-shard building blocks.
+// sk_api.cu -- C ABI (include/softmax_b200.h) for device buffers: launch
+// planning, workspaces, tuning, the row-statistics building blocks.  The
+// host-buffer pipeline lives in sk_host.cu, the fused column shard in
+// sk_colshard.cu (shared internals: sk_internal.h).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -24,9 +26,10 @@
 #include "sk_cluster.cuh"
 #include "sk_gres.cuh"
 #include "sk_rows_mw.cuh"
+#include "sk_internal.h"
 
 namespace sk {
-namespace {
+namespace detail {
 
 thread_local std::string g_last_error;
 
@@ -36,11 +39,6 @@ int cuda_fail(cudaError_t e, const char* what) {
   if (e == cudaErrorMemoryAllocation) return SK_ERR_RESOURCE;
   return SK_ERR_CUDA;
 }
-#define SK_CUDA(call)                                   \
-  do {                                                  \
-    cudaError_t _e = (call);                            \
-    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
-  } while (0)
 
 int arg_fail(const std::string& msg) {
   g_last_error = msg;
@@ -48,10 +46,6 @@ int arg_fail(const std::string& msg) {
 }
 
 // ---------------------------------------------------------------- device info
-struct DevInfo {
-  int sms = 0;
-  bool coop = false;
-};
 DevInfo dev_info(int dev) {
   static std::mutex mu;
   static std::map<int, DevInfo> cache;
@@ -105,7 +99,7 @@ std::atomic<int> g_vec8{0};          // 256-bit K1 path (measured no faster: off
 std::atomic<int> g_gres{1};       // K3g grid-resident rows: 0 off, 1 when it out-scores K3c, 2 force
 std::atomic<int> g_gres_p{0};     // force K3g CTAs per row (0 = auto)
 std::atomic<int> g_gres_diag{0};
-std::atomic<unsigned> g_gres_spins{kGresSpinLimit};  // exchange timeout (polls), tests shorten it  // K3g timing diagnostics (1: skip the group exchange -- wrong results)
+std::atomic<unsigned> g_gres_spins{kGresSpinLimit};  // exchange timeout (polls), tests shorten it
 std::atomic<int> g_gres_st{0};
 std::atomic<int> g_gres_sleep{128};
 std::atomic<int> g_gres_split{-1};   // K3g poller warp: -1 auto (lag >= 2), 0 off, 1 on
@@ -114,32 +108,6 @@ bool gres_split(int nstages) {
   return v < 0 ? nstages >= 4 : v != 0;
 }  // K3g poller back-off between polls (ns)    // force K3g ring depth (0 = as deep as smem allows)
 std::atomic<int> g_k3_impl{3};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
-
-// Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.
-template <typename... Args>
-cudaError_t launch_k(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                     bool coop, Args... args) {
-  void* argv[] = {static_cast<void*>(&args)...};
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  int n = 0;
-  if (coop) {
-    attr[n].id = cudaLaunchAttributeCooperative;
-    attr[n].val.cooperative = 1;
-    ++n;
-  } else if (g_pdl.load()) {
-    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[n].val.programmaticStreamSerializationAllowed = 1;
-    ++n;
-  }
-  cfg.attrs = attr;
-  cfg.numAttrs = n;
-  return cudaLaunchKernelExC(&cfg, fn, argv);
-}
 
 // ------------------------------------------------------------------ K1 table
 using K1Fn = void (*)(const float*, float*, int64_t, int, int64_t, int64_t,
@@ -456,11 +424,6 @@ int plan_split(int64_t rows, int64_t cols, Plan& p) {
 // merged per row); nvr of them run in this launch (nvr = world when one GPU
 // emulates all ranks, 1 on a real rank).  Deterministic in its inputs, so
 // every rank of a column shard derives the same plan.
-struct GresChoice {
-  int P = 0, st = 0, groups = 0;
-  int64_t slice = 0;
-  double score = 0.0;
-};
 // Step-time model, fitted to a (P, stages) grid measured on B200 (c4, c5b;
 // profiles/r1_gres_grid.jsonl) and checked against the best measured plan of
 // ten other long-row shapes (it picks it, within ~5%, on all of them):
@@ -486,7 +449,6 @@ double gres_time_us(int64_t rows, int P, int st, int64_t slice, int groups, int 
 // same bits -- as the whole matrix: row sharding stays communication-free and
 // bit-identical.  At 2048 rows the choice equals the per-shape best on every
 // measured long-row shape.
-constexpr int64_t kGresPlanRows = 2048;
 
 GresChoice plan_gres(int64_t rows, int64_t cols, int mode, const DevInfo& di, int world, int nvr) {
   GresChoice best;
@@ -1008,116 +970,11 @@ int softmax_dev(const float* x, float* y, int64_t rows, int64_t cols, int64_t ld
   return launch_plan(p, x, y, rows, cols, ldx, ldy, mode, bad, ws, s, workspace != nullptr);
 }
 
-// ------------------------------------------------ pipelined host-buffer path
-// Three streams (H2D copy engine, compute, D2H copy engine) over a ring of
-// kRing device buffer pairs, ordered by events: chunk k's kernel waits for its
-// H2D, its D2H waits for its kernel, and slot reuse waits for the kernel / D2H
-// that last used the slot.  H2D of chunk k+1, compute of chunk k and D2H of
-// chunk k-1 run concurrently, so a call costs ~max(H2D, D2H) + one chunk.
-constexpr int kRing = 4;
-struct HostCtx {
-  std::mutex mu;
-  bool init = false;
-  cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
-  cudaEvent_t ev_h2d[kRing] = {}, ev_k[kRing] = {}, ev_d2h[kRing] = {};
-  float* dx[kRing] = {};
-  float* dy[kRing] = {};
-  unsigned long long* dbad = nullptr;  // one bad-row flag per chunk
-  unsigned long long* hbad = nullptr;  // pinned mirror
-  int64_t flag_cap = 0;
-  size_t cap_bytes = 0;
-};
-std::mutex g_host_mu;
-std::map<int, HostCtx*> g_host;
-std::atomic<int> g_host_chunk_kb{0};  // 0: auto
-std::atomic<int> g_host_zero_copy{0};  // K1/K2 rows read/write pinned host memory directly
-
-// Device-visible address of a page-locked (cudaHostAlloc / registered) host
-// buffer, or nullptr for pageable memory.
-const void* mapped_device_ptr(const void* h) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
-    (void)cudaGetLastError();
-    return nullptr;
-  }
-  if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
-  return a.devicePointer;
-}
-
-HostCtx* host_ctx(int dev) {
-  std::lock_guard<std::mutex> g(g_host_mu);
-  HostCtx*& c = g_host[dev];
-  if (!c) c = new HostCtx();
-  return c;
-}
-
-
-// ------------------------------------------------ fused column shard (K3g)
-// Every rank holds a [rows, cols] column shard and one exchange block:
-// [0, 256) ctl words (epoch, finished CTAs, abort) | [256, ...) slot arrays
-// [2][groups][2L+2][world*P] x 16 B.  Rank r's K3g CTAs store their row pairs
-// into EVERY rank's block (peer pointers over NVLink) and poll only their
-// own, so the per-row (max, sum) all-reduce of the column shard happens inside
-// the kernel, overlapped with the streaming -- no NCCL call on the data path.
-constexpr size_t kXBlockBytes = size_t(2) << 20;
-constexpr size_t kXSlots = 256;
-
-int colshard_launch(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
-                    int64_t ldy, int mode, int rank, int world, int nvr, void* const* blocks,
-                    unsigned long long* bad, cudaStream_t s, char* desc, int desc_len) {
-  if (world < 1 || world > kGresMaxWorld) return arg_fail("world must be 1..8");
-  if (nvr != 1 && nvr != world) return arg_fail("bad virtual rank count");
-  if (rank < 0 || rank >= world) return arg_fail("rank out of range");
-  if (rows < 0 || cols < 1 || ldx < cols || ldy < cols) return arg_fail("bad shard shape");
-  if (mode < 0 || mode > 2) return arg_fail("mode must be SK_MODE_CLIPPED/EXACT/APPROX");
-  if (!blocks) return arg_fail("null exchange blocks");
-  for (int r = 0; r < world; ++r)
-    if (!blocks[r]) return arg_fail("null exchange block");
-  const bool aligned = cols % 4 == 0 && ldx % 4 == 0 && ldy % 4 == 0 &&
-                       reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
-                       reinterpret_cast<uintptr_t>(y) % 16 == 0;
-  if (!desc && rows > 0 && (!x || !y)) return arg_fail("null buffer");
-  if (!desc && !aligned) return arg_fail("fused column shard needs cols % 4 == 0 and 16-B aligned rows");
-  int dev = 0;
-  SK_CUDA(cudaGetDevice(&dev));
-  const DevInfo di = dev_info(dev);
-  if (!di.coop) return arg_fail("device cannot co-schedule the fused column shard");
-  const GresChoice gc = plan_gres(kGresPlanRows, cols, mode, di, world, nvr);
-  if (gc.P == 0) return arg_fail("shard row too long for the fused column shard (use the split path)");
-  const bool split = gres_split(gc.st);
-  const int lag = gc.st >= 5 ? 3 : gc.st == 4 ? 2 : 1;
-  const size_t need = kXSlots + 2 * size_t(gc.groups) * gres_slot_sets(lag) * world * gc.P * 16;
-  if (need > kXBlockBytes) return arg_fail("exchange block too small for this plan");
-  if (desc) {
-    snprintf(desc, desc_len, "k3_gres_colshard world=%d nvr=%d nseg=%d seglen=%lld stages=%d groups=%d threads=%d",
-             world, nvr, gc.P, (long long)gc.slice, gc.st, gc.groups, split ? kGresBlock : kGresThreads);
-    return SK_OK;
-  }
-  if (rows == 0) return SK_OK;
-  GresComm comm = {};
-  for (int r = 0; r < world; ++r)
-    comm.dst[r] = reinterpret_cast<unsigned long long*>(static_cast<char*>(blocks[r]) + kXSlots);
-  comm.ctl = reinterpret_cast<unsigned*>(blocks[nvr == 1 ? rank : 0]);
-  comm.shard_stride = nvr == 1 ? 0 : cols;
-  comm.world = world;
-  comm.rank0 = nvr == 1 ? rank : 0;
-  comm.nvr = nvr;
-  comm.sys = (world > 1 && nvr == 1) ? 1 : 0;  // peers are other GPUs
-  comm.spin_limit = g_gres_spins.load();
-  const size_t smem = size_t(gc.st) * gc.slice * sizeof(float);
-  int P = gc.P, slice = static_cast<int>(gc.slice), nst = gc.st;
-  const int grid = gc.groups * gc.P * nvr;
-  SK_CUDA(launch_k(gres_fn(mode, gc.st, split), dim3(static_cast<unsigned>(grid)),
-                   dim3(split ? kGresBlock : kGresThreads), smem, s, true, x, y, rows, cols, ldx,
-                   ldy, P, slice, nst, comm, bad, shift_scale(), g_gres_sleep.load(),
-                   g_gres_diag.load()));
-  return SK_OK;
-}
-
-}  // namespace
+}  // namespace detail
 }  // namespace sk
 
 using namespace sk;
+using namespace sk::detail;
 
 extern "C" {
 
@@ -1135,20 +992,6 @@ const char* sk_status_string(int status) {
 }
 
 const char* sk_last_error(void) { return g_last_error.c_str(); }
-
-void* sk_alloc_pinned(size_t bytes) {
-  void* p = nullptr;
-  if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
-    g_last_error = "cudaHostAlloc failed";
-    (void)cudaGetLastError();
-    return nullptr;
-  }
-  return p;
-}
-
-void sk_free_pinned(void* p) {
-  if (p) cudaFreeHost(p);
-}
 
 int sk_set_tuning(const char* key, int value) {
   if (!key) return SK_ERR_ARGUMENT;
@@ -1240,165 +1083,6 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
   return SK_OK;
 }
 
-int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_t cols,
-                        int mode, int device, int64_t* bad_row_out) {
-  if (bad_row_out) *bad_row_out = -1;
-  int st = check_common(x_host, y_host, rows, cols, cols, cols, mode);
-  if (st) return st;
-  if (rows == 0) return SK_OK;
-  SK_CUDA(cudaSetDevice(device));
-  HostCtx* c = host_ctx(device);
-  std::lock_guard<std::mutex> g(c->mu);
-  if (!c->init) {
-    SK_CUDA(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
-    SK_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
-    SK_CUDA(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
-    for (int i = 0; i < kRing; ++i) {
-      SK_CUDA(cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming));
-      SK_CUDA(cudaEventCreateWithFlags(&c->ev_k[i], cudaEventDisableTiming));
-      SK_CUDA(cudaEventCreateWithFlags(&c->ev_d2h[i], cudaEventDisableTiming));
-    }
-    c->init = true;
-  }
-  // Zero-copy: a row that fits one CTA (K1/K2) is read from and written to
-  // pinned host memory directly by the kernel -- PCIe reads and (posted) writes
-  // proceed concurrently inside one launch, with no staging copies, events or
-  // chunk pipeline.  Long rows (K3/K4 re-read segments) keep the staged path.
-  if (g_host_zero_copy.load() && cols <= kSegCap) {
-    const float* xd = static_cast<const float*>(mapped_device_ptr(x_host));
-    float* yd = static_cast<float*>(const_cast<void*>(mapped_device_ptr(y_host)));
-    if (xd && yd) {
-      if (c->flag_cap < 1) {
-        SK_CUDA(cudaMalloc(&c->dbad, 64 * sizeof(unsigned long long)));
-        SK_CUDA(cudaMemset(c->dbad, 0xFF, 64 * sizeof(unsigned long long)));
-        SK_CUDA(cudaMallocHost(&c->hbad, 64 * sizeof(unsigned long long)));
-        c->flag_cap = 64;
-      }
-      st = softmax_dev(xd, yd, rows, cols, cols, cols, mode, c->dbad, nullptr, 0, c->s_comp);
-      if (st) return st;
-      SK_CUDA(cudaMemcpyAsync(c->hbad, c->dbad, sizeof(unsigned long long),
-                              cudaMemcpyDeviceToHost, c->s_comp));
-      SK_CUDA(cudaStreamSynchronize(c->s_comp));
-      if (c->hbad[0] == SK_EXCHANGE_ABORTED) {
-        SK_CUDA(cudaMemset(c->dbad, 0xFF, sizeof(unsigned long long)));
-        g_last_error = "row-statistics exchange timed out";
-        return SK_ERR_CUDA;
-      }
-      if (c->hbad[0] != SK_NO_BAD_ROW) {
-        const int64_t row = static_cast<int64_t>(c->hbad[0]);
-        SK_CUDA(cudaMemset(c->dbad, 0xFF, sizeof(unsigned long long)));
-        if (bad_row_out) *bad_row_out = row;
-        g_last_error = "non-finite logits in row " + std::to_string(row);
-        return SK_ERR_NONFINITE;
-      }
-      return SK_OK;
-    }
-  }
-  const int64_t row_bytes = cols * 4;
-  const int64_t total = rows * row_bytes;
-  // Chunk schedule: steady chunks of ~1/4 of the job (4..16 MiB; tunable),
-  // ramped 1/8, 1/4, 1/2 at both ends: the first H2D and the last D2H are
-  // the only transfers that cannot overlap the other direction, so they are
-  // made small (each ramp chunk costs ~10 us of issue + DMA setup, paid once).
-  // Whole rows.
-  int64_t chunk_bytes = std::min<int64_t>(std::max<int64_t>(total / 4, 4 << 20), 16 << 20);
-  if (g_host_chunk_kb.load() > 0) chunk_bytes = int64_t(g_host_chunk_kb.load()) << 10;
-  const int64_t big = std::min(rows, std::max<int64_t>(1, chunk_bytes / row_bytes));
-  std::vector<int64_t> sched;  // rows per chunk
-  {
-    std::vector<int64_t> head;
-    for (int64_t r = big / 8; r >= 1 && r < big; r *= 2) head.push_back(r);
-    int64_t left = rows;
-    std::vector<int64_t> tail;
-    for (int64_t r : head) {  // ramp up at the start and down at the end
-      if (left >= 2 * r + 2 * big && r * row_bytes >= (int64_t(512) << 10)) {
-        sched.push_back(r);
-        tail.push_back(r);
-        left -= 2 * r;
-      }
-    }
-    while (left > 0) {
-      const int64_t r = std::min(big, left);
-      sched.push_back(r);
-      left -= r;
-    }
-    for (auto it = tail.rbegin(); it != tail.rend(); ++it) sched.push_back(*it);
-  }
-  const size_t need = size_t(big * row_bytes);
-  if (c->cap_bytes < need) {
-    SK_CUDA(cudaDeviceSynchronize());
-    for (int i = 0; i < kRing; ++i) {
-      if (c->dx[i]) cudaFree(c->dx[i]);
-      if (c->dy[i]) cudaFree(c->dy[i]);
-      c->dx[i] = c->dy[i] = nullptr;
-    }
-    c->cap_bytes = 0;
-    for (int i = 0; i < kRing; ++i) {
-      SK_CUDA(cudaMalloc(&c->dx[i], need));
-      SK_CUDA(cudaMalloc(&c->dy[i], need));
-    }
-    c->cap_bytes = need;
-  }
-  const int64_t nchunks = static_cast<int64_t>(sched.size());
-  if (c->flag_cap < nchunks) {
-    SK_CUDA(cudaDeviceSynchronize());
-    if (c->dbad) cudaFree(c->dbad);
-    if (c->hbad) cudaFreeHost(c->hbad);
-    c->dbad = nullptr;
-    c->hbad = nullptr;
-    c->flag_cap = 0;
-    const int64_t cap = std::max<int64_t>(nchunks, 64);
-    SK_CUDA(cudaMalloc(&c->dbad, cap * sizeof(unsigned long long)));
-    SK_CUDA(cudaMemset(c->dbad, 0xFF, cap * sizeof(unsigned long long)));
-    SK_CUDA(cudaMallocHost(&c->hbad, cap * sizeof(unsigned long long)));
-    c->flag_cap = cap;
-  }
-  std::vector<int64_t> start(nchunks + 1, 0);
-  for (int64_t k = 0; k < nchunks; ++k) start[k + 1] = start[k] + sched[k];
-  for (int64_t k = 0; k < nchunks; ++k) {
-    const int i = static_cast<int>(k % kRing);
-    const int64_t r0 = start[k];
-    const int64_t nr = sched[k];
-    const size_t bytes = size_t(nr * row_bytes);
-    // input slot free once the kernel that last read it is done
-    if (k >= kRing) SK_CUDA(cudaStreamWaitEvent(c->s_h2d, c->ev_k[i], 0));
-    SK_CUDA(cudaMemcpyAsync(c->dx[i], x_host + r0 * cols, bytes, cudaMemcpyHostToDevice,
-                            c->s_h2d));
-    SK_CUDA(cudaEventRecord(c->ev_h2d[i], c->s_h2d));
-    SK_CUDA(cudaStreamWaitEvent(c->s_comp, c->ev_h2d[i], 0));
-    // output slot free once the D2H that last read it is done
-    if (k >= kRing) SK_CUDA(cudaStreamWaitEvent(c->s_comp, c->ev_d2h[i], 0));
-    st = softmax_dev(c->dx[i], c->dy[i], nr, cols, cols, cols, mode, c->dbad + k, nullptr, 0,
-                     c->s_comp);
-    if (st) return st;
-    SK_CUDA(cudaEventRecord(c->ev_k[i], c->s_comp));
-    SK_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_k[i], 0));
-    SK_CUDA(cudaMemcpyAsync(y_host + r0 * cols, c->dy[i], bytes, cudaMemcpyDeviceToHost,
-                            c->s_d2h));
-    SK_CUDA(cudaEventRecord(c->ev_d2h[i], c->s_d2h));
-  }
-  // every chunk's non-finite flag in one small copy after the last kernel
-  // (one DMA instead of one per chunk between the bulk transfers)
-  SK_CUDA(cudaMemcpyAsync(c->hbad, c->dbad, size_t(nchunks) * sizeof(unsigned long long),
-                          cudaMemcpyDeviceToHost, c->s_d2h));
-  SK_CUDA(cudaStreamSynchronize(c->s_d2h));
-  for (int64_t k = 0; k < nchunks; ++k) {
-    if (c->hbad[k] == SK_EXCHANGE_ABORTED) {
-      SK_CUDA(cudaMemset(c->dbad, 0xFF, nchunks * sizeof(unsigned long long)));
-      g_last_error = "row-statistics exchange timed out";
-      return SK_ERR_CUDA;
-    }
-    if (c->hbad[k] != SK_NO_BAD_ROW) {
-      const int64_t row = start[k] + static_cast<int64_t>(c->hbad[k]);
-      SK_CUDA(cudaMemset(c->dbad, 0xFF, nchunks * sizeof(unsigned long long)));
-      if (bad_row_out) *bad_row_out = row;
-      g_last_error = "non-finite logits in row " + std::to_string(row);
-      return SK_ERR_NONFINITE;
-    }
-  }
-  return SK_OK;
-}
-
 size_t sk_row_stats_workspace_bytes(int64_t rows, int64_t cols) {
   const int64_t nch = (cols + kSplitChunk - 1) / kSplitChunk;
   return ws_layout(std::max<int64_t>(rows, 0), nch).total;
@@ -1471,79 +1155,6 @@ int sk_normalize_f32(const float* x, float* y, int64_t rows, int64_t cols, int64
   SK_CUDA(launch_k(norm, dim3(g), dim3(kSplitThreads), 0, s, false, x, y, rows, cols, ldx, ldy,
                    nch, row_max, row_sum));
   return SK_OK;
-}
-
-size_t sk_xchg_block_bytes(void) { return kXBlockBytes; }
-
-int sk_xchg_alloc(int device, void** block) {
-  if (!block) return arg_fail("null output pointer");
-  int prev = 0;
-  SK_CUDA(cudaGetDevice(&prev));
-  SK_CUDA(cudaSetDevice(device));
-  void* b = nullptr;
-  cudaError_t e = cudaMalloc(&b, kXBlockBytes);  // plain cudaMalloc: IPC-exportable
-  if (e == cudaSuccess) e = cudaMemset(b, 0, kXBlockBytes);
-  cudaSetDevice(prev);
-  if (e != cudaSuccess) return cuda_fail(e, "sk_xchg_alloc");
-  *block = b;
-  return SK_OK;
-}
-
-int sk_xchg_free(void* block) {
-  if (block) SK_CUDA(cudaFree(block));
-  return SK_OK;
-}
-
-int sk_ipc_handle(const void* dev_ptr, void* handle) {
-  if (!dev_ptr || !handle) return arg_fail("null pointer");
-  cudaIpcMemHandle_t h;
-  SK_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
-  std::memcpy(handle, &h, sizeof(h));
-  return SK_OK;
-}
-
-int sk_ipc_open(const void* handle, void** dev_ptr) {
-  if (!handle || !dev_ptr) return arg_fail("null pointer");
-  cudaIpcMemHandle_t h;
-  std::memcpy(&h, handle, sizeof(h));
-  SK_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
-  return SK_OK;
-}
-
-int sk_ipc_close(void* dev_ptr) {
-  if (dev_ptr) SK_CUDA(cudaIpcCloseMemHandle(dev_ptr));
-  return SK_OK;
-}
-
-int sk_colshard_softmax_f32(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
-                            int64_t ldy, int mode, int rank, int world, void* const* blocks,
-                            unsigned long long* bad_row, void* stream) {
-  if (!bad_row) return arg_fail("bad_row flag required");
-  return colshard_launch(x, y, rows, cols, ldx, ldy, mode, rank, world, 1, blocks, bad_row,
-                         static_cast<cudaStream_t>(stream), nullptr, 0);
-}
-
-int sk_colshard_emulate_f32(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
-                            int64_t ldy, int mode, int world, void* const* blocks,
-                            unsigned long long* bad_row, void* stream) {
-  if (!bad_row) return arg_fail("bad_row flag required");
-  if (world < 1 || cols % world) return arg_fail("cols must split evenly over world");
-  return colshard_launch(x, y, rows, cols / world, ldx, ldy, mode, 0, world, world, blocks,
-                         bad_row, static_cast<cudaStream_t>(stream), nullptr, 0);
-}
-
-int sk_describe_colshard_plan(int64_t rows, int64_t cols, int world, int emulate, int device,
-                              char* buf, int buflen) {
-  if (!buf || buflen < 1) return arg_fail("null buffer");
-  int prev = 0;
-  SK_CUDA(cudaGetDevice(&prev));
-  SK_CUDA(cudaSetDevice(device));
-  void* fake[kGresMaxWorld];
-  for (auto& f : fake) f = reinterpret_cast<void*>(256);
-  const int st = colshard_launch(nullptr, nullptr, rows, cols, cols, cols, 0, 0, world,
-                                 emulate ? world : 1, fake, nullptr, nullptr, buf, buflen);
-  cudaSetDevice(prev);
-  return st;
 }
 
 }  // extern "C"

@@ -1,0 +1,242 @@
+// sk_host.cu -- sk_softmax_f32_host: the reference-facing call on HOST
+// buffers (kernels.softmax(Matrix2D), kernels.py:350-362) as a pipelined
+// H2D -> kernel -> D2H over three streams, plus page-locked allocation.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "sk_internal.h"
+
+namespace sk {
+namespace detail {
+
+// ------------------------------------------------ pipelined host-buffer path
+// Three streams (H2D copy engine, compute, D2H copy engine) over a ring of
+// kRing device buffer pairs, ordered by events: chunk k's kernel waits for its
+// H2D, its D2H waits for its kernel, and slot reuse waits for the kernel / D2H
+// that last used the slot.  H2D of chunk k+1, compute of chunk k and D2H of
+// chunk k-1 run concurrently, so a call costs ~max(H2D, D2H) + one chunk.
+constexpr int kRing = 4;
+struct HostCtx {
+  std::mutex mu;
+  bool init = false;
+  cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_h2d[kRing] = {}, ev_k[kRing] = {}, ev_d2h[kRing] = {};
+  float* dx[kRing] = {};
+  float* dy[kRing] = {};
+  unsigned long long* dbad = nullptr;  // one bad-row flag per chunk
+  unsigned long long* hbad = nullptr;  // pinned mirror
+  int64_t flag_cap = 0;
+  size_t cap_bytes = 0;
+};
+std::mutex g_host_mu;
+std::map<int, HostCtx*> g_host;
+std::atomic<int> g_host_chunk_kb{0};  // 0: auto
+std::atomic<int> g_host_zero_copy{0};  // K1/K2 rows read/write pinned host memory directly
+
+// Device-visible address of a page-locked (cudaHostAlloc / registered) host
+// buffer, or nullptr for pageable memory.
+const void* mapped_device_ptr(const void* h) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
+  return a.devicePointer;
+}
+
+HostCtx* host_ctx(int dev) {
+  std::lock_guard<std::mutex> g(g_host_mu);
+  HostCtx*& c = g_host[dev];
+  if (!c) c = new HostCtx();
+  return c;
+}
+
+}  // namespace detail
+}  // namespace sk
+
+using namespace sk;
+using namespace sk::detail;
+
+extern "C" {
+
+void* sk_alloc_pinned(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+    g_last_error = "cudaHostAlloc failed";
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void sk_free_pinned(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_t cols,
+                        int mode, int device, int64_t* bad_row_out) {
+  if (bad_row_out) *bad_row_out = -1;
+  int st = check_common(x_host, y_host, rows, cols, cols, cols, mode);
+  if (st) return st;
+  if (rows == 0) return SK_OK;
+  SK_CUDA(cudaSetDevice(device));
+  HostCtx* c = host_ctx(device);
+  std::lock_guard<std::mutex> g(c->mu);
+  if (!c->init) {
+    SK_CUDA(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+    SK_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
+    SK_CUDA(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+    for (int i = 0; i < kRing; ++i) {
+      SK_CUDA(cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming));
+      SK_CUDA(cudaEventCreateWithFlags(&c->ev_k[i], cudaEventDisableTiming));
+      SK_CUDA(cudaEventCreateWithFlags(&c->ev_d2h[i], cudaEventDisableTiming));
+    }
+    c->init = true;
+  }
+  // Zero-copy: a row that fits one CTA (K1/K2) is read from and written to
+  // pinned host memory directly by the kernel -- PCIe reads and (posted) writes
+  // proceed concurrently inside one launch, with no staging copies, events or
+  // chunk pipeline.  Long rows (K3/K4 re-read segments) keep the staged path.
+  if (g_host_zero_copy.load() && cols <= kOneCtaRowMax) {
+    const float* xd = static_cast<const float*>(mapped_device_ptr(x_host));
+    float* yd = static_cast<float*>(const_cast<void*>(mapped_device_ptr(y_host)));
+    if (xd && yd) {
+      if (c->flag_cap < 1) {
+        SK_CUDA(cudaMalloc(&c->dbad, 64 * sizeof(unsigned long long)));
+        SK_CUDA(cudaMemset(c->dbad, 0xFF, 64 * sizeof(unsigned long long)));
+        SK_CUDA(cudaMallocHost(&c->hbad, 64 * sizeof(unsigned long long)));
+        c->flag_cap = 64;
+      }
+      st = softmax_dev(xd, yd, rows, cols, cols, cols, mode, c->dbad, nullptr, 0, c->s_comp);
+      if (st) return st;
+      SK_CUDA(cudaMemcpyAsync(c->hbad, c->dbad, sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, c->s_comp));
+      SK_CUDA(cudaStreamSynchronize(c->s_comp));
+      if (c->hbad[0] == SK_EXCHANGE_ABORTED) {
+        SK_CUDA(cudaMemset(c->dbad, 0xFF, sizeof(unsigned long long)));
+        g_last_error = "row-statistics exchange timed out";
+        return SK_ERR_CUDA;
+      }
+      if (c->hbad[0] != SK_NO_BAD_ROW) {
+        const int64_t row = static_cast<int64_t>(c->hbad[0]);
+        SK_CUDA(cudaMemset(c->dbad, 0xFF, sizeof(unsigned long long)));
+        if (bad_row_out) *bad_row_out = row;
+        g_last_error = "non-finite logits in row " + std::to_string(row);
+        return SK_ERR_NONFINITE;
+      }
+      return SK_OK;
+    }
+  }
+  const int64_t row_bytes = cols * 4;
+  const int64_t total = rows * row_bytes;
+  // Chunk schedule: steady chunks of ~1/4 of the job (4..16 MiB; tunable),
+  // ramped 1/8, 1/4, 1/2 at both ends: the first H2D and the last D2H are
+  // the only transfers that cannot overlap the other direction, so they are
+  // made small (each ramp chunk costs ~10 us of issue + DMA setup, paid once).
+  // Whole rows.
+  int64_t chunk_bytes = std::min<int64_t>(std::max<int64_t>(total / 4, 4 << 20), 16 << 20);
+  if (g_host_chunk_kb.load() > 0) chunk_bytes = int64_t(g_host_chunk_kb.load()) << 10;
+  const int64_t big = std::min(rows, std::max<int64_t>(1, chunk_bytes / row_bytes));
+  std::vector<int64_t> sched;  // rows per chunk
+  {
+    std::vector<int64_t> head;
+    for (int64_t r = big / 8; r >= 1 && r < big; r *= 2) head.push_back(r);
+    int64_t left = rows;
+    std::vector<int64_t> tail;
+    for (int64_t r : head) {  // ramp up at the start and down at the end
+      if (left >= 2 * r + 2 * big && r * row_bytes >= (int64_t(512) << 10)) {
+        sched.push_back(r);
+        tail.push_back(r);
+        left -= 2 * r;
+      }
+    }
+    while (left > 0) {
+      const int64_t r = std::min(big, left);
+      sched.push_back(r);
+      left -= r;
+    }
+    for (auto it = tail.rbegin(); it != tail.rend(); ++it) sched.push_back(*it);
+  }
+  const size_t need = size_t(big * row_bytes);
+  if (c->cap_bytes < need) {
+    SK_CUDA(cudaDeviceSynchronize());
+    for (int i = 0; i < kRing; ++i) {
+      if (c->dx[i]) cudaFree(c->dx[i]);
+      if (c->dy[i]) cudaFree(c->dy[i]);
+      c->dx[i] = c->dy[i] = nullptr;
+    }
+    c->cap_bytes = 0;
+    for (int i = 0; i < kRing; ++i) {
+      SK_CUDA(cudaMalloc(&c->dx[i], need));
+      SK_CUDA(cudaMalloc(&c->dy[i], need));
+    }
+    c->cap_bytes = need;
+  }
+  const int64_t nchunks = static_cast<int64_t>(sched.size());
+  if (c->flag_cap < nchunks) {
+    SK_CUDA(cudaDeviceSynchronize());
+    if (c->dbad) cudaFree(c->dbad);
+    if (c->hbad) cudaFreeHost(c->hbad);
+    c->dbad = nullptr;
+    c->hbad = nullptr;
+    c->flag_cap = 0;
+    const int64_t cap = std::max<int64_t>(nchunks, 64);
+    SK_CUDA(cudaMalloc(&c->dbad, cap * sizeof(unsigned long long)));
+    SK_CUDA(cudaMemset(c->dbad, 0xFF, cap * sizeof(unsigned long long)));
+    SK_CUDA(cudaMallocHost(&c->hbad, cap * sizeof(unsigned long long)));
+    c->flag_cap = cap;
+  }
+  std::vector<int64_t> start(nchunks + 1, 0);
+  for (int64_t k = 0; k < nchunks; ++k) start[k + 1] = start[k] + sched[k];
+  for (int64_t k = 0; k < nchunks; ++k) {
+    const int i = static_cast<int>(k % kRing);
+    const int64_t r0 = start[k];
+    const int64_t nr = sched[k];
+    const size_t bytes = size_t(nr * row_bytes);
+    // input slot free once the kernel that last read it is done
+    if (k >= kRing) SK_CUDA(cudaStreamWaitEvent(c->s_h2d, c->ev_k[i], 0));
+    SK_CUDA(cudaMemcpyAsync(c->dx[i], x_host + r0 * cols, bytes, cudaMemcpyHostToDevice,
+                            c->s_h2d));
+    SK_CUDA(cudaEventRecord(c->ev_h2d[i], c->s_h2d));
+    SK_CUDA(cudaStreamWaitEvent(c->s_comp, c->ev_h2d[i], 0));
+    // output slot free once the D2H that last read it is done
+    if (k >= kRing) SK_CUDA(cudaStreamWaitEvent(c->s_comp, c->ev_d2h[i], 0));
+    st = softmax_dev(c->dx[i], c->dy[i], nr, cols, cols, cols, mode, c->dbad + k, nullptr, 0,
+                     c->s_comp);
+    if (st) return st;
+    SK_CUDA(cudaEventRecord(c->ev_k[i], c->s_comp));
+    SK_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_k[i], 0));
+    SK_CUDA(cudaMemcpyAsync(y_host + r0 * cols, c->dy[i], bytes, cudaMemcpyDeviceToHost,
+                            c->s_d2h));
+    SK_CUDA(cudaEventRecord(c->ev_d2h[i], c->s_d2h));
+  }
+  // every chunk's non-finite flag in one small copy after the last kernel
+  // (one DMA instead of one per chunk between the bulk transfers)
+  SK_CUDA(cudaMemcpyAsync(c->hbad, c->dbad, size_t(nchunks) * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, c->s_d2h));
+  SK_CUDA(cudaStreamSynchronize(c->s_d2h));
+  for (int64_t k = 0; k < nchunks; ++k) {
+    if (c->hbad[k] == SK_EXCHANGE_ABORTED) {
+      SK_CUDA(cudaMemset(c->dbad, 0xFF, nchunks * sizeof(unsigned long long)));
+      g_last_error = "row-statistics exchange timed out";
+      return SK_ERR_CUDA;
+    }
+    if (c->hbad[k] != SK_NO_BAD_ROW) {
+      const int64_t row = start[k] + static_cast<int64_t>(c->hbad[k]);
+      SK_CUDA(cudaMemset(c->dbad, 0xFF, nchunks * sizeof(unsigned long long)));
+      if (bad_row_out) *bad_row_out = row;
+      g_last_error = "non-finite logits in row " + std::to_string(row);
+      return SK_ERR_NONFINITE;
+    }
+  }
+  return SK_OK;
+}
+
+}  // extern "C"
