@@ -85,29 +85,36 @@ void ensure_smem_attr(const void* fn, size_t smem) {
     cur = smem;
   }
 }
-std::atomic<int> g_k1_lpr{0}, g_k1_nv{0}, g_k1_u{0}, g_grid_mult{0}, g_seg_len{0};
-std::atomic<int> g_seg_align{0};  // K3 grid = whole multiple of nseg (row groups never straddle)
-std::atomic<int> g_k1_pf{-1};     // -1: table default, 0/1 force register prefetch
-std::atomic<int> g_pdl{1};        // programmatic dependent launch on every kernel
-std::atomic<int> g_chunk_mb{24};  // K3 row-chunk size (MB of input) kept L2 resident
+// Tuning knobs (sk_set_tuning); defaults are the measured-best settings.
+// K1
+std::atomic<int> g_k1_lpr{0}, g_k1_nv{0}, g_k1_u{0};  // force a K1 shape (0 = table default)
+std::atomic<int> g_k1_pf{-1};      // -1: table default, 0/1 force register prefetch
+std::atomic<int> g_grid_mult{0};   // K1 grid = SMs x occupancy x mult (0 = one batch per warp)
+std::atomic<int> g_vec8{0};        // 256-bit K1 path (measured no faster: off by default)
+std::atomic<int> g_pdl{1};         // programmatic dependent launch on every kernel
+// K3 alternatives (K3w warp queue and the older designs kept for comparison)
+std::atomic<int> g_seg_len{0};     // K3 segment length (0 = default)
+std::atomic<int> g_seg_align{0};   // K3 grid = whole multiple of nseg (row groups never straddle)
+std::atomic<int> g_chunk_mb{24};   // K3 row-chunk size (MB of input) kept L2 resident
 std::atomic<int> g_chunk_mb_set{0};  // chunk_mb explicitly tuned (overrides the K3 warp lag)
-std::atomic<int> g_chunk_occ_div{2};
-std::atomic<int> g_claim_batch{0};
-std::atomic<int> g_cluster_k3{1};    // use the cluster-resident K3 when a row fits
+std::atomic<int> g_chunk_occ_div{2};  // K3 chunk grid = SMs x occupancy / div
+std::atomic<int> g_claim_batch{0};    // K3 warp queue: tasks per atomic claim (0 = static)
+std::atomic<int> g_k3_impl{3};  // 0 CTA queue, 1 smem-resident, 2 chunked, 3 warp queue, 4 registers, 5 cluster only
+// K3c (cluster-resident rows)
+std::atomic<int> g_cluster_k3{1};    // allow the cluster kernel (fallback to K3g)
 std::atomic<int> g_cluster_size{0};  // force a K3c cluster size (0 = auto)
-std::atomic<int> g_vec8{0};          // 256-bit K1 path (measured no faster: off by default)   // K3 warp queue: tasks per atomic claim (0 = static)  // K3 grid = SMs*occupancy/div: two launches co-reside
-std::atomic<int> g_gres{1};       // K3g grid-resident rows: 0 off, 1 when it out-scores K3c, 2 force
-std::atomic<int> g_gres_p{0};     // force K3g CTAs per row (0 = auto)
-std::atomic<int> g_gres_diag{0};
+// K3g (grid-resident rows)
+std::atomic<int> g_gres{1};        // 0 off, 1 auto, 2 force
+std::atomic<int> g_gres_p{0};      // force CTAs per row (0 = planner)
+std::atomic<int> g_gres_st{0};     // force ring depth (0 = planner)
+std::atomic<int> g_gres_split{-1};  // separate poller warp: -1 auto (depth >= 4), 0 off, 1 on
+std::atomic<int> g_gres_sleep{128};  // poller back-off between polls (ns)
+std::atomic<int> g_gres_diag{0};     // timing diagnostics (1: wait only for the own slot -- wrong results)
 std::atomic<unsigned> g_gres_spins{kGresSpinLimit};  // exchange timeout (polls), tests shorten it
-std::atomic<int> g_gres_st{0};
-std::atomic<int> g_gres_sleep{128};
-std::atomic<int> g_gres_split{-1};   // K3g poller warp: -1 auto (lag >= 2), 0 off, 1 on
 bool gres_split(int nstages) {
   const int v = g_gres_split.load();
   return v < 0 ? nstages >= 4 : v != 0;
-}  // K3g poller back-off between polls (ns)    // force K3g ring depth (0 = as deep as smem allows)
-std::atomic<int> g_k3_impl{3};    // 0: ordered task queue (k3_dyn), 1: smem-resident (k_seg), 2: chunked launches (k3_chunk)
+}
 
 // ------------------------------------------------------------------ K1 table
 using K1Fn = void (*)(const float*, float*, int64_t, int, int64_t, int64_t,
