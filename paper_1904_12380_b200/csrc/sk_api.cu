@@ -354,32 +354,42 @@ enum PathKind { kPathK1 = 0, kPathSeg = 1, kPathSplit = 2, kPathK1m = 3 };
 // ------------------------------------------------------------ K1m table
 using K1mFn = K1Fn;
 struct K1mEntry {
-  int wpr, nv;
+  int vec, wpr, nv;
   K1mFn fn[3];
 };
-#define SK_K1M(WPR, NV)                                                                  \
+#define SK_K1M(VEC, WPR, NV)                                                             \
   K1mEntry {                                                                             \
-    WPR, NV, {                                                                           \
-      &k1m_rows<kClipAccurate, WPR, NV>, &k1m_rows<kAccurate, WPR, NV>,                  \
-          &k1m_rows<kApprox, WPR, NV>                                                    \
+    VEC, WPR, NV, {                                                                      \
+      &k1m_rows<kClipAccurate, WPR, NV, VEC>, &k1m_rows<kAccurate, WPR, NV, VEC>,        \
+          &k1m_rows<kApprox, WPR, NV, VEC>                                               \
     }                                                                                    \
   }
-const K1mEntry kK1mTable[] = {SK_K1M(2, 16), SK_K1M(4, 8), SK_K1M(4, 12), SK_K1M(4, 16),
-                              SK_K1M(8, 8)};
+const K1mEntry kK1mTable[] = {
+    // 128-bit rows
+    SK_K1M(4, 2, 16), SK_K1M(4, 4, 8), SK_K1M(4, 4, 12), SK_K1M(4, 4, 16), SK_K1M(4, 8, 8),
+    // 32-bit rows (any length / alignment): 1025..8192 floats
+    SK_K1M(1, 2, 48), SK_K1M(1, 4, 32), SK_K1M(1, 4, 48), SK_K1M(1, 8, 32)};
 #undef SK_K1M
-const K1mEntry* k1m_find(int wpr, int nv) {
+const K1mEntry* k1m_find(int vec, int wpr, int nv) {
   for (const auto& e : kK1mTable)
-    if (e.wpr == wpr && e.nv == nv) return &e;
+    if (e.vec == vec && e.wpr == wpr && e.nv == nv) return &e;
   return nullptr;
 }
 constexpr int64_t kK1mMaxCols = 8192;
 std::atomic<int> g_k1m{1}, g_k1m_wpr{0}, g_k1m_nv{0};
 // measured (scripts/medium_rows.py): 16384x4096 80.5 us with (2,16) vs 101.5
 // for K2; 8192x6144 62.4 (4,12); 8192x8192 80.1 (4,16) vs 88.6 for K2
-void k1m_default(int64_t cols, int& wpr, int& nv) {
-  if (cols <= 4096) { wpr = 2; nv = 16; }
-  else if (cols <= 6144) { wpr = 4; nv = 12; }
-  else { wpr = 4; nv = 16; }
+void k1m_default(int vec, int64_t cols, int& wpr, int& nv) {
+  if (vec == 4) {
+    if (cols <= 4096) { wpr = 2; nv = 16; }
+    else if (cols <= 6144) { wpr = 4; nv = 12; }
+    else { wpr = 4; nv = 16; }
+  } else {  // 32-bit accesses
+    if (cols <= 3072) { wpr = 2; nv = 48; }
+    else if (cols <= 4096) { wpr = 4; nv = 32; }
+    else if (cols <= 6144) { wpr = 4; nv = 48; }
+    else { wpr = 8; nv = 32; }
+  }
 }
 
 struct Plan {
@@ -502,20 +512,20 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
   PathKind kind;
   if (force >= 0) kind = static_cast<PathKind>(force);
   else if (cols <= 1024 || (vec && cols <= kK1MaxCols)) kind = kPathK1;
-  else if (vec && cols <= kK1mMaxCols && g_k1m.load()) kind = kPathK1m;
+  else if (cols <= kK1mMaxCols && g_k1m.load()) kind = kPathK1m;
   else if (vec) kind = kPathSeg;
   else kind = kPathSplit;
   if (kind == kPathK1 && cols > kK1MaxCols) return arg_fail("k1 path needs cols <= 3072");
   if (kind == kPathSeg && !vec) return arg_fail("seg path needs 16-B aligned rows");
 
   if (kind == kPathK1m) {
-    if (!vec) return arg_fail("k1m path needs 16-B aligned rows");
+    const int vw = vec ? 4 : 1;
     int wpr, nv;
-    k1m_default(cols, wpr, nv);
+    k1m_default(vw, cols, wpr, nv);
     if (g_k1m_wpr.load() > 0) { wpr = g_k1m_wpr; nv = g_k1m_nv; }
-    const K1mEntry* e = k1m_find(wpr, nv);
+    const K1mEntry* e = k1m_find(vw, wpr, nv);
     if (!e) return arg_fail("no K1m instantiation for the requested shape");
-    if (int64_t(wpr) * 32 * nv * 4 < cols) return arg_fail("K1m shape does not cover cols");
+    if (int64_t(wpr) * 32 * nv * vw < cols) return arg_fail("K1m shape does not cover cols");
     p.kind = kPathK1m;
     p.k1m = e;
     p.threads = kRowsThreads;
@@ -1066,8 +1076,8 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
   st = make_plan(rows, cols, ldx, ldy, x_addr, y_addr, 0, device, p);
   if (st) return st;
   if (p.kind == kPathK1m)
-    snprintf(buf, buflen, "k1m wpr=%d nv=%d threads=%d grid=%lld", p.k1m->wpr, p.k1m->nv,
-             p.threads, (long long)p.grid);
+    snprintf(buf, buflen, "k1m vec=%d wpr=%d nv=%d threads=%d grid=%lld", p.k1m->vec,
+             p.k1m->wpr, p.k1m->nv, p.threads, (long long)p.grid);
   else if (p.kind == kPathK1)
     snprintf(buf, buflen, "k1 vec=%d lpr=%d nv=%d u=%d pf=%d threads=%d grid=%lld", p.k1->vec,
              p.k1->lpr, p.k1->nv, p.k1->u, p.k1->pf, p.threads, (long long)p.grid);

@@ -21,20 +21,26 @@
 
 namespace sk {
 
-template <int MODE, int WPR, int NV>
+// VEC = 4: 128-bit accesses (cols % 4 == 0, 16-B aligned rows); VEC = 1:
+// 32-bit coalesced accesses for rows of any length / alignment.  Thread t of
+// a row holds vectors j*T + t, j < NV (T = 32*WPR threads per row).
+template <int MODE, int WPR, int NV, int VEC>
 __global__ void __launch_bounds__(kRowsThreads, 2)
     k1m_rows(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int cols,
              int64_t ldx, int64_t ldy, unsigned long long* __restrict__ bad_row,
              float shift_scale) {
   static_assert(WPR == 2 || WPR == 4 || WPR == 8, "WPR");
+  static_assert(VEC == 1 || VEC == 4, "VEC");
+  static_assert((NV * VEC) % 2 == 0, "packed pairs");
   constexpr int T = WPR * 32;  // threads per row
+  constexpr int E = NV * VEC;  // floats per thread
   __shared__ float red_m[kRowsThreads / 32];
   __shared__ double red_s[kRowsThreads / 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rw = warp / WPR;  // row slot of this warp in the block
   const int t = (warp % WPR) * 32 + lane;
   const int rpc = static_cast<int>(blockDim.x >> 5) / WPR;
-  const int nvec = cols >> 2;  // 128-bit path: cols % 4 == 0
+  const int nvec = VEC == 4 ? cols >> 2 : cols;
   pdl_wait();
   pdl_launch_dependents();
 
@@ -42,20 +48,29 @@ __global__ void __launch_bounds__(kRowsThreads, 2)
     const int64_t r = r0 + rw;
     const bool rv = r < rows;
     const float* xr = x + (rv ? r : 0) * ldx;
-    float4 v[NV];
+    float v[E];
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const int q = j * T + t;
-      v[j] = (rv && q < nvec) ? ld_stream4(xr + 4 * q)
-                              : make_float4(kPadLogit, kPadLogit, kPadLogit, kPadLogit);
+      if (rv && q < nvec) {
+        if constexpr (VEC == 4) {
+          const float4 a = ld_stream4(xr + 4 * q);
+          v[4 * j] = a.x; v[4 * j + 1] = a.y; v[4 * j + 2] = a.z; v[4 * j + 3] = a.w;
+        } else {
+          v[j] = ld_stream1(xr + q);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) v[VEC * j + k] = kPadLogit;
+      }
     }
     // ---- row max + finite check
     float mu = kPadLogit;
     u64 z = f2pk(0.0f, 0.0f);
 #pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      mu = fmaxf(mu, fmaxf(fmaxf(v[j].x, v[j].y), fmaxf(v[j].z, v[j].w)));
-      z = nf_acc2(nf_acc2(z, v[j].x, v[j].y), v[j].z, v[j].w);
+    for (int e = 0; e < E; e += 2) {
+      mu = fmaxf(mu, fmaxf(v[e], v[e + 1]));
+      z = nf_acc2(z, v[e], v[e + 1]);
     }
     const bool bad = rv && nf_bad(z);
     mu = group_max<32>(mu);
@@ -68,11 +83,13 @@ __global__ void __launch_bounds__(kRowsThreads, 2)
     // ---- exp(clip(x - m)) kept in registers, row sum
     u64 acc = f2pk(0.0f, 0.0f);
 #pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      const float2 a = sexp2<MODE>(v[j].x, v[j].y, m);
-      const float2 b = sexp2<MODE>(v[j].z, v[j].w, m);
-      v[j] = make_float4(a.x, a.y, b.x, b.y);
-      if (j * T + t < nvec) acc = f2add(f2add(acc, f2pk(a.x, a.y)), f2pk(b.x, b.y));
+    for (int e = 0; e < E; e += 2) {
+      float2 a = sexp2<MODE>(v[e], v[e + 1], m);
+      v[e] = a.x;
+      v[e + 1] = a.y;
+      if ((e / VEC) * T + t >= nvec) a.x = 0.0f;  // padding contributes nothing
+      if (((e + 1) / VEC) * T + t >= nvec) a.y = 0.0f;
+      acc = f2add(acc, f2pk(a.x, a.y));
     }
     const float2 a2 = f2up(acc);
     const double sw = group_sum<32>(static_cast<double>(a2.x + a2.y));
@@ -89,9 +106,13 @@ __global__ void __launch_bounds__(kRowsThreads, 2)
       for (int j = 0; j < NV; ++j) {
         const int q = j * T + t;
         if (q < nvec) {
-          const float2 p = scale2<MODE>(make_float2(v[j].x, v[j].y), rcp);
-          const float2 o = scale2<MODE>(make_float2(v[j].z, v[j].w), rcp);
-          st_stream4(yr + 4 * q, make_float4(p.x, p.y, o.x, o.y));
+          if constexpr (VEC == 4) {
+            const float2 p = scale2<MODE>(make_float2(v[4 * j], v[4 * j + 1]), rcp);
+            const float2 o = scale2<MODE>(make_float2(v[4 * j + 2], v[4 * j + 3]), rcp);
+            st_stream4(yr + 4 * q, make_float4(p.x, p.y, o.x, o.y));
+          } else {
+            st_stream1(yr + q, scale1<MODE>(v[j], rcp));
+          }
         }
       }
     }

@@ -201,11 +201,13 @@ def test_k1_medium_rows(rows, C, oracle):
 
 
 @pytest.mark.parametrize("rows,C", [(300, 8192), (4096, 4000), (2048, 5000), (64, 6144),
-                                    (3, 8192), (1000, 3076)])
+                                    (3, 8192), (1000, 3076), (4096, 5001), (300, 8191),
+                                    (2000, 1025), (7, 3001), (513, 4097), (64, 6143)])
 def test_k1m_medium_rows(rows, C, oracle):
-    """128-bit rows of 3073..8192 floats held in the registers of 2-8 warps
-    (K1m): every mode, clip firing, a large negative row, strided pitch, row
-    blocks bit-identical to the whole matrix, non-finite detection."""
+    """Rows held in the registers of 2-8 warps (K1m): 128-bit rows of
+    3073..8192 floats and rows of any length (32-bit accesses) from 1025 up --
+    every mode, clip firing, a large negative row, strided pitch, row blocks
+    bit-identical to the whole matrix, non-finite detection."""
     from paper_1904_12380_b200 import tensor
 
     x = np.empty((rows, C), np.float32)
@@ -221,6 +223,8 @@ def test_k1m_medium_rows(rows, C, oracle):
         assert_parity(oracle, y, ref, approx=(mode == 2), what=(rows, C, mode, plan))
     y, _ = gu.softmax_abi(x, 0, ldx=C + 12, ldy=C + 4)
     assert_parity(oracle, y, oracle.softmax_ref(x), what=(rows, C, "strided"))
+    y, _ = gu.softmax_abi(x, 0, x_offset=1, y_offset=3, ldx=C + 3, ldy=C + 1)
+    assert_parity(oracle, y, oracle.softmax_ref(x), what=(rows, C, "unaligned"))
     whole, _ = gu.softmax_abi(x, 0)
     part, _ = gu.softmax_abi(x[rows // 3:], 0)
     assert np.array_equal(part.view(np.uint32), whole[rows // 3:].view(np.uint32))
