@@ -368,7 +368,8 @@ const K1mEntry kK1mTable[] = {
     // 128-bit rows
     SK_K1M(4, 2, 16), SK_K1M(4, 4, 8), SK_K1M(4, 4, 12), SK_K1M(4, 4, 16), SK_K1M(4, 8, 8),
     // 32-bit rows (any length / alignment): 1025..8192 floats
-    SK_K1M(1, 2, 48), SK_K1M(1, 4, 32), SK_K1M(1, 4, 48), SK_K1M(1, 8, 32)};
+    SK_K1M(1, 2, 24), SK_K1M(1, 2, 32), SK_K1M(1, 2, 48), SK_K1M(1, 4, 32), SK_K1M(1, 4, 48),
+    SK_K1M(1, 8, 32)};
 #undef SK_K1M
 const K1mEntry* k1m_find(int vec, int wpr, int nv) {
   for (const auto& e : kK1mTable)
@@ -385,7 +386,9 @@ void k1m_default(int vec, int64_t cols, int& wpr, int& nv) {
     else if (cols <= 6144) { wpr = 4; nv = 12; }
     else { wpr = 4; nv = 16; }
   } else {  // 32-bit accesses
-    if (cols <= 3072) { wpr = 2; nv = 48; }
+    if (cols <= 1536) { wpr = 2; nv = 24; }
+    else if (cols <= 2048) { wpr = 2; nv = 32; }
+    else if (cols <= 3072) { wpr = 2; nv = 48; }
     else if (cols <= 4096) { wpr = 4; nv = 32; }
     else if (cols <= 6144) { wpr = 4; nv = 48; }
     else { wpr = 8; nv = 32; }

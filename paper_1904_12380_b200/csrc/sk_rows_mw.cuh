@@ -1,5 +1,6 @@
-// sk_rows_mw.cuh -- K1m: medium rows (3 K .. 8 K floats) in the registers of
-// WPR warps.
+// sk_rows_mw.cuh -- K1m: medium rows (128-bit rows of 3 K .. 8 K floats, and
+// rows of any length / alignment from 1 K to 8 K floats with 32-bit accesses)
+// in the registers of WPR warps.
 //
 // K1 (sk_rows.cuh) gives a row to LPR lanes of one warp; past ~3 K floats a
 // warp's registers run out.  K1m spreads a row over WPR warps of a 256-thread
@@ -13,8 +14,8 @@
 // Same operation order as K1 (kernels.py:136-189): row max, exp(clip(x - m))
 // kept in registers, f64 row sum (lane fp32 pairs -> f64 butterfly -> WPR warp
 // partials in fixed order), y = e * (1/(float)S) with the reference's flush.
-// The result depends only on (WPR, NV), never on the grid, so row blocks keep
-// their bits.
+// The result depends only on (VEC, WPR, NV), never on the grid, so row blocks
+// keep their bits.
 #pragma once
 #include "sk_common.cuh"
 #include "sk_rows.cuh"
