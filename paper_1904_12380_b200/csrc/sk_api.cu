@@ -268,15 +268,27 @@ int max_active_clusters(const void* fn, int cs, size_t smem) {
 
 bool gres_split(int nstages);
 constexpr int64_t kGresSmemMax = 225 * 1024;  // ring bytes per K3g CTA (227 KB opt-in minus statics)
-template <int L, bool SPLIT>
+template <int L, bool SPLIT, bool UNAL = false>
 const void* gres_fn_l(int mode) {
   switch (mode) {
-    case kClipAccurate: return reinterpret_cast<const void*>(&k3_gres<kClipAccurate, L, SPLIT>);
-    case kAccurate: return reinterpret_cast<const void*>(&k3_gres<kAccurate, L, SPLIT>);
-    default: return reinterpret_cast<const void*>(&k3_gres<kApprox, L, SPLIT>);
+    case kClipAccurate: return reinterpret_cast<const void*>(&k3_gres<kClipAccurate, L, SPLIT, UNAL>);
+    case kAccurate: return reinterpret_cast<const void*>(&k3_gres<kAccurate, L, SPLIT, UNAL>);
+    default: return reinterpret_cast<const void*>(&k3_gres<kApprox, L, SPLIT, UNAL>);
   }
 }
 // ring depth 2 and 3 run lag 1; 4 -> lag 2; 5 -> lag 3
+const void* gres_fn(int mode, int nstages, bool split);
+// rows of any alignment: the two schedules the planner uses (depth 2-3 with
+// the publisher polling, depth 4 with a poller warp); nullptr otherwise
+const void* gres_fn_unal(int mode, int nstages, bool split) {
+  if (nstages <= 3 && !split) return gres_fn_l<1, false, true>(mode);
+  if (nstages == 4 && split) return gres_fn_l<2, true, true>(mode);
+  return nullptr;
+}
+const void* gres_fn(int mode, int nstages, bool split, bool unal) {
+  if (unal) return gres_fn_unal(mode, nstages, split);
+  return gres_fn(mode, nstages, split);
+}
 const void* gres_fn(int mode, int nstages, bool split) {
   if (split)
     return nstages >= 5 ? gres_fn_l<3, true>(mode)
@@ -400,6 +412,7 @@ struct Plan {
   // K1
   const K1Entry* k1 = nullptr;
   const K1mEntry* k1m = nullptr;
+  bool unal = false;  // K3g over rows of any alignment
   // seg (K2: nseg == 1; K3: nseg > 1)
   int nseg = 1, seglen = 0, threads = 0, lag = 0;
   int k3 = 0;  // 0 none/K2, 1 dyn, 2 smem, 3 chunk
@@ -470,7 +483,8 @@ double gres_time_us(int64_t rows, int P, int st, int64_t slice, int groups, int 
 // bit-identical.  At 2048 rows the choice equals the per-shape best on every
 // measured long-row shape.
 
-GresChoice plan_gres(int64_t rows, int64_t cols, int mode, const DevInfo& di, int world, int nvr) {
+GresChoice plan_gres(int64_t rows, int64_t cols, int mode, const DevInfo& di, int world, int nvr,
+                     bool unal) {
   GresChoice best;
   double best_t = 0.0;
   for (int P = 1; P * world <= kGresMaxSlots && P * nvr <= di.sms; ++P) {
@@ -487,8 +501,8 @@ GresChoice plan_gres(int64_t rows, int64_t cols, int mode, const DevInfo& di, in
       if (g_gres_st.load() >= 2 && st != g_gres_st.load()) continue;
       const size_t smem = size_t(st) * slice * sizeof(float);
       const bool split = gres_split(st);
-      if (occupancy(gres_fn(mode, st, split), split ? kGresBlock : kGresThreads, smem) < 1)
-        continue;
+      const void* fn = gres_fn(mode, st, split, unal);
+      if (!fn || occupancy(fn, split ? kGresBlock : kGresThreads, smem) < 1) continue;
       const double t = gres_time_us(rows, P, st, slice, groups, world, nvr);
       if (best.P == 0 || t < best_t) {
         best_t = t;
@@ -521,6 +535,24 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
   if (kind == kPathK1 && cols > kK1MaxCols) return arg_fail("k1 path needs cols <= 3072");
   if (kind == kPathSeg && !vec) return arg_fail("seg path needs 16-B aligned rows");
 
+  if (kind == kPathSplit && force < 0 && !vec && cols > kK1mMaxCols && g_gres.load() != 0 &&
+      di.coop) {
+    // rows of any alignment too long for one CTA: K3g with TMA on each slice's
+    // aligned middle (1.7x the split path's 12 B/element on a 50257-wide vocab)
+    const GresChoice gc = plan_gres(kGresPlanRows, cols, mode, di, 1, 1, true);
+    if (gc.P > 0) {
+      p.kind = kPathSeg;
+      p.k3 = 7;
+      p.unal = true;
+      p.nseg = gc.P;
+      p.seglen = static_cast<int>(gc.slice);
+      p.lag = gc.st;
+      p.threads = gres_split(gc.st) ? kGresBlock : kGresThreads;
+      p.smem = size_t(gc.st) * gc.slice * sizeof(float);
+      p.grid = int64_t(gc.groups) * gc.P;
+      return SK_OK;
+    }
+  }
   if (kind == kPathK1m) {
     const int vw = vec ? 4 : 1;
     int wpr, nv;
@@ -571,7 +603,8 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     const int gres = g_gres.load();
     if ((cols > kSegCap || gres == 2) && (impl0 == 5 || impl0 == 3)) {
       GresChoice gc;
-      if (gres != 0 && impl0 != 5 && di.coop) gc = plan_gres(kGresPlanRows, cols, mode, di, 1, 1);
+      if (gres != 0 && impl0 != 5 && di.coop)
+        gc = plan_gres(kGresPlanRows, cols, mode, di, 1, 1, false);
       if (gc.P > 0) {
         p.kind = kPathSeg;
         p.k3 = 7;
@@ -915,7 +948,7 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
       comm.sys = 0;
       comm.spin_limit = g_gres_spins.load();
       int P = p.nseg, slice = p.seglen, nst = p.lag;
-      SK_CUDA(launch_k(gres_fn(mode, p.lag, p.threads == kGresBlock), dim3(static_cast<unsigned>(p.grid)),
+      SK_CUDA(launch_k(gres_fn(mode, p.lag, p.threads == kGresBlock, p.unal), dim3(static_cast<unsigned>(p.grid)),
                        dim3(p.threads), p.smem, s, true, x, y, rows, cols, ldx, ldy, P, slice, nst, comm,
                        bad, sh, g_gres_sleep.load(), g_gres_diag.load()));
     } else if (p.k3 == 5) {

@@ -43,7 +43,7 @@ int colshard_launch(const float* x, float* y, int64_t rows, int64_t cols, int64_
   SK_CUDA(cudaGetDevice(&dev));
   const DevInfo di = dev_info(dev);
   if (!di.coop) return arg_fail("device cannot co-schedule the fused column shard");
-  const GresChoice gc = plan_gres(kGresPlanRows, cols, mode, di, world, nvr);
+  const GresChoice gc = plan_gres(kGresPlanRows, cols, mode, di, world, nvr, false);
   if (gc.P == 0) return arg_fail("shard row too long for the fused column shard (use the split path)");
   const bool split = gres_split(gc.st);
   const int lag = gc.st >= 5 ? 3 : gc.st == 4 ? 2 : 1;

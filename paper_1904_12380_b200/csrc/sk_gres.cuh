@@ -135,10 +135,32 @@ __device__ __forceinline__ int gres_bar2(unsigned k) { return 2 + L + int(k % un
 template <int L>
 __device__ __forceinline__ int gres_bar3(unsigned k) { return 3 + 2 * L + int(k % unsigned(L)); }
 
+// UNAL: rows of any length / alignment.  A slice [c0, c0+len) of a row is
+// staged as its 16-B aligned middle [h, h+nmid) by TMA (h <= 3 head floats,
+// nmid % 4 == 0, <= 3 tail floats), the head and tail being read straight
+// from global memory.  Every thread still processes the same LOGICAL groups
+// of 4 consecutive elements as the aligned kernel, with the same operations,
+// so the result does not depend on where the row happens to sit in memory.
+struct SliceGeom {
+  int h, nmid;
+};
+__device__ __forceinline__ SliceGeom slice_geom(const float* g, int len) {
+  int h = static_cast<int>(((16u - (reinterpret_cast<uintptr_t>(g) & 15u)) & 15u) >> 2);
+  if (h > len) h = len;
+  return {h, ((len - h) >> 2) << 2};
+}
+// element e of the slice: staged middle from smem, head / tail from global
+__device__ __forceinline__ float slice_elem(const float* sm, const float* g, SliceGeom sg, int e,
+                                            int len) {
+  if (e >= len) return kPadLogit;
+  const int i = e - sg.h;
+  return (i >= 0 && i < sg.nmid) ? sm[i] : __ldg(g + e);
+}
+
 // L: rows between a row's local pass and its output pass (ring depth L + 2).
 // SPLIT: a separate poller warp (block 576) vs the publisher warp polling
 // after each publication (block 544).
-template <int MODE, int L, bool SPLIT>
+template <int MODE, int L, bool SPLIT, bool UNAL = false>
 __global__ void __launch_bounds__(kGresBlock, 1)
     k3_gres(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
             int64_t ldx, int64_t ldy, int P, int slice, int nstages, const GresComm comm,
@@ -169,8 +191,9 @@ __global__ void __launch_bounds__(kGresBlock, 1)
   y += v * comm.shard_stride;
   const int64_t c0 = int64_t(prank) * slice;
   const int64_t rem = cols - c0;
-  const int len = rem <= 0 ? 0 : static_cast<int>(rem < slice ? rem : slice);  // % 4 == 0
-  const int nvec = len >> 2;
+  const int len = rem <= 0 ? 0 : static_cast<int>(rem < slice ? rem : slice);
+  // logical float4 groups of the slice (the last one partial when UNAL)
+  const int nvec = UNAL ? (len + 3) >> 2 : len >> 2;
   if (tid == 0) {
     for (int s = 0; s < nstages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -247,10 +270,17 @@ __global__ void __launch_bounds__(kGresBlock, 1)
   } else if (warp == NW) {
     // ------------------------------------------------ publisher + TMA warp
     auto issue = [&](int64_t row, int stage) {
-      mbar_arrive_expect_tx(&bars[stage], static_cast<uint32_t>(len) * 4u);
-      if (len > 0)
-        tma_load_1d(stage_buf + size_t(stage) * slice, x + row * ldx + c0,
-                    static_cast<uint32_t>(len) * 4u, &bars[stage]);
+      const float* src = x + row * ldx + c0;
+      int n = len;
+      if constexpr (UNAL) {
+        const SliceGeom sg = slice_geom(src, len);
+        src += sg.h;
+        n = sg.nmid;
+      }
+      mbar_arrive_expect_tx(&bars[stage], static_cast<uint32_t>(n) * 4u);
+      if (n > 0)
+        tma_load_1d(stage_buf + size_t(stage) * slice, src, static_cast<uint32_t>(n) * 4u,
+                    &bars[stage]);
     };
     if (lane == 0)
       for (int s = 0; s < nstages; ++s) {
@@ -302,15 +332,42 @@ __global__ void __launch_bounds__(kGresBlock, 1)
       const int b = static_cast<int>(j % unsigned(NB));
       const float M = bc_m[b];
       const float rcp = recip_of_sum(bc_s[b]);
-      const float4* sb =
-          reinterpret_cast<const float4*>(stage_buf + size_t(j % unsigned(nstages)) * slice);
-      float* yr = y + (g + int64_t(j) * G) * ldy + c0;
+      const float* sm = stage_buf + size_t(j % unsigned(nstages)) * slice;
+      const float4* sb = reinterpret_cast<const float4*>(sm);
+      const int64_t orow = g + int64_t(j) * G;
+      float* yr = y + orow * ldy + c0;
+      if constexpr (UNAL) {
+        const float* xg = x + orow * ldx + c0;
+        const SliceGeom sg = slice_geom(xg, len);
+        const bool yv = (reinterpret_cast<uintptr_t>(yr) & 15u) == 0;
+#pragma unroll 2
+        for (int q = tid; q < nvec; q += kGresCompute) {
+          const int e = 4 * q;
+          const float4 v4 = (sg.h == 0 && e + 3 < sg.nmid)
+                                ? sb[q]
+                                : make_float4(slice_elem(sm, xg, sg, e, len),
+                                              slice_elem(sm, xg, sg, e + 1, len),
+                                              slice_elem(sm, xg, sg, e + 2, len),
+                                              slice_elem(sm, xg, sg, e + 3, len));
+          const float2 a = scale2<MODE>(sexp2<MODE>(v4.x, v4.y, M), rcp);
+          const float2 c = scale2<MODE>(sexp2<MODE>(v4.z, v4.w, M), rcp);
+          if (yv && e + 3 < len) {
+            st_stream4(yr + e, make_float4(a.x, a.y, c.x, c.y));
+          } else {
+            const float o[4] = {a.x, a.y, c.x, c.y};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (e + i < len) st_stream1(yr + e + i, o[i]);
+          }
+        }
+      } else {
 #pragma unroll 4
-      for (int q = tid; q < nvec; q += kGresCompute) {
-        const float4 v4 = sb[q];
-        const float2 a = scale2<MODE>(sexp2<MODE>(v4.x, v4.y, M), rcp);
-        const float2 c = scale2<MODE>(sexp2<MODE>(v4.z, v4.w, M), rcp);
-        st_stream4(yr + 4 * q, make_float4(a.x, a.y, c.x, c.y));
+        for (int q = tid; q < nvec; q += kGresCompute) {
+          const float4 v4 = sb[q];
+          const float2 a = scale2<MODE>(sexp2<MODE>(v4.x, v4.y, M), rcp);
+          const float2 c = scale2<MODE>(sexp2<MODE>(v4.z, v4.w, M), rcp);
+          st_stream4(yr + 4 * q, make_float4(a.x, a.y, c.x, c.y));
+        }
       }
       fence_proxy_async_smem();  // generic smem reads before the TMA refill
       bar_arrive_n(gres_bar3<L>(j), kGresThreads);
@@ -320,13 +377,27 @@ __global__ void __launch_bounds__(kGresBlock, 1)
     for (int64_t row = g; row < rows; row += G, ++k) {
       const int stage = static_cast<int>(k % unsigned(nstages));
       mbar_wait(&bars[stage], (k / unsigned(nstages)) & 1u);
-      const float4* sb = reinterpret_cast<const float4*>(stage_buf + size_t(stage) * slice);
+      const float* sm = stage_buf + size_t(stage) * slice;
+      const float4* sb = reinterpret_cast<const float4*>(sm);
+      const float* xg = x + row * ldx + c0;
+      const SliceGeom sg = UNAL ? slice_geom(xg, len) : SliceGeom{0, len};
+      // logical group q of the slice (aligned: straight from the staged row)
+      auto group = [&](int q) -> float4 {
+        if constexpr (UNAL) {
+          const int e = 4 * q;
+          if (!(sg.h == 0 && e + 3 < sg.nmid))
+            return make_float4(slice_elem(sm, xg, sg, e, len), slice_elem(sm, xg, sg, e + 1, len),
+                               slice_elem(sm, xg, sg, e + 2, len),
+                               slice_elem(sm, xg, sg, e + 3, len));
+        }
+        return sb[q];
+      };
 
       float mt = kPadLogit;
       u64 z = f2pk(0.0f, 0.0f);
 #pragma unroll 4
       for (int q = tid; q < nvec; q += kGresCompute) {
-        const float4 v4 = sb[q];
+        const float4 v4 = group(q);
         mt = fmaxf(mt, fmaxf(fmaxf(v4.x, v4.y), fmaxf(v4.z, v4.w)));
         z = nf_acc2(nf_acc2(z, v4.x, v4.y), v4.z, v4.w);
       }
@@ -335,9 +406,14 @@ __global__ void __launch_bounds__(kGresBlock, 1)
       u64 acc = f2pk(0.0f, 0.0f);
 #pragma unroll 4
       for (int q = tid; q < nvec; q += kGresCompute) {
-        const float4 v4 = sb[q];
-        const float2 a = sexp2<MODE>(v4.x, v4.y, mw);
-        const float2 c = sexp2<MODE>(v4.z, v4.w, mw);
+        const float4 v4 = group(q);
+        float2 a = sexp2<MODE>(v4.x, v4.y, mw);
+        float2 c = sexp2<MODE>(v4.z, v4.w, mw);
+        if (UNAL && 4 * q + 3 >= len) {  // padding of the last partial group
+          if (4 * q + 1 >= len) a.y = 0.0f;
+          if (4 * q + 2 >= len) c.x = 0.0f;
+          if (4 * q + 3 >= len) c.y = 0.0f;
+        }
         acc = f2add(f2add(acc, f2pk(a.x, a.y)), f2pk(c.x, c.y));
       }
       const float2 acc2 = f2up(acc);

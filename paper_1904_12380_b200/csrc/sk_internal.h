@@ -77,7 +77,8 @@ struct GresChoice {
   double score = 0.0;
 };
 
-GresChoice plan_gres(int64_t rows, int64_t cols, int mode, const DevInfo& di, int world, int nvr);
+GresChoice plan_gres(int64_t rows, int64_t cols, int mode, const DevInfo& di, int world, int nvr,
+                     bool unal);
 const void* gres_fn(int mode, int nstages, bool split);
 bool gres_split(int nstages);
 // the K3g plan is modelled at this row count: plans (hence bits) depend on C only

@@ -367,6 +367,35 @@ def test_rows_at_and_beyond_chip_capacity(C, oracle):
     assert_parity(oracle, y, oracle.softmax_ref(x, True, nthreads=0), what=plan)
 
 
+@pytest.mark.parametrize("rows,C", [(40, 50257), (7, 262147), (3, 1_000_003), (300, 8193),
+                                    (13, 20001)])
+def test_k3g_unaligned_rows(rows, C, oracle):
+    """Rows of any length / alignment past one CTA: K3g stages each slice's
+    16-B aligned middle by TMA and reads the <= 3 head / tail floats from
+    global memory -- every mode, ragged last group, clip, unaligned bases and
+    pitches; the bits match the aligned kernel on the same data."""
+    from paper_1904_12380_b200 import tensor
+
+    x = np.empty((rows, C), np.float32)
+    tensor.fill_normal_array(x, C % 1000 + rows, 4.0)
+    x[0, 1] = -400.0
+    x[rows - 1, C - 1] = 30.0
+    plan = gu.plan(rows, C)
+    assert plan.startswith("k3_gres_unal"), plan
+    for mode in (0, 1, 2):
+        ref = oracle.softmax_ref(x, clip=(mode == 0))
+        y, bad = gu.softmax_abi(x, mode)
+        assert bad == gu.NO_BAD
+        assert_parity(oracle, y, ref, approx=(mode == 2), what=(rows, C, mode, plan))
+    y0, _ = gu.softmax_abi(x, 0)
+    for xo, yo, ldx, ldy in ((1, 0, C + 3, C + 1), (3, 2, C + 1, C + 6)):
+        y, _ = gu.softmax_abi(x, 0, x_offset=xo, y_offset=yo, ldx=ldx, ldy=ldy)
+        assert np.array_equal(y.view(np.uint32), y0.view(np.uint32)), (xo, yo, ldx, ldy)
+    x2 = x.copy()
+    x2[rows // 2, C // 2] = np.nan
+    assert gu.softmax_abi(x2, 0)[1] == rows // 2
+
+
 def test_seg_lengths_all_agree(oracle):
     x = configs.generate("c4", 0, 4)[:, :100000].copy()
     ref = oracle.softmax_ref(x)
