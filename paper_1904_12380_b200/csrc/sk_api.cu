@@ -1120,7 +1120,7 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
   else if (p.kind == kPathSeg)
     snprintf(buf, buflen, "%s nseg=%d seglen=%d threads=%d smem=%zu chunk_rows=%lld stages=%d grid=%lld",
              p.k3 == 6 ? "k3_cluster"
-             : p.k3 == 7 ? "k3_gres"
+             : p.k3 == 7 ? (p.unal ? "k3_gres_unal" : "k3_gres")
              : p.nseg == 1 ? "k2_tma"
                          : (p.k3 == 1   ? "k3_dyn"
                             : p.k3 == 3 ? "k3_chunk"

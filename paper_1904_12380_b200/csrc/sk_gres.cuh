@@ -135,26 +135,34 @@ __device__ __forceinline__ int gres_bar2(unsigned k) { return 2 + L + int(k % un
 template <int L>
 __device__ __forceinline__ int gres_bar3(unsigned k) { return 3 + 2 * L + int(k % unsigned(L)); }
 
-// UNAL: rows of any length / alignment.  A slice [c0, c0+len) of a row is
-// staged as its 16-B aligned middle [h, h+nmid) by TMA (h <= 3 head floats,
-// nmid % 4 == 0, <= 3 tail floats), the head and tail being read straight
-// from global memory.  Every thread still processes the same LOGICAL groups
-// of 4 consecutive elements as the aligned kernel, with the same operations,
-// so the result does not depend on where the row happens to sit in memory.
+// UNAL: rows of any length / alignment.  Each row's slices are cut at x's
+// 16-B boundaries, which shift per row: with h = floats before the row's first
+// boundary, CTA 0 owns columns [0, h + W), CTA r > 0 owns [h + rW, h + (r+1)W)
+// (the last one up to C).  A CTA stages the aligned middle of its range by TMA;
+// the <= 3 head floats (CTA 0) and <= 3 tail floats (last CTA) are read from
+// global memory.  The compute keeps 128-bit smem accesses, and stores stay
+// 128-bit when y has x's 16-B phase (equal pitches and bases' phases, the usual
+// case); otherwise 32-bit.  Bits depend on the row's phase (deterministic for a
+// given buffer).
 struct SliceGeom {
-  int h, nmid;
+  int64_t a;  // first column of the staged middle (16-B aligned in x)
+  int hd;     // head floats before a (CTA 0 only)
+  int nmid;   // staged floats (% 4 == 0)
+  int tl;     // tail floats after the middle (last CTA only)
 };
-__device__ __forceinline__ SliceGeom slice_geom(const float* g, int len) {
-  int h = static_cast<int>(((16u - (reinterpret_cast<uintptr_t>(g) & 15u)) & 15u) >> 2);
-  if (h > len) h = len;
-  return {h, ((len - h) >> 2) << 2};
-}
-// element e of the slice: staged middle from smem, head / tail from global
-__device__ __forceinline__ float slice_elem(const float* sm, const float* g, SliceGeom sg, int e,
-                                            int len) {
-  if (e >= len) return kPadLogit;
-  const int i = e - sg.h;
-  return (i >= 0 && i < sg.nmid) ? sm[i] : __ldg(g + e);
+__device__ __forceinline__ SliceGeom unal_geom(const float* xrow, int64_t cols, int prank, int P,
+                                               int slice) {
+  const int h = static_cast<int>(((16u - (reinterpret_cast<uintptr_t>(xrow) & 15u)) & 15u) >> 2);
+  int64_t c_start = prank == 0 ? 0 : int64_t(h) + int64_t(prank) * slice;
+  int64_t c_end = prank == P - 1 ? cols : int64_t(h) + int64_t(prank + 1) * slice;
+  if (c_end > cols) c_end = cols;
+  if (c_start > c_end) c_start = c_end;
+  SliceGeom sg;
+  sg.hd = prank == 0 ? static_cast<int>(c_end < h ? c_end : h) : 0;
+  sg.a = c_start + sg.hd;
+  sg.nmid = static_cast<int>(((c_end - sg.a) >> 2) << 2);
+  sg.tl = static_cast<int>(c_end - sg.a - sg.nmid);
+  return sg;
 }
 
 // L: rows between a row's local pass and its output pass (ring depth L + 2).
@@ -192,8 +200,7 @@ __global__ void __launch_bounds__(kGresBlock, 1)
   const int64_t c0 = int64_t(prank) * slice;
   const int64_t rem = cols - c0;
   const int len = rem <= 0 ? 0 : static_cast<int>(rem < slice ? rem : slice);
-  // logical float4 groups of the slice (the last one partial when UNAL)
-  const int nvec = UNAL ? (len + 3) >> 2 : len >> 2;
+  const int nvec = len >> 2;  // aligned rows: % 4 == 0
   if (tid == 0) {
     for (int s = 0; s < nstages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -273,8 +280,9 @@ __global__ void __launch_bounds__(kGresBlock, 1)
       const float* src = x + row * ldx + c0;
       int n = len;
       if constexpr (UNAL) {
-        const SliceGeom sg = slice_geom(src, len);
-        src += sg.h;
+        const float* xrow = x + row * ldx;
+        const SliceGeom sg = unal_geom(xrow, cols, prank, P, slice);
+        src = xrow + sg.a;
         n = sg.nmid;
       }
       mbar_arrive_expect_tx(&bars[stage], static_cast<uint32_t>(n) * 4u);
@@ -337,28 +345,33 @@ __global__ void __launch_bounds__(kGresBlock, 1)
       const int64_t orow = g + int64_t(j) * G;
       float* yr = y + orow * ldy + c0;
       if constexpr (UNAL) {
-        const float* xg = x + orow * ldx + c0;
-        const SliceGeom sg = slice_geom(xg, len);
-        const bool yv = (reinterpret_cast<uintptr_t>(yr) & 15u) == 0;
-#pragma unroll 2
-        for (int q = tid; q < nvec; q += kGresCompute) {
-          const int e = 4 * q;
-          const float4 v4 = (sg.h == 0 && e + 3 < sg.nmid)
-                                ? sb[q]
-                                : make_float4(slice_elem(sm, xg, sg, e, len),
-                                              slice_elem(sm, xg, sg, e + 1, len),
-                                              slice_elem(sm, xg, sg, e + 2, len),
-                                              slice_elem(sm, xg, sg, e + 3, len));
+        const float* xrow = x + orow * ldx;
+        float* yrow = y + orow * ldy;
+        const SliceGeom sg = unal_geom(xrow, cols, prank, P, slice);
+        float* ym = yrow + sg.a;
+        const bool yv = (reinterpret_cast<uintptr_t>(ym) & 15u) == 0;
+        const int nq = sg.nmid >> 2;
+#pragma unroll 4
+        for (int q = tid; q < nq; q += kGresCompute) {
+          const float4 v4 = sb[q];
           const float2 a = scale2<MODE>(sexp2<MODE>(v4.x, v4.y, M), rcp);
           const float2 c = scale2<MODE>(sexp2<MODE>(v4.z, v4.w, M), rcp);
-          if (yv && e + 3 < len) {
-            st_stream4(yr + e, make_float4(a.x, a.y, c.x, c.y));
+          if (yv) {
+            st_stream4(ym + 4 * q, make_float4(a.x, a.y, c.x, c.y));
           } else {
-            const float o[4] = {a.x, a.y, c.x, c.y};
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              if (e + i < len) st_stream1(yr + e + i, o[i]);
+            st_stream1(ym + 4 * q, a.x);
+            st_stream1(ym + 4 * q + 1, a.y);
+            st_stream1(ym + 4 * q + 2, c.x);
+            st_stream1(ym + 4 * q + 3, c.y);
           }
+        }
+        // head (CTA 0) and tail (last CTA): <= 3 floats each, from global
+        if (tid < sg.hd) {
+          const int64_t col = sg.a - sg.hd + tid;
+          st_stream1(yrow + col, scale1<MODE>(sexp1<MODE>(__ldg(xrow + col), M), rcp));
+        } else if (tid >= 32 && tid < 32 + sg.tl) {
+          const int64_t col = sg.a + sg.nmid + (tid - 32);
+          st_stream1(yrow + col, scale1<MODE>(sexp1<MODE>(__ldg(xrow + col), M), rcp));
         }
       } else {
 #pragma unroll 4
@@ -377,43 +390,36 @@ __global__ void __launch_bounds__(kGresBlock, 1)
     for (int64_t row = g; row < rows; row += G, ++k) {
       const int stage = static_cast<int>(k % unsigned(nstages));
       mbar_wait(&bars[stage], (k / unsigned(nstages)) & 1u);
-      const float* sm = stage_buf + size_t(stage) * slice;
-      const float4* sb = reinterpret_cast<const float4*>(sm);
-      const float* xg = x + row * ldx + c0;
-      const SliceGeom sg = UNAL ? slice_geom(xg, len) : SliceGeom{0, len};
-      // logical group q of the slice (aligned: straight from the staged row)
-      auto group = [&](int q) -> float4 {
-        if constexpr (UNAL) {
-          const int e = 4 * q;
-          if (!(sg.h == 0 && e + 3 < sg.nmid))
-            return make_float4(slice_elem(sm, xg, sg, e, len), slice_elem(sm, xg, sg, e + 1, len),
-                               slice_elem(sm, xg, sg, e + 2, len),
-                               slice_elem(sm, xg, sg, e + 3, len));
-        }
-        return sb[q];
-      };
+      const float4* sb = reinterpret_cast<const float4*>(stage_buf + size_t(stage) * slice);
+      int nq = nvec;  // staged float4 groups
+      SliceGeom sg{0, 0, 0, 0};
+      const float* xrow = x + row * ldx;
+      if constexpr (UNAL) {
+        sg = unal_geom(xrow, cols, prank, P, slice);
+        nq = sg.nmid >> 2;
+      }
+      // head / tail floats (UNAL): threads 0..2 (head) and 32..34 (tail)
+      const bool edge = UNAL && ((tid < sg.hd) || (tid >= 32 && tid < 32 + sg.tl));
+      const float xe = edge ? __ldg(xrow + (tid < 32 ? sg.a - sg.hd + tid : sg.a + sg.nmid + (tid - 32)))
+                            : kPadLogit;
 
-      float mt = kPadLogit;
+      float mt = xe;
       u64 z = f2pk(0.0f, 0.0f);
+      if (edge) z = nf_acc2(z, xe, 0.0f);
 #pragma unroll 4
-      for (int q = tid; q < nvec; q += kGresCompute) {
-        const float4 v4 = group(q);
+      for (int q = tid; q < nq; q += kGresCompute) {
+        const float4 v4 = sb[q];
         mt = fmaxf(mt, fmaxf(fmaxf(v4.x, v4.y), fmaxf(v4.z, v4.w)));
         z = nf_acc2(nf_acc2(z, v4.x, v4.y), v4.z, v4.w);
       }
       if (nf_bad(z)) atomicMin(bad_row, static_cast<unsigned long long>(row));
       const float mw = group_max<32>(mt);  // warp-local max: no CTA barrier
-      u64 acc = f2pk(0.0f, 0.0f);
+      u64 acc = f2pk(edge ? sexp1<MODE>(xe, mw) : 0.0f, 0.0f);
 #pragma unroll 4
-      for (int q = tid; q < nvec; q += kGresCompute) {
-        const float4 v4 = group(q);
-        float2 a = sexp2<MODE>(v4.x, v4.y, mw);
-        float2 c = sexp2<MODE>(v4.z, v4.w, mw);
-        if (UNAL && 4 * q + 3 >= len) {  // padding of the last partial group
-          if (4 * q + 1 >= len) a.y = 0.0f;
-          if (4 * q + 2 >= len) c.x = 0.0f;
-          if (4 * q + 3 >= len) c.y = 0.0f;
-        }
+      for (int q = tid; q < nq; q += kGresCompute) {
+        const float4 v4 = sb[q];
+        const float2 a = sexp2<MODE>(v4.x, v4.y, mw);
+        const float2 c = sexp2<MODE>(v4.z, v4.w, mw);
         acc = f2add(f2add(acc, f2pk(a.x, a.y)), f2pk(c.x, c.y));
       }
       const float2 acc2 = f2up(acc);

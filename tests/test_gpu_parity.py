@@ -370,10 +370,10 @@ def test_rows_at_and_beyond_chip_capacity(C, oracle):
 @pytest.mark.parametrize("rows,C", [(40, 50257), (7, 262147), (3, 1_000_003), (300, 8193),
                                     (13, 20001)])
 def test_k3g_unaligned_rows(rows, C, oracle):
-    """Rows of any length / alignment past one CTA: K3g stages each slice's
-    16-B aligned middle by TMA and reads the <= 3 head / tail floats from
-    global memory -- every mode, ragged last group, clip, unaligned bases and
-    pitches; the bits match the aligned kernel on the same data."""
+    """Rows of any length / alignment past one CTA: K3g cuts each row's
+    slices at x's 16-B boundaries, stages them by TMA and reads the <= 3 head
+    / tail floats from global memory -- every mode, clip, unaligned bases and
+    pitches (y in and out of x's phase), non-finite detection, determinism."""
     from paper_1904_12380_b200 import tensor
 
     x = np.empty((rows, C), np.float32)
@@ -387,10 +387,13 @@ def test_k3g_unaligned_rows(rows, C, oracle):
         y, bad = gu.softmax_abi(x, mode)
         assert bad == gu.NO_BAD
         assert_parity(oracle, y, ref, approx=(mode == 2), what=(rows, C, mode, plan))
-    y0, _ = gu.softmax_abi(x, 0)
-    for xo, yo, ldx, ldy in ((1, 0, C + 3, C + 1), (3, 2, C + 1, C + 6)):
+    ref = oracle.softmax_ref(x)
+    for xo, yo, ldx, ldy in ((1, 0, C + 3, C + 1), (3, 2, C + 1, C + 6), (2, 2, C + 2, C + 2)):
         y, _ = gu.softmax_abi(x, 0, x_offset=xo, y_offset=yo, ldx=ldx, ldy=ldy)
-        assert np.array_equal(y.view(np.uint32), y0.view(np.uint32)), (xo, yo, ldx, ldy)
+        assert_parity(oracle, y, ref, what=(rows, C, xo, yo, ldx, ldy))
+    y1, _ = gu.softmax_abi(x, 0)
+    y2, _ = gu.softmax_abi(x, 0)
+    assert np.array_equal(y1.view(np.uint32), y2.view(np.uint32))
     x2 = x.copy()
     x2[rows // 2, C // 2] = np.nan
     assert gu.softmax_abi(x2, 0)[1] == rows // 2
