@@ -30,13 +30,18 @@ def main():
     p.add_argument("--reps", type=int, default=3)
     p.add_argument("--rows", type=int, default=0, help="use only the first N rows")
     p.add_argument("--mode", type=int, default=0)
+    p.add_argument("--shape", default="", help="RxC: synthetic N(0,4^2) matrix instead of a config")
     args = p.parse_args()
     import os
 
     for kv in os.environ.get("SK_TUNING", "").split():
         k, v = kv.split("=")
         _native.set_tuning(k, int(v))
-    spec = configs.get(args.config)
+    if args.shape:
+        r, c = map(int, args.shape.lower().split("x"))
+        spec = configs.InputSpec(f"shape{r}x{c}", r, c, "normal", 11, sigma=4.0)
+    else:
+        spec = configs.get(args.config)
     rows = args.rows or spec.rows
     x = configs.generate(spec)[:rows] if spec.plant_count else configs.generate(spec, 0, rows)
     xd = torch.from_numpy(x).cuda()
