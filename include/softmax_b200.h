@@ -182,32 +182,30 @@ void sk_free_pinned(void* p);
 
 /*
  * Process-wide tuning / test hooks (not needed for normal use):
- *   "path"           -1 auto, 0 force K1 (rows in registers), 1 force TMA
- *                    segments (K2/K3), 2 force split (K4)
+ *   "path"           -1 auto, 0 force K1 (rows in registers), 1 force the TMA
+ *                    paths (K2 / K3g / K3c), 2 force split (K4), 3 force K1m
  *   "k1_lpr","k1_nv","k1_u"  force a K1 instantiation (lanes per row,
  *                    float4s per lane, rows per lane-group batch)
+ *   "k1_pf", "pdl"   K1 register prefetch (-1 table default), PDL on launches (1)
  *   "vec8"           1: K1 uses 256-bit loads/stores when cols % 8 == 0 and rows
  *                    are 32-B aligned (measured no faster than 128-bit; default 0)
  *   "grid_mult"      K1 grid = SMs * occupancy * grid_mult (default: one row batch
  *                    per warp, i.e. no grid-stride loop)
- *   "seg_len"        target segment length (floats) for K2/K3
- *   "chunk_mb"       K3 re-read distance / row-chunk size in MB (default 24)
- *   "chunk_occ_div"  K3 grid = SMs * occupancy / div (default 2: consecutive
- *                    launches co-reside so STATS(k+1) overlaps NORMALIZE(k-1))
- *   "k3_impl"        long rows: 3 (default) warp-task queue with L2 re-read,
- *                    0 CTA-task queue, 1 smem-resident cooperative, 2 one launch
- *                    per L2-sized row chunk, 4 register-resident warp tasks
- *   "cluster_k3"     1 (default): rows of 8193..~450K floats are held in one
- *                    thread-block cluster (2..16 CTAs, 2-3 stage smem ring per CTA,
- *                    DSMEM push exchange); 0: use "k3_impl"
+ *   "k1m"            1 (default): rows of 1025..8192 floats not taken by K1 go to
+ *                    K1m (WPR warps hold a row in registers); 0: K2 / K4 instead
+ *   "k1m_wpr","k1m_nv"  force a K1m instantiation (warps per row, vectors per thread)
+ *   "k3_impl"        long rows (> 8192): 3 (default) K3g, else K3c; 5 K3c only
+ *   "gres"           K3g: 1 (default) auto, 0 off, 2 force (also for C <= 8192)
+ *   "gres_p","gres_st","gres_split"  force K3g CTAs per row, ring depth (2..5),
+ *                    separate poller warp (-1 auto: depth >= 4)
+ *   "gres_sleep"     K3g poller back-off (ns, default 128)
+ *   "gres_timeout_spins"  polls before a missing peer aborts an exchange (0 = default)
+ *   "gres_diag"      1: K3g waits for its own slot only (timing diagnostic; wrong results)
+ *   "cluster_k3"     1 (default): K3c may serve rows K3g cannot (fallback)
  *   "cluster_size"   force the K3c cluster size (0 = auto: most SMs covered)
  *   "cluster_onex"   1: K3c exchanges one (max, sum) pair per row and recomputes
  *                    exp; 0 (default): two exchanges (max, then sum), exp kept in smem
- *   "claim_batch"    K3 warp queue: 0 (default) static round-robin tasks on a
- *                    cooperative grid, n > 0 tasks claimed n per atomic
- *   "k1_pf", "pdl"   K1 register prefetch (-1 table default), PDL on launches (1)
- *   "seg_align"      1 (default): K3 grid is a whole multiple of the row's
- *                    segment count, so row groups never straddle CTAs
+ *   "cluster_tpb"    K3c threads per CTA (512 default, or 1024)
  *   "host_chunk_kb"  sk_softmax_f32_host chunk size in KiB (0 = auto, ~1/4 of the job)
  *   "host_zero_copy" 1: pinned host buffers with rows <= 8192 are read and written
  *                    by the kernel directly over PCIe (measured no faster than

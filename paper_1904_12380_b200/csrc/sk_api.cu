@@ -19,10 +19,6 @@
 #include "sk_rows.cuh"
 #include "sk_seg.cuh"
 #include "sk_split.cuh"
-#include "sk_chunk.cuh"
-#include "sk_dyn.cuh"
-#include "sk_warp3.cuh"
-#include "sk_reg3.cuh"
 #include "sk_cluster.cuh"
 #include "sk_gres.cuh"
 #include "sk_rows_mw.cuh"
@@ -92,14 +88,8 @@ std::atomic<int> g_k1_pf{-1};      // -1: table default, 0/1 force register pref
 std::atomic<int> g_grid_mult{0};   // K1 grid = SMs x occupancy x mult (0 = one batch per warp)
 std::atomic<int> g_vec8{0};        // 256-bit K1 path (measured no faster: off by default)
 std::atomic<int> g_pdl{1};         // programmatic dependent launch on every kernel
-// K3 alternatives (K3w warp queue and the older designs kept for comparison)
-std::atomic<int> g_seg_len{0};     // K3 segment length (0 = default)
-std::atomic<int> g_seg_align{0};   // K3 grid = whole multiple of nseg (row groups never straddle)
-std::atomic<int> g_chunk_mb{24};   // K3 row-chunk size (MB of input) kept L2 resident
-std::atomic<int> g_chunk_mb_set{0};  // chunk_mb explicitly tuned (overrides the K3 warp lag)
-std::atomic<int> g_chunk_occ_div{2};  // K3 chunk grid = SMs x occupancy / div
-std::atomic<int> g_claim_batch{0};    // K3 warp queue: tasks per atomic claim (0 = static)
-std::atomic<int> g_k3_impl{3};  // 0 CTA queue, 1 smem-resident, 2 chunked, 3 warp queue, 4 registers, 5 cluster only
+// long rows: 3 = K3g, else K3c (default); 5 = K3c only
+std::atomic<int> g_k3_impl{3};
 // K3c (cluster-resident rows)
 std::atomic<int> g_cluster_k3{1};    // allow the cluster kernel (fallback to K3g)
 std::atomic<int> g_cluster_size{0};  // force a K3c cluster size (0 = auto)
@@ -297,40 +287,6 @@ const void* gres_fn(int mode, int nstages, bool split) {
          : nstages == 4 ? gres_fn_l<2, false>(mode) : gres_fn_l<1, false>(mode);
 }
 
-template <int NV>
-const void* reg3_fn(int mode) {
-  switch (mode) {
-    case kClipAccurate: return reinterpret_cast<const void*>(&k3_reg<kClipAccurate, NV>);
-    case kAccurate: return reinterpret_cast<const void*>(&k3_reg<kAccurate, NV>);
-    default: return reinterpret_cast<const void*>(&k3_reg<kApprox, NV>);
-  }
-}
-template <int NV>
-const void* warp3_fn(int mode) {
-  switch (mode) {
-    case kClipAccurate: return reinterpret_cast<const void*>(&k3_warp<kClipAccurate, NV>);
-    case kAccurate: return reinterpret_cast<const void*>(&k3_warp<kAccurate, NV>);
-    default: return reinterpret_cast<const void*>(&k3_warp<kApprox, NV>);
-  }
-}
-constexpr int64_t kWarpSeg = 1024;  // K3 warp task: 32 lanes x 8 float4
-template <int NV>
-const void* dyn_fn(int mode) {
-  switch (mode) {
-    case kClipAccurate: return reinterpret_cast<const void*>(&k3_dyn<kClipAccurate, NV>);
-    case kAccurate: return reinterpret_cast<const void*>(&k3_dyn<kAccurate, NV>);
-    default: return reinterpret_cast<const void*>(&k3_dyn<kApprox, NV>);
-  }
-}
-template <int NV>
-const void* chunk_fn(int mode) {
-  switch (mode) {
-    case kClipAccurate: return reinterpret_cast<const void*>(&k3_chunk<kClipAccurate, NV>);
-    case kAccurate: return reinterpret_cast<const void*>(&k3_chunk<kAccurate, NV>);
-    default: return reinterpret_cast<const void*>(&k3_chunk<kApprox, NV>);
-  }
-}
-constexpr int64_t kChunkSeg = 4096;  // default K3 segment (256 threads x 4 float4)
 constexpr int kSegNV = 4;
 constexpr int kSegMaxThreads = 512;
 constexpr int64_t kSegCap = int64_t(kSegMaxThreads) * kSegNV * 4;  // 8192 floats / CTA
@@ -415,7 +371,7 @@ struct Plan {
   bool unal = false;  // K3g over rows of any alignment
   // seg (K2: nseg == 1; K3: nseg > 1)
   int nseg = 1, seglen = 0, threads = 0, lag = 0;
-  int k3 = 0;  // 0 none/K2, 1 dyn, 2 smem, 3 chunk
+  int k3 = 0;  // 0 K2, 6 K3c (cluster), 7 K3g (grid-resident)
   int64_t chunk_rows = 0;
   size_t smem = 0;
   // split
@@ -658,86 +614,21 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
       }
       if (impl0 == 5) return arg_fail("cluster K3 cannot launch on this device");
     }
-    const bool chunked = cols > kSegCap && impl0 != 1;
-    const bool warp3 = cols > kSegCap && (impl0 == 3 || impl0 == 4);
-    int64_t target = g_seg_len.load() > 0 ? g_seg_len.load() : (chunked ? kChunkSeg : kSegCap);
-    if (warp3)  // warp tasks: 2048 floats (default) or 1024 / 512
-      target = g_seg_len.load() == 1024 ? 1024 : g_seg_len.load() == 512 ? 512 : 2048;
-    target = std::min<int64_t>(target, kSegCap);
-    const int64_t nseg = (cols + target - 1) / target;
-    // warp tasks use fixed-size segments (the last one shorter)
-    const int64_t seglen = warp3 ? target : align_up((cols + nseg - 1) / nseg, 4);
+    if (cols > kSegCap) {
+      if (force >= 0 && impl0 == 5) return arg_fail("cluster K3 cannot launch on this device");
+      return plan_split(rows, cols, p);  // beyond on-chip residency: K4
+    }
+    // K2: one CTA per row, TMA into a 2-stage shared-memory ring (the fallback
+    // for rows <= 8192 when K1/K1m are switched off)
     p.kind = kPathSeg;
-    p.nseg = static_cast<int>(nseg);
-    p.seglen = static_cast<int>(seglen);
-    const int64_t items = rows * nseg;
-    const int impl = g_k3_impl.load();
-    if (nseg > 1 && impl == 4) {
-      // K3 registers: static warp tasks, cooperative
-      p.k3 = 5;
-      p.threads = kReg3Threads;
-      p.smem = 0;
-      const void* fn = seglen == 2048 ? reg3_fn<16>(mode)
-                       : seglen == 512 ? reg3_fn<4>(mode) : reg3_fn<8>(mode);
-      const int occ = occupancy(fn, p.threads, 0);
-      p.grid = int64_t(di.sms) * std::max(occ, 1);
-      const int64_t warps = p.grid * (p.threads / 32);
-      if (!di.coop || occ < 1 || nseg > warps) return plan_split(rows, cols, p);
-      return SK_OK;
-    }
-    if (nseg > 1 && impl == 3) {
-      p.k3 = 4;
-      p.threads = kWarp3Threads;
-      p.smem = 0;
-      const void* fn = seglen == 2048 ? warp3_fn<16>(mode) : warp3_fn<8>(mode);
-      const int occ = occupancy(fn, p.threads, 0);
-      p.grid = int64_t(di.sms) * std::max(occ, 1);
-      // re-read distance: 1.5x the in-flight window (one task per resident warp)
-      // unless chunk_mb overrides it; the window plus the lag stay well inside L2
-      const int64_t window = p.grid * (p.threads / 32) * seglen * 4;
-      int64_t lag_bytes = window * 3 / 2;
-      if (g_chunk_mb_set.load()) lag_bytes = int64_t(std::max(1, g_chunk_mb.load())) << 20;
-      p.chunk_rows = std::min(rows, std::max<int64_t>(1, lag_bytes / (cols * 4)));
-      if (g_claim_batch.load() == 0 && (!di.coop || occ < 1)) return plan_split(rows, cols, p);
-      return SK_OK;
-    }
-    if (nseg > 1 && (impl == 0 || impl == 2)) {
-      p.threads = kChunkThreads;
-      p.smem = 0;
-      const int nv = seglen <= int64_t(kChunkThreads) * 4 * 4 ? 4 : 8;
-      const void* fn = impl == 0 ? (nv == 4 ? dyn_fn<4>(mode) : dyn_fn<8>(mode))
-                                 : (nv == 4 ? chunk_fn<4>(mode) : chunk_fn<8>(mode));
-      const int occ = occupancy(fn, p.threads, 0);
-      const int64_t chunk_bytes = int64_t(std::max(1, g_chunk_mb.load())) << 20;
-      p.chunk_rows = std::max<int64_t>(1, chunk_bytes / (cols * 4));
-      p.chunk_rows = std::min(p.chunk_rows, rows);
-      if (impl == 0) {
-        // K3 dyn: one launch, ordered task queue, lag = chunk_rows rows
-        p.k3 = 1;
-        p.grid = int64_t(di.sms) * std::max(occ, 1);
-      } else {
-        // K3 chunk: one launch per row chunk (+1)
-        p.k3 = 3;
-        const int div = std::max(1, g_chunk_occ_div.load());
-        p.grid = std::max<int64_t>(di.sms, int64_t(di.sms) * std::max(occ, 1) / div);
-      }
-      return SK_OK;  // no co-residency requirement
-    } else {
-      // K2 (nseg == 1) or smem-resident K3: TMA segments into a 2-stage ring
-      if (nseg > 1) p.k3 = 2;
-      int threads = static_cast<int>(align_up((seglen / 4 + kSegNV - 1) / kSegNV, 32));
-      threads = std::max(threads, 64);
-      p.threads = threads;
-      p.smem = size_t(kSegStages) * threads * kSegNV * 4 * sizeof(float);
-      const SegFn fn = seg_fn<kSegNV>(mode);
-      const int occ = occupancy(reinterpret_cast<const void*>(fn), threads, p.smem);
-      p.grid = std::min(items, int64_t(di.sms) * std::max(occ, 1));
-    }
-    if (nseg > 1 && g_seg_align.load() && p.grid >= nseg) p.grid = p.grid / nseg * nseg;
-    if (nseg > 1 && (!di.coop || nseg > p.grid)) {
-      if (force >= 0) return arg_fail("seg path cannot co-schedule this row split");
-      return plan_split(rows, cols, p);  // rows too long to co-schedule
-    }
+    p.nseg = 1;
+    p.seglen = static_cast<int>(align_up(cols, 4));
+    int threads = static_cast<int>(align_up((p.seglen / 4 + kSegNV - 1) / kSegNV, 32));
+    threads = std::max(threads, 64);
+    p.threads = threads;
+    p.smem = size_t(kSegStages) * threads * kSegNV * 4 * sizeof(float);
+    const int occ = occupancy(reinterpret_cast<const void*>(seg_fn<kSegNV>(mode)), threads, p.smem);
+    p.grid = std::min(rows, int64_t(di.sms) * std::max(occ, 1));
     return SK_OK;
   }
   return plan_split(rows, cols, p);
@@ -884,25 +775,7 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
     unsigned* cnt = reinterpret_cast<unsigned*>(ws + l.cnt);
     RowPartial* part = reinterpret_cast<RowPartial*>(ws + l.part);
     const int nseg = p.nseg, seglen = p.seglen;
-    // K3 row counters start at zero every launch (the workspace is shared by
-    // launches of different shapes, so no state is assumed across launches).
-    if (nseg > 1 && p.k3 != 1 && p.k3 != 4 && p.k3 != 5 && p.k3 != 6 && p.k3 != 7) SK_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(unsigned), s));
-    if (p.k3 == 3) {
-      const void* fn = p.seglen <= kChunkThreads * 16 ? chunk_fn<4>(mode) : chunk_fn<8>(mode);
-      float* rmax = reinterpret_cast<float*>(ws + l.rmax);
-      double* rsum = reinterpret_cast<double*>(ws + l.rsum);
-      const int64_t nchunks = (rows + p.chunk_rows - 1) / p.chunk_rows;
-      for (int64_t k = 0; k <= nchunks; ++k) {
-        const int64_t s0 = k * p.chunk_rows;
-        const int64_t sr = k < nchunks ? std::min(p.chunk_rows, rows - s0) : 0;
-        const int64_t n0 = (k - 1) * p.chunk_rows;
-        const int64_t nr = k >= 1 ? std::min(p.chunk_rows, rows - n0) : 0;
-        const int wait_first = k == 0 ? 1 : 0;
-        SK_CUDA(launch_k(fn, dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), 0, s, false, x,
-                         y, cols, ldx, ldy, nseg, seglen, s0, sr, std::max<int64_t>(n0, 0), nr,
-                         wait_first, cnt, part, rmax, rsum, bad, sh));
-      }
-    } else if (p.k3 == 6) {
+    if (p.k3 == 6) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(static_cast<unsigned>(p.grid));
       cfg.blockDim = dim3(p.threads);
@@ -951,39 +824,6 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
       SK_CUDA(launch_k(gres_fn(mode, p.lag, p.threads == kGresBlock, p.unal), dim3(static_cast<unsigned>(p.grid)),
                        dim3(p.threads), p.smem, s, true, x, y, rows, cols, ldx, ldy, P, slice, nst, comm,
                        bad, sh, g_gres_sleep.load(), g_gres_diag.load()));
-    } else if (p.k3 == 5) {
-      const void* fn = p.seglen == 2048 ? reg3_fn<16>(mode)
-                       : p.seglen == 512 ? reg3_fn<4>(mode) : reg3_fn<8>(mode);
-      unsigned* ready = reinterpret_cast<unsigned*>(ws + l.ready);
-      float* rmax = reinterpret_cast<float*>(ws + l.rmax);
-      double* rsum = reinterpret_cast<double*>(ws + l.rsum);
-      SK_CUDA(cudaMemsetAsync(ws + l.ctrl, 0, l.part - l.ctrl, s));
-      SK_CUDA(launch_k(fn, dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), 0, s, true, x, y,
-                       rows, cols, ldx, ldy, nseg, cnt, ready, part, rmax, rsum, bad, sh));
-    } else if (p.k3 == 4) {
-      const void* fn = p.seglen == 2048 ? warp3_fn<16>(mode) : warp3_fn<8>(mode);
-      unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ws + l.ctrl);
-      unsigned* ready = reinterpret_cast<unsigned*>(ws + l.ready);
-      float* rmax = reinterpret_cast<float*>(ws + l.rmax);
-      double* rsum = reinterpret_cast<double*>(ws + l.rsum);
-      SK_CUDA(cudaMemsetAsync(ws + l.ctrl, 0, l.part - l.ctrl, s));
-      const int64_t lag = p.chunk_rows;
-      const int batch = std::max(0, g_claim_batch.load());
-      SK_CUDA(launch_k(fn, dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), 0, s,
-                       batch == 0, x, y, rows, cols, ldx, ldy, nseg, lag, batch, ctr, cnt, ready,
-                       part, rmax, rsum, bad, sh));
-    } else if (p.k3 == 1) {
-      const void* fn = p.seglen <= kChunkThreads * 16 ? dyn_fn<4>(mode) : dyn_fn<8>(mode);
-      unsigned long long* ctr = reinterpret_cast<unsigned long long*>(ws + l.ctrl);
-      unsigned* ready = reinterpret_cast<unsigned*>(ws + l.ready);
-      float* rmax = reinterpret_cast<float*>(ws + l.rmax);
-      double* rsum = reinterpret_cast<double*>(ws + l.rsum);
-      SK_CUDA(cudaMemsetAsync(ws + l.ctrl, 0, l.part - l.ctrl, s));
-      const int64_t lag = p.chunk_rows;
-      const int batch = std::max(1, g_claim_batch.load());
-      SK_CUDA(launch_k(fn, dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), 0, s, false, x, y,
-                       rows, cols, ldx, ldy, nseg, seglen, lag, batch, ctr, cnt, ready, part, rmax,
-                       rsum, bad, sh));
     } else {
       SK_CUDA(launch_k(reinterpret_cast<const void*>(seg_fn<kSegNV>(mode)),
                        dim3(static_cast<unsigned>(p.grid)), dim3(p.threads), p.smem, s, nseg > 1,
@@ -1054,17 +894,9 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "k1_nv") g_k1_nv = value;
   else if (k == "k1_u") g_k1_u = value;
   else if (k == "grid_mult") g_grid_mult = value;
-  else if (k == "seg_len") g_seg_len = value;
   else if (k == "skip_max_shift") g_skip_max_shift = value;
-  else if (k == "seg_align") g_seg_align = value;
   else if (k == "k1_pf") g_k1_pf = value;
   else if (k == "pdl") g_pdl = value;
-  else if (k == "chunk_mb") {
-    g_chunk_mb = value > 0 ? value : 24;
-    g_chunk_mb_set = value > 0;
-  }
-  else if (k == "chunk_occ_div") g_chunk_occ_div = value;
-  else if (k == "claim_batch") g_claim_batch = value;
   else if (k == "host_chunk_kb") g_host_chunk_kb = value;
   else if (k == "host_zero_copy") g_host_zero_copy = value;
   else if (k == "cluster_k3") g_cluster_k3 = value;
@@ -1072,7 +904,10 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "vec8") g_vec8 = value;
   else if (k == "cluster_onex") g_cluster_onex = value;
   else if (k == "cluster_tpb") g_cluster_tpb = value;
-  else if (k == "k3_impl") g_k3_impl = value;
+  else if (k == "k3_impl") {
+    if (value != 3 && value != 5) return arg_fail("k3_impl: 3 (K3g, then K3c) or 5 (K3c only)");
+    g_k3_impl = value;
+  }
   else if (k == "gres") g_gres = value;
   else if (k == "gres_p") g_gres_p = value;
   else if (k == "gres_st") g_gres_st = value;
@@ -1121,13 +956,7 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
     snprintf(buf, buflen, "%s nseg=%d seglen=%d threads=%d smem=%zu chunk_rows=%lld stages=%d grid=%lld",
              p.k3 == 6 ? "k3_cluster"
              : p.k3 == 7 ? (p.unal ? "k3_gres_unal" : "k3_gres")
-             : p.nseg == 1 ? "k2_tma"
-                         : (p.k3 == 1   ? "k3_dyn"
-                            : p.k3 == 3 ? "k3_chunk"
-                            : p.k3 == 4 ? "k3_warp"
-                            : p.k3 == 5 ? "k3_reg"
-                            : p.k3 == 6 ? "k3_cluster"
-                                        : "k3_smem"),
+             : "k2_tma",
              p.nseg, p.seglen,
              p.threads, p.smem, (long long)p.chunk_rows, p.lag, (long long)p.grid);
   else

@@ -41,7 +41,7 @@ def run(x, mode=0, off=0, ld=None):
         print("FAIL", x.shape, mode, off, ld, _native.describe_plan(rows, cols), d)
 
 
-for C in (1, 3, 50, 128, 129, 1000, 1025, 4097, 8192, 8200, 20000, 65537):
+for C in (1, 3, 50, 128, 129, 1000, 1025, 2048, 3072, 4097, 6001, 8192, 8200, 20000, 65537):
     rows = 3 if C > 4096 else 9
     x = np.empty((rows, C), np.float32)
     tensor.fill_normal_array(x, C, 5.0)
@@ -49,15 +49,12 @@ for C in (1, 3, 50, 128, 129, 1000, 1025, 4097, 8192, 8200, 20000, 65537):
         run(x, mode)
     run(x, 0, off=1)
     run(x, 0, ld=C + 5)
-for impl in (0, 1, 2, 3, 4):
+x = np.empty((4, 30000), np.float32)
+tensor.fill_normal_array(x, 7, 5.0)
+for impl in (3, 5):  # K3g, K3c
     _native.set_tuning("k3_impl", impl)
-    x = np.empty((4, 30000), np.float32)
-    tensor.fill_normal_array(x, 7, 5.0)
     run(x)
 _native.set_tuning("k3_impl", 3)
-_native.set_tuning("claim_batch", 4)
-run(x)
-_native.set_tuning("claim_batch", 0)
 _native.set_tuning("path", 2)
 run(x)
 _native.set_tuning("path", -1)

@@ -90,7 +90,6 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--config", default="c2")
     p.add_argument("--reps", type=int, default=200)
-    p.add_argument("--seg-lens", default="1024,2048,4096")
     p.add_argument("--grid-mults", default="1,2")
     p.add_argument("--shape", default="", help="RxC: synthetic N(0,4^2) matrix instead of a config")
     p.add_argument("--gres-ps", default="0,10,12,16,24,37,48,74",
@@ -164,47 +163,25 @@ def main():
         _native.set_tuning("pdl", 0)
         record("default pdl=0", bench_once(xs, ys, rows, cols, args.reps, s))
         _native.set_tuning("pdl", 1)
-        _native.set_tuning("cluster_onex", 1)
-        record("cluster one exchange", bench_once(xs, ys, rows, cols, args.reps, s))
+        resident(record, xs, ys, rows, cols, args, s)
+        _native.set_tuning("k3_impl", 5)  # K3c variants
+        for onex, tpb in ((1, 512), (0, 1024)):
+            _native.set_tuning("cluster_onex", onex)
+            _native.set_tuning("cluster_tpb", tpb)
+            try:
+                record(f"k3_cluster onex={onex} tpb={tpb}", bench_once(xs, ys, rows, cols, args.reps, s))
+            except Exception as e:  # noqa: BLE001
+                print(json.dumps({"variant": f"cluster onex={onex} tpb={tpb}", "error": str(e)}))
         _native.set_tuning("cluster_onex", 0)
-        _native.set_tuning("cluster_tpb", 1024)
-        record("cluster 1024 threads", bench_once(xs, ys, rows, cols, args.reps, s))
         _native.set_tuning("cluster_tpb", 512)
-        for csz in (16, 14, 12, 10, 9, 8):
+        for csz in (16, 12, 10, 8):
             _native.set_tuning("cluster_size", csz)
             try:
-                record(f"cluster size {csz}", bench_once(xs, ys, rows, cols, args.reps, s))
+                record(f"k3_cluster size {csz}", bench_once(xs, ys, rows, cols, args.reps, s))
             except Exception as e:  # noqa: BLE001
                 print(json.dumps({"variant": f"cluster {csz}", "error": str(e)}))
         _native.set_tuning("cluster_size", 0)
-        _native.set_tuning("cluster_k3", 0)
-        record("k3_warp (cluster off)", bench_once(xs, ys, rows, cols, args.reps, s))
-        _native.set_tuning("pdl", 0)
-        _native.set_tuning("cluster_k3", 1)
-        record("cluster pdl=0", bench_once(xs, ys, rows, cols, args.reps, s))
-        _native.set_tuning("pdl", 1)
-        for impl, mbs, sls, bs in ((3, (0,), (2048,), (0, 4)),):
-            _native.set_tuning("k3_impl", impl)
-            _native.set_tuning("cluster_k3", 0)
-            for b in bs:
-                _native.set_tuning("claim_batch", b)
-                for mb in mbs:
-                    _native.set_tuning("chunk_mb", mb)
-                    for sl in sls:
-                        _native.set_tuning("seg_len", sl)
-                        record(f"k3 impl={impl} seg_len={sl} chunk_mb={mb} batch={b}",
-                               bench_once(xs, ys, rows, cols, args.reps, s))
-        _native.set_tuning("claim_batch", 0)
-        _native.set_tuning("chunk_mb", 0)
-        _native.set_tuning("cluster_k3", 1)
-        _native.set_tuning("k3_impl", 1)
-        _native.set_tuning("cluster_k3", 0)
-        record("k3_smem", bench_once(xs, ys, rows, cols, args.reps, s))
         _native.set_tuning("k3_impl", 3)
-        _native.set_tuning("cluster_k3", 1)
-        _native.set_tuning("path", 2)
-        record("split(k4)", bench_once(xs, ys, rows, cols, max(10, args.reps // 4), s))
-        _native.set_tuning("path", -1)
     # our own streaming copy kernel of the same bytes, several grid sizes
     L = _native.lib()
     for blocks in (0, 592, 1184, 2368, 4736):

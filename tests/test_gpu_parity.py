@@ -29,8 +29,8 @@ def assert_parity(oracle, y, ref, approx=False, what=""):
 @pytest.fixture(autouse=True)
 def _reset_tuning():
     yield
-    for k, v in (("path", -1), ("k1_lpr", 0), ("grid_mult", 0), ("seg_len", 0),
-                 ("skip_max_shift", 0), ("k3_impl", 3), ("cluster_k3", 1), ("chunk_mb", 0),
+    for k, v in (("path", -1), ("k1_lpr", 0), ("grid_mult", 0),
+                 ("skip_max_shift", 0), ("k3_impl", 3), ("cluster_k3", 1),
                  ("gres", 1), ("gres_p", 0), ("gres_st", 0), ("gres_split", -1), ("cluster_onex", 0), ("k1m", 1),
                  ("k1m_wpr", 0), ("k1m_nv", 0)):
         _native.set_tuning(k, v)
@@ -262,40 +262,34 @@ def test_k1m_instantiations_and_k2_fallback(oracle):
             _native.set_tuning("k1m_nv", 0)
 
 
-@pytest.mark.parametrize("impl", [0, 1, 2, 3, "3b", 4, 5, "5x2", "g"])
-def test_every_k3_implementation(impl, oracle):
-    """Long-row kernels: ordered CTA queue (0), smem-resident cooperative (1),
-    per-chunk launches (2), ordered warp queue (3) -- all against the oracle,
-    on a ragged width (last segment partial) and several chunk sizes."""
+@pytest.mark.parametrize("impl", ["g", "c", "c1x", "split"])
+def test_every_long_row_kernel(impl, oracle):
+    """Long-row kernels on the same ragged rows (last slice partial, clip
+    firing): K3g grid-resident rows (g), K3c cluster-resident rows with two
+    exchanges (c) or one (c1x), and the split path (K4) -- all against the
+    oracle."""
     x = configs.generate("c4", 0, 40)[:, :200_004].copy()
     x[3, 777] = -500.0
     ref = oracle.softmax_ref(x)
-    if impl == "3b":  # warp queue with batched atomic claims instead of static tasks
-        impl = 3
-        _native.set_tuning("claim_batch", 4)
-    if impl == "5x2":  # cluster kernel with the one-exchange schedule
-        impl = 5
-        _native.set_tuning("cluster_onex", 1)
-    if impl == "g":  # grid-resident rows, global-memory exchange
-        impl = 3
-        _native.set_tuning("gres", 2)
-    else:
-        _native.set_tuning("gres", 0)
-    _native.set_tuning("cluster_k3", 1 if impl == 5 else 0)
-    _native.set_tuning("k3_impl", impl)
     try:
-        for mb in (1, 3, 0):
-            _native.set_tuning("chunk_mb", mb)
-            y, bad = gu.softmax_abi(x, 0)
-            assert bad == gu.NO_BAD
-            assert_parity(oracle, y, ref, what=(impl, mb, gu.plan(*x.shape)))
+        if impl == "g":
+            _native.set_tuning("gres", 2)
+        elif impl in ("c", "c1x"):
+            _native.set_tuning("k3_impl", 5)
+            _native.set_tuning("cluster_onex", 1 if impl == "c1x" else 0)
+        else:
+            _native.set_tuning("path", 2)
+        plan = gu.plan(*x.shape)
+        assert plan.split()[0] == {"g": "k3_gres", "c": "k3_cluster", "c1x": "k3_cluster",
+                                   "split": "k4_split"}[impl], plan
+        y, bad = gu.softmax_abi(x, 0)
+        assert bad == gu.NO_BAD
+        assert_parity(oracle, y, ref, what=(impl, plan))
     finally:
-        _native.set_tuning("claim_batch", 0)
-        _native.set_tuning("cluster_onex", 0)
         _native.set_tuning("gres", 1)
-        _native.set_tuning("cluster_k3", 1)
         _native.set_tuning("k3_impl", 3)
-        _native.set_tuning("chunk_mb", 0)
+        _native.set_tuning("cluster_onex", 0)
+        _native.set_tuning("path", -1)
 
 
 @pytest.mark.parametrize("P,st,split", [(2, 0, -1), (3, 2, 1), (10, 0, 1), (14, 3, -1), (14, 3, 1),
@@ -397,15 +391,6 @@ def test_k3g_unaligned_rows(rows, C, oracle):
     x2 = x.copy()
     x2[rows // 2, C // 2] = np.nan
     assert gu.softmax_abi(x2, 0)[1] == rows // 2
-
-
-def test_seg_lengths_all_agree(oracle):
-    x = configs.generate("c4", 0, 4)[:, :100000].copy()
-    ref = oracle.softmax_ref(x)
-    for sl in (2048, 4096, 8192):
-        _native.set_tuning("seg_len", sl)
-        y, _ = gu.softmax_abi(x, 0)
-        assert_parity(oracle, y, ref, what=sl)
 
 
 # ---------------------------------------------------------------- errors / faults
