@@ -473,6 +473,20 @@ GresChoice plan_gres(int64_t rows, int64_t cols, int mode, const DevInfo& di, in
   return best;
 }
 
+// Single-device K3g plan: a function of the row length alone (row blocks
+// keep their bits) -- unless that plan would leave more than half the SMs
+// idle (rows x P < SMs / 2: decode-sized batches over wide vocabularies),
+// where latency matters more and the plan is modelled at the actual row count
+// (8 x 50257: P 3 -> 18).  Row-sharded jobs above that size keep C-only plans.
+GresChoice plan_gres_for(int64_t rows, int64_t cols, int mode, const DevInfo& di, bool unal) {
+  GresChoice gc = plan_gres(kGresPlanRows, cols, mode, di, 1, 1, unal);
+  if (gc.P > 0 && rows * gc.P * 2 < di.sms) {
+    const GresChoice gl = plan_gres(rows, cols, mode, di, 1, 1, unal);
+    if (gl.P > 0) gc = gl;
+  }
+  return gc;
+}
+
 int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa, uint64_t ya,
               int mode, int dev, Plan& p) {
   const DevInfo di = dev_info(dev);
@@ -495,7 +509,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
       di.coop) {
     // rows of any alignment too long for one CTA: K3g with TMA on each slice's
     // aligned middle (1.7x the split path's 12 B/element on a 50257-wide vocab)
-    const GresChoice gc = plan_gres(kGresPlanRows, cols, mode, di, 1, 1, true);
+    const GresChoice gc = plan_gres_for(rows, cols, mode, di, true);
     if (gc.P > 0) {
       p.kind = kPathSeg;
       p.k3 = 7;
@@ -559,8 +573,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     const int gres = g_gres.load();
     if ((cols > kSegCap || gres == 2) && (impl0 == 5 || impl0 == 3)) {
       GresChoice gc;
-      if (gres != 0 && impl0 != 5 && di.coop)
-        gc = plan_gres(kGresPlanRows, cols, mode, di, 1, 1, false);
+      if (gres != 0 && impl0 != 5 && di.coop) gc = plan_gres_for(rows, cols, mode, di, false);
       if (gc.P > 0) {
         p.kind = kPathSeg;
         p.k3 = 7;

@@ -1,0 +1,38 @@
+#!/usr/bin/env python
+"""LLM-style shapes (batch x vocabulary): default plan, latency per call and
+effective GB/s, against this library's copy kernel of the same bytes."""
+
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "scripts"))
+
+import torch  # noqa: E402
+
+from paper_1904_12380_b200 import _native, configs  # noqa: E402
+from row_length_sweep import copy_us  # noqa: E402
+from sweep import bench_once  # noqa: E402
+
+
+def main():
+    s = torch.cuda.Stream()
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    for rows, C in ((1, 32000), (8, 50257), (32, 151936), (64, 128256), (256, 32000),
+                    (1024, 50257), (4096, 32000), (4096, 128256)):
+        spec = configs.InputSpec(f"v{rows}x{C}", rows, C, "normal", 5, sigma=3.0)
+        x0 = torch.from_numpy(configs.generate(spec)).cuda()
+        R = max(2, -(-3 * l2 // (8 * rows * C)))
+        xs = [x0] + [x0.clone() for _ in range(R - 1)]
+        ys = [torch.empty_like(x0) for _ in range(R)]
+        us = bench_once(xs, ys, rows, C, 200, s)
+        cu = copy_us(xs, ys, rows * C, 20, s)
+        print(json.dumps({"rows": rows, "cols": C, "plan": _native.describe_plan(rows, C)[:40],
+                          "us": round(us, 2), "gbs": round(8.0 * rows * C / us / 1e3),
+                          "copy_us": round(cu, 2), "vs_copy": round(cu / us, 3)}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -431,6 +431,24 @@ def test_skip_max_shift_fault_is_caught(oracle):
 
 
 # ---------------------------------------------------------------- invariants
+@pytest.mark.parametrize("rows,C", [(1, 32000), (8, 50257), (3, 262144), (5, 1_048_576)])
+def test_small_batches_wide_rows(rows, C, oracle):
+    """Decode-sized batches over wide rows: the K3g plan is re-modelled at the
+    actual row count (more CTAs per row) when the row-length-only plan would
+    leave most SMs idle -- still matching the oracle."""
+    from paper_1904_12380_b200 import tensor
+
+    x = np.empty((rows, C), np.float32)
+    tensor.fill_normal_array(x, C + 17 * rows, 3.0)
+    x[0, C // 3] = 25.0
+    plan = gu.plan(rows, C)
+    assert plan.startswith("k3_gres"), plan
+    for mode in (0, 1):
+        y, bad = gu.softmax_abi(x, mode)
+        assert bad == gu.NO_BAD
+        assert_parity(oracle, y, oracle.softmax_ref(x, clip=(mode == 0)), what=(rows, C, plan))
+
+
 def test_shift_invariance_and_order():
     x = configs.generate("c3", 0, None)[:256]
     base, _ = gu.softmax_abi(x)
@@ -458,10 +476,11 @@ def test_deterministic_and_row_shard_bitwise():
         b, _ = gu.softmax_abi(x[split:])
         assert np.array_equal(np.concatenate([a, b]).view(np.uint32), y1.view(np.uint32))
     spec = configs.get("c4")
-    x = configs.generate(spec, 0, 16)
+    x = configs.generate(spec, 0, 24)
     y, _ = gu.softmax_abi(x)
-    a, _ = gu.softmax_abi(x[5:9])
-    assert np.array_equal(a.view(np.uint32), y[5:9].view(np.uint32))
+    a, _ = gu.softmax_abi(x[5:17])  # 12 rows: still the row-length-only plan
+    assert gu.plan(12, spec.cols) == gu.plan(24, spec.cols)
+    assert np.array_equal(a.view(np.uint32), y[5:17].view(np.uint32))
 
 
 def test_host_path_equals_device_path():
