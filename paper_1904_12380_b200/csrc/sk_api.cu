@@ -473,17 +473,18 @@ GresChoice plan_gres(int64_t rows, int64_t cols, int mode, const DevInfo& di, in
   return best;
 }
 
-// Single-device K3g plan: a function of the row length alone (row blocks
-// keep their bits) -- unless that plan would leave more than half the SMs
-// idle (rows x P < SMs / 2: decode-sized batches over wide vocabularies),
-// where latency matters more and the plan is modelled at the actual row count
-// (8 x 50257: P 3 -> 18).  Row-sharded jobs above that size keep C-only plans.
-GresChoice plan_gres_for(int64_t rows, int64_t cols, int mode, const DevInfo& di, bool unal) {
-  GresChoice gc = plan_gres(kGresPlanRows, cols, mode, di, 1, 1, unal);
-  if (gc.P > 0 && rows * gc.P * 2 < di.sms) {
-    const GresChoice gl = plan_gres(rows, cols, mode, di, 1, 1, unal);
-    if (gl.P > 0) gc = gl;
-  }
+// Single-device K3g plan: a function of the row length alone, so row blocks
+// keep their bits.  K3g's per-CTA pipeline needs a few row steps to amortise
+// its fill (first slice in flight), its exchange round trip and its launch
+// (cooperative, no PDL): with <= 3 row steps per group (decode-sized batches
+// over wide rows) the caller is told to take the latency path instead --
+// measured: 1 x 32000 K3c 3.45 us vs K3g 6.18; 32 x 151936 split 14.3 vs
+// K3g 15.6; 8 x 50257 split 7.0 vs 8.3.  Larger jobs (c4 row-sharded 8 ways:
+// 64 rows, 7 steps) keep the C-only plan.
+GresChoice plan_gres_for(int64_t rows, int64_t cols, int mode, const DevInfo& di, bool unal,
+                         bool* latency) {
+  const GresChoice gc = plan_gres(kGresPlanRows, cols, mode, di, 1, 1, unal);
+  *latency = gc.P > 0 && g_gres.load() != 2 && (rows + gc.groups - 1) / gc.groups <= 3;
   return gc;
 }
 
@@ -509,8 +510,9 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
       di.coop) {
     // rows of any alignment too long for one CTA: K3g with TMA on each slice's
     // aligned middle (1.7x the split path's 12 B/element on a 50257-wide vocab)
-    const GresChoice gc = plan_gres_for(rows, cols, mode, di, true);
-    if (gc.P > 0) {
+    bool latency = false;
+    const GresChoice gc = plan_gres_for(rows, cols, mode, di, true, &latency);
+    if (gc.P > 0 && !latency) {
       p.kind = kPathSeg;
       p.k3 = 7;
       p.unal = true;
@@ -573,8 +575,10 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     const int gres = g_gres.load();
     if ((cols > kSegCap || gres == 2) && (impl0 == 5 || impl0 == 3)) {
       GresChoice gc;
-      if (gres != 0 && impl0 != 5 && di.coop) gc = plan_gres_for(rows, cols, mode, di, false);
-      if (gc.P > 0) {
+      bool latency = false;
+      if (gres != 0 && impl0 != 5 && di.coop) gc = plan_gres_for(rows, cols, mode, di, false, &latency);
+      if (latency && rows > 2) return plan_split(rows, cols, p);
+      if (gc.P > 0 && !latency) {
         p.kind = kPathSeg;
         p.k3 = 7;
         p.nseg = gc.P;

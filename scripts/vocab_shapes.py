@@ -27,11 +27,23 @@ def main():
         R = max(2, -(-3 * l2 // (8 * rows * C)))
         xs = [x0] + [x0.clone() for _ in range(R - 1)]
         ys = [torch.empty_like(x0) for _ in range(R)]
-        us = bench_once(xs, ys, rows, C, 200, s)
         cu = copy_us(xs, ys, rows * C, 20, s)
-        print(json.dumps({"rows": rows, "cols": C, "plan": _native.describe_plan(rows, C)[:40],
-                          "us": round(us, 2), "gbs": round(8.0 * rows * C / us / 1e3),
-                          "copy_us": round(cu, 2), "vs_copy": round(cu / us, 3)}), flush=True)
+        variants = [("default", {})] + ([("k3c", {"k3_impl": 5}), ("split", {"path": 2})]
+                                        if len(sys.argv) > 1 else [])
+        for tag, tun in variants:
+            for k, v in tun.items():
+                _native.set_tuning(k, v)
+            try:
+                us = bench_once(xs, ys, rows, C, 200, s)
+                print(json.dumps({"rows": rows, "cols": C, "variant": tag,
+                                  "plan": _native.describe_plan(rows, C)[:40],
+                                  "us": round(us, 2), "gbs": round(8.0 * rows * C / us / 1e3),
+                                  "copy_us": round(cu, 2), "vs_copy": round(cu / us, 3)}),
+                      flush=True)
+            except Exception as e:  # noqa: BLE001
+                print(json.dumps({"rows": rows, "cols": C, "variant": tag, "error": str(e)[:80]}))
+            _native.set_tuning("k3_impl", 3)
+            _native.set_tuning("path", -1)
 
 
 if __name__ == "__main__":

@@ -348,21 +348,26 @@ def test_k3_gres_full_c4_rowsums():
 def test_rows_at_and_beyond_chip_capacity(C, oracle):
     """4 M floats: K3g at its largest group (148 CTAs, 2-stage ring).  Longer
     rows than the chip's shared memory holds (> 148 x 225 KB / 2 stages) fall
-    back to the warp queue / split path; all match the oracle."""
+    back to the split path; all match the oracle."""
     from paper_1904_12380_b200 import tensor
 
     x = np.empty((3, C), np.float32)
     tensor.fill_normal_array(x, 17, 3.0)
     x[1, C // 3] = -400.0
-    plan = gu.plan(3, C)
-    assert ("k3_gres" in plan) == (C <= 148 * 28_800), plan
-    y, bad = gu.softmax_abi(x, 0)
+    fits = C <= 148 * 28_800
+    _native.set_tuning("gres", 2 if fits else 1)  # 3 rows alone would take the latency path
+    try:
+        plan = gu.plan(3, C)
+        assert ("k3_gres" in plan) == fits, plan
+        y, bad = gu.softmax_abi(x, 0)
+    finally:
+        _native.set_tuning("gres", 1)
     assert bad == gu.NO_BAD
     assert_parity(oracle, y, oracle.softmax_ref(x, True, nthreads=0), what=plan)
 
 
-@pytest.mark.parametrize("rows,C", [(40, 50257), (7, 262147), (3, 1_000_003), (300, 8193),
-                                    (13, 20001)])
+@pytest.mark.parametrize("rows,C", [(200, 50257), (40, 262147), (8, 1_000_003), (600, 8193),
+                                    (300, 20001)])
 def test_k3g_unaligned_rows(rows, C, oracle):
     """Rows of any length / alignment past one CTA: K3g cuts each row's
     slices at x's 16-B boundaries, stages them by TMA and reads the <= 3 head
@@ -431,18 +436,20 @@ def test_skip_max_shift_fault_is_caught(oracle):
 
 
 # ---------------------------------------------------------------- invariants
-@pytest.mark.parametrize("rows,C", [(1, 32000), (8, 50257), (3, 262144), (5, 1_048_576)])
-def test_small_batches_wide_rows(rows, C, oracle):
-    """Decode-sized batches over wide rows: the K3g plan is re-modelled at the
-    actual row count (more CTAs per row) when the row-length-only plan would
-    leave most SMs idle -- still matching the oracle."""
+@pytest.mark.parametrize("rows,C,kind", [(1, 32000, "k3_cluster"), (8, 50257, "k4_split"),
+                                         (3, 262144, "k4_split"), (2, 65536, "k3_cluster"),
+                                         (32, 151936, "k4_split"), (512, 262144, "k3_gres")])
+def test_small_batches_wide_rows(rows, C, kind, oracle):
+    """Decode-sized batches over wide rows: with <= 3 row steps per K3g group
+    the latency path is taken (cluster kernel for 1-2 rows, split otherwise);
+    larger jobs keep K3g -- all matching the oracle."""
     from paper_1904_12380_b200 import tensor
 
     x = np.empty((rows, C), np.float32)
     tensor.fill_normal_array(x, C + 17 * rows, 3.0)
     x[0, C // 3] = 25.0
     plan = gu.plan(rows, C)
-    assert plan.startswith("k3_gres"), plan
+    assert plan.startswith(kind), plan
     for mode in (0, 1):
         y, bad = gu.softmax_abi(x, mode)
         assert bad == gu.NO_BAD
