@@ -483,11 +483,12 @@ def test_deterministic_and_row_shard_bitwise():
         b, _ = gu.softmax_abi(x[split:])
         assert np.array_equal(np.concatenate([a, b]).view(np.uint32), y1.view(np.uint32))
     spec = configs.get("c4")
-    x = configs.generate(spec, 0, 24)
+    x = configs.generate(spec, 0, 64)  # c4 sharded 8 ways
     y, _ = gu.softmax_abi(x)
-    a, _ = gu.softmax_abi(x[5:17])  # 12 rows: still the row-length-only plan
-    assert gu.plan(12, spec.cols) == gu.plan(24, spec.cols)
-    assert np.array_equal(a.view(np.uint32), y[5:17].view(np.uint32))
+    a, _ = gu.softmax_abi(x[5:45])  # a 40-row block: same (row-length-only) plan
+    assert gu.plan(40, spec.cols).split(" grid=")[0] == gu.plan(64, spec.cols).split(" grid=")[0]
+    assert gu.plan(40, spec.cols).startswith("k3_gres")
+    assert np.array_equal(a.view(np.uint32), y[5:45].view(np.uint32))
 
 
 def test_host_path_equals_device_path():
