@@ -8,25 +8,23 @@
 // CTA `rank` of the group holds columns [rank*W, (rank+1)*W) of the row in
 // shared memory (TMA ring of NS stages, like K3c).
 //
-// One exchange per row, overlapped with the next row.  Each compute warp
+// One exchange per row, overlapped with the next rows.  Each compute warp
 // reduces its share of the slice to a pair (m_w, s_w = sum exp(clip(x - m_w)))
-// without any CTA barrier; the exchange warp merges the 16 pairs into the CTA
-// pair (fixed order, s_w scaled by exp(m_w - m)) and publishes it as one
-// sequence-tagged 16-B slot of the group's slot array (one relaxed store: no
-// counter, no release fence); it then polls the P slots -- the poll returns
-// the data itself -- and merges the pairs in rank order, so M and S are
-// bit-identical in every CTA of the row.  Meanwhile the compute warps already run row k+1's local pass;
-// only then do they write row k: y = exp(clip(x - M)) * (1/(float)S), the exp
-// recomputed against the GLOBAL max from the untouched slice (reference order,
-// kernels.py:144-188).  The group round trip (store to L2 + one polling
-// load) therefore hides behind a full row step instead of stalling it.  Slots alternate by
-// row parity (a CTA can run at most one exchange ahead of its group).
+// without any CTA barrier; the publisher warp merges the 16 pairs into the
+// CTA pair (fixed order, s_w scaled by exp(m_w - m)) and stores it as one
+// epoch-tagged 16-B slot of the group's slot array (one relaxed store: no
+// counter, no release fence, no per-launch memset); a poller polls the P slots
+// -- the poll returns the data itself -- and merges them in rank order, so M
+// and S are bit-identical in every CTA of the row.  Meanwhile the compute
+// warps run the local passes of the next rows; row k is written L rows later,
+// y = exp(clip(x - M)) * (1/(float)S), the exp recomputed against the GLOBAL
+// max from the untouched slice (reference order, kernels.py:144-188).
 //
-// Warp specialisation keeps the handshake off the data path: warp 16 merges
-// and publishes each row's CTA pair and issues the TMA refills, warp 17 polls
-// and merges the group's pairs -- so a slow poll never delays this CTA's next
-// publication (which would chain the group into a per-row convoy), and no
-// fence ever waits on the compute warps' output stores.  Named barriers:
+// Roles: warps 0-15 compute; warp 16 publishes and issues the TMA refills; at
+// lag 1 (ring depth 2-3) warp 16 also polls right after publishing, at lag >= 2
+// (depth 4-5) warp 17 polls, so a slow poll never delays the next publication
+// (which would chain the group into a per-row convoy).  No fence ever waits on
+// the compute warps' output stores.  Named barriers:
 //   bar1  compute -> publisher  "warp pairs of row k in smem"
 //   bar2  poller -> compute     "(M, S) of row k in smem"
 //   bar3  compute -> publisher  "row k's stage consumed (proxy-fenced): refill"
