@@ -88,6 +88,7 @@ std::atomic<int> g_k1_pf{-1};      // -1: table default, 0/1 force register pref
 std::atomic<int> g_grid_mult{0};   // K1 grid = SMs x occupancy x mult (0 = one batch per warp)
 std::atomic<int> g_vec8{0};        // 256-bit K1 path (measured no faster: off by default)
 std::atomic<int> g_pdl{1};         // programmatic dependent launch on every kernel
+std::atomic<int> g_coop_pdl{0};    // ... also on cooperative launches (K3g)
 // long rows: 3 = K3g, else K3c (default); 5 = K3c only
 std::atomic<int> g_k3_impl{3};
 // K3c (cluster-resident rows)
@@ -932,6 +933,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "gres_sleep") g_gres_sleep = value;
   else if (k == "gres_split") g_gres_split = value;
   else if (k == "k1m") g_k1m = value;
+  else if (k == "coop_pdl") g_coop_pdl = value;
   else if (k == "k1m_wpr") g_k1m_wpr = value;
   else if (k == "k1m_nv") g_k1m_nv = value;
   else if (k == "gres_timeout_spins") g_gres_spins = value > 0 ? unsigned(value) : kGresSpinLimit;

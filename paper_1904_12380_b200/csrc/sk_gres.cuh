@@ -202,10 +202,12 @@ __global__ void __launch_bounds__(kGresBlock, 1)
   if (tid == 0) {
     for (int s = 0; s < nstages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
-    epoch_s = ld_relaxed_u32(comm.ctl);
   }
   __syncthreads();
-  pdl_wait();
+  pdl_wait();  // (PDL only) the previous launch's epoch advance is visible after this
+  if (tid == 0) epoch_s = ld_relaxed_u32(comm.ctl);
+  __syncthreads();
+  pdl_launch_dependents();
   const unsigned epoch = epoch_s;
 
   // slot array layout: [epoch parity][group][NS sets][WP] x 16 B.  The epoch

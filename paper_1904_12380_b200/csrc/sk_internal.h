@@ -35,7 +35,8 @@ int check_common(const float* x, const void* y, int64_t rows, int64_t cols, int6
 inline constexpr int64_t kOneCtaRowMax = 8192;
 
 // tuning knobs read outside sk_api.cu (sk_set_tuning writes them)
-extern std::atomic<int> g_pdl, g_gres_sleep, g_gres_diag, g_host_chunk_kb, g_host_zero_copy;
+extern std::atomic<int> g_pdl, g_coop_pdl, g_gres_sleep, g_gres_diag, g_host_chunk_kb,
+    g_host_zero_copy;
 extern std::atomic<unsigned> g_gres_spins;
 
 // Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.
@@ -54,7 +55,8 @@ cudaError_t launch_k(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStr
     attr[n].id = cudaLaunchAttributeCooperative;
     attr[n].val.cooperative = 1;
     ++n;
-  } else if (g_pdl.load()) {
+  }
+  if ((!coop || g_coop_pdl.load()) && g_pdl.load()) {
     attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[n].val.programmaticStreamSerializationAllowed = 1;
     ++n;
