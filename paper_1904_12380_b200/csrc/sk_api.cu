@@ -88,7 +88,7 @@ std::atomic<int> g_k1_pf{-1};      // -1: table default, 0/1 force register pref
 std::atomic<int> g_grid_mult{0};   // K1 grid = SMs x occupancy x mult (0 = one batch per warp)
 std::atomic<int> g_vec8{0};        // 256-bit K1 path (measured no faster: off by default)
 std::atomic<int> g_pdl{1};         // programmatic dependent launch on every kernel
-std::atomic<int> g_coop_pdl{0};    // ... also on cooperative launches (K3g)
+std::atomic<int> g_coop_pdl{1};    // ... also on cooperative launches (K3g; measured -0.6..1.3 us/launch)
 // long rows: 3 = K3g, else K3c (default); 5 = K3c only
 std::atomic<int> g_k3_impl{3};
 // K3c (cluster-resident rows)
