@@ -55,6 +55,10 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graph", action="store_true")
+    p.add_argument("--colshard", action="store_true",
+                   help="column-sharded run (config c5b's mode): each of N ranks owns C/N "
+                        "columns of every row; one fused kernel per rank with the row-statistics "
+                        "exchange inside it over NVLink peer memory (sharding.FusedColumnShard)")
     return p.parse_args()
 
 
@@ -405,10 +409,144 @@ def run_ours(args):
     return 0
 
 
+def run_colshard(args):
+    """Column-sharded softmax: rank r owns columns [r*C/N, (r+1)*C/N) of every
+    row of the config; each step is ONE fused K3g launch per rank whose CTAs
+    exchange per-row (max, sum) pairs with every rank over NVLink peer memory
+    (sk_colshard_softmax_f32).  Strong scaling over the config's matrix; the
+    timed region is max over ranks as in run_ours."""
+    import torch
+
+    world, rank, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_1904_12380_b200 as sk
+    from paper_1904_12380_b200 import _native, configs, sharding
+
+    spec = configs.get(args.config)
+    if spec.cols % world or (spec.cols // world) % 4:
+        raise SystemExit(f"{spec.name}: {spec.cols} columns do not split into {world} aligned shards")
+    w = spec.cols // world
+    rows = spec.rows
+    x_host = configs.generate_cols(spec, rank * w, w)
+    pair_bytes = 8 * rows * w
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    R = max(2, -(-3 * l2 // pair_bytes))
+    xs = [torch.from_numpy(x_host).to(dev)]
+    xs += [xs[0].clone() for _ in range(R - 1)]
+    ys = [torch.empty_like(xs[0]) for _ in range(R)]
+    fc = sharding.FusedColumnShard()
+    variant = sk.KernelVariant.REFERENCE_CLIPPED
+    stream = torch.cuda.Stream(dev)
+
+    def launch(i):
+        fc(xs[i % R], variant, out=ys[i % R], check_finite=False)
+
+    with torch.cuda.stream(stream):
+        for i in range(max(args.warmup, 3)):
+            launch(i)
+    stream.synchronize()
+    parity = None
+    if rank == 0 and world == 1:
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import oracle
+
+        sel = np.unique(np.linspace(0, rows - 1, 4).astype(int))
+        got = ys[(max(args.warmup, 3) - 1) % R][torch.from_numpy(sel).to(dev)].cpu().numpy()
+        parity = oracle.parity(got, oracle.softmax_ref(x_host[sel], True))
+    graph = None
+    G = R * max(1, 8 // R)
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            with torch.cuda.graph(graph, stream=stream):
+                for i in range(G):
+                    launch(i)
+            graph.replay()
+        stream.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    sampler.mark()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        done = 0
+        if graph is not None:
+            while done + G <= args.steps:
+                graph.replay()
+                done += G
+        while done < args.steps:
+            launch(done)
+            done += 1
+        e1.record(stream)
+    stream.synchronize()
+    sampler.mark()
+    if world > 1:
+        torch.distributed.barrier()
+    t = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(t.item())
+    sampler.stop()
+    # end to end: this rank's shard from pinned host memory, fused kernel, back
+    e2e_steps = max(1, args.e2e_steps)
+    hin = torch.from_numpy(x_host).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        xd = hin.to(dev, non_blocking=True)
+        yd = fc(xd, variant, check_finite=False)
+        hout.copy_(yd, non_blocking=True)
+        torch.cuda.synchronize(dev)
+    te = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
+    if world > 1:
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+    bytes_step = 8.0 * rows * spec.cols  # the whole matrix, all ranks
+    peak, peak_src = peaks()
+    kern_us = ms_max / args.steps * 1e3
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": bytes_step * args.steps / (ms_max / 1e3) / 1e9,
+            "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32",
+            "data": f"synthetic: {spec.describe()}",
+            "config": {"workload": spec.describe(), "rows": rows, "cols_per_gpu": w,
+                       "parallelism": f"column-shard x{world}, fused in-kernel (max, sum) exchange",
+                       "plan": _native.describe_colshard_plan(rows, w, world),
+                       "l2": f"rotating {R} resident buffer pairs vs {l2 >> 20} MiB L2"},
+            "rows_per_s": rows * args.steps / (ms_max / 1e3),
+            "roofline": {"bound": "hbm", "achieved": 8.0 * rows * w / (kern_us * 1e-6) / 1e9,
+                         "peak": peak, "unit": "GB/s",
+                         "frac": 8.0 * rows * w / (kern_us * 1e-6) / 1e9 / peak,
+                         "traffic": None, "peak_source": peak_src, "avg_launch_us": kern_us},
+            "e2e": {"value": bytes_step * e2e_steps / float(te.item()) / 1e9, "unit": "GB/s",
+                    "h2d_bytes_per_step": int(4 * rows * w), "d2h_bytes_per_step": int(4 * rows * w)},
+            "gpu_launches": args.steps, "clocks": sampler.summary(), "parity": parity,
+        }), flush=True)
+    fc.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.colshard:
+        return run_colshard(args)
     return run_ours(args)
 
 

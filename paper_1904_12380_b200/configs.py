@@ -106,6 +106,29 @@ def generate(spec: InputSpec | str, row_start: int = 0, row_count: int | None = 
     return out
 
 
+def generate_cols(spec: InputSpec | str, col_start: int, col_count: int,
+                  out: np.ndarray | None = None, nthreads: int = 0) -> np.ndarray:
+    """Columns ``[col_start, col_start + col_count)`` of every row of the config
+    (a column shard: rank r of N owns columns [r*C/N, (r+1)*C/N)); element
+    (r, c) is element r*C + c of the config's stream, as in ``generate``."""
+    if isinstance(spec, str):
+        spec = get(spec)
+    if spec.plant_count:
+        raise ArgumentError(f"{spec.name}: planted positions need the whole matrix")
+    if col_start < 0 or col_count < 0 or col_start + col_count > spec.cols:
+        raise ArgumentError("column range outside the config")
+    if out is None:
+        out = np.empty((spec.rows, col_count), dtype=np.float32)
+    out = out.reshape(spec.rows, col_count)
+    for r in range(spec.rows):
+        start = r * spec.cols + col_start
+        if spec.dist == "normal":
+            fill_normal_array(out[r], spec.seed, spec.sigma, start, nthreads)
+        else:
+            fill_uniform_array(out[r], spec.seed, spec.low, spec.high, start, nthreads)
+    return out
+
+
 def generate_rows_extended(spec: InputSpec | str, row_start: int, row_count: int,
                            out: np.ndarray | None = None, nthreads: int = 0) -> np.ndarray:
     """Rows of the config's stream beyond ``spec.rows`` (weak scaling: rank r

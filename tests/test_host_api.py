@@ -194,3 +194,14 @@ def test_torch_ops_register_without_a_gpu():
         assert str(op.default._schema) == "softmax_b200::" + schema
     with pytest.raises((NotImplementedError, RuntimeError)):
         ops.softmax_fwd(torch.zeros(2, 3), True)
+
+
+def test_generate_cols_matches_full_rows():
+    """A column shard generated alone equals the same columns of the whole
+    matrix (every rank of a column-sharded run builds its shard independently)."""
+    spec = configs.InputSpec("t", 7, 1000, "normal", 3, sigma=2.0)
+    full = configs.generate(spec)
+    for c0, w in ((0, 250), (250, 250), (333, 1), (999, 1), (1, 998)):
+        assert np.array_equal(configs.generate_cols(spec, c0, w), full[:, c0:c0 + w])
+    u = configs.InputSpec("u", 3, 64, "uniform", 5, low=-1.0, high=1.0)
+    assert np.array_equal(configs.generate_cols(u, 16, 32), configs.generate(u)[:, 16:48])
