@@ -52,3 +52,25 @@ def test_cli_verify_and_bench(capsys):
     assert bench_cli.main(["profile", "--reps", "5", "--batch-size", "8",
                            "--variant", "ReferenceClipped"]) == 0
     assert "Profiling Report" in capsys.readouterr().out
+
+
+def test_bench_colshard_mode():
+    """bench.py --colshard (the fused column shard's benchmark) at world size 1:
+    one JSON line with the contract's keys, parity against the oracle."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--config", "c4", "--colshard",
+                        "--steps", "12", "--warmup", "3", "--e2e-steps", "1"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    for k in ("metric", "value", "unit", "n_gpus", "ms_per_step", "roofline", "e2e",
+              "gpu_launches", "clocks", "config"):
+        assert k in line, k
+    assert line["config"]["plan"].startswith("k3_gres_colshard world=1")
+    assert line["parity"]["ok"], line["parity"]
+    assert line["value"] > 1000
