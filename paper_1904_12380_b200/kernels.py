@@ -169,7 +169,7 @@ def softmax_into(x, out, variant: KernelVariant, cfg: LaneConfig = LaneConfig(),
             raise ArgumentError(f"expected float32 {name}, got {t.dtype}")
         if t.dim() != 2:
             raise ArgumentError(f"{name} must be 2-D [rows, cols], got {t.dim()}-D")
-        if t.shape[0] > 1 and t.shape[1] > 0 and t.stride(1) != 1:
+        if t.shape[1] > 1 and t.stride(1) != 1:  # a single row too (x[0:1, ::2])
             raise ArgumentError(f"{name} must have unit column stride")
     if x.shape != out.shape:
         raise ArgumentError(f"shape mismatch {tuple(x.shape)} vs {tuple(out.shape)}")
@@ -254,7 +254,7 @@ def row_stats_device(x, variant: KernelVariant = KernelVariant.REFERENCE_CLIPPED
     _sync_fault_hook()
     if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.float32 or x.dim() != 2:
         raise ArgumentError("x must be a 2-D float32 CUDA tensor")
-    if x.shape[0] > 1 and x.stride(1) != 1:
+    if x.shape[1] > 1 and x.stride(1) != 1:
         raise ArgumentError("x must have unit column stride")
     rows, cols = x.shape
     if cols < 1:

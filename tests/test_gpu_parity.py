@@ -545,3 +545,18 @@ def test_exp_accuracy_exhaustive():
         assert u.value <= ulp_bound, (mode, u.value)
         if mode == 2:
             assert r.value <= 1e-5  # FullVectorizedApproxExp tolerance, bench.py:52
+
+
+def test_device_api_argument_errors():
+    """softmax / softmax_into on CUDA tensors reject what the kernels cannot
+    read: non-unit column stride (a single-row view too), wrong dtype / rank /
+    device, mismatched shapes -- as ArgumentError, like the reference."""
+    t = gu.torch()
+    x = t.randn(4, 64, device="cuda")
+    for bad in (x[:, ::2], x[0:1, ::2], x.t(), x.double(), x[0], x.cpu()):
+        with pytest.raises(sk.ArgumentError):
+            sk.softmax(bad, sk.KernelVariant.REFERENCE_CLIPPED)
+    with pytest.raises(sk.ArgumentError):
+        sk.softmax_into(x, t.empty(4, 65, device="cuda"), sk.KernelVariant.REFERENCE_CLIPPED)
+    y = sk.softmax(x[1:3, 8:40], sk.KernelVariant.REFERENCE_CLIPPED)  # strided rows are fine
+    assert t.allclose(y, t.softmax(x[1:3, 8:40], dim=1), atol=1e-6)
