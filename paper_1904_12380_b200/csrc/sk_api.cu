@@ -490,7 +490,7 @@ GresChoice plan_gres_for(int64_t rows, int64_t cols, int mode, const DevInfo& di
 }
 
 int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa, uint64_t ya,
-              int mode, int dev, Plan& p) {
+              int mode, int dev, Plan& p, bool bulk = false) {
   const DevInfo di = dev_info(dev);
   const bool vec = (cols % 4 == 0) && (ldx % 4 == 0) && (ldy % 4 == 0) && (xa % 16 == 0) &&
                    (ya % 16 == 0);
@@ -513,6 +513,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     // aligned middle (1.7x the split path's 12 B/element on a 50257-wide vocab)
     bool latency = false;
     const GresChoice gc = plan_gres_for(rows, cols, mode, di, true, &latency);
+    if (bulk) latency = false;
     if (gc.P > 0 && !latency) {
       p.kind = kPathSeg;
       p.k3 = 7;
@@ -578,6 +579,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
       GresChoice gc;
       bool latency = false;
       if (gres != 0 && impl0 != 5 && di.coop) gc = plan_gres_for(rows, cols, mode, di, false, &latency);
+      if (bulk) latency = false;
       if (latency && rows > 2) return plan_split(rows, cols, p);
       if (gc.P > 0 && !latency) {
         p.kind = kPathSeg;
@@ -855,7 +857,7 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
 
 int softmax_dev(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx, int64_t ldy,
                 int mode, unsigned long long* bad, void* workspace, size_t ws_bytes,
-                cudaStream_t s) {
+                cudaStream_t s, bool bulk) {
   int st = check_common(x, y, rows, cols, ldx, ldy, mode);
   if (st) return st;
   if (rows == 0) return SK_OK;
@@ -866,7 +868,7 @@ int softmax_dev(const float* x, float* y, int64_t rows, int64_t cols, int64_t ld
   SK_CUDA(cudaGetDevice(&dev));
   Plan p;
   st = make_plan(rows, cols, ldx, ldy, reinterpret_cast<uint64_t>(x),
-                 reinterpret_cast<uint64_t>(y), mode, dev, p);
+                 reinterpret_cast<uint64_t>(y), mode, dev, p, bulk);
   if (st) return st;
   const size_t need = plan_ws_bytes(p, rows);
   char* ws = static_cast<char*>(workspace);

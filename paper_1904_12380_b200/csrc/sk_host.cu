@@ -208,8 +208,11 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
     SK_CUDA(cudaStreamWaitEvent(c->s_comp, c->ev_h2d[i], 0));
     // output slot free once the D2H that last read it is done
     if (k >= kRing) SK_CUDA(cudaStreamWaitEvent(c->s_comp, c->ev_d2h[i], 0));
+    // a chunk of this job: the job's throughput plan (never the latency path a
+    // small standalone call would take), so every chunk keeps the whole job's bits
+    const bool whole = nr == rows;
     st = softmax_dev(c->dx[i], c->dy[i], nr, cols, cols, cols, mode, c->dbad + k, nullptr, 0,
-                     c->s_comp);
+                     c->s_comp, !whole);
     if (st) return st;
     SK_CUDA(cudaEventRecord(c->ev_k[i], c->s_comp));
     SK_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_k[i], 0));

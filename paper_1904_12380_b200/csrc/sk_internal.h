@@ -67,10 +67,13 @@ cudaError_t launch_k(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStr
 }
 
 
-// the device-buffer softmax (plan + launch), as sk_softmax_f32
+// the device-buffer softmax (plan + launch), as sk_softmax_f32.  bulk: the
+// rows are one chunk of a larger pipelined job (the host-buffer path), so the
+// plan is the throughput plan of the row length -- never the latency path a
+// small standalone call would take -- and chunks keep the whole job's bits.
 int softmax_dev(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx, int64_t ldy,
                 int mode, unsigned long long* bad, void* workspace, size_t ws_bytes,
-                cudaStream_t s);
+                cudaStream_t s, bool bulk = false);
 
 // K3g planning and kernels (sk_api.cu), used by the fused column shard
 struct GresChoice {

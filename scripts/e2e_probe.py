@@ -54,7 +54,7 @@ def main():
         spec = configs.get(name)
         m = sk.Matrix2D.from_array(configs.generate(spec), pinned=True)
         out = sk.alloc_matrix(spec.rows, spec.cols, pinned=True)
-        for zc, kb in ((1, 0), (0, 0), (0, 512), (0, 1024), (0, 2048), (0, 4096), (0, 8192)):
+        for zc, kb in ((0, 0), (0, 2048), (0, 4096), (0, 6144), (0, 8192), (0, 12288), (0, 16384)):
             _native.set_tuning("host_zero_copy", zc)
             _native.set_tuning("host_chunk_kb", kb)
             sk.softmax(m, sk.KernelVariant.REFERENCE_CLIPPED, out=out)

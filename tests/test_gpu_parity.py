@@ -491,6 +491,24 @@ def test_deterministic_and_row_shard_bitwise():
     assert np.array_equal(a.view(np.uint32), y[5:45].view(np.uint32))
 
 
+@pytest.mark.parametrize("name", ["c4"])
+def test_host_path_chunks_keep_device_bits(name):
+    """The host-buffer pipeline splits a long-row job into small row chunks;
+    each chunk takes the job's throughput plan (not the latency path a small
+    standalone call would take), so the result is bit-identical to the
+    device path on the whole matrix."""
+    spec = configs.get(name)
+    x = configs.generate(spec, 0, 96)
+    dev, _ = gu.softmax_abi(x)
+    _native.set_tuning("host_chunk_kb", 4096)  # 4-row chunks
+    try:
+        m = sk.Matrix2D.from_array(x, pinned=True)
+        out = sk.softmax(m, sk.KernelVariant.REFERENCE_CLIPPED)
+    finally:
+        _native.set_tuning("host_chunk_kb", 0)
+    assert np.array_equal(out.view2d.view(np.uint32), dev.view(np.uint32))
+
+
 def test_host_path_equals_device_path():
     x = configs.generate("c3")
     dev, _ = gu.softmax_abi(x)
