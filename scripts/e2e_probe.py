@@ -20,6 +20,14 @@ def gbs(nbytes, sec):
 
 
 def main():
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="c2,c4")
+    ap.add_argument("--chunks-kb", default="0,2048,4096,8192,16384,32768",
+                    help="host_chunk_kb values (0 = auto)")
+    ap.add_argument("--zero-copy", action="store_true", help="also time the zero-copy path")
+    args = ap.parse_args()
     n = 64 << 20  # 64 MiB
     h = torch.empty(n // 4, dtype=torch.float32, pin_memory=True)
     h2 = torch.empty_like(h, pin_memory=True)
@@ -50,11 +58,14 @@ def main():
     torch.cuda.synchronize()
     res["bidir_GBps_total"] = gbs(20 * n, time.perf_counter() - t)
     print(json.dumps(res), flush=True)
-    for name in ("c2", "c4"):
+    for name in args.configs.split(","):
         spec = configs.get(name)
         m = sk.Matrix2D.from_array(configs.generate(spec), pinned=True)
         out = sk.alloc_matrix(spec.rows, spec.cols, pinned=True)
-        for zc, kb in ((0, 0), (0, 2048), (0, 4096), (0, 6144), (0, 8192), (0, 12288), (0, 16384)):
+        cases = [(0, int(k)) for k in args.chunks_kb.split(",")]
+        if args.zero_copy:
+            cases.insert(0, (1, 0))
+        for zc, kb in cases:
             _native.set_tuning("host_zero_copy", zc)
             _native.set_tuning("host_chunk_kb", kb)
             sk.softmax(m, sk.KernelVariant.REFERENCE_CLIPPED, out=out)
@@ -69,7 +80,7 @@ def main():
                               "bitwise_equal_device": ok,
                               "e2e_GBps": gbs(8 * spec.rows * spec.cols, dt)}), flush=True)
     _native.set_tuning("host_chunk_kb", 0)
-    _native.set_tuning("host_zero_copy", 1)
+    _native.set_tuning("host_zero_copy", 0)
 
 
 if __name__ == "__main__":
