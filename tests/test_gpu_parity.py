@@ -578,3 +578,31 @@ def test_device_api_argument_errors():
         sk.softmax_into(x, t.empty(4, 65, device="cuda"), sk.KernelVariant.REFERENCE_CLIPPED)
     y = sk.softmax(x[1:3, 8:40], sk.KernelVariant.REFERENCE_CLIPPED)  # strided rows are fine
     assert t.allclose(y, t.softmax(x[1:3, 8:40], dim=1), atol=1e-6)
+
+
+def test_concurrent_streams_long_rows(oracle):
+    """K3g is a cooperative grid that spins on its groups' exchanges: several
+    streams launching it concurrently (and a K1 job beside them) must neither
+    deadlock nor corrupt each other -- each launch's CTAs are co-resident by
+    construction and each stream has its own exchange block."""
+    t = gu.torch()
+    x1 = t.from_numpy(configs.generate("c4", 0, 64)).cuda()
+    x2 = t.from_numpy(configs.generate("c4", 64, 64)).cuda()
+    x3 = t.from_numpy(configs.generate("c2", 0, 8192)).cuda()
+    ys = [t.empty_like(x) for x in (x1, x2, x3)]
+    streams = [t.cuda.Stream() for _ in range(3)]
+    _native.set_tuning("gres_timeout_spins", 1 << 20)  # a deadlock would abort, not hang
+    try:
+        for _ in range(20):
+            for x, y, s in zip((x1, x2, x3), ys, streams):
+                with t.cuda.stream(s):
+                    sk.softmax_into(x, y, sk.KernelVariant.REFERENCE_CLIPPED, check_finite=False)
+        t.cuda.synchronize()
+        from paper_1904_12380_b200.kernels import check_device_flag
+
+        check_device_flag()  # raises on an aborted exchange
+    finally:
+        _native.set_tuning("gres_timeout_spins", 0)
+    for x, y in zip((x1, x2, x3), ys):
+        ref = oracle.softmax_ref(x.cpu().numpy(), True, nthreads=0)
+        assert oracle.parity(y.cpu().numpy(), ref)["ok"]
