@@ -141,7 +141,20 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("SK_BENCH_SHARE_DEVICE") == "1":
+        # test hook (tests/test_gpu_tools.py): every rank on cuda:0 over gloo, to
+        # exercise the N>1 row-shard path on a 1-GPU box; its numbers mean nothing
+        local = 0
     return world, rank, local
+
+
+def init_group(dev):
+    import torch.distributed as dist
+
+    if os.environ.get("SK_BENCH_SHARE_DEVICE") == "1":
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
 
 
 # ------------------------------------------------------------------ reference
@@ -241,9 +254,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
+        init_group(dev)
 
     import paper_1904_12380_b200 as sk
     from paper_1904_12380_b200 import _native, configs
@@ -421,9 +432,7 @@ def run_colshard(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
+        init_group(dev)
     import paper_1904_12380_b200 as sk
     from paper_1904_12380_b200 import _native, configs, sharding
 

@@ -57,6 +57,26 @@ def main():
             h2.copy_(d2, non_blocking=True)
     torch.cuda.synchronize()
     res["bidir_GBps_total"] = gbs(20 * n, time.perf_counter() - t)
+    # two streams per direction, half the bytes each (more copy engines busy?)
+    s3, s4 = torch.cuda.Stream(), torch.cuda.Stream()
+    hh, hh2, dh, dh2 = h.view(2, -1), h2.view(2, -1), d.view(2, -1), d2.view(2, -1)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(10):
+        for i, (sa, sb) in enumerate(((s1, s2), (s3, s4))):
+            with torch.cuda.stream(sa):
+                dh[i].copy_(hh[i], non_blocking=True)
+            with torch.cuda.stream(sb):
+                hh2[i].copy_(dh2[i], non_blocking=True)
+    torch.cuda.synchronize()
+    res["bidir_2x2_GBps_total"] = gbs(20 * n, time.perf_counter() - t)
+    t = time.perf_counter()
+    for _ in range(10):
+        for i, sa in enumerate((s1, s3)):
+            with torch.cuda.stream(sa):
+                dh[i].copy_(hh[i], non_blocking=True)
+    torch.cuda.synchronize()
+    res["h2d_2streams_GBps"] = gbs(10 * n, time.perf_counter() - t)
     print(json.dumps(res), flush=True)
     for name in args.configs.split(","):
         spec = configs.get(name)

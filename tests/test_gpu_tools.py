@@ -74,3 +74,23 @@ def test_bench_colshard_mode():
     assert line["config"]["plan"].startswith("k3_gres_colshard world=1")
     assert line["parity"]["ok"], line["parity"]
     assert line["value"] > 1000
+
+
+def test_bench_row_shard_under_torchrun():
+    """bench.py's N>1 row-shard path (torchrun, barrier, max-over-ranks) at
+    world size 2 on one GPU: SK_BENCH_SHARE_DEVICE puts both ranks on cuda:0
+    over gloo (row shards never wait on each other; the numbers mean nothing,
+    the code path is what is checked)."""
+    import json
+
+    from tests.test_bench_contract import _torchrun
+
+    r = _torchrun(2, "--steps", "64", "--warmup", "3", "--e2e-steps", "1",
+                  "--no-cpu-baseline", env={"SK_BENCH_SHARE_DEVICE": "1"})
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["global_rows"] == 2 * 65536
+    assert d["parity"]["ok"] and d["e2e"]["bitwise_equal_device_path"]
+    assert d["gpu_launches"] == 64 and d["value"] > 0
