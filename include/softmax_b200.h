@@ -200,7 +200,8 @@ void sk_free_pinned(void* p);
  *                    separate poller warp (-1 auto: depth >= 4)
  *   "gres_sleep"     K3g poller back-off (ns, default 128)
  *   "gres_timeout_spins"  polls before a missing peer aborts an exchange (0 = default)
- *   "gres_diag"      1: K3g waits for its own slot only (timing diagnostic; wrong results)
+ *   "gres_diag"      1: K3g waits for its own slot only, 2: K3g skips the math
+ *                    (timing diagnostics; wrong results)
  *   "cluster_k3"     1 (default): K3c may serve rows K3g cannot (fallback)
  *   "cluster_size"   force the K3c cluster size (0 = auto: most SMs covered)
  *   "cluster_onex"   1: K3c exchanges one (max, sum) pair per row and recomputes

@@ -20,6 +20,9 @@
 // y = exp(clip(x - M)) * (1/(float)S), the exp recomputed against the GLOBAL
 // max from the untouched slice (reference order, kernels.py:144-188).
 //
+// Timing diagnostics (gres_diag, results wrong): bit 0 waits for the CTA's
+// own slot only (no group exchange), bit 1 skips the math (the ring as a copy).
+//
 // Roles: warps 0-15 compute; warp 16 publishes and issues the TMA refills; at
 // lag 1 (ring depth 2-3) warp 16 also polls right after publishing, at lag >= 2
 // (depth 4-5) warp 17 polls, so a slow poll never delays the next publication
@@ -373,6 +376,8 @@ __global__ void __launch_bounds__(kGresBlock, 1)
           const int64_t col = sg.a + sg.nmid + (tid - 32);
           st_stream1(yrow + col, scale1<MODE>(sexp1<MODE>(__ldg(xrow + col), M), rcp));
         }
+      } else if (diag & 2) {  // timing only: the ring as a plain copy (no math)
+        for (int q = tid; q < nvec; q += kGresCompute) st_stream4(yr + 4 * q, sb[q]);
       } else {
 #pragma unroll 4
         for (int q = tid; q < nvec; q += kGresCompute) {
@@ -406,6 +411,7 @@ __global__ void __launch_bounds__(kGresBlock, 1)
       float mt = xe;
       u64 z = f2pk(0.0f, 0.0f);
       if (edge) z = nf_acc2(z, xe, 0.0f);
+      if (!UNAL && (diag & 2)) nq = 0;  // timing only: skip the local pass
 #pragma unroll 4
       for (int q = tid; q < nq; q += kGresCompute) {
         const float4 v4 = sb[q];

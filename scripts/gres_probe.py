@@ -23,7 +23,7 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--points", default="14:3,16:3,20:4,24:4", help="P:stages,...")
     ap.add_argument("--reps", type=int, default=60)
-    ap.add_argument("--diags", default="0,1", help="gres_diag values: 1 skips the group exchange")
+    ap.add_argument("--diags", default="0,1", help="gres_diag values: 1 skips the group exchange, 2 the math, 3 both")
     ap.add_argument("--sleeps", default="128", help="poller back-off values (ns)")
     ap.add_argument("--splits", default="-1", help="poller warp: -1 auto, 0 off, 1 on")
     args = ap.parse_args()
@@ -53,6 +53,11 @@ def main():
             print(json.dumps({"config": spec.name, "P": P, "stages": st, "diag": d, "sleep": sl, "split": sp, "us": us,
                               "gbs": 8.0 * spec.rows * spec.cols / us / 1e3}), flush=True)
     _native.set_tuning("gres_diag", 0)
+    from row_length_sweep import copy_us  # noqa: E402
+
+    cu = copy_us(xs, ys, spec.rows * spec.cols, args.reps, s)
+    print(json.dumps({"config": spec.name, "copy_us": cu, "gbs": 8.0 * spec.rows * spec.cols / cu / 1e3}),
+          flush=True)
 
 
 if __name__ == "__main__":
