@@ -232,7 +232,7 @@ def cpu_baseline(spec, seconds: float):
             "sample": f"{rows} rows x {spec.cols} cols of {spec.name}, {n} passes in {dt:.1f}s, "
                       f"1 thread (reference contract: single-threaded), "
                       f"C restatement bit-exact to the reference; host has "
-                      f"{oracle.cpu_count()} cores",
+                      f"{oracle.cpu_count()} cores (sched_getaffinity)",
             "rows_per_s": rows * n / dt}
 
 
@@ -334,6 +334,7 @@ def run_ours(args):
     e1 = torch.cuda.Event(enable_timing=True)
     launches = 0
     sampler.mark()
+    marks = []  # (event, launches so far) at every graph replay boundary
     with torch.cuda.stream(stream):
         e0.record(stream)
         done = 0
@@ -341,6 +342,9 @@ def run_ours(args):
             while done + G <= args.steps:
                 graph.replay()
                 done += G
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(stream)
+                marks.append((ev, done))
         while done < args.steps:
             launch(done)
             done += 1
@@ -348,6 +352,12 @@ def run_ours(args):
         e1.record(stream)
     stream.synchronize()
     sampler.mark()
+    # per-launch time of each replay (G launches): the spread of the timed region
+    per = []
+    prev, prev_n = e0, 0
+    for ev, n in marks:
+        per.append(prev.elapsed_time(ev) * 1e3 / (n - prev_n))
+        prev, prev_n = ev, n
     if world > 1:
         torch.distributed.barrier()
     ms = e0.elapsed_time(e1)
@@ -403,6 +413,10 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic_from_profiles(spec.name, plan),
                          "peak_source": peak_src, "avg_launch_us": kern_us,
+                         "median_launch_us": statistics.median(per) if per else kern_us,
+                         "min_launch_us": min(per) if per else kern_us,
+                         "replays": len(per), "launches_per_replay": G if per else 1,
+                         "frac_nominal_8000": achieved / 8000.0,
                          "algorithmic_bytes_per_launch": bytes_step},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_gbs, "unit": "GB/s", "h2d_bytes_per_step": int(4 * rows * cols),

@@ -173,6 +173,21 @@ int sk_exp_f32(float* buf, int64_t n, int mode, void* stream);
 int sk_sumscale_f32(float* buf, int64_t rows, int64_t cols, int64_t ld, void* stream);
 
 /*
+ * The reference's 1-D component operations (kernels.py:229-276; test-level
+ * API there) on the device, composed with the phase kernels above:
+ *   sk_row_sum_f32      row_sum[r] = sum_c x[r,c] accumulated in f64
+ *                       (row_sum_scalar kernels.py:258-260, rounded to f32 by the caller)
+ *   sk_shift_scale_f32  y = (x - shift) * scale, IEEE: subtract_broadcast
+ *                       (kernels.py:234-236, scale 1) and scale_reciprocal
+ *                       (kernels.py:263-269, shift 0, scale = 1/(float)sum)
+ * row_max_scalar / row_stats use sk_row_stats_f32; exp_batch uses sk_exp_f32.
+ */
+int sk_row_sum_f32(const float* x, int64_t rows, int64_t cols, int64_t ldx, double* row_sum,
+                   void* stream);
+int sk_shift_scale_f32(const float* x, float* y, int64_t n, float shift, float scale,
+                       void* stream);
+
+/*
  * Page-locked host memory for Matrix2D buffers (tensor.py:90-103 allocates
  * with np.zeros; pinned memory lets sk_softmax_f32_host reach full PCIe
  * bandwidth).  Returns NULL on failure (-> ResourceError).

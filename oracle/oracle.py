@@ -32,13 +32,12 @@ _lib = None
 def lib() -> ctypes.CDLL:
     global _lib
     if _lib is None:
-        if not LIB_PATH.exists():
-            import sys
+        import sys
 
-            sys.path.insert(0, str(HERE.parent))
-            from paper_1904_12380_b200._build import build_oracle
+        sys.path.insert(0, str(HERE.parent))
+        from paper_1904_12380_b200._build import build_oracle
 
-            build_oracle()
+        build_oracle()  # no-op unless missing or older than sk_oracle.c
         L = ctypes.CDLL(str(LIB_PATH))
         L.sko_softmax_f32.restype = c_int64
         L.sko_softmax_f32.argtypes = [c_void_p, c_void_p, c_int64, c_int64, c_int, c_int]
@@ -53,6 +52,10 @@ def lib() -> ctypes.CDLL:
         L.sko_philox_raw.restype = None
         L.sko_philox_raw.argtypes = [c_uint64, c_uint64, c_void_p, c_int64]
         L.sko_max_threads.restype = c_int
+        L.sko_seq_max.restype = c_float
+        L.sko_seq_max.argtypes = [c_void_p, c_int64]
+        L.sko_seq_sum_wide.restype = c_float
+        L.sko_seq_sum_wide.argtypes = [c_void_p, c_int64]
         _lib = L
     return _lib
 
@@ -102,6 +105,49 @@ def lanes_max(a: np.ndarray, W: int) -> np.float32:
 def lanes_sum(a: np.ndarray, W: int) -> np.float32:
     a = np.ascontiguousarray(a, dtype=np.float32)
     return np.float32(lib().sko_lanes_sum(a.ctypes.data, a.size, W))
+
+
+# ---- the 1-D component operations (reference kernels.py:229-276) -----------
+# Restated with the same arithmetic: strict scans in C, IEEE fp32 elementwise
+# ops in numpy, and numpy's own exp for exp_batch / row_stats (the reference
+# calls np.exp there: kernels.py:254, 275).
+def _row(a) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    if a.ndim != 1 or a.size == 0:
+        raise ValueError("expected a non-empty 1-D row")
+    return a
+
+
+def row_max_scalar(a) -> np.float32:
+    a = _row(a)
+    return np.float32(lib().sko_seq_max(a.ctypes.data, a.size))
+
+
+def subtract_broadcast(a, v: float) -> np.ndarray:
+    return _row(a) - np.float32(v)
+
+
+def value_clip(x: float) -> np.float32:
+    x32 = np.float32(x)
+    return x32 if x32 > np.float32(-64.0) else np.float32(-64.0)
+
+
+def exp_batch(a) -> np.ndarray:
+    return np.exp(np.asarray(a, dtype=np.float32))
+
+
+def row_sum_scalar(a) -> np.float32:
+    a = _row(a)
+    return np.float32(lib().sko_seq_sum_wide(a.ctypes.data, a.size))
+
+
+def scale_reciprocal(a, s: float) -> np.ndarray:
+    return _row(a) * (np.float32(1.0) / np.float32(s))
+
+
+def row_stats(a) -> tuple[np.float32, np.float32]:
+    m = row_max_scalar(a)
+    return m, row_sum_scalar(np.exp(subtract_broadcast(a, m)))
 
 
 def philox_raw(seed: int, start: int, n: int) -> np.ndarray:

@@ -114,6 +114,19 @@ int sko_max_threads(void) {
 #endif
 }
 
+/* --- kernels.py:119-133 _seq_max / _seq_sum_wide (component ops) --------- */
+float sko_seq_max(const float* x, int64_t n) {
+  float m = x[0];
+  for (int64_t i = 1; i < n; ++i)
+    if (x[i] > m) m = x[i];
+  return m;
+}
+float sko_seq_sum_wide(const float* x, int64_t n) {
+  double acc = (double)x[0];
+  for (int64_t i = 1; i < n; ++i) acc += (double)x[i];
+  return (float)acc;
+}
+
 /* --- simd_reduce.py:149-189 _lanes_max (bitwise = strict scan) --------- */
 float sko_lanes_max(const float* x, int64_t n, int W) {
   float lanes[64];

@@ -10,6 +10,16 @@ mirror of the reference interface.  There is no CPU fallback.
 from .errors import ArgumentError, NumericDomainError, ResourceError, SoftmaxKitError
 from .lanes import LaneConfig
 from .tensor import FillSpec, Matrix2D, alloc_matrix, fill_uniform
+from . import components
+from .components import (
+    exp_batch,
+    row_max_scalar,
+    row_stats,
+    row_sum_scalar,
+    scale_reciprocal,
+    subtract_broadcast,
+    value_clip,
+)
 from .kernels import (
     CLIP_FLOOR,
     FLT_MIN_NORMAL,
@@ -41,4 +51,12 @@ __all__ = [
     "softmax",
     "softmax_into",
     "variant_mode",
+    "components",
+    "row_max_scalar",
+    "subtract_broadcast",
+    "value_clip",
+    "exp_batch",
+    "row_sum_scalar",
+    "scale_reciprocal",
+    "row_stats",
 ]

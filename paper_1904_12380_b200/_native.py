@@ -64,6 +64,8 @@ SIGNATURES: dict[str, tuple] = {
                               c_void_p]),
     "sk_exp_f32": (c_int, [c_void_p, c_int64, c_int, c_void_p]),
     "sk_sumscale_f32": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p]),
+    "sk_row_sum_f32": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p]),
+    "sk_shift_scale_f32": (c_int, [c_void_p, c_void_p, c_int64, c_float, c_float, c_void_p]),
     "sk_alloc_pinned": (c_void_p, [c_size_t]),
     "sk_free_pinned": (None, [c_void_p]),
     "sk_set_tuning": (c_int, [c_char_p, c_int]),

@@ -10,6 +10,13 @@
 //   sk_sumscale_f32  kernels.py:177-189  S = sum(row) (f64), r = 1/(float)S,
 //                                        y = e*r, y < FLT_MIN -> +0, in place
 //
+// and the reference's 1-D component operations (kernels.py:229-276), which
+// compose into the same phases:
+//
+//   sk_row_sum_f32      kernels.py:258-260  S = sum(row) accumulated in f64
+//   sk_shift_scale_f32  kernels.py:234-236  y = x - v        (scale 1: exact)
+//                       kernels.py:263-269  y = x * (1/s)    (shift 0: exact)
+//
 // One CTA per row, grid-stride over columns, any row pitch / alignment.
 #include <cuda_runtime.h>
 
@@ -59,11 +66,26 @@ __global__ void __launch_bounds__(kPhaseThreads)
   }
 }
 
+// exp over the whole float range for the unclipped modes: like sexp1, but a
+// result below FLT_MIN comes out subnormal (as np.exp / glibc expf give it,
+// exp_batch kernels.py:245-255) instead of flushed: ex2 of t + 32 (exact for
+// these t), then an exact scale by 2^-32 that rounds once into the subnormal
+// range.  Not on the fused path, which flushes such outputs anyway.
+__device__ __forceinline__ float exp_subnormal(float s) {
+  s = fmaxf(s, -104.0f);  // exp(-104) < 2^-150 (rounds to 0); keeps t finite
+  const float t = s * kLog2eHi;
+  const float d = fmaf(fmaf(s, kLog2eHi, -t), kLn2, s * kLog2eLoLn2);
+  const float p = ex2_ftz(t + 32.0f);
+  return __fmul_rn(fmaf(p, d, p), 2.3283064365386963e-10f);  // 2^-32
+}
+
 template <int MODE>
 __global__ void k_exp(float* __restrict__ buf, int64_t n) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-    buf[i] = sexp1<MODE>(buf[i], 0.0f);
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float v = buf[i];
+    buf[i] = (MODE == kAccurate && v < -87.0f) ? exp_subnormal(v) : sexp1<MODE>(v, 0.0f);
+  }
 }
 
 __global__ void __launch_bounds__(kPhaseThreads)
@@ -75,6 +97,34 @@ __global__ void __launch_bounds__(kPhaseThreads)
   s = cta_reduce_sum(s, red);
   const float rcp = recip_of_sum(s);
   for (int64_t c = threadIdx.x; c < cols; c += kPhaseThreads) r[c] = scale_flush(r[c], rcp);
+}
+
+__global__ void __launch_bounds__(kPhaseThreads)
+    k_rowsum(const float* __restrict__ x, int64_t cols, int64_t ldx, double* __restrict__ out) {
+  __shared__ double red[kPhaseThreads / 32];
+  const float* r = x + int64_t(blockIdx.x) * ldx;
+  double s = 0.0;
+  for (int64_t c = threadIdx.x; c < cols; c += kPhaseThreads) s += static_cast<double>(r[c]);
+  s = cta_reduce_sum(s, red);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+// y = (x - shift) * scale: IEEE subtract then multiply, so shift = v, scale = 1
+// is exactly x - v and shift = 0, scale = r exactly x * r (NaN/Inf propagate)
+__global__ void k_shift_scale(const float* __restrict__ x, float* __restrict__ y, int64_t n,
+                              float shift, float scale) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    y[i] = __fmul_rn(__fsub_rn(x[i], shift), scale);
+}
+
+unsigned elementwise_grid(int64_t n) {
+  int sms = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (n + 255) / 256;
+  return static_cast<unsigned>(want < int64_t(sms) * 16 ? want : int64_t(sms) * 16);
 }
 
 bool bad_shape(const void* a, const void* b, int64_t rows, int64_t cols, int64_t ld1,
@@ -100,12 +150,7 @@ int sk_maxsub_f32(const float* x, float* y, int64_t rows, int64_t cols, int64_t 
 int sk_exp_f32(float* buf, int64_t n, int mode, void* stream) {
   if (n < 0 || (n > 0 && !buf) || mode < 0 || mode > 2) return SK_ERR_ARGUMENT;
   if (n == 0) return SK_OK;
-  int sms = 148;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t want = (n + 255) / 256;
-  const unsigned grid = static_cast<unsigned>(want < int64_t(sms) * 16 ? want : int64_t(sms) * 16);
+  const unsigned grid = sk::elementwise_grid(n);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   switch (mode) {
     case 0: sk::k_exp<sk::kClipAccurate><<<grid, 256, 0, s>>>(buf, n); break;
@@ -120,6 +165,24 @@ int sk_sumscale_f32(float* buf, int64_t rows, int64_t cols, int64_t ld, void* st
   if (rows == 0) return SK_OK;
   sk::k_sumscale<<<static_cast<unsigned>(rows), sk::kPhaseThreads, 0,
                    static_cast<cudaStream_t>(stream)>>>(buf, cols, ld);
+  return cudaGetLastError() == cudaSuccess ? SK_OK : SK_ERR_CUDA;
+}
+
+int sk_row_sum_f32(const float* x, int64_t rows, int64_t cols, int64_t ldx, double* row_sum,
+                   void* stream) {
+  if (sk::bad_shape(x, row_sum, rows, cols, ldx, cols)) return SK_ERR_ARGUMENT;
+  if (rows == 0) return SK_OK;
+  sk::k_rowsum<<<static_cast<unsigned>(rows), sk::kPhaseThreads, 0,
+                 static_cast<cudaStream_t>(stream)>>>(x, cols, ldx, row_sum);
+  return cudaGetLastError() == cudaSuccess ? SK_OK : SK_ERR_CUDA;
+}
+
+int sk_shift_scale_f32(const float* x, float* y, int64_t n, float shift, float scale,
+                       void* stream) {
+  if (n < 0 || (n > 0 && (!x || !y))) return SK_ERR_ARGUMENT;
+  if (n == 0) return SK_OK;
+  sk::k_shift_scale<<<sk::elementwise_grid(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      x, y, n, shift, scale);
   return cudaGetLastError() == cudaSuccess ? SK_OK : SK_ERR_CUDA;
 }
 

@@ -28,6 +28,11 @@ def golden():
 
 
 @pytest.fixture(scope="session")
+def golden_components():
+    return np.load(GOLDEN / "golden_components.npz")
+
+
+@pytest.fixture(scope="session")
 def golden_meta():
     import json
 

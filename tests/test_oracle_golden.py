@@ -93,3 +93,30 @@ def test_metrics():
     assert o.max_rowsum_dev(np.array([[0.5, 0.6]])) == pytest.approx(0.1)
     assert o.max_rel_err(np.array([[np.nan, 1.0]]), ref) == float("inf")
     assert o.max_rel_err(np.array([[1e-30, 1.0]]), np.array([[0.0, 1.0]])) == float("inf")
+
+
+def _component_rows(g):
+    return sorted({k.split("/")[0] for k in g.files if k.endswith("/row")})
+
+
+def test_component_ops_bit_exact(golden_components, oracle):
+    """The oracle's restatement of the 1-D component operations
+    (kernels.py:229-276) reproduces the reference's outputs bit for bit."""
+    g = golden_components
+    for x, y in zip(g["clip/x"], g["clip/y"]):
+        assert bits(oracle.value_clip(x)) == bits(y)
+    for name in _component_rows(g):
+        r = g[f"{name}/row"]
+        m = oracle.row_max_scalar(r)
+        assert bits(m) == bits(g[f"{name}/max"][0]), name
+        sh = oracle.subtract_broadcast(r, m)
+        assert np.array_equal(bits(sh), bits(g[f"{name}/sub_max"])), name
+        assert np.array_equal(bits(oracle.subtract_broadcast(r, 3.25)), bits(g[f"{name}/sub_325"]))
+        e = oracle.exp_batch(sh)
+        assert np.array_equal(bits(e), bits(g[f"{name}/exp"])), name
+        s = oracle.row_sum_scalar(e)
+        assert bits(s) == bits(g[f"{name}/sum_exp"][0]), name
+        assert bits(oracle.row_sum_scalar(r)) == bits(g[f"{name}/sum_row"][0]), name
+        assert np.array_equal(bits(oracle.scale_reciprocal(e, s)), bits(g[f"{name}/scaled"])), name
+        st = oracle.row_stats(r)
+        assert np.array_equal(bits(np.array(st, np.float32)), bits(g[f"{name}/stats"])), name
