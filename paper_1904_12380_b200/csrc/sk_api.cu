@@ -98,13 +98,14 @@ std::atomic<int> g_cluster_size{0};  // force a K3c cluster size (0 = auto)
 std::atomic<int> g_gres{1};        // 0 off, 1 auto, 2 force
 std::atomic<int> g_gres_p{0};      // force CTAs per row (0 = planner)
 std::atomic<int> g_gres_st{0};     // force ring depth (0 = planner)
-std::atomic<int> g_gres_split{-1};  // separate poller warp: -1 auto (depth >= 4), 0 off, 1 on
+std::atomic<int> g_gres_lag{0};    // force the lag (rows between local and output pass; 0 = planner)
+std::atomic<int> g_gres_split{-1};  // separate poller warp: -1 auto (lag >= 2), 0 off, 1 on
 std::atomic<int> g_gres_sleep{128};  // poller back-off between polls (ns)
 std::atomic<int> g_gres_diag{0};     // timing diagnostics (1: wait only for the own slot -- wrong results)
 std::atomic<unsigned> g_gres_spins{kGresSpinLimit};  // exchange timeout (polls), tests shorten it
-bool gres_split(int nstages) {
+bool gres_split(int lag) {
   const int v = g_gres_split.load();
-  return v < 0 ? nstages >= 4 : v != 0;
+  return v < 0 ? lag >= 2 : v != 0;
 }
 
 // ------------------------------------------------------------------ K1 table
@@ -257,7 +258,7 @@ int max_active_clusters(const void* fn, int cs, size_t smem) {
   return n;
 }
 
-bool gres_split(int nstages);
+bool gres_split(int lag);
 constexpr int64_t kGresSmemMax = 225 * 1024;  // ring bytes per K3g CTA (227 KB opt-in minus statics)
 template <int L, bool SPLIT, bool UNAL = false>
 const void* gres_fn_l(int mode) {
@@ -267,25 +268,25 @@ const void* gres_fn_l(int mode) {
     default: return reinterpret_cast<const void*>(&k3_gres<kApprox, L, SPLIT, UNAL>);
   }
 }
-// ring depth 2 and 3 run lag 1; 4 -> lag 2; 5 -> lag 3
-const void* gres_fn(int mode, int nstages, bool split);
-// rows of any alignment: the two schedules the planner uses (depth 2-3 with
-// the publisher polling, depth 4 with a poller warp); nullptr otherwise
-const void* gres_fn_unal(int mode, int nstages, bool split) {
-  if (nstages <= 3 && !split) return gres_fn_l<1, false, true>(mode);
-  if (nstages == 4 && split) return gres_fn_l<2, true, true>(mode);
+// lag 1..3 (the ring depth is a launch argument >= lag + 2, or 2 at lag 1)
+const void* gres_fn(int mode, int lag, bool split);
+// rows of any alignment: the two schedules the planner uses (lag 1 with the
+// publisher polling, lag 2 with a poller warp); nullptr otherwise
+const void* gres_fn_unal(int mode, int lag, bool split) {
+  if (lag == 1 && !split) return gres_fn_l<1, false, true>(mode);
+  if (lag == 2 && split) return gres_fn_l<2, true, true>(mode);
   return nullptr;
 }
-const void* gres_fn(int mode, int nstages, bool split, bool unal) {
-  if (unal) return gres_fn_unal(mode, nstages, split);
-  return gres_fn(mode, nstages, split);
+const void* gres_fn(int mode, int lag, bool split, bool unal) {
+  if (unal) return gres_fn_unal(mode, lag, split);
+  return gres_fn(mode, lag, split);
 }
-const void* gres_fn(int mode, int nstages, bool split) {
+const void* gres_fn(int mode, int lag, bool split) {
   if (split)
-    return nstages >= 5 ? gres_fn_l<3, true>(mode)
-           : nstages == 4 ? gres_fn_l<2, true>(mode) : gres_fn_l<1, true>(mode);
-  return nstages >= 5 ? gres_fn_l<3, false>(mode)
-         : nstages == 4 ? gres_fn_l<2, false>(mode) : gres_fn_l<1, false>(mode);
+    return lag >= 3 ? gres_fn_l<3, true>(mode)
+           : lag == 2 ? gres_fn_l<2, true>(mode) : gres_fn_l<1, true>(mode);
+  return lag >= 3 ? gres_fn_l<3, false>(mode)
+         : lag == 2 ? gres_fn_l<2, false>(mode) : gres_fn_l<1, false>(mode);
 }
 
 constexpr int kSegNV = 4;
@@ -371,7 +372,8 @@ struct Plan {
   const K1mEntry* k1m = nullptr;
   bool unal = false;  // K3g over rows of any alignment
   // seg (K2: nseg == 1; K3: nseg > 1)
-  int nseg = 1, seglen = 0, threads = 0, lag = 0;
+  int nseg = 1, seglen = 0, threads = 0, lag = 0;  // lag: ring depth (K2/K3c/K3g)
+  int glag = 0;                                     // K3g: rows between local and output pass
   int k3 = 0;  // 0 K2, 6 K3c (cluster), 7 K3g (grid-resident)
   int64_t chunk_rows = 0;
   size_t smem = 0;
@@ -456,15 +458,19 @@ GresChoice plan_gres(int64_t rows, int64_t cols, int mode, const DevInfo& di, in
     if (groups < 1 || (rows + groups - 1) / groups >= (int64_t(1) << 31)) continue;
     for (int st = 2; st <= st_max; ++st) {
       if (g_gres_st.load() >= 2 && st != g_gres_st.load()) continue;
+      // lag: the forced one, else the classic schedule (depth 2-3 lag 1, 4 lag 2, 5 lag 3)
+      const int lag = g_gres_lag.load() > 0 ? g_gres_lag.load() : std::max(1, std::min(3, st - 2));
+      if (lag > 3 || (st < lag + 2 && !(st == 2 && lag == 1))) continue;
       const size_t smem = size_t(st) * slice * sizeof(float);
-      const bool split = gres_split(st);
-      const void* fn = gres_fn(mode, st, split, unal);
+      const bool split = gres_split(lag);
+      const void* fn = gres_fn(mode, lag, split, unal);
       if (!fn || occupancy(fn, split ? kGresBlock : kGresThreads, smem) < 1) continue;
       const double t = gres_time_us(rows, P, st, slice, groups, world, nvr);
       if (best.P == 0 || t < best_t) {
         best_t = t;
         best.P = P;
         best.st = st;
+        best.lag = lag;
         best.groups = groups;
         best.slice = slice;
         best.score = 1.0 / t;
@@ -521,7 +527,8 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
       p.nseg = gc.P;
       p.seglen = static_cast<int>(gc.slice);
       p.lag = gc.st;
-      p.threads = gres_split(gc.st) ? kGresBlock : kGresThreads;
+      p.glag = gc.lag;
+      p.threads = gres_split(gc.lag) ? kGresBlock : kGresThreads;
       p.smem = size_t(gc.st) * gc.slice * sizeof(float);
       p.grid = int64_t(gc.groups) * gc.P;
       return SK_OK;
@@ -587,7 +594,8 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
         p.nseg = gc.P;
         p.seglen = static_cast<int>(gc.slice);
         p.lag = gc.st;
-        p.threads = gres_split(gc.st) ? kGresBlock : kGresThreads;
+        p.glag = gc.lag;
+        p.threads = gres_split(gc.lag) ? kGresBlock : kGresThreads;
         p.smem = size_t(gc.st) * gc.slice * sizeof(float);
         p.grid = int64_t(gc.groups) * gc.P;
         return SK_OK;
@@ -664,7 +672,7 @@ struct GresWs {
 GresWs gres_ws(const Plan& p) {
   GresWs w;
   const size_t groups = size_t(p.grid / p.nseg);
-  const int lag = p.lag >= 5 ? 3 : p.lag == 4 ? 2 : 1;
+  const int lag = p.glag;
   w.total = align_up(w.slots + 2 * groups * gres_slot_sets(lag) * p.nseg * 16, 256);
   return w;
 }
@@ -841,7 +849,7 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
       comm.sys = 0;
       comm.spin_limit = g_gres_spins.load();
       int P = p.nseg, slice = p.seglen, nst = p.lag;
-      SK_CUDA(launch_k(gres_fn(mode, p.lag, p.threads == kGresBlock, p.unal), dim3(static_cast<unsigned>(p.grid)),
+      SK_CUDA(launch_k(gres_fn(mode, p.glag, p.threads == kGresBlock, p.unal), dim3(static_cast<unsigned>(p.grid)),
                        dim3(p.threads), p.smem, s, true, x, y, rows, cols, ldx, ldy, P, slice, nst, comm,
                        bad, sh, g_gres_sleep.load(), g_gres_diag.load()));
     } else {
@@ -934,6 +942,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "gres_diag") g_gres_diag = value;
   else if (k == "gres_sleep") g_gres_sleep = value;
   else if (k == "gres_split") g_gres_split = value;
+  else if (k == "gres_lag") g_gres_lag = value;
   else if (k == "k1m") g_k1m = value;
   else if (k == "coop_pdl") g_coop_pdl = value;
   else if (k == "k1m_wpr") g_k1m_wpr = value;
@@ -983,6 +992,10 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
   else
     snprintf(buf, buflen, "k4_split vec=%d nch=%d grid=%lld", p.vec ? 4 : 1, p.nch,
              (long long)p.grid);
+  if (p.kind == kPathSeg && p.k3 == 7) {
+    const size_t n = strlen(buf);
+    if (n < size_t(buflen)) snprintf(buf + n, size_t(buflen) - n, " lag=%d", p.glag);
+  }
   return SK_OK;
 }
 

@@ -45,13 +45,13 @@ int colshard_launch(const float* x, float* y, int64_t rows, int64_t cols, int64_
   if (!di.coop) return arg_fail("device cannot co-schedule the fused column shard");
   const GresChoice gc = plan_gres(kGresPlanRows, cols, mode, di, world, nvr, false);
   if (gc.P == 0) return arg_fail("shard row too long for the fused column shard (use the split path)");
-  const bool split = gres_split(gc.st);
-  const int lag = gc.st >= 5 ? 3 : gc.st == 4 ? 2 : 1;
+  const bool split = gres_split(gc.lag);
+  const int lag = gc.lag;
   const size_t need = kXSlots + 2 * size_t(gc.groups) * gres_slot_sets(lag) * world * gc.P * 16;
   if (need > kXBlockBytes) return arg_fail("exchange block too small for this plan");
   if (desc) {
-    snprintf(desc, desc_len, "k3_gres_colshard world=%d nvr=%d nseg=%d seglen=%lld stages=%d groups=%d threads=%d",
-             world, nvr, gc.P, (long long)gc.slice, gc.st, gc.groups, split ? kGresBlock : kGresThreads);
+    snprintf(desc, desc_len, "k3_gres_colshard world=%d nvr=%d nseg=%d seglen=%lld stages=%d lag=%d groups=%d threads=%d",
+             world, nvr, gc.P, (long long)gc.slice, gc.st, gc.lag, gc.groups, split ? kGresBlock : kGresThreads);
     return SK_OK;
   }
   if (rows == 0) return SK_OK;
@@ -68,7 +68,7 @@ int colshard_launch(const float* x, float* y, int64_t rows, int64_t cols, int64_
   const size_t smem = size_t(gc.st) * gc.slice * sizeof(float);
   int P = gc.P, slice = static_cast<int>(gc.slice), nst = gc.st;
   const int grid = gc.groups * gc.P * nvr;
-  SK_CUDA(launch_k(gres_fn(mode, gc.st, split), dim3(static_cast<unsigned>(grid)),
+  SK_CUDA(launch_k(gres_fn(mode, gc.lag, split), dim3(static_cast<unsigned>(grid)),
                    dim3(split ? kGresBlock : kGresThreads), smem, s, true, x, y, rows, cols, ldx,
                    ldy, P, slice, nst, comm, bad, shift_scale(), g_gres_sleep.load(),
                    g_gres_diag.load()));

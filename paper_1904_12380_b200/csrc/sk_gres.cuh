@@ -31,9 +31,10 @@
 //   bar1  compute -> publisher  "warp pairs of row k in smem"
 //   bar2  poller -> compute     "(M, S) of row k in smem"
 //   bar3  compute -> publisher  "row k's stage consumed (proxy-fenced): refill"
-// With a ring of NS stages the output pass of row k runs after the local pass
-// of row k+L, L = NS-2 (one row loading, L+1 resident awaiting statistics);
-// the group round trip hides behind L row steps.  HBM and L2 each see
+// With a ring of NS >= L+2 stages the output pass of row k runs after the
+// local pass of row k+L: L+1 rows resident awaiting statistics, NS-L-1 rows
+// loading ahead.  The group round trip hides behind L row steps; the loads in
+// flight per SM (NS-L-1 slices) set the streaming rate for short slices.  HBM and L2 each see
 // 8 B/element: the row never leaves the chip between its three smem passes.
 #pragma once
 #include "sk_common.cuh"
@@ -43,7 +44,7 @@ namespace sk {
 constexpr int kGresCompute = 512;                   // 16 compute warps
 constexpr int kGresThreads = kGresCompute + 32;     // compute + one hand-off warp per barrier
 constexpr int kGresBlock = kGresCompute + 64;       // + publisher/TMA warp + poller warp
-constexpr int kGresStages = 5;                      // maximum ring depth (lag <= 3)
+constexpr int kGresStages = 8;                      // maximum ring depth (lag <= 3, + loads ahead)
 constexpr unsigned kGresSpinLimit = 1u << 24;       // ~10 s of polling: abort, never hang
 
 __device__ __forceinline__ void bar_sync_n(int id, int n) {
@@ -222,45 +223,46 @@ __global__ void __launch_bounds__(kGresBlock, 1)
   };
 
 
-  // wait for the group's pairs of row k in this rank's slot array, merge them
-  // in slot order (identical (M, S) on every CTA of the row, on every rank)
-  // and broadcast through smem slot k % NB.  diag & 1 (timing only): wait for
-  // this CTA's own slot, not the group's.
-  auto poll_merge = [&](unsigned k) {
-    const int pp = (diag & 1) ? 1 : WP;
-    const unsigned long long* sl = slot_set(gres_dst(comm, myr), k);
-    const unsigned tag = gres_tag(epoch, k);
-    unsigned long long wa[kGresMaxSlots / 32], wb[kGresMaxSlots / 32];
-    unsigned spins = 0;
-    while (true) {  // lane l reads slots l, l+32, ... until every word carries the tag
-      bool ok = true;
+  // Row k's pairs in this rank's slot array: lane l loads slots l, l+32, ...;
+  // true (warp-uniform) once every word carries row k's tag.  diag & 1 (timing
+  // only): this CTA's own slot instead of the group's.
+  constexpr int NI = kGresMaxSlots / 32;
+  const int pp = (diag & 1) ? 1 : WP;
+  unsigned long long* const mine = gres_dst(comm, myr);
+  auto poll_load = [&](unsigned k, unsigned long long (&wa)[NI], unsigned long long (&wb)[NI]) {
+    const unsigned long long* sl = slot_set(mine, k);
 #pragma unroll
-      for (int i = 0; i < kGresMaxSlots / 32; ++i) {
-        const int j = lane + 32 * i;
-        if (j < pp) {
-          ld_slot2(sl + 2 * ((diag & 1) ? gi : j), wa[i], wb[i], sys);
-          ok = ok && static_cast<unsigned>(wa[i] >> 32) == tag &&
-               static_cast<unsigned>(wb[i] >> 32) == tag;
-        }
-      }
-      if (__all_sync(0xffffffffu, ok)) break;
-      // back off: a spinning poller steals issue slots from its sub-partition's compute warps
-      if (SPLIT && poll_ns > 0) __nanosleep(static_cast<unsigned>(poll_ns));
-      if ((++spins & 0xFFFu) == 0) {  // a stuck peer raises abort: never hang the GPU
-        if (ld_relaxed_u32(comm.ctl + 2) || spins >= comm.spin_limit) {
-          if (lane == 0) atomicExch(comm.ctl + 2, 1u);
-          break;
-        }
-      }
+    for (int i = 0; i < NI; ++i)
+      if (lane + 32 * i < pp) ld_slot2(sl + 2 * ((diag & 1) ? gi : lane + 32 * i), wa[i], wb[i], sys);
+  };
+  auto poll_ok = [&](unsigned k, const unsigned long long (&wa)[NI], const unsigned long long (&wb)[NI]) {
+    const unsigned tag = gres_tag(epoch, k);
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+      if (lane + 32 * i < pp)
+        ok = ok && static_cast<unsigned>(wa[i] >> 32) == tag && static_cast<unsigned>(wb[i] >> 32) == tag;
+    return __all_sync(0xffffffffu, ok);
+  };
+  // a stuck peer raises abort: never hang the GPU (checked every 4096 polls)
+  auto poll_abort = [&](unsigned& spins) {
+    if ((++spins & 0xFFFu) == 0 && (ld_relaxed_u32(comm.ctl + 2) || spins >= comm.spin_limit)) {
+      if (lane == 0) atomicExch(comm.ctl + 2, 1u);
+      return true;
     }
+    return false;
+  };
+  // merge the pairs in slot order (identical (M, S) on every CTA of the row,
+  // on every rank) and broadcast through smem slot k % NB
+  auto merge_bcast = [&](unsigned k, const unsigned long long (&wa)[NI], const unsigned long long (&wb)[NI]) {
     float Mg = kPadLogit;
 #pragma unroll
-    for (int i = 0; i < kGresMaxSlots / 32; ++i)
+    for (int i = 0; i < NI; ++i)
       if (lane + 32 * i < pp) Mg = fmaxf(Mg, __uint_as_float(static_cast<unsigned>(wa[i])));
     Mg = group_max<32>(Mg);
     double S = 0.0;
 #pragma unroll
-    for (int i = 0; i < kGresMaxSlots / 32; ++i)
+    for (int i = 0; i < NI; ++i)
       if (lane + 32 * i < pp) {
         const float mj = __uint_as_float(static_cast<unsigned>(wa[i]));
         double sj = static_cast<double>(__uint_as_float(static_cast<unsigned>(wb[i])));
@@ -273,6 +275,20 @@ __global__ void __launch_bounds__(kGresBlock, 1)
       bc_m[b] = Mg * shift_scale;  // shift_scale = 0: fault hook
       bc_s[b] = S;
     }
+  };
+  // wait for row k's pairs and merge them (the poller warp, or the publisher at lag 1)
+  auto poll_merge = [&](unsigned k) {
+    unsigned long long wa[NI], wb[NI];
+    unsigned spins = 0;
+    while (true) {
+      poll_load(k, wa, wb);
+      if (poll_ok(k, wa, wb)) break;
+      // back off: a spinning poller steals issue slots from its sub-partition's
+      // compute warps, and its loads queue behind the publishers' stores
+      if (SPLIT && poll_ns > 0) __nanosleep(static_cast<unsigned>(poll_ns));
+      if (poll_abort(spins)) break;
+    }
+    merge_bcast(k, wa, wb);
   };
 
   if (g >= G) {

@@ -77,15 +77,15 @@ int softmax_dev(const float* x, float* y, int64_t rows, int64_t cols, int64_t ld
 
 // K3g planning and kernels (sk_api.cu), used by the fused column shard
 struct GresChoice {
-  int P = 0, st = 0, groups = 0;
+  int P = 0, st = 0, lag = 0, groups = 0;  // ring depth st >= lag + 2
   int64_t slice = 0;
   double score = 0.0;
 };
 
 GresChoice plan_gres(int64_t rows, int64_t cols, int mode, const DevInfo& di, int world, int nvr,
                      bool unal);
-const void* gres_fn(int mode, int nstages, bool split);
-bool gres_split(int nstages);
+const void* gres_fn(int mode, int lag, bool split);
+bool gres_split(int lag);
 // the K3g plan is modelled at this row count: plans (hence bits) depend on C only
 inline constexpr int64_t kGresPlanRows = 2048;
 

@@ -21,7 +21,8 @@ from sweep import bench_once  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c4")
-    ap.add_argument("--points", default="14:3,16:3,20:4,24:4", help="P:stages,...")
+    ap.add_argument("--points", default="14:3,16:3,20:4,24:4",
+                    help="P:stages[:lag],... (lag 0 / absent: the classic lag for the depth)")
     ap.add_argument("--reps", type=int, default=60)
     ap.add_argument("--diags", default="0,1", help="gres_diag values: 1 skips the group exchange, 2 the math, 3 both")
     ap.add_argument("--sleeps", default="128", help="poller back-off values (ns)")
@@ -34,11 +35,16 @@ def main():
     xs = [x0] + [x0.clone() for _ in range(R - 1)]
     ys = [torch.empty_like(x0) for _ in range(R)]
     s = torch.cuda.Stream()
+    # float64 torch reference of the clipped softmax (timing script check only)
+    sh = (x0.double() - x0.double().amax(1, keepdim=True)).clamp_min(-64.0).exp_()
+    ref = (sh / sh.sum(1, keepdim=True)).float()
+    del sh
     _native.set_tuning("gres", 2)
     for pt in args.points.split(","):
-        P, st = map(int, pt.split(":"))
+        P, st, lag = (list(map(int, pt.split(":"))) + [0])[:3]
         _native.set_tuning("gres_p", P)
         _native.set_tuning("gres_st", st)
+        _native.set_tuning("gres_lag", lag)
         for d, sl, sp in [(d, sl, sp) for d in map(int, args.diags.split(","))
                           for sl in map(int, args.sleeps.split(","))
                           for sp in map(int, args.splits.split(","))]:
@@ -48,11 +54,18 @@ def main():
             try:
                 us = bench_once(xs, ys, spec.rows, spec.cols, args.reps, s)
             except Exception as e:  # noqa: BLE001
-                print(json.dumps({"P": P, "stages": st, "error": str(e)}), flush=True)
+                print(json.dumps({"P": P, "stages": st, "lag": lag, "error": str(e)}), flush=True)
                 continue
-            print(json.dumps({"config": spec.name, "P": P, "stages": st, "diag": d, "sleep": sl, "split": sp, "us": us,
-                              "gbs": 8.0 * spec.rows * spec.cols / us / 1e3}), flush=True)
+            rec = {"config": spec.name, "P": P, "stages": st, "lag": lag, "diag": d, "sleep": sl, "split": sp,
+                   "us": us, "gbs": 8.0 * spec.rows * spec.cols / us / 1e3}
+            if d == 0:
+                torch.cuda.synchronize()
+                y = ys[0]
+                rec["max_rel"] = float(((y - ref).abs() / ref).max())
+                rec["plan"] = _native.describe_plan(spec.rows, spec.cols)
+            print(json.dumps(rec), flush=True)
     _native.set_tuning("gres_diag", 0)
+    _native.set_tuning("gres_lag", 0)
     from row_length_sweep import copy_us  # noqa: E402
 
     cu = copy_us(xs, ys, spec.rows * spec.cols, args.reps, s)

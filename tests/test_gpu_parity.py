@@ -31,7 +31,7 @@ def _reset_tuning():
     yield
     for k, v in (("path", -1), ("k1_lpr", 0), ("grid_mult", 0),
                  ("skip_max_shift", 0), ("k3_impl", 3), ("cluster_k3", 1),
-                 ("gres", 1), ("gres_p", 0), ("gres_st", 0), ("gres_split", -1), ("cluster_onex", 0), ("k1m", 1),
+                 ("gres", 1), ("gres_p", 0), ("gres_st", 0), ("gres_lag", 0), ("gres_split", -1), ("cluster_onex", 0), ("k1m", 1),
                  ("k1m_wpr", 0), ("k1m_nv", 0)):
         _native.set_tuning(k, v)
 
@@ -325,6 +325,45 @@ def test_k3_gres_group_sizes(P, st, split, oracle):
         _native.set_tuning("gres", 1)
         _native.set_tuning("gres_p", 0)
         _native.set_tuning("gres_st", 0)
+        _native.set_tuning("gres_split", -1)
+
+
+@pytest.mark.parametrize("P,st,lag,split", [(14, 3, 1, -1), (37, 8, 3, -1), (37, 6, 1, -1),
+                                            (37, 6, 1, 1), (24, 5, 2, -1), (74, 8, 2, 0),
+                                            (148, 8, 3, -1), (20, 4, 1, 1)])
+def test_k3_gres_lag_depth_decoupled(P, st, lag, split, oracle):
+    """K3g with the lag (rows between a row's local and output pass) set apart
+    from the ring depth: st - lag - 1 rows load ahead.  Many row steps per
+    group (so every ring slot and barrier id rotates several times), a ragged
+    last slice, clip firing, every mode; plus a non-finite row."""
+    C = 120_004
+    rows = (148 // P) * 5 + 7 if P < 148 else 23
+    x = configs.generate("c4", 1, rows)[:, :C].copy()
+    x[2, 1234] = -500.0
+    x[rows - 1, :] -= 400.0
+    _native.set_tuning("gres", 2)
+    _native.set_tuning("gres_p", P)
+    _native.set_tuning("gres_st", st)
+    _native.set_tuning("gres_lag", lag)
+    _native.set_tuning("gres_split", split)
+    try:
+        plan = gu.plan(rows, C)
+        assert plan.startswith("k3_gres nseg=%d " % P), plan
+        assert "stages=%d " % st in plan and plan.endswith(" lag=%d" % lag), plan
+        for mode in (0, 1, 2):
+            ref = oracle.softmax_ref(x, clip=(mode == 0))
+            y, bad = gu.softmax_abi(x, mode)
+            assert bad == gu.NO_BAD
+            assert_parity(oracle, y, ref, approx=(mode == 2), what=(P, st, lag, mode, plan))
+        x2 = x.copy()
+        x2[rows - 2, 17] = -np.inf
+        x2[rows - 3, C - 2] = np.nan
+        assert gu.softmax_abi(x2, 0)[1] == rows - 3
+    finally:
+        _native.set_tuning("gres", 1)
+        _native.set_tuning("gres_p", 0)
+        _native.set_tuning("gres_st", 0)
+        _native.set_tuning("gres_lag", 0)
         _native.set_tuning("gres_split", -1)
 
 
