@@ -337,31 +337,40 @@ struct K1mEntry {
 const K1mEntry kK1mTable[] = {
     // 128-bit rows
     SK_K1M(4, 2, 16), SK_K1M(4, 4, 8), SK_K1M(4, 4, 12), SK_K1M(4, 4, 16), SK_K1M(4, 8, 8),
-    // 32-bit rows (any length / alignment): 1025..8192 floats
+    SK_K1M(4, 8, 12), SK_K1M(4, 8, 16),
+    // 32-bit rows (any length / alignment): 1025..16384 floats
     SK_K1M(1, 2, 24), SK_K1M(1, 2, 32), SK_K1M(1, 2, 48), SK_K1M(1, 4, 32), SK_K1M(1, 4, 48),
-    SK_K1M(1, 8, 32)};
+    SK_K1M(1, 8, 32), SK_K1M(1, 8, 48), SK_K1M(1, 8, 64)};
 #undef SK_K1M
 const K1mEntry* k1m_find(int vec, int wpr, int nv) {
   for (const auto& e : kK1mTable)
     if (e.vec == vec && e.wpr == wpr && e.nv == nv) return &e;
   return nullptr;
 }
-constexpr int64_t kK1mMaxCols = 8192;
+constexpr int64_t kK1mCap = 16384;  // widest row a K1m instantiation holds
 std::atomic<int> g_k1m{1}, g_k1m_wpr{0}, g_k1m_nv{0};
+// widest row the planner gives K1m.  Measured (scripts/wide_k1m.py,
+// profiles/r1c_wide_k1m.jsonl): a 256-thread block holding a 12288 / 16384-float
+// row beats K3g's one-CTA rows by 2-16% (1024x16384 26.1 vs 30.3 us)
+std::atomic<int> g_k1m_max{16384};
 // measured (scripts/medium_rows.py): 16384x4096 80.5 us with (2,16) vs 101.5
 // for K2; 8192x6144 62.4 (4,12); 8192x8192 80.1 (4,16) vs 88.6 for K2
 void k1m_default(int vec, int64_t cols, int& wpr, int& nv) {
   if (vec == 4) {
     if (cols <= 4096) { wpr = 2; nv = 16; }
     else if (cols <= 6144) { wpr = 4; nv = 12; }
-    else { wpr = 4; nv = 16; }
+    else if (cols <= 8192) { wpr = 4; nv = 16; }
+    else if (cols <= 12288) { wpr = 8; nv = 12; }  // a 256-thread block per row
+    else { wpr = 8; nv = 16; }
   } else {  // 32-bit accesses
     if (cols <= 1536) { wpr = 2; nv = 24; }
     else if (cols <= 2048) { wpr = 2; nv = 32; }
     else if (cols <= 3072) { wpr = 2; nv = 48; }
     else if (cols <= 4096) { wpr = 4; nv = 32; }
     else if (cols <= 6144) { wpr = 4; nv = 48; }
-    else { wpr = 8; nv = 32; }
+    else if (cols <= 8192) { wpr = 8; nv = 32; }
+    else if (cols <= 12288) { wpr = 8; nv = 48; }
+    else { wpr = 8; nv = 64; }
   }
 }
 
@@ -504,16 +513,17 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
                     (xa % 32 == 0) && (ya % 32 == 0) && g_vec8.load();
   p.vec = vec;
   const int force = g_force_path.load();
+  const int64_t k1m_max = std::min<int64_t>(g_k1m_max.load(), kK1mCap);
   PathKind kind;
   if (force >= 0) kind = static_cast<PathKind>(force);
   else if (cols <= 1024 || (vec && cols <= kK1MaxCols)) kind = kPathK1;
-  else if (cols <= kK1mMaxCols && g_k1m.load()) kind = kPathK1m;
+  else if (cols <= k1m_max && g_k1m.load()) kind = kPathK1m;
   else if (vec) kind = kPathSeg;
   else kind = kPathSplit;
   if (kind == kPathK1 && cols > kK1MaxCols) return arg_fail("k1 path needs cols <= 3072");
   if (kind == kPathSeg && !vec) return arg_fail("seg path needs 16-B aligned rows");
 
-  if (kind == kPathSplit && force < 0 && !vec && cols > kK1mMaxCols && g_gres.load() != 0 &&
+  if (kind == kPathSplit && force < 0 && !vec && cols > k1m_max && g_gres.load() != 0 &&
       di.coop) {
     // rows of any alignment too long for one CTA: K3g with TMA on each slice's
     // aligned middle (1.7x the split path's 12 B/element on a 50257-wide vocab)
@@ -947,6 +957,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "coop_pdl") g_coop_pdl = value;
   else if (k == "k1m_wpr") g_k1m_wpr = value;
   else if (k == "k1m_nv") g_k1m_nv = value;
+  else if (k == "k1m_max_cols") g_k1m_max = value > 0 ? value : 16384;
   else if (k == "gres_timeout_spins") g_gres_spins = value > 0 ? unsigned(value) : kGresSpinLimit;
   else return arg_fail("unknown tuning key " + k);
   return SK_OK;

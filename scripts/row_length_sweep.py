@@ -46,8 +46,11 @@ def main():
     total = 16 << 20
     s = torch.cuda.Stream()
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
-    for C in (50, 128, 256, 512, 1000, 1024, 1536, 2048, 3072, 4096, 6144, 8192, 12288, 16384,
-              32768, 65536, 131072, 262144, 524288, 1048576, 2097152):
+    cs = (50, 128, 256, 512, 1000, 1024, 1536, 2048, 3072, 4096, 6144, 8192, 12288, 16384,
+          32768, 65536, 131072, 262144, 524288, 1048576, 2097152)
+    if len(sys.argv) > 1:  # C,C,...
+        cs = tuple(map(int, sys.argv[1].split(",")))
+    for C in cs:
         rows = max(8, total // C)
         spec = configs.InputSpec(f"len{C}", rows, C, "normal", 7, sigma=4.0)
         x0 = torch.from_numpy(configs.generate(spec)).cuda()

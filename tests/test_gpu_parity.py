@@ -202,10 +202,12 @@ def test_k1_medium_rows(rows, C, oracle):
 
 @pytest.mark.parametrize("rows,C", [(300, 8192), (4096, 4000), (2048, 5000), (64, 6144),
                                     (3, 8192), (1000, 3076), (4096, 5001), (300, 8191),
-                                    (2000, 1025), (7, 3001), (513, 4097), (64, 6143)])
+                                    (2000, 1025), (7, 3001), (513, 4097), (64, 6143),
+                                    (300, 12288), (37, 16384), (1000, 10000), (129, 12289),
+                                    (64, 16383), (5, 9001), (2, 16384)])
 def test_k1m_medium_rows(rows, C, oracle):
     """Rows held in the registers of 2-8 warps (K1m): 128-bit rows of
-    3073..8192 floats and rows of any length (32-bit accesses) from 1025 up --
+    3073..16384 floats and rows of any length (32-bit accesses) from 1025 up --
     every mode, clip firing, a large negative row, strided pitch, row blocks
     bit-identical to the whole matrix, non-finite detection."""
     from paper_1904_12380_b200 import tensor
@@ -235,16 +237,16 @@ def test_k1m_medium_rows(rows, C, oracle):
 
 def test_k1m_instantiations_and_k2_fallback(oracle):
     """Every K1m (warps per row, vectors per lane) shape that covers the row,
-    and the TMA block-per-row K2 (k1m off) on the same rows -- including 6144
-    columns, where K2 needs exactly 48 KB of dynamic shared memory."""
+    and the TMA block-per-row K2 / K3g (k1m off) on the same rows -- including
+    6144 columns, where K2 needs exactly 48 KB of dynamic shared memory."""
     from paper_1904_12380_b200 import tensor
 
-    for C in (4096, 6144, 8192):
+    for C in (4096, 6144, 8192, 12288, 16384):
         x = np.empty((40, C), np.float32)
         tensor.fill_normal_array(x, C, 4.0)
         ref = oracle.softmax_ref(x)
         try:
-            for wpr, nv in ((2, 16), (4, 8), (4, 12), (4, 16), (8, 8)):
+            for wpr, nv in ((2, 16), (4, 8), (4, 12), (4, 16), (8, 8), (8, 12), (8, 16)):
                 if wpr * 32 * nv * 4 < C:
                     continue
                 _native.set_tuning("k1m_wpr", wpr)
@@ -253,9 +255,12 @@ def test_k1m_instantiations_and_k2_fallback(oracle):
                 assert_parity(oracle, y, ref, what=(C, wpr, nv))
             _native.set_tuning("k1m_wpr", 0)
             _native.set_tuning("k1m", 0)
-            assert gu.plan(40, C).startswith("k2_tma"), gu.plan(40, C)
+            # k1m off: K2 up to 8192 columns; beyond, what took 8193..16384 before
+            # K1m did (K3g, or the split latency path for a 40-row job)
+            plan = gu.plan(40, C)
+            assert plan.startswith("k2_tma") if C <= 8192 else plan.startswith(("k3_gres ", "k4_split")), plan
             y, _ = gu.softmax_abi(x, 0)
-            assert_parity(oracle, y, ref, what=(C, "k2"))
+            assert_parity(oracle, y, ref, what=(C, "k1m off"))
         finally:
             _native.set_tuning("k1m", 1)
             _native.set_tuning("k1m_wpr", 0)
@@ -405,7 +410,7 @@ def test_rows_at_and_beyond_chip_capacity(C, oracle):
     assert_parity(oracle, y, oracle.softmax_ref(x, True, nthreads=0), what=plan)
 
 
-@pytest.mark.parametrize("rows,C", [(200, 50257), (40, 262147), (8, 1_000_003), (600, 8193),
+@pytest.mark.parametrize("rows,C", [(200, 50257), (40, 262147), (8, 1_000_003), (600, 16385),
                                     (300, 20001)])
 def test_k3g_unaligned_rows(rows, C, oracle):
     """Rows of any length / alignment past one CTA: K3g cuts each row's
