@@ -130,6 +130,7 @@ const K1Entry kK1Table[] = {
     SK_K1(4, 32, 4, 1, 0), SK_K1(4, 32, 8, 1, 0), SK_K1(4, 32, 1, 2, 0), SK_K1(4, 32, 2, 1, 0),
     SK_K1(4, 8, 4, 1, 1), SK_K1(4, 16, 2, 1, 1), SK_K1(4, 16, 4, 1, 1), SK_K1(4, 32, 2, 1, 1),
     SK_K1(4, 32, 4, 1, 1), SK_K1(4, 32, 8, 1, 1), SK_K1(4, 16, 1, 4, 1), SK_K1(4, 8, 1, 4, 1),
+    SK_K1(4, 4, 1, 8, 0), SK_K1(4, 8, 1, 8, 0), SK_K1(4, 16, 1, 8, 0), SK_K1(4, 16, 1, 8, 1),
     // medium rows: a warp holds up to 2048 / 3072 floats in registers
     SK_K1(4, 32, 16, 1, 0), SK_K1(4, 32, 24, 1, 0),
     // 256-bit path (cols % 8 == 0, 32-B aligned rows)
@@ -139,7 +140,8 @@ const K1Entry kK1Table[] = {
     // 32-bit path (any pitch / alignment)
     SK_K1(1, 8, 1, 4, 0), SK_K1(1, 16, 1, 4, 0), SK_K1(1, 32, 1, 4, 0), SK_K1(1, 16, 4, 2, 0),
     SK_K1(1, 32, 2, 2, 0), SK_K1(1, 32, 4, 1, 0), SK_K1(1, 32, 8, 1, 0), SK_K1(1, 32, 16, 1, 0),
-    SK_K1(1, 32, 32, 1, 0), SK_K1(1, 16, 4, 2, 1), SK_K1(1, 16, 4, 1, 1),
+    SK_K1(1, 32, 32, 1, 0), SK_K1(1, 16, 4, 2, 1), SK_K1(1, 16, 4, 1, 1), SK_K1(1, 16, 4, 4, 0),
+    SK_K1(1, 16, 4, 4, 1), SK_K1(1, 16, 4, 8, 0),
 };
 #undef SK_K1
 
@@ -154,9 +156,19 @@ constexpr int64_t kK1MaxCols = 3072;  // 128-bit rows up to here take K1
 // default K1 shape per row length (covers cols <= 1024; 128-bit rows <= 3072).  gm: grid multiplier
 // over SMs x occupancy; 0 = non-persistent (one row batch per warp, grid = rows /
 // rows-per-CTA), which measured fastest for every shape (c5a: 7.0 TB/s).
-void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u, int& pf, int& gm) {
+// The (VEC, LPR, NV) shape -- hence the bits -- is a function of C alone;
+// only U (rows per lane group), PF and the grid follow the job size.  Rows of
+// <= 64 floats in a large job (>= 4 Mi elements) stream with a persistent
+// grid (2 waves, grid-stride) and, when a row group would otherwise carry one
+// row, two rows per lane group: measured at 64 MiB (profiles/
+// r1c_k1_small_rows_sweep2.jsonl) C = 48 / 52 25.7 / 25.3 us vs 33.3 / 31.3,
+// C = 50 (32-bit) 33.3 vs 41.7, C = 8 / 20 -4 / -4 %.
+constexpr int64_t kK1LargeJob = int64_t(1) << 22;
+void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u, int& pf, int& gm,
+                int64_t elems = 0) {
   pf = 0;
   gm = 0;
+  const bool large = elems >= kK1LargeJob;
   if (vec == 8) {
     if (cols <= 64) { lpr = 8; nv = 1; u = 4; }
     else if (cols <= 128) { lpr = 16; nv = 1; u = 2; }
@@ -164,9 +176,9 @@ void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u, int& pf, int& 
     else if (cols <= 512) { lpr = 32; nv = 2; u = 1; }
     else { lpr = 32; nv = 4; u = 1; }
   } else if (vec == 4) {
-    if (cols <= 16) { lpr = 4; nv = 1; u = 4; }
-    else if (cols <= 32) { lpr = 8; nv = 1; u = 4; }
-    else if (cols <= 64) { lpr = 16; nv = 1; u = 4; }
+    if (cols <= 16) { lpr = 4; nv = 1; u = 4; gm = large ? 2 : 0; }
+    else if (cols <= 32) { lpr = 8; nv = 1; u = 4; gm = large ? 2 : 0; }
+    else if (cols <= 64) { lpr = 8; nv = 2; u = 2; gm = large ? 2 : 0; }
     else if (cols <= 128) { lpr = 8; nv = 4; u = 1; }
     else if (cols <= 256) { lpr = 16; nv = 4; u = 2; }
     else if (cols <= 512) { lpr = 32; nv = 4; u = 1; }
@@ -179,7 +191,10 @@ void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u, int& pf, int& 
     if (cols <= 8) { lpr = 8; nv = 1; u = 4; }
     else if (cols <= 16) { lpr = 16; nv = 1; u = 4; }
     else if (cols <= 32) { lpr = 32; nv = 1; u = 4; }
-    else if (cols <= 64) { lpr = 16; nv = 4; u = 1; pf = 1; }
+    else if (cols <= 64) {
+      lpr = 16; nv = 4;
+      if (large) { u = 2; gm = 2; } else { u = 1; pf = 1; }
+    }
     else if (cols <= 128) { lpr = 32; nv = 4; u = 1; }
     else if (cols <= 256) { lpr = 32; nv = 8; u = 1; }
     else if (cols <= 512) { lpr = 32; nv = 16; u = 1; }
@@ -562,7 +577,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
   if (kind == kPathK1) {
     int lpr, nv, u, pf, gm;
     const int vw = vec8 ? 8 : vec ? 4 : 1;
-    k1_default(vw, cols, lpr, nv, u, pf, gm);
+    k1_default(vw, cols, lpr, nv, u, pf, gm, rows * cols);
     if (g_k1_lpr.load() > 0) { lpr = g_k1_lpr; nv = g_k1_nv; u = g_k1_u; }
     if (g_k1_pf.load() >= 0) pf = g_k1_pf.load();
     if (g_grid_mult.load() > 0) gm = g_grid_mult.load();
