@@ -170,6 +170,29 @@ def test_k1_instantiations_all_agree(oracle):
         _native.set_tuning("k1_pf", -1)
 
 
+@pytest.mark.parametrize("C", [8, 20, 36, 48, 50, 64, 63])
+def test_k1_short_rows_job_size_keeps_bits(C, oracle):
+    """Short rows: the K1 shape is a function of C, while rows per lane group,
+    prefetch and the persistent grid follow the job size -- a large job
+    (>= 4 Mi elements) and a small row block of it must give the same bits,
+    and both match the oracle."""
+    from paper_1904_12380_b200 import tensor
+
+    rows = (1 << 22) // C + 777
+    x = np.empty((rows, C), np.float32)
+    tensor.fill_normal_array(x, C + 5, 4.0)
+    x[3, C // 2] = -300.0
+    big_plan, small_plan = gu.plan(rows, C), gu.plan(999, C)
+    key = lambda p: p.split(" u=")[0]  # noqa: E731 -- vec / lpr / nv
+    assert key(big_plan) == key(small_plan), (big_plan, small_plan)
+    whole, bad = gu.softmax_abi(x, 0)
+    assert bad == gu.NO_BAD
+    part, _ = gu.softmax_abi(x[rows - 999:], 0)
+    assert np.array_equal(part.view(np.uint32), whole[rows - 999:].view(np.uint32)), (big_plan, small_plan)
+    idx = np.r_[0:2000, rows - 2000:rows]
+    assert_parity(oracle, whole[idx], oracle.softmax_ref(x[idx]), what=(C, big_plan))
+
+
 @pytest.mark.parametrize("rows,C", [(300, 2048), (37, 1536), (4096, 3072), (5, 2052),
                                     (2000, 1028), (1, 3072)])
 def test_k1_medium_rows(rows, C, oracle):
