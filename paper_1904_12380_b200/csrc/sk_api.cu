@@ -87,6 +87,7 @@ std::atomic<int> g_k1_lpr{0}, g_k1_nv{0}, g_k1_u{0};  // force a K1 shape (0 = t
 std::atomic<int> g_k1_pf{-1};      // -1: table default, 0/1 force register prefetch
 std::atomic<int> g_grid_mult{0};   // K1 grid = SMs x occupancy x mult (0 = one batch per warp)
 std::atomic<int> g_vec8{0};        // 256-bit K1 path (measured no faster: off by default)
+std::atomic<int> g_vec2_max{128};  // widest even row the 64-bit K1 path takes (0: off)
 std::atomic<int> g_pdl{1};         // programmatic dependent launch on every kernel
 std::atomic<int> g_coop_pdl{1};    // ... also on cooperative launches (K3g; measured -0.6..1.3 us/launch)
 // long rows: 3 = K3g, else K3c (default); 5 = K3c only
@@ -137,6 +138,12 @@ const K1Entry kK1Table[] = {
     SK_K1(8, 8, 1, 4, 0), SK_K1(8, 16, 1, 2, 0), SK_K1(8, 16, 1, 4, 0), SK_K1(8, 8, 2, 1, 0),
     SK_K1(8, 8, 2, 2, 0), SK_K1(8, 16, 2, 1, 0), SK_K1(8, 32, 1, 1, 0), SK_K1(8, 32, 1, 2, 0),
     SK_K1(8, 32, 2, 1, 0), SK_K1(8, 32, 4, 1, 0), SK_K1(8, 16, 1, 1, 0),
+    // 64-bit path (even cols, 8-B aligned rows)
+    SK_K1(2, 8, 4, 1, 0), SK_K1(2, 8, 4, 2, 0), SK_K1(2, 8, 4, 1, 1), SK_K1(2, 16, 2, 1, 0),
+    SK_K1(2, 16, 2, 2, 0), SK_K1(2, 16, 2, 1, 1), SK_K1(2, 4, 8, 1, 0), SK_K1(2, 4, 8, 2, 0),
+    SK_K1(2, 8, 2, 2, 0), SK_K1(2, 8, 2, 4, 0), SK_K1(2, 16, 4, 1, 0), SK_K1(2, 32, 2, 1, 0), SK_K1(2, 32, 4, 1, 0),
+    SK_K1(2, 8, 8, 1, 0), SK_K1(2, 16, 1, 4, 0), SK_K1(2, 8, 1, 4, 0), SK_K1(2, 4, 2, 4, 0),
+    SK_K1(2, 4, 2, 8, 0), SK_K1(2, 4, 4, 4, 0), SK_K1(2, 8, 8, 2, 0), SK_K1(2, 16, 4, 2, 0), SK_K1(2, 8, 2, 1, 1),
     // 32-bit path (any pitch / alignment)
     SK_K1(1, 8, 1, 4, 0), SK_K1(1, 16, 1, 4, 0), SK_K1(1, 32, 1, 4, 0), SK_K1(1, 16, 4, 2, 0),
     SK_K1(1, 32, 2, 2, 0), SK_K1(1, 32, 4, 1, 0), SK_K1(1, 32, 8, 1, 0), SK_K1(1, 32, 16, 1, 0),
@@ -187,6 +194,25 @@ void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u, int& pf, int& 
     // 1.1-1.3x faster than the TMA block-per-row K2 from 1536 to 3072 columns
     else if (cols <= 2048) { lpr = 32; nv = 16; u = 1; }
     else { lpr = 32; nv = 24; u = 1; }
+  } else if (vec == 2) {
+    // 64-bit rows (even C, not a multiple of 4, 8-B pitch): half the memory
+    // instructions of the 32-bit shapes and fewer lanes per row (fewer
+    // shuffle levels), which is what bounds short rows.  Measured at 64 MiB
+    // (profiles/r1d_k1_vec2_*.jsonl): 1.19-1.32x over the 32-bit plan for
+    // C = 34..126, 2.6-2.9x for C = 10..30; rows per lane group follow the
+    // job size (>= 1 Mi elements: 2-4) without changing the bits.
+    const bool mid = elems >= (int64_t(1) << 20);
+    if (cols <= 16) { lpr = 4; nv = 2; u = 4; }
+    else if (cols <= 32) {
+      lpr = 8; nv = 2;
+      if (mid) u = 4; else { u = 1; pf = 1; }
+    }
+    else if (cols <= 64) {
+      lpr = 8; nv = 4;
+      if (mid) u = 2; else { u = 1; pf = 1; }
+    }
+    else if (cols <= 128) { lpr = 16; nv = 4; u = mid ? 2 : 1; }
+    else { lpr = 32; nv = 4; u = 1; }
   } else {
     if (cols <= 8) { lpr = 8; nv = 1; u = 4; }
     else if (cols <= 16) { lpr = 16; nv = 1; u = 4; }
@@ -526,6 +552,9 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
                    (ya % 16 == 0);
   const bool vec8 = vec && (cols % 8 == 0) && (ldx % 8 == 0) && (ldy % 8 == 0) &&
                     (xa % 32 == 0) && (ya % 32 == 0) && g_vec8.load();
+  // 64-bit K1 rows: even rows on 8-B pitches / bases that rule out 128-bit ones
+  const bool vec2 = !vec && cols > 8 && (cols % 2 == 0) && (ldx % 2 == 0) && (ldy % 2 == 0) &&
+                    (xa % 8 == 0) && (ya % 8 == 0) && cols <= g_vec2_max.load();
   p.vec = vec;
   const int force = g_force_path.load();
   const int64_t k1m_max = std::min<int64_t>(g_k1m_max.load(), kK1mCap);
@@ -576,7 +605,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
   }
   if (kind == kPathK1) {
     int lpr, nv, u, pf, gm;
-    const int vw = vec8 ? 8 : vec ? 4 : 1;
+    const int vw = vec8 ? 8 : vec ? 4 : vec2 ? 2 : 1;
     k1_default(vw, cols, lpr, nv, u, pf, gm, rows * cols);
     if (g_k1_lpr.load() > 0) { lpr = g_k1_lpr; nv = g_k1_nv; u = g_k1_u; }
     if (g_k1_pf.load() >= 0) pf = g_k1_pf.load();
@@ -955,6 +984,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "cluster_k3") g_cluster_k3 = value;
   else if (k == "cluster_size") g_cluster_size = value;
   else if (k == "vec8") g_vec8 = value;
+  else if (k == "vec2_max") g_vec2_max = value;
   else if (k == "cluster_onex") g_cluster_onex = value;
   else if (k == "cluster_tpb") g_cluster_tpb = value;
   else if (k == "k3_impl") {

@@ -5,7 +5,8 @@
 //   _exp_rows_scalar     kernels.py:171-174
 //   _sumscale_rows_scalar kernels.py:177-189
 // with one pass: each row is read from HBM once (128-bit streaming loads when
-// the row pitch allows, 32-bit coalesced loads otherwise), reduced with
+// the row pitch allows, else 64-bit for even rows on 8-B pitches, else 32-bit
+// coalesced loads), reduced with
 // __shfl_xor inside an aligned group of LPR lanes, and written once.
 //
 // Work unit: one warp owns U * (32/LPR) consecutive rows per iteration; lane
@@ -51,6 +52,9 @@ __device__ __forceinline__ void k1_load(RowBatch<VEC, LPR, NV, U>& B, const floa
           const float4 t = ld_stream4(xr + c);
           B.v[u][4 * j] = t.x; B.v[u][4 * j + 1] = t.y;
           B.v[u][4 * j + 2] = t.z; B.v[u][4 * j + 3] = t.w;
+        } else if constexpr (VEC == 2) {
+          const float2 t = ld_stream2(xr + c);
+          B.v[u][2 * j] = t.x; B.v[u][2 * j + 1] = t.y;
         } else {
           B.v[u][j] = ld_stream1(xr + c);
         }
@@ -145,6 +149,8 @@ __device__ __forceinline__ void k1_process(RowBatch<VEC, LPR, NV, U>& B, float* 
           const float2 b =
               scale2<MODE>(make_float2(B.v[u][4 * j + 2], B.v[u][4 * j + 3]), rcp[u]);
           st_stream4(yr + c, make_float4(a.x, a.y, b.x, b.y));
+        } else if constexpr (VEC == 2) {
+          st_stream2(yr + c, scale2<MODE>(make_float2(B.v[u][2 * j], B.v[u][2 * j + 1]), rcp[u]));
         } else {
           st_stream1(yr + c, scale1<MODE>(B.v[u][j], rcp[u]));
         }
@@ -185,7 +191,7 @@ __global__ void __launch_bounds__(kRowsThreads, (k1_min_blocks<VEC, NV, U, PF>()
     k1_rows(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int cols,
             int64_t ldx, int64_t ldy, unsigned long long* __restrict__ bad_row,
             float shift_scale) {
-  static_assert(VEC == 1 || VEC == 4 || VEC == 8, "VEC");
+  static_assert(VEC == 1 || VEC == 2 || VEC == 4 || VEC == 8, "VEC");
   static_assert(LPR >= 1 && LPR <= 32 && (LPR & (LPR - 1)) == 0, "LPR");
   constexpr int ROWS_ITER = U * (32 / LPR);
   const int lane = threadIdx.x & 31;

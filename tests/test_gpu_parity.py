@@ -32,7 +32,8 @@ def _reset_tuning():
     for k, v in (("path", -1), ("k1_lpr", 0), ("grid_mult", 0),
                  ("skip_max_shift", 0), ("k3_impl", 3), ("cluster_k3", 1),
                  ("gres", 1), ("gres_p", 0), ("gres_st", 0), ("gres_lag", 0), ("gres_split", -1), ("cluster_onex", 0), ("k1m", 1),
-                 ("k1m_wpr", 0), ("k1m_nv", 0)):
+                 ("k1m_wpr", 0), ("k1m_nv", 0), ("k1_nv", 0), ("k1_u", 0), ("k1_pf", -1),
+                 ("vec2_max", 128)):
         _native.set_tuning(k, v)
 
 
@@ -170,7 +171,44 @@ def test_k1_instantiations_all_agree(oracle):
         _native.set_tuning("k1_pf", -1)
 
 
-@pytest.mark.parametrize("C", [8, 20, 36, 48, 50, 64, 63])
+def test_k1_vec2_instantiations_all_agree(oracle):
+    """Every 64-bit K1 instantiation (even rows on 8-B pitches) against the
+    oracle, on row lengths it covers, plus the 32-bit plan of the same rows."""
+    from paper_1904_12380_b200 import tensor
+
+    shapes = {10: ((4, 2, 4, 0), (4, 2, 8, 0), (8, 1, 4, 0)),
+              26: ((8, 2, 4, 0), (8, 2, 2, 0), (8, 2, 1, 1), (4, 4, 4, 0), (16, 1, 4, 0)),
+              50: ((8, 4, 1, 0), (8, 4, 2, 0), (8, 4, 1, 1), (16, 2, 1, 0), (16, 2, 2, 0),
+                   (16, 2, 1, 1), (4, 8, 1, 0), (4, 8, 2, 0)),
+              98: ((16, 4, 1, 0), (16, 4, 2, 0), (8, 8, 1, 0), (8, 8, 2, 0), (32, 2, 1, 0)),
+              202: ((32, 4, 1, 0),)}
+    for C, shp in shapes.items():
+        x = np.empty((3001, C), np.float32)
+        tensor.fill_normal_array(x, C, 4.0)
+        x[7, 1] = -500.0
+        ref = oracle.softmax_ref(x)
+        if C <= 128:
+            assert "vec=2" in gu.plan(3001, C), gu.plan(3001, C)
+        _native.set_tuning("vec2_max", 256)
+        for lpr, nv, u, pf in shp:
+            _native.set_tuning("k1_lpr", lpr)
+            _native.set_tuning("k1_nv", nv)
+            _native.set_tuning("k1_u", u)
+            _native.set_tuning("k1_pf", pf)
+            assert f"vec=2 lpr={lpr} nv={nv} u={u}" in gu.plan(3001, C)
+            y, _ = gu.softmax_abi(x, 0)
+            assert_parity(oracle, y, ref, what=(C, lpr, nv, u, pf))
+        for k in ("k1_lpr", "k1_nv", "k1_u"):
+            _native.set_tuning(k, 0)
+        _native.set_tuning("k1_pf", -1)
+        _native.set_tuning("vec2_max", 0)
+        assert "vec=1" in gu.plan(3001, C)
+        y, _ = gu.softmax_abi(x, 0)
+        assert_parity(oracle, y, ref, what=(C, "32-bit"))
+        _native.set_tuning("vec2_max", 128)
+
+
+@pytest.mark.parametrize("C", [8, 10, 18, 20, 26, 36, 48, 50, 64, 63, 98, 126])
 def test_k1_short_rows_job_size_keeps_bits(C, oracle):
     """Short rows: the K1 shape is a function of C, while rows per lane group,
     prefetch and the persistent grid follow the job size -- a large job
