@@ -143,12 +143,17 @@ const K1Entry kK1Table[] = {
     SK_K1(2, 16, 2, 2, 0), SK_K1(2, 16, 2, 1, 1), SK_K1(2, 4, 8, 1, 0), SK_K1(2, 4, 8, 2, 0),
     SK_K1(2, 8, 2, 2, 0), SK_K1(2, 8, 2, 4, 0), SK_K1(2, 16, 4, 1, 0), SK_K1(2, 32, 2, 1, 0), SK_K1(2, 32, 4, 1, 0),
     SK_K1(2, 8, 8, 1, 0), SK_K1(2, 16, 1, 4, 0), SK_K1(2, 8, 1, 4, 0), SK_K1(2, 4, 2, 4, 0),
-    SK_K1(2, 4, 2, 8, 0), SK_K1(2, 4, 4, 4, 0), SK_K1(2, 8, 8, 2, 0), SK_K1(2, 16, 4, 2, 0), SK_K1(2, 8, 2, 1, 1),
+    SK_K1(2, 4, 2, 8, 0), SK_K1(2, 4, 4, 4, 0), SK_K1(2, 8, 8, 2, 0), SK_K1(2, 16, 4, 2, 0), SK_K1(2, 8, 2, 1, 1), SK_K1(2, 4, 2, 1, 1), SK_K1(2, 4, 2, 2, 0), SK_K1(2, 16, 4, 1, 1),
     // 32-bit path (any pitch / alignment)
     SK_K1(1, 8, 1, 4, 0), SK_K1(1, 16, 1, 4, 0), SK_K1(1, 32, 1, 4, 0), SK_K1(1, 16, 4, 2, 0),
     SK_K1(1, 32, 2, 2, 0), SK_K1(1, 32, 4, 1, 0), SK_K1(1, 32, 8, 1, 0), SK_K1(1, 32, 16, 1, 0),
     SK_K1(1, 32, 32, 1, 0), SK_K1(1, 16, 4, 2, 1), SK_K1(1, 16, 4, 1, 1), SK_K1(1, 16, 4, 4, 0),
-    SK_K1(1, 16, 4, 4, 1), SK_K1(1, 16, 4, 8, 0),
+    SK_K1(1, 16, 4, 4, 1), SK_K1(1, 16, 4, 8, 0), SK_K1(1, 8, 8, 1, 0), SK_K1(1, 8, 8, 2, 0),
+    SK_K1(1, 4, 16, 1, 0), SK_K1(1, 4, 8, 2, 0), SK_K1(1, 8, 4, 2, 0), SK_K1(1, 8, 4, 4, 0),
+    SK_K1(1, 16, 8, 1, 0), SK_K1(1, 16, 8, 2, 0), SK_K1(1, 8, 16, 1, 0), SK_K1(1, 4, 4, 4, 0),
+    SK_K1(1, 8, 2, 4, 0), SK_K1(1, 4, 4, 1, 1), SK_K1(1, 4, 4, 2, 0), SK_K1(1, 8, 4, 1, 1),
+    SK_K1(1, 8, 8, 1, 1), SK_K1(1, 16, 8, 1, 1), SK_K1(1, 4, 2, 4, 0), SK_K1(1, 2, 4, 4, 0),
+    SK_K1(1, 2, 4, 8, 0), SK_K1(1, 4, 2, 8, 0), SK_K1(1, 2, 4, 1, 1), SK_K1(1, 2, 4, 2, 0),
 };
 #undef SK_K1
 
@@ -202,7 +207,12 @@ void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u, int& pf, int& 
     // C = 34..126, 2.6-2.9x for C = 10..30; rows per lane group follow the
     // job size (>= 1 Mi elements: 2-4) without changing the bits.
     const bool mid = elems >= (int64_t(1) << 20);
-    if (cols <= 16) { lpr = 4; nv = 2; u = 4; }
+    if (cols <= 16) {
+      lpr = 4; nv = 2;
+      if (elems >= (int64_t(1) << 21)) u = 4;
+      else if (elems >= (int64_t(1) << 18)) u = 2;
+      else { u = 1; pf = 1; }
+    }
     else if (cols <= 32) {
       lpr = 8; nv = 2;
       if (mid) u = 4; else { u = 1; pf = 1; }
@@ -211,17 +221,35 @@ void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u, int& pf, int& 
       lpr = 8; nv = 4;
       if (mid) u = 2; else { u = 1; pf = 1; }
     }
-    else if (cols <= 128) { lpr = 16; nv = 4; u = mid ? 2 : 1; }
+    else if (cols <= 128) {
+      lpr = 16; nv = 4;
+      if (mid) u = 2; else { u = 1; pf = 1; }
+    }
     else { lpr = 32; nv = 4; u = 1; }
   } else {
-    if (cols <= 8) { lpr = 8; nv = 1; u = 4; }
-    else if (cols <= 16) { lpr = 16; nv = 1; u = 4; }
-    else if (cols <= 32) { lpr = 32; nv = 1; u = 4; }
-    else if (cols <= 64) {
-      lpr = 16; nv = 4;
-      if (large) { u = 2; gm = 2; } else { u = 1; pf = 1; }
+    // 32-bit rows: few lanes per row (2 / 4 / 8 / 8 / 16 for C <= 8 / 16 /
+    // 32 / 64 / 128) -- short rows are bound by instructions per element
+    // (memory instructions, shuffle levels), not by sectors.  Measured at
+    // 64 MiB (profiles/r1d_k1_odd_*.jsonl): 1.1-2.7x the former 8-32-lane
+    // shapes; small jobs take one row per group with prefetch.
+    const bool mid = elems >= (int64_t(1) << 20);
+    if (cols <= 8) {
+      lpr = 2; nv = 4;
+      if (elems >= (int64_t(1) << 21)) u = 4; else { u = 1; pf = 1; }
     }
-    else if (cols <= 128) { lpr = 32; nv = 4; u = 1; }
+    else if (cols <= 16) {
+      lpr = 4; nv = 4;
+      if (large) u = 4; else { u = 1; pf = 1; }
+    }
+    else if (cols <= 32) { lpr = 8; nv = 4; u = large ? 4 : 2; }
+    else if (cols <= 64) {
+      lpr = 8; nv = 8;
+      if (large) { u = 2; gm = 2; } else if (mid) u = 2; else { u = 1; pf = 1; }
+    }
+    else if (cols <= 128) {
+      lpr = 16; nv = 8;
+      if (mid) u = 2; else { u = 1; pf = 1; }
+    }
     else if (cols <= 256) { lpr = 32; nv = 8; u = 1; }
     else if (cols <= 512) { lpr = 32; nv = 16; u = 1; }
     else { lpr = 32; nv = 32; u = 1; }

@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--rows4096", action="store_true", help="also 4096-row jobs (config c1's size)")
     ap.add_argument("--shapes", default="8:4:1,8:4:2,16:2:1,16:2:2,4:8:1,4:8:2,8:2:4,16:1:4,8:1:4",
                     help="forced 64-bit K1 shapes LPR:NV:U[:PF] (those covering C are run)")
+    ap.add_argument("--vec1", action="store_true", help="forced shapes are 32-bit (odd rows)")
     ap.add_argument("--reps", type=int, default=2000)
     args = ap.parse_args()
     s = torch.cuda.Stream()
@@ -53,10 +54,14 @@ def main():
             del sh
             cu = copy_us(xs, ys, rows * C, 50, s)
             points = [("v1", {"vec2_max": 0}), ("v2", {})]
+            vw = 1 if args.vec1 else 2
             for shp in filter(None, args.shapes.split(",")):
                 lpr, nv, u, pf = (list(map(int, shp.split(":"))) + [0])[:4]
-                if lpr * nv * 2 >= C and lpr * (nv - 1) * 2 < C:
-                    points.append((shp, {"k1_lpr": lpr, "k1_nv": nv, "k1_u": u, "k1_pf": pf}))
+                if C <= lpr * nv * vw < 2 * C:
+                    t = {"k1_lpr": lpr, "k1_nv": nv, "k1_u": u, "k1_pf": pf}
+                    if args.vec1:
+                        t["vec2_max"] = 0
+                    points.append((shp, t))
             for tag, tun in points:
                 reset()
                 for k, v in tun.items():

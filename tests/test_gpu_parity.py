@@ -208,7 +208,7 @@ def test_k1_vec2_instantiations_all_agree(oracle):
         _native.set_tuning("vec2_max", 128)
 
 
-@pytest.mark.parametrize("C", [8, 10, 18, 20, 26, 36, 48, 50, 64, 63, 98, 126])
+@pytest.mark.parametrize("C", [3, 5, 8, 10, 13, 18, 20, 25, 26, 36, 48, 50, 64, 63, 75, 98, 126, 127])
 def test_k1_short_rows_job_size_keeps_bits(C, oracle):
     """Short rows: the K1 shape is a function of C, while rows per lane group,
     prefetch and the persistent grid follow the job size -- a large job
