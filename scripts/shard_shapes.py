@@ -30,7 +30,7 @@ def parse_points(s):
             out.append((tok, {"k3_impl": 5}))
         elif tok == "split":
             out.append((tok, {"path": 2}))
-        elif tok.startswith("t"):  # t<diag>: default plan, diag bits that keep results (8: TMA stores)
+        elif tok.startswith("t"):  # t<diag>: default plan with diag bits that keep results (experiments)
             out.append((tok, {"gres_diag": int(tok[1:])}))
         elif tok.startswith("d"):  # d<diag>: default plan, parts switched off
             out.append((tok, {"gres": 2, "gres_diag": int(tok[1:])}))
