@@ -132,6 +132,9 @@ const K1Entry kK1Table[] = {
     SK_K1(4, 8, 4, 1, 1), SK_K1(4, 16, 2, 1, 1), SK_K1(4, 16, 4, 1, 1), SK_K1(4, 32, 2, 1, 1),
     SK_K1(4, 32, 4, 1, 1), SK_K1(4, 32, 8, 1, 1), SK_K1(4, 16, 1, 4, 1), SK_K1(4, 8, 1, 4, 1),
     SK_K1(4, 4, 1, 8, 0), SK_K1(4, 8, 1, 8, 0), SK_K1(4, 16, 1, 8, 0), SK_K1(4, 16, 1, 8, 1),
+    SK_K1(4, 4, 2, 4, 0), SK_K1(4, 4, 2, 2, 0), SK_K1(4, 4, 4, 2, 0), SK_K1(4, 4, 4, 1, 0),
+    SK_K1(4, 4, 8, 1, 0), SK_K1(4, 4, 4, 1, 1), SK_K1(4, 4, 8, 1, 1), SK_K1(4, 8, 8, 1, 0),
+    SK_K1(4, 8, 8, 2, 0), SK_K1(4, 4, 16, 1, 0),
     // medium rows: a warp holds up to 2048 / 3072 floats in registers
     SK_K1(4, 32, 16, 1, 0), SK_K1(4, 32, 24, 1, 0),
     // 256-bit path (cols % 8 == 0, 32-B aligned rows)
@@ -189,10 +192,12 @@ void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u, int& pf, int& 
     else { lpr = 32; nv = 4; u = 1; }
   } else if (vec == 4) {
     if (cols <= 16) { lpr = 4; nv = 1; u = 4; gm = large ? 2 : 0; }
-    else if (cols <= 32) { lpr = 8; nv = 1; u = 4; gm = large ? 2 : 0; }
-    else if (cols <= 64) { lpr = 8; nv = 2; u = 2; gm = large ? 2 : 0; }
+    // 17-64 floats: 4 lanes per row (profiles/r1d_k1_vec4_sweep.jsonl: 1.07-1.25x
+    // the 8-lane shapes at 8-64 MiB); 129-256: one row per group unless large
+    else if (cols <= 32) { lpr = 4; nv = 2; u = 2; gm = large ? 2 : 0; }
+    else if (cols <= 64) { lpr = 4; nv = 4; u = 1; gm = large ? 2 : 0; }
     else if (cols <= 128) { lpr = 8; nv = 4; u = 1; }
-    else if (cols <= 256) { lpr = 16; nv = 4; u = 2; }
+    else if (cols <= 256) { lpr = 16; nv = 4; u = large ? 2 : 1; }
     else if (cols <= 512) { lpr = 32; nv = 4; u = 1; }
     else if (cols <= 1024) { lpr = 32; nv = 8; u = 1; }
     // medium rows: a whole warp holds the row in registers -- measured

@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--shapes", default="8:4:1,8:4:2,16:2:1,16:2:2,4:8:1,4:8:2,8:2:4,16:1:4,8:1:4",
                     help="forced 64-bit K1 shapes LPR:NV:U[:PF] (those covering C are run)")
     ap.add_argument("--vec1", action="store_true", help="forced shapes are 32-bit (odd rows)")
+    ap.add_argument("--vw", type=int, default=2, help="vector width of the forced shapes (2, or 4 for 128-bit rows)")
     ap.add_argument("--reps", type=int, default=2000)
     args = ap.parse_args()
     s = torch.cuda.Stream()
@@ -54,7 +55,7 @@ def main():
             del sh
             cu = copy_us(xs, ys, rows * C, 50, s)
             points = [("v1", {"vec2_max": 0}), ("v2", {})]
-            vw = 1 if args.vec1 else 2
+            vw = 1 if args.vec1 else args.vw
             for shp in filter(None, args.shapes.split(",")):
                 lpr, nv, u, pf = (list(map(int, shp.split(":"))) + [0])[:4]
                 if C <= lpr * nv * vw < 2 * C:
