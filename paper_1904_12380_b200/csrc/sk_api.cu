@@ -135,6 +135,17 @@ const K1Entry kK1Table[] = {
     SK_K1(4, 4, 2, 4, 0), SK_K1(4, 4, 2, 2, 0), SK_K1(4, 4, 4, 2, 0), SK_K1(4, 4, 4, 1, 0),
     SK_K1(4, 4, 8, 1, 0), SK_K1(4, 4, 4, 1, 1), SK_K1(4, 4, 8, 1, 1), SK_K1(4, 8, 8, 1, 0),
     SK_K1(4, 8, 8, 2, 0), SK_K1(4, 4, 16, 1, 0),
+    // exact-fit vectors per lane (kK1Fit): no padded slots for C just above 2^k
+    SK_K1(4, 4, 3, 1, 0), SK_K1(4, 8, 3, 1, 0), SK_K1(4, 16, 3, 1, 0), SK_K1(4, 16, 3, 2, 0),
+    SK_K1(4, 32, 3, 1, 0), SK_K1(4, 32, 5, 1, 0), SK_K1(4, 32, 6, 1, 0), SK_K1(4, 32, 7, 1, 0),
+    SK_K1(4, 32, 12, 1, 0), SK_K1(4, 32, 20, 1, 0),
+    SK_K1(2, 8, 3, 2, 0), SK_K1(2, 8, 3, 1, 1), SK_K1(2, 16, 3, 2, 0), SK_K1(2, 16, 3, 1, 1),
+    SK_K1(1, 2, 3, 4, 0), SK_K1(1, 2, 3, 1, 1), SK_K1(1, 4, 3, 4, 0), SK_K1(1, 4, 3, 1, 1),
+    SK_K1(1, 8, 3, 4, 0), SK_K1(1, 8, 3, 2, 0), SK_K1(1, 8, 5, 2, 0), SK_K1(1, 8, 5, 1, 1),
+    SK_K1(1, 8, 6, 2, 0), SK_K1(1, 8, 6, 1, 1), SK_K1(1, 8, 7, 2, 0), SK_K1(1, 8, 7, 1, 1),
+    SK_K1(1, 16, 5, 2, 0), SK_K1(1, 16, 5, 1, 1), SK_K1(1, 16, 6, 2, 0), SK_K1(1, 16, 6, 1, 1),
+    SK_K1(1, 16, 7, 2, 0), SK_K1(1, 16, 7, 1, 1), SK_K1(1, 32, 5, 1, 0), SK_K1(1, 32, 6, 1, 0),
+    SK_K1(1, 32, 7, 1, 0),
     // medium rows: a warp holds up to 2048 / 3072 floats in registers
     SK_K1(4, 32, 16, 1, 0), SK_K1(4, 32, 24, 1, 0),
     // 256-bit path (cols % 8 == 0, 32-B aligned rows)
@@ -164,6 +175,28 @@ const K1Entry* k1_find(int vec, int lpr, int nv, int u, int pf) {
   for (const auto& e : kK1Table)
     if (e.vec == vec && e.lpr == lpr && e.nv == nv && e.u == u && e.pf == pf) return &e;
   return nullptr;
+}
+
+// (VEC, LPR, NV) shapes the planner may shrink NV to -- the fewest vectors per
+// lane that cover the row -- for every rows-per-group / prefetch variant the
+// job-size policy of k1_default picks, so the shape (hence the bits) stays a
+// function of C alone.
+struct K1Fit {
+  int vec, lpr, nv;
+};
+constexpr K1Fit kK1Fit[] = {{4, 4, 3},  {4, 8, 3},  {4, 16, 3}, {4, 32, 3},  {4, 32, 5},
+                            {4, 32, 6}, {4, 32, 7}, {4, 32, 12}, {4, 32, 20}, {2, 8, 3},
+                            {2, 16, 3}, {1, 2, 3},  {1, 4, 3},  {1, 8, 3},   {1, 8, 5},
+                            {1, 8, 6},  {1, 8, 7},  {1, 16, 5}, {1, 16, 6},  {1, 16, 7},
+                            {1, 32, 5}, {1, 32, 6}, {1, 32, 7}};
+std::atomic<int> g_k1_fit{1};
+int k1_fit_nv(int vec, int lpr, int nv, int64_t cols) {
+  if (!g_k1_fit.load()) return nv;
+  const int fit = static_cast<int>((cols + int64_t(lpr) * vec - 1) / (int64_t(lpr) * vec));
+  if (fit >= nv) return nv;
+  for (const auto& f : kK1Fit)
+    if (f.vec == vec && f.lpr == lpr && f.nv == fit) return fit;
+  return nv;
 }
 
 constexpr int64_t kK1MaxCols = 3072;  // 128-bit rows up to here take K1
@@ -640,6 +673,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     int lpr, nv, u, pf, gm;
     const int vw = vec8 ? 8 : vec ? 4 : vec2 ? 2 : 1;
     k1_default(vw, cols, lpr, nv, u, pf, gm, rows * cols);
+    nv = k1_fit_nv(vw, lpr, nv, cols);
     if (g_k1_lpr.load() > 0) { lpr = g_k1_lpr; nv = g_k1_nv; u = g_k1_u; }
     if (g_k1_pf.load() >= 0) pf = g_k1_pf.load();
     if (g_grid_mult.load() > 0) gm = g_grid_mult.load();
@@ -1032,6 +1066,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "gres_split") g_gres_split = value;
   else if (k == "gres_lag") g_gres_lag = value;
   else if (k == "k1m") g_k1m = value;
+  else if (k == "k1_fit") g_k1_fit = value;
   else if (k == "coop_pdl") g_coop_pdl = value;
   else if (k == "k1m_wpr") g_k1m_wpr = value;
   else if (k == "k1m_nv") g_k1m_nv = value;
