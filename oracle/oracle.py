@@ -164,16 +164,30 @@ def max_abs_err(got: np.ndarray, ref: np.ndarray) -> float:
     return float(np.max(np.abs(g - np.asarray(ref, dtype=np.float64)))) if g.size else 0.0
 
 
+#: the flush threshold of the unclipped rungs (kernels.py:101, :186-188)
+FLT_MIN_NORMAL = 1.1754943508222875e-38
+
+
 def max_rel_err(got: np.ndarray, ref: np.ndarray) -> float:
     """Largest |got - ref| / |ref| over ref != 0; inf if got is non-finite or
     differs from an exact-zero reference (oracle.py:52-61 assumes ref > 0,
-    which the clip guarantees; unclipped references may hold exact zeros)."""
+    which the clip guarantees; unclipped references may hold exact zeros).
+
+    Flush boundary: the unclipped rungs flush y < FLT_MIN to +0, so a value
+    within the relative tolerance of FLT_MIN may legitimately land on either
+    side.  A zero against a value <= FLT_MIN * (1 + 1e-5) counts as a match;
+    any other zero / non-zero disagreement is inf."""
     g = np.asarray(got, dtype=np.float64)
     r = np.asarray(ref, dtype=np.float64)
     if not np.isfinite(g).all():
         return float("inf")
     if g.size == 0:
         return 0.0
+    edge = FLT_MIN_NORMAL * (1.0 + 1e-5)
+    flip = ((r == 0) & (g != 0) & (np.abs(g) <= edge)) | ((g == 0) & (r != 0) & (np.abs(r) <= edge))
+    if flip.any():
+        g = np.where(flip, 0.0, g)
+        r = np.where(flip, 0.0, r)
     nz = r != 0
     if np.any(g[~nz] != 0):
         return float("inf")

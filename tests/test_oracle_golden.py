@@ -93,6 +93,12 @@ def test_metrics():
     assert o.max_rowsum_dev(np.array([[0.5, 0.6]])) == pytest.approx(0.1)
     assert o.max_rel_err(np.array([[np.nan, 1.0]]), ref) == float("inf")
     assert o.max_rel_err(np.array([[1e-30, 1.0]]), np.array([[0.0, 1.0]])) == float("inf")
+    # flush boundary (unclipped rungs): FLT_MIN within the relative tolerance
+    # may land on either side of the y < FLT_MIN -> 0 flush
+    fm = np.float32(1.1754943508222875e-38)
+    assert o.max_rel_err(np.array([[fm, 1.0]]), np.array([[0.0, 1.0]])) == 0.0
+    assert o.max_rel_err(np.array([[0.0, 1.0]]), np.array([[fm, 1.0]])) == 0.0
+    assert o.max_rel_err(np.array([[fm * 1.001, 1.0]]), np.array([[0.0, 1.0]])) == float("inf")
 
 
 def _component_rows(g):
