@@ -138,7 +138,10 @@ const K1Entry kK1Table[] = {
     // exact-fit vectors per lane (kK1Fit): no padded slots for C just above 2^k
     SK_K1(4, 4, 3, 1, 0), SK_K1(4, 8, 3, 1, 0), SK_K1(4, 16, 3, 1, 0), SK_K1(4, 16, 3, 2, 0),
     SK_K1(4, 32, 3, 1, 0), SK_K1(4, 32, 5, 1, 0), SK_K1(4, 32, 6, 1, 0), SK_K1(4, 32, 7, 1, 0),
-    SK_K1(4, 32, 12, 1, 0), SK_K1(4, 32, 20, 1, 0),
+    SK_K1(4, 32, 12, 1, 0), SK_K1(4, 32, 20, 1, 0), SK_K1(4, 32, 9, 1, 0), SK_K1(4, 32, 10, 1, 0),
+    SK_K1(4, 32, 11, 1, 0), SK_K1(4, 32, 13, 1, 0), SK_K1(4, 32, 14, 1, 0), SK_K1(4, 32, 15, 1, 0),
+    SK_K1(4, 32, 17, 1, 0), SK_K1(4, 32, 18, 1, 0), SK_K1(4, 32, 19, 1, 0), SK_K1(4, 32, 21, 1, 0),
+    SK_K1(4, 32, 22, 1, 0), SK_K1(4, 32, 23, 1, 0),
     SK_K1(2, 8, 3, 2, 0), SK_K1(2, 8, 3, 1, 1), SK_K1(2, 16, 3, 2, 0), SK_K1(2, 16, 3, 1, 1),
     SK_K1(1, 2, 3, 4, 0), SK_K1(1, 2, 3, 1, 1), SK_K1(1, 4, 3, 4, 0), SK_K1(1, 4, 3, 1, 1),
     SK_K1(1, 8, 3, 4, 0), SK_K1(1, 8, 3, 2, 0), SK_K1(1, 8, 5, 2, 0), SK_K1(1, 8, 5, 1, 1),
@@ -185,7 +188,10 @@ struct K1Fit {
   int vec, lpr, nv;
 };
 constexpr K1Fit kK1Fit[] = {{4, 4, 3},  {4, 8, 3},  {4, 16, 3}, {4, 32, 3},  {4, 32, 5},
-                            {4, 32, 6}, {4, 32, 7}, {4, 32, 12}, {4, 32, 20}, {2, 8, 3},
+                            {4, 32, 6}, {4, 32, 7}, {4, 32, 9},  {4, 32, 10}, {4, 32, 11},
+                            {4, 32, 12}, {4, 32, 13}, {4, 32, 14}, {4, 32, 15}, {4, 32, 17},
+                            {4, 32, 18}, {4, 32, 19}, {4, 32, 20}, {4, 32, 21}, {4, 32, 22},
+                            {4, 32, 23}, {2, 8, 3},
                             {2, 16, 3}, {1, 2, 3},  {1, 4, 3},  {1, 8, 3},   {1, 8, 5},
                             {1, 8, 6},  {1, 8, 7},  {1, 16, 5}, {1, 16, 6},  {1, 16, 7},
                             {1, 32, 5}, {1, 32, 6}, {1, 32, 7}};
