@@ -451,6 +451,10 @@ const K1mEntry kK1mTable[] = {
     // 128-bit rows
     SK_K1M(4, 2, 16), SK_K1M(4, 4, 8), SK_K1M(4, 4, 12), SK_K1M(4, 4, 16), SK_K1M(4, 8, 8),
     SK_K1M(4, 8, 12), SK_K1M(4, 8, 16),
+    // exact fit (fewest float4 per thread covering the row, k1m_fit_nv)
+    SK_K1M(4, 2, 13), SK_K1M(4, 2, 14), SK_K1M(4, 2, 15), SK_K1M(4, 4, 9), SK_K1M(4, 4, 10),
+    SK_K1M(4, 4, 11), SK_K1M(4, 4, 13), SK_K1M(4, 4, 14), SK_K1M(4, 4, 15), SK_K1M(4, 8, 9),
+    SK_K1M(4, 8, 10), SK_K1M(4, 8, 11), SK_K1M(4, 8, 13), SK_K1M(4, 8, 14), SK_K1M(4, 8, 15),
     // 32-bit rows (any length / alignment): 1025..16384 floats
     SK_K1M(1, 2, 24), SK_K1M(1, 2, 32), SK_K1M(1, 2, 48), SK_K1M(1, 4, 32), SK_K1M(1, 4, 48),
     SK_K1M(1, 8, 32), SK_K1M(1, 8, 48), SK_K1M(1, 8, 64)};
@@ -664,6 +668,10 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     const int vw = vec ? 4 : 1;
     int wpr, nv;
     k1m_default(vw, cols, wpr, nv);
+    if (vw == 4 && g_k1_fit.load()) {  // exact fit: the fewest float4 per thread
+      const int fit = static_cast<int>((cols + int64_t(wpr) * 128 - 1) / (int64_t(wpr) * 128));
+      if (fit < nv && k1m_find(vw, wpr, fit)) nv = fit;
+    }
     if (g_k1m_wpr.load() > 0) { wpr = g_k1m_wpr; nv = g_k1m_nv; }
     const K1mEntry* e = k1m_find(vw, wpr, nv);
     if (!e) return arg_fail("no K1m instantiation for the requested shape");
