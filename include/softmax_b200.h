@@ -204,6 +204,10 @@ void sk_free_pinned(void* p);
  *   "k1_pf", "pdl"   K1 register prefetch (-1 table default), PDL on launches (1)
  *   "vec8"           1: K1 uses 256-bit loads/stores when cols % 8 == 0 and rows
  *                    are 32-B aligned (measured no faster than 128-bit; default 0)
+ *   "vec2_max"       widest even row (not a multiple of 4, 8-B pitch / bases) K1
+ *                    loads as 64-bit pairs (default 128; 0: 32-bit accesses)
+ *   "k1_fit"         1 (default): K1 / K1m shrink the vectors per lane to the fewest
+ *                    that cover the row (no padded slots); 0: power-of-two shapes
  *   "grid_mult"      K1 grid = SMs * occupancy * grid_mult (default: one row batch
  *                    per warp, i.e. no grid-stride loop)
  *   "k1m"            1 (default): rows of 1025..8192 floats not taken by K1 go to
