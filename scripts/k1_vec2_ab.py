@@ -38,7 +38,7 @@ def main():
                     help="forced 64-bit K1 shapes LPR:NV:U[:PF] (those covering C are run)")
     ap.add_argument("--vec1", action="store_true", help="forced shapes are 32-bit (odd rows)")
     ap.add_argument("--vw", type=int, default=2, help="vector width of the forced shapes (2, or 4 for 128-bit rows)")
-    ap.add_argument("--ab", default="", help="A/B a tuning knob: <knob>=0 against the default")
+    ap.add_argument("--ab", default="", help="A/B a tuning knob: <knob>[=<value>, default 0] against the default")
     ap.add_argument("--reps", type=int, default=2000)
     args = ap.parse_args()
     s = torch.cuda.Stream()
@@ -56,8 +56,11 @@ def main():
             ref = (sh / sh.sum(1, keepdim=True)).float()
             del sh
             cu = copy_us(xs, ys, rows * C, 50, s)
-            points = ([(f"{args.ab}=0", {args.ab: 0}), ("default", {})] if args.ab
-                      else [("v1", {"vec2_max": 0}), ("v2", {})])
+            if args.ab:
+                knob, _, val = args.ab.partition("=")
+                points = [(f"{knob}={val or 0}", {knob: int(val or 0)}), ("default", {})]
+            else:
+                points = [("v1", {"vec2_max": 0}), ("v2", {})]
             vw = 1 if args.vec1 else args.vw
             for shp in filter(None, args.shapes.split(",")):
                 lpr, nv, u, pf = (list(map(int, shp.split(":"))) + [0])[:4]
