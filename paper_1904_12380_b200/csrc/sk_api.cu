@@ -148,7 +148,11 @@ const K1Entry kK1Table[] = {
     SK_K1(1, 8, 6, 2, 0), SK_K1(1, 8, 6, 1, 1), SK_K1(1, 8, 7, 2, 0), SK_K1(1, 8, 7, 1, 1),
     SK_K1(1, 16, 5, 2, 0), SK_K1(1, 16, 5, 1, 1), SK_K1(1, 16, 6, 2, 0), SK_K1(1, 16, 6, 1, 1),
     SK_K1(1, 16, 7, 2, 0), SK_K1(1, 16, 7, 1, 1), SK_K1(1, 32, 5, 1, 0), SK_K1(1, 32, 6, 1, 0),
-    SK_K1(1, 32, 7, 1, 0),
+    SK_K1(1, 32, 7, 1, 0), SK_K1(1, 32, 9, 1, 0), SK_K1(1, 32, 10, 1, 0), SK_K1(1, 32, 11, 1, 0),
+    SK_K1(1, 32, 12, 1, 0), SK_K1(1, 32, 13, 1, 0), SK_K1(1, 32, 14, 1, 0), SK_K1(1, 32, 15, 1, 0),
+    SK_K1(1, 32, 17, 1, 0), SK_K1(1, 32, 18, 1, 0), SK_K1(1, 32, 19, 1, 0), SK_K1(1, 32, 20, 1, 0),
+    SK_K1(1, 32, 21, 1, 0), SK_K1(1, 32, 22, 1, 0), SK_K1(1, 32, 23, 1, 0), SK_K1(1, 32, 24, 1, 0),
+
     // medium rows: a warp holds up to 2048 / 3072 floats in registers
     SK_K1(4, 32, 16, 1, 0), SK_K1(4, 32, 24, 1, 0),
     // 256-bit path (cols % 8 == 0, 32-B aligned rows)
@@ -194,7 +198,10 @@ constexpr K1Fit kK1Fit[] = {{4, 4, 3},  {4, 8, 3},  {4, 16, 3}, {4, 32, 3},  {4,
                             {4, 32, 23}, {2, 8, 3},
                             {2, 16, 3}, {1, 2, 3},  {1, 4, 3},  {1, 8, 3},   {1, 8, 5},
                             {1, 8, 6},  {1, 8, 7},  {1, 16, 5}, {1, 16, 6},  {1, 16, 7},
-                            {1, 32, 5}, {1, 32, 6}, {1, 32, 7}};
+                            {1, 32, 5}, {1, 32, 6}, {1, 32, 7},  {1, 32, 9},  {1, 32, 10},
+                            {1, 32, 11}, {1, 32, 12}, {1, 32, 13}, {1, 32, 14}, {1, 32, 15},
+                            {1, 32, 17}, {1, 32, 18}, {1, 32, 19}, {1, 32, 20}, {1, 32, 21},
+                            {1, 32, 22}, {1, 32, 23}, {1, 32, 24}};  // 25-31: measured slower
 std::atomic<int> g_k1_fit{1};
 int k1_fit_nv(int vec, int lpr, int nv, int64_t cols) {
   if (!g_k1_fit.load()) return nv;
