@@ -226,6 +226,10 @@ void sk_free_pinned(void* p);
  *   "cluster_onex"   1: K3c exchanges one (max, sum) pair per row and recomputes
  *                    exp; 0 (default): two exchanges (max, then sum), exp kept in smem
  *   "cluster_tpb"    K3c threads per CTA (512 default, or 1024)
+ *   "k4_fuse_combine" 1 (default): the split path merges each row's partial
+ *                    statistics inside its normalize pass (2 launches) when the
+ *                    job has <= 4096 (row, chunk) items; 2: always; 0: a separate
+ *                    combine kernel (3 launches; same bits either way)
  *   "host_chunk_kb"  sk_softmax_f32_host chunk size in KiB (0 = auto, ~1/4 of the job)
  *   "host_zero_copy" 1: pinned host buffers with rows <= 8192 are read and written
  *                    by the kernel directly over PCIe (measured no faster than

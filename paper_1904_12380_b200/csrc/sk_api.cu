@@ -881,6 +881,7 @@ int check_common(const float* x, const void* y, int64_t rows, int64_t cols, int6
   return SK_OK;
 }
 
+std::atomic<int> g_k4_fuse_combine{1};  // split path: merge the row stats inside normalize
 int launch_split(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
                  int64_t ldy, int mode, bool v4, unsigned long long* bad, char* ws, int nch,
                  bool normalize, float* rmax_out, double* rsum_out, cudaStream_t s) {
@@ -901,6 +902,31 @@ int launch_split(const float* x, float* y, int64_t rows, int64_t cols, int64_t l
                                  : reinterpret_cast<const void*>(&k4_stats<kApprox, 1>));
   SK_CUDA(launch_k(stats, g, dim3(kSplitThreads), 0, s, false, x, rows, cols, ldx, nch, part,
                    bad, sh));
+  if (normalize && !rmax_out && !rsum_out && g_k4_fuse_combine.load() &&
+      (rows * nch <= 4096 || g_k4_fuse_combine.load() == 2)) {
+    // two launches: the row statistics are merged inside the normalize pass --
+    // for decode-sized jobs, where the third launch is a visible share
+    // (8x50257 6.90 -> 6.53 us, 32x151936 15.6 -> 14.7, 64x128256 21.6 -> 19.9);
+    // with many items every item re-merging its row's partials costs more
+    // (1024x50257: 118 -> 125 us), profiles/r1d_split_fused_combine.jsonl
+    const void* nr;
+    switch (mode) {
+      case kClipAccurate:
+        nr = v4 ? reinterpret_cast<const void*>(&k4_normalize_rows<kClipAccurate, 4>)
+                : reinterpret_cast<const void*>(&k4_normalize_rows<kClipAccurate, 1>);
+        break;
+      case kAccurate:
+        nr = v4 ? reinterpret_cast<const void*>(&k4_normalize_rows<kAccurate, 4>)
+                : reinterpret_cast<const void*>(&k4_normalize_rows<kAccurate, 1>);
+        break;
+      default:
+        nr = v4 ? reinterpret_cast<const void*>(&k4_normalize_rows<kApprox, 4>)
+                : reinterpret_cast<const void*>(&k4_normalize_rows<kApprox, 1>);
+    }
+    SK_CUDA(launch_k(nr, g, dim3(kSplitThreads), 0, s, false, x, y, rows, cols, ldx, ldy, nch,
+                     static_cast<const RowPartial*>(part)));
+    return SK_OK;
+  }
   SK_CUDA(launch_k(reinterpret_cast<const void*>(&k4_combine),
                    dim3(static_cast<unsigned>((rows * 32 + 255) / 256)), dim3(256), 0, s, false,
                    static_cast<const RowPartial*>(part), rows, nch, rmax, rsum));
@@ -1088,6 +1114,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "gres_lag") g_gres_lag = value;
   else if (k == "k1m") g_k1m = value;
   else if (k == "k1_fit") g_k1_fit = value;
+  else if (k == "k4_fuse_combine") g_k4_fuse_combine = value;
   else if (k == "coop_pdl") g_coop_pdl = value;
   else if (k == "k1m_wpr") g_k1m_wpr = value;
   else if (k == "k1m_nv") g_k1m_nv = value;

@@ -121,6 +121,19 @@ __global__ void __launch_bounds__(kSplitThreads)
   }
 }
 
+// a row's (M, S) from its nch partials, by one warp in a fixed order (every
+// caller -- k4_combine, k4_normalize_rows -- gets the same bits)
+__device__ __forceinline__ void k4_combine_row(const RowPartial* __restrict__ rp, int nch, int lane,
+                                               float& M, double& S) {
+  M = kPadLogit;
+  for (int q = lane; q < nch; q += 32) M = fmaxf(M, rp[q].m);
+  M = group_max<32>(M);
+  S = 0.0;
+  for (int q = lane; q < nch; q += 32)
+    S += rp[q].s * static_cast<double>(rp[q].m == M ? 1.0f : expf(rp[q].m - M));
+  S = group_sum<32>(S);
+}
+
 // one warp per row
 __global__ void k4_combine(const RowPartial* __restrict__ partials, int64_t rows, int nch,
                            float* __restrict__ row_max, double* __restrict__ row_sum) {
@@ -129,14 +142,9 @@ __global__ void k4_combine(const RowPartial* __restrict__ partials, int64_t rows
   const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
-  const RowPartial* rp = partials + row * nch;
-  float M = kPadLogit;
-  for (int q = lane; q < nch; q += 32) M = fmaxf(M, rp[q].m);
-  M = group_max<32>(M);
-  double S = 0.0;
-  for (int q = lane; q < nch; q += 32)
-    S += rp[q].s * static_cast<double>(rp[q].m == M ? 1.0f : expf(rp[q].m - M));
-  S = group_sum<32>(S);
+  float M;
+  double S;
+  k4_combine_row(partials + row * nch, nch, lane, M, S);
   if (lane == 0) {
     row_max[row] = M;
     row_sum[row] = S;
@@ -154,14 +162,11 @@ __global__ void k4_rescale(const float* __restrict__ local_max,
   sum[i] *= static_cast<double>(d == 0.0f ? 1.0f : expf(d));
 }
 
+// y of item w = (row, chunk) given the row's M and 1/S
 template <int MODE, int VEC>
-__global__ void __launch_bounds__(kSplitThreads)
-    k4_normalize(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
-                 int64_t ldx, int64_t ldy, int nch, const float* __restrict__ row_max,
-                 const double* __restrict__ row_sum) {
-  pdl_wait();
-  pdl_launch_dependents();
-  const int64_t w = blockIdx.x;
+__device__ __forceinline__ void k4_normalize_item(const float* __restrict__ x, float* __restrict__ y,
+                                                  int64_t cols, int64_t ldx, int64_t ldy, int nch,
+                                                  int64_t w, float M, float r) {
   const int64_t row = w / nch;
   const int ch = static_cast<int>(w - row * nch);
   const int64_t c0 = int64_t(ch) * kSplitChunk;
@@ -169,8 +174,6 @@ __global__ void __launch_bounds__(kSplitThreads)
   float* yr = y + row * ldy + c0;
   const int64_t rem = cols - c0;
   const int len = static_cast<int>(rem < kSplitChunk ? rem : kSplitChunk);
-  const float M = row_max[row];
-  const float r = recip_of_sum(row_sum[row]);
   if constexpr (VEC == 4) {
 #pragma unroll
     for (int i = 0; i < kSplitPerThread / 4; ++i) {
@@ -189,6 +192,44 @@ __global__ void __launch_bounds__(kSplitThreads)
       if (c < len) st_stream1(yr + c, scale1<MODE>(sexp1<MODE>(ld_stream1(xr + c), M), r));
     }
   }
+}
+
+template <int MODE, int VEC>
+__global__ void __launch_bounds__(kSplitThreads)
+    k4_normalize(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
+                 int64_t ldx, int64_t ldy, int nch, const float* __restrict__ row_max,
+                 const double* __restrict__ row_sum) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int64_t row = blockIdx.x / nch;
+  k4_normalize_item<MODE, VEC>(x, y, cols, ldx, ldy, nch, blockIdx.x, row_max[row],
+                               recip_of_sum(row_sum[row]));
+}
+
+// combine + normalize in one launch: warp 0 of every item merges its row's
+// partials (k4_combine_row: the three-kernel path's bits), the block
+// normalizes the item -- the split path as two launches
+template <int MODE, int VEC>
+__global__ void __launch_bounds__(kSplitThreads)
+    k4_normalize_rows(const float* __restrict__ x, float* __restrict__ y, int64_t rows,
+                      int64_t cols, int64_t ldx, int64_t ldy, int nch,
+                      const RowPartial* __restrict__ partials) {
+  __shared__ float M_s;
+  __shared__ double S_s;
+  pdl_wait();
+  pdl_launch_dependents();
+  const int64_t row = blockIdx.x / nch;
+  if (threadIdx.x < 32) {
+    float M;
+    double S;
+    k4_combine_row(partials + row * nch, nch, threadIdx.x, M, S);
+    if (threadIdx.x == 0) {
+      M_s = M;
+      S_s = S;
+    }
+  }
+  __syncthreads();
+  k4_normalize_item<MODE, VEC>(x, y, cols, ldx, ldy, nch, blockIdx.x, M_s, recip_of_sum(S_s));
 }
 
 }  // namespace sk

@@ -20,7 +20,8 @@ from row_length_sweep import copy_us  # noqa: E402
 from sweep import bench_once  # noqa: E402
 
 KNOBS = ("gres", "gres_p", "gres_st", "gres_lag", "gres_diag", "path", "k3_impl")
-DEFAULTS = {"gres": 1, "gres_p": 0, "gres_st": 0, "gres_lag": 0, "gres_diag": 0, "path": -1, "k3_impl": 3}
+DEFAULTS = {"gres": 1, "gres_p": 0, "gres_st": 0, "gres_lag": 0, "gres_diag": 0, "path": -1, "k3_impl": 3,
+            "k4_fuse_combine": 1}
 
 
 def parse_points(s):
@@ -28,8 +29,10 @@ def parse_points(s):
     for tok in filter(None, s.split(",")):
         if tok == "k3c":
             out.append((tok, {"k3_impl": 5}))
-        elif tok == "split":
+        elif tok == "split":  # split path, row statistics merged inside normalize (2 launches)
             out.append((tok, {"path": 2}))
+        elif tok == "split3":  # split path as three launches (stats, combine, normalize)
+            out.append((tok, {"path": 2, "k4_fuse_combine": 0}))
         elif tok.startswith("t"):  # t<diag>: default plan with diag bits that keep results (experiments)
             out.append((tok, {"gres_diag": int(tok[1:])}))
         elif tok.startswith("d"):  # d<diag>: default plan, parts switched off
