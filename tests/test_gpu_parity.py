@@ -171,6 +171,30 @@ def test_k1_instantiations_all_agree(oracle):
         _native.set_tuning("k1_pf", -1)
 
 
+@pytest.mark.parametrize("rows,C", [(8, 50257), (32, 151936), (3, 20000), (40, 262147)])
+def test_split_fused_combine_keeps_bits(rows, C, oracle):
+    """The split path with the row statistics merged inside the normalize pass
+    (two launches) gives the three-launch path's bits, and both match the oracle."""
+    from paper_1904_12380_b200 import tensor
+
+    x = np.empty((rows, C), np.float32)
+    tensor.fill_normal_array(x, C + rows, 5.0)
+    x[1, 7] = -500.0
+    ref = oracle.softmax_ref(x)
+    outs = []
+    try:
+        _native.set_tuning("path", 2)
+        for fuse in (0, 1, 2):
+            _native.set_tuning("k4_fuse_combine", fuse)
+            y, bad = gu.softmax_abi(x, 0)
+            assert bad == gu.NO_BAD
+            assert_parity(oracle, y, ref, what=(rows, C, fuse))
+            outs.append(y)
+    finally:
+        _native.set_tuning("k4_fuse_combine", 1)
+    assert all(np.array_equal(o.view(np.uint32), outs[0].view(np.uint32)) for o in outs[1:])
+
+
 def test_k1_vec2_instantiations_all_agree(oracle):
     """Every 64-bit K1 instantiation (even rows on 8-B pitches) against the
     oracle, on row lengths it covers, plus the 32-bit plan of the same rows."""
