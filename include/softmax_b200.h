@@ -230,6 +230,9 @@ void sk_free_pinned(void* p);
  *                    statistics inside its normalize pass (2 launches) when the
  *                    job has <= 4096 (row, chunk) items; 2: always; 0: a separate
  *                    combine kernel (3 launches; same bits either way)
+ *   "latency_steps"  K3g row steps per group up to which a long-row job takes the
+ *                    latency path (cluster / split kernels) instead (default 3;
+ *                    4-6 measured no better, profiles/r1d_latency_threshold_ab.jsonl)
  *   "host_chunk_kb"  sk_softmax_f32_host chunk size in KiB (0 = auto, ~1/4 of the job)
  *   "host_zero_copy" 1: pinned host buffers with rows <= 8192 are read and written
  *                    by the kernel directly over PCIe (measured no faster than

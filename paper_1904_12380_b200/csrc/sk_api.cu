@@ -102,6 +102,7 @@ std::atomic<int> g_gres_st{0};     // force ring depth (0 = planner)
 std::atomic<int> g_gres_lag{0};    // force the lag (rows between local and output pass; 0 = planner)
 std::atomic<int> g_gres_split{-1};  // separate poller warp: -1 auto (lag >= 2), 0 off, 1 on
 std::atomic<int> g_gres_sleep{128};  // poller back-off between polls (ns)
+std::atomic<int> g_latency_steps{3};  // K3g row steps per group up to which the latency path is taken
 std::atomic<int> g_gres_diag{0};     // timing diagnostics (1: wait only for the own slot -- wrong results)
 std::atomic<unsigned> g_gres_spins{kGresSpinLimit};  // exchange timeout (polls), tests shorten it
 bool gres_split(int lag) {
@@ -624,7 +625,8 @@ GresChoice plan_gres(int64_t rows, int64_t cols, int mode, const DevInfo& di, in
 GresChoice plan_gres_for(int64_t rows, int64_t cols, int mode, const DevInfo& di, bool unal,
                          bool* latency) {
   const GresChoice gc = plan_gres(kGresPlanRows, cols, mode, di, 1, 1, unal);
-  *latency = gc.P > 0 && g_gres.load() != 2 && (rows + gc.groups - 1) / gc.groups <= 3;
+  *latency = gc.P > 0 && g_gres.load() != 2 &&
+             (rows + gc.groups - 1) / gc.groups <= g_latency_steps.load();
   return gc;
 }
 
@@ -1115,6 +1117,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "k1m") g_k1m = value;
   else if (k == "k1_fit") g_k1_fit = value;
   else if (k == "k4_fuse_combine") g_k4_fuse_combine = value;
+  else if (k == "latency_steps") g_latency_steps = value;
   else if (k == "coop_pdl") g_coop_pdl = value;
   else if (k == "k1m_wpr") g_k1m_wpr = value;
   else if (k == "k1m_nv") g_k1m_nv = value;

@@ -21,7 +21,7 @@ from sweep import bench_once  # noqa: E402
 
 KNOBS = ("gres", "gres_p", "gres_st", "gres_lag", "gres_diag", "path", "k3_impl")
 DEFAULTS = {"gres": 1, "gres_p": 0, "gres_st": 0, "gres_lag": 0, "gres_diag": 0, "path": -1, "k3_impl": 3,
-            "k4_fuse_combine": 1}
+            "k4_fuse_combine": 1, "latency_steps": 3}
 
 
 def parse_points(s):
@@ -33,6 +33,8 @@ def parse_points(s):
             out.append((tok, {"path": 2}))
         elif tok == "split3":  # split path as three launches (stats, combine, normalize)
             out.append((tok, {"path": 2, "k4_fuse_combine": 0}))
+        elif tok.startswith("lat"):  # lat<n>: latency path up to n K3g row steps per group
+            out.append((tok, {"latency_steps": int(tok[3:])}))
         elif tok.startswith("t"):  # t<diag>: default plan with diag bits that keep results (experiments)
             out.append((tok, {"gres_diag": int(tok[1:])}))
         elif tok.startswith("d"):  # d<diag>: default plan, parts switched off
