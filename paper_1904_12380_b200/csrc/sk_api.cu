@@ -463,6 +463,9 @@ const K1mEntry kK1mTable[] = {
     SK_K1M(4, 2, 13), SK_K1M(4, 2, 14), SK_K1M(4, 2, 15), SK_K1M(4, 4, 9), SK_K1M(4, 4, 10),
     SK_K1M(4, 4, 11), SK_K1M(4, 4, 13), SK_K1M(4, 4, 14), SK_K1M(4, 4, 15), SK_K1M(4, 8, 9),
     SK_K1M(4, 8, 10), SK_K1M(4, 8, 11), SK_K1M(4, 8, 13), SK_K1M(4, 8, 14), SK_K1M(4, 8, 15),
+    SK_K1M(1, 2, 18), SK_K1M(1, 2, 20), SK_K1M(1, 2, 28), SK_K1M(1, 2, 36), SK_K1M(1, 2, 40),
+    SK_K1M(1, 4, 28), SK_K1M(1, 4, 36), SK_K1M(1, 4, 40), SK_K1M(1, 8, 28), SK_K1M(1, 8, 36),
+    SK_K1M(1, 8, 40), SK_K1M(1, 8, 52), SK_K1M(1, 8, 56),
     // 32-bit rows (any length / alignment): 1025..16384 floats
     SK_K1M(1, 2, 24), SK_K1M(1, 2, 32), SK_K1M(1, 2, 48), SK_K1M(1, 4, 32), SK_K1M(1, 4, 48),
     SK_K1M(1, 8, 32), SK_K1M(1, 8, 48), SK_K1M(1, 8, 64)};
@@ -677,9 +680,10 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     const int vw = vec ? 4 : 1;
     int wpr, nv;
     k1m_default(vw, cols, wpr, nv);
-    if (vw == 4 && g_k1_fit.load()) {  // exact fit: the fewest float4 per thread
-      const int fit = static_cast<int>((cols + int64_t(wpr) * 128 - 1) / (int64_t(wpr) * 128));
-      if (fit < nv && k1m_find(vw, wpr, fit)) nv = fit;
+    if (g_k1_fit.load()) {  // fit: the fewest instantiated vectors per thread covering the row
+      const int need = static_cast<int>((cols + int64_t(wpr) * 32 * vw - 1) / (int64_t(wpr) * 32 * vw));
+      for (const auto& f : kK1mTable)
+        if (f.vec == vw && f.wpr == wpr && f.nv >= need && f.nv < nv) nv = f.nv;
     }
     if (g_k1m_wpr.load() > 0) { wpr = g_k1m_wpr; nv = g_k1m_nv; }
     const K1mEntry* e = k1m_find(vw, wpr, nv);
