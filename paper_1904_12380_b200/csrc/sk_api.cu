@@ -153,6 +153,7 @@ const K1Entry kK1Table[] = {
     SK_K1(1, 32, 12, 1, 0), SK_K1(1, 32, 13, 1, 0), SK_K1(1, 32, 14, 1, 0), SK_K1(1, 32, 15, 1, 0),
     SK_K1(1, 32, 17, 1, 0), SK_K1(1, 32, 18, 1, 0), SK_K1(1, 32, 19, 1, 0), SK_K1(1, 32, 20, 1, 0),
     SK_K1(1, 32, 21, 1, 0), SK_K1(1, 32, 22, 1, 0), SK_K1(1, 32, 23, 1, 0), SK_K1(1, 32, 24, 1, 0),
+    SK_K1(1, 32, 36, 1, 0), SK_K1(1, 32, 40, 1, 0),
 
     // medium rows: a warp holds up to 2048 / 3072 floats in registers
     SK_K1(4, 32, 16, 1, 0), SK_K1(4, 32, 24, 1, 0),
@@ -204,6 +205,7 @@ constexpr K1Fit kK1Fit[] = {{4, 4, 3},  {4, 8, 3},  {4, 16, 3}, {4, 32, 3},  {4,
                             {1, 32, 17}, {1, 32, 18}, {1, 32, 19}, {1, 32, 20}, {1, 32, 21},
                             {1, 32, 22}, {1, 32, 23}, {1, 32, 24}};  // 25-31: measured slower
 std::atomic<int> g_k1_fit{1};
+std::atomic<int> g_k1_wide32{1280};  // 32-bit rows up to here take K1 (one warp per row), not K1m
 int k1_fit_nv(int vec, int lpr, int nv, int64_t cols) {
   if (!g_k1_fit.load()) return nv;
   const int fit = static_cast<int>((cols + int64_t(lpr) * vec - 1) / (int64_t(lpr) * vec));
@@ -304,7 +306,9 @@ void k1_default(int vec, int64_t cols, int& lpr, int& nv, int& u, int& pf, int& 
     }
     else if (cols <= 256) { lpr = 32; nv = 8; u = 1; }
     else if (cols <= 512) { lpr = 32; nv = 16; u = 1; }
-    else { lpr = 32; nv = 32; u = 1; }
+    else if (cols <= 1024) { lpr = 32; nv = 32; u = 1; }
+    else if (cols <= 1152) { lpr = 32; nv = 36; u = 1; }  // one warp per row (g_k1_wide32)
+    else { lpr = 32; nv = 40; u = 1; }
   }
 }
 
@@ -648,7 +652,8 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
   const int64_t k1m_max = std::min<int64_t>(g_k1m_max.load(), kK1mCap);
   PathKind kind;
   if (force >= 0) kind = static_cast<PathKind>(force);
-  else if (cols <= 1024 || (vec && cols <= kK1MaxCols)) kind = kPathK1;
+  else if (cols <= 1024 || (vec && cols <= kK1MaxCols) || (!vec && cols <= g_k1_wide32.load()))
+    kind = kPathK1;
   else if (cols <= k1m_max && g_k1m.load()) kind = kPathK1m;
   else if (vec) kind = kPathSeg;
   else kind = kPathSplit;
@@ -1120,6 +1125,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "gres_lag") g_gres_lag = value;
   else if (k == "k1m") g_k1m = value;
   else if (k == "k1_fit") g_k1_fit = value;
+  else if (k == "k1_wide32") g_k1_wide32 = value;
   else if (k == "k4_fuse_combine") g_k4_fuse_combine = value;
   else if (k == "latency_steps") g_latency_steps = value;
   else if (k == "coop_pdl") g_coop_pdl = value;

@@ -23,6 +23,13 @@ from row_length_sweep import copy_us  # noqa: E402
 from sweep import bench_once  # noqa: E402
 
 
+# library defaults of the knobs a set may touch (sk_api.cu)
+DEFAULTS = {"path": -1, "k1m_wpr": 0, "k1m_nv": 0, "k1_lpr": 0, "k1_nv": 0, "k1_u": 0, "k1_pf": -1,
+            "gres": 1, "gres_p": 0, "gres_st": 0, "gres_lag": 0, "k3_impl": 3, "k1m": 1, "k1_fit": 1,
+            "k1_wide32": 1280, "vec2_max": 128, "k4_fuse_combine": 1, "latency_steps": 3,
+            "grid_mult": 0}
+
+
 def parse_sets(s):
     out = []
     for part in s.split(";"):
@@ -31,6 +38,9 @@ def parse_sets(s):
             out.append(("default", {}))
             continue
         kv = dict((k, int(v)) for k, v in (t.split("=") for t in part.split(",")))
+        unknown = set(kv) - set(DEFAULTS)
+        if unknown:
+            raise SystemExit(f"no default recorded for {sorted(unknown)}")
         out.append((part, kv))
     return out
 
@@ -72,9 +82,7 @@ def main():
                 rec["error"] = str(e)[:100]
             print(json.dumps(rec), flush=True)
             for k in kv:  # back to the library defaults
-                _native.set_tuning(k, {"path": -1, "k1m_wpr": 0, "k1m_nv": 0, "k1_lpr": 0, "k1_nv": 0,
-                                       "k1_u": 0, "k1_pf": -1, "gres": 1, "gres_p": 0, "gres_st": 0,
-                                       "gres_lag": 0, "k3_impl": 3, "k1m": 1}.get(k, 1))
+                _native.set_tuning(k, DEFAULTS[k])
         del xs, ys, x0, ref
         torch.cuda.empty_cache()
 
