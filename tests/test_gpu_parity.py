@@ -287,7 +287,7 @@ def test_k1_medium_rows(rows, C, oracle):
 
 @pytest.mark.parametrize("rows,C", [(300, 8192), (4096, 4000), (2048, 5000), (64, 6144),
                                     (3, 8192), (1000, 3076), (4096, 5001), (300, 8191),
-                                    (2000, 1025), (7, 3001), (513, 4097), (64, 6143),
+                                    (2000, 1283), (7, 3001), (513, 4097), (64, 6143),
                                     (300, 12288), (37, 16384), (1000, 10000), (129, 12289),
                                     (64, 16383), (5, 9001), (2, 16384)])
 def test_k1m_medium_rows(rows, C, oracle):
@@ -317,6 +317,34 @@ def test_k1m_medium_rows(rows, C, oracle):
     assert np.array_equal(part.view(np.uint32), whole[rows // 3:].view(np.uint32))
     x2 = x.copy()
     x2[rows - 1, 5] = np.inf
+    assert gu.softmax_abi(x2, 0)[1] == rows - 1
+
+
+@pytest.mark.parametrize("rows,C", [(2000, 1025), (300, 1151), (37, 1153), (5, 1279), (4100, 1280)])
+def test_k1_one_warp_32bit_rows(rows, C, oracle):
+    """32-bit rows of 1025..1280 floats held by one warp (K1, 36 / 40 floats per
+    lane): every mode, clip firing, strided / unaligned views, row blocks
+    bit-identical to the whole matrix, non-finite detection."""
+    from paper_1904_12380_b200 import tensor
+
+    x = np.empty((rows, C), np.float32)
+    tensor.fill_normal_array(x, 5 * C + rows, 5.0)
+    x[0, C - 1] = -300.0
+    x[rows // 2, :] -= 500.0
+    plan = gu.plan(rows, C)
+    assert plan.startswith("k1 ") and "lpr=32" in plan, plan
+    for mode in (0, 1, 2):
+        ref = oracle.softmax_ref(x, clip=(mode == 0))
+        y, bad = gu.softmax_abi(x, mode)
+        assert bad == gu.NO_BAD
+        assert_parity(oracle, y, ref, approx=(mode == 2), what=(rows, C, mode, plan))
+    y, _ = gu.softmax_abi(x, 0, x_offset=1, y_offset=3, ldx=C + 3, ldy=C + 1)
+    assert_parity(oracle, y, oracle.softmax_ref(x), what=(rows, C, "unaligned"))
+    whole, _ = gu.softmax_abi(x, 0)
+    part, _ = gu.softmax_abi(x[rows // 3:], 0)
+    assert np.array_equal(part.view(np.uint32), whole[rows // 3:].view(np.uint32))
+    x2 = x.copy()
+    x2[rows - 1, 5] = np.nan
     assert gu.softmax_abi(x2, 0)[1] == rows - 1
 
 
