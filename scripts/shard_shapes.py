@@ -19,7 +19,6 @@ from paper_1904_12380_b200 import _native, configs  # noqa: E402
 from row_length_sweep import copy_us  # noqa: E402
 from sweep import bench_once  # noqa: E402
 
-KNOBS = ("gres", "gres_p", "gres_st", "gres_lag", "gres_diag", "path", "k3_impl")
 DEFAULTS = {"gres": 1, "gres_p": 0, "gres_st": 0, "gres_lag": 0, "gres_diag": 0, "path": -1, "k3_impl": 3,
             "k4_fuse_combine": 1, "latency_steps": 3}
 
