@@ -206,6 +206,8 @@ void sk_free_pinned(void* p);
  *                    are 32-B aligned (measured no faster than 128-bit; default 0)
  *   "vec2_max"       widest even row (not a multiple of 4, 8-B pitch / bases) K1
  *                    loads as 64-bit pairs (default 128; 0: 32-bit accesses)
+ *   "k1_threads"     K1 threads per block (default 128; halved down to 64 while a
+ *                    job has fewer blocks than SMs)
  *   "k1_wide32"      32-bit rows up to this length take K1 with one warp per row
  *                    (36 / 40 floats per lane) instead of K1m (default 1280)
  *   "k1_fit"         1 (default): K1 / K1m shrink the vectors per lane to the fewest

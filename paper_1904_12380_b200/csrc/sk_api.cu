@@ -205,6 +205,10 @@ constexpr K1Fit kK1Fit[] = {{4, 4, 3},  {4, 8, 3},  {4, 16, 3}, {4, 32, 3},  {4,
                             {1, 32, 17}, {1, 32, 18}, {1, 32, 19}, {1, 32, 20}, {1, 32, 21},
                             {1, 32, 22}, {1, 32, 23}, {1, 32, 24}};  // 25-31: measured slower
 std::atomic<int> g_k1_fit{1};
+// K1 block size, shrunk to 64 for small jobs: 128 measured 0.5-2.5 % faster
+// than 256 (c2 11.57 vs 11.61-11.66 us, c3 11.77 vs 12.05-12.11,
+// profiles/r1d_k1_block_size_ab.jsonl); the bits do not depend on it
+std::atomic<int> g_k1_threads{128};
 std::atomic<int> g_k1_wide32{1280};  // 32-bit rows up to here take K1 (one warp per row), not K1m
 int k1_fit_nv(int vec, int lpr, int nv, int64_t cols) {
   if (!g_k1_fit.load()) return nv;
@@ -717,7 +721,7 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     // block size: 256 threads, halved (to 64) while the job would occupy fewer
     // CTAs than SMs -- a small job then spreads over the chip.  Each row is one
     // warp's work whatever the block size, so the bits do not change.
-    int threads = kRowsThreads;
+    int threads = std::max(32, std::min(g_k1_threads.load(), kRowsThreads));
     auto rows_per = [&](int t) { return int64_t(t / 32) * u * (32 / lpr); };
     while (threads > 64 && (rows + rows_per(threads) - 1) / rows_per(threads) < di.sms) threads /= 2;
     p.threads = threads;
@@ -1125,6 +1129,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "gres_lag") g_gres_lag = value;
   else if (k == "k1m") g_k1m = value;
   else if (k == "k1_fit") g_k1_fit = value;
+  else if (k == "k1_threads") g_k1_threads = value;
   else if (k == "k1_wide32") g_k1_wide32 = value;
   else if (k == "k4_fuse_combine") g_k4_fuse_combine = value;
   else if (k == "latency_steps") g_latency_steps = value;
