@@ -217,6 +217,7 @@ void sk_free_pinned(void* p);
  *   "k1m"            1 (default): rows of 1025..8192 floats not taken by K1 go to
  *                    K1m (WPR warps hold a row in registers); 0: K2 / K4 instead
  *   "k1m_wpr","k1m_nv"  force a K1m instantiation (warps per row, vectors per thread)
+ *   "k1m_threads"    K1m threads per block (0, default: one row = 32 * WPR threads)
  *   "k3_impl"        long rows (> 8192): 3 (default) K3g, else K3c; 5 K3c only
  *   "gres"           K3g: 1 (default) auto, 0 off, 2 force (also for C <= 8192)
  *   "gres_p","gres_st","gres_split"  force K3g CTAs per row, ring depth (2..5),

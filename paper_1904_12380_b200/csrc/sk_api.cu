@@ -485,6 +485,7 @@ const K1mEntry* k1m_find(int vec, int wpr, int nv) {
 }
 constexpr int64_t kK1mCap = 16384;  // widest row a K1m instantiation holds
 std::atomic<int> g_k1m{1}, g_k1m_wpr{0}, g_k1m_nv{0};
+std::atomic<int> g_k1m_threads{0};  // K1m threads per block (0: one row, 32 * WPR)
 // widest row the planner gives K1m.  Measured (scripts/wide_k1m.py,
 // profiles/r1c_wide_k1m.jsonl): a 256-thread block holding a 12288 / 16384-float
 // row beats K3g's one-CTA rows by 2-16% (1024x16384 26.1 vs 30.3 us)
@@ -700,8 +701,13 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     if (int64_t(wpr) * 32 * nv * vw < cols) return arg_fail("K1m shape does not cover cols");
     p.kind = kPathK1m;
     p.k1m = e;
-    p.threads = kRowsThreads;
-    const int64_t rpc = kRowsThreads / 32 / wpr;
+    // block: one row (32 * WPR threads) -- 1.10-1.25x over 256-thread blocks
+    // holding 2-4 rows (4096 floats 23.9 -> 21.5 us, 1501 44.2 -> 35.4,
+    // profiles/r1d_k1m_block_size_ab.jsonl; same bits); the k1m_threads knob
+    // forces a size that still holds a whole row
+    const int kt = g_k1m_threads.load();
+    p.threads = (kt >= 32 * wpr && kt <= kRowsThreads) ? kt : 32 * wpr;
+    const int64_t rpc = p.threads / 32 / wpr;
     p.grid = std::max<int64_t>(1, std::min<int64_t>((rows + rpc - 1) / rpc, INT32_MAX));
     return SK_OK;
   }
@@ -1130,6 +1136,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "k1m") g_k1m = value;
   else if (k == "k1_fit") g_k1_fit = value;
   else if (k == "k1_threads") g_k1_threads = value;
+  else if (k == "k1m_threads") g_k1m_threads = value;
   else if (k == "k1_wide32") g_k1_wide32 = value;
   else if (k == "k4_fuse_combine") g_k4_fuse_combine = value;
   else if (k == "latency_steps") g_latency_steps = value;

@@ -27,7 +27,7 @@ from sweep import bench_once  # noqa: E402
 DEFAULTS = {"path": -1, "k1m_wpr": 0, "k1m_nv": 0, "k1_lpr": 0, "k1_nv": 0, "k1_u": 0, "k1_pf": -1,
             "gres": 1, "gres_p": 0, "gres_st": 0, "gres_lag": 0, "k3_impl": 3, "k1m": 1, "k1_fit": 1,
             "k1_wide32": 1280, "vec2_max": 128, "k4_fuse_combine": 1, "latency_steps": 3,
-            "grid_mult": 0, "k1_threads": 128}
+            "grid_mult": 0, "k1_threads": 128, "k1m_threads": 0}
 
 
 def parse_sets(s):
