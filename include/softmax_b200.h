@@ -239,6 +239,9 @@ void sk_free_pinned(void* p);
  *                    latency path (cluster / split kernels) instead (default 3;
  *                    4-6 measured no better, profiles/r1d_latency_threshold_ab.jsonl)
  *   "host_chunk_kb"  sk_softmax_f32_host chunk size in KiB (0 = auto, ~1/4 of the job)
+ *   "host_threads"   host threads copying pageable caller buffers through the
+ *                    page-locked staging slots of sk_softmax_f32_host (0 = auto,
+ *                    min(16, hardware threads))
  *   "host_zero_copy" 1: pinned host buffers with rows <= 8192 are read and written
  *                    by the kernel directly over PCIe (measured no faster than
  *                    staging on this box, so 0 by default)

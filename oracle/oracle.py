@@ -19,7 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import c_float, c_int, c_int64, c_uint64, c_void_p
+from ctypes import c_double, c_float, c_int, c_int64, c_uint64, c_void_p
 from pathlib import Path
 
 import numpy as np
@@ -29,15 +29,30 @@ LIB_PATH = HERE / "libsk_oracle.so"
 _lib = None
 
 
+def build(force: bool = False) -> Path:
+    """gcc the C restatement into libsk_oracle.so next to it (test
+    infrastructure; self-contained so that loading the checker never imports
+    the product package or maps its library)."""
+    import subprocess
+
+    src = HERE / "sk_oracle.c"
+    if not force and LIB_PATH.exists() and LIB_PATH.stat().st_mtime >= src.stat().st_mtime:
+        return LIB_PATH
+    tmp = LIB_PATH.with_suffix(".so.tmp")
+    # -O2, no -ffast-math: the f64 left-to-right sum and IEEE reciprocal are the contract.
+    cmd = ["gcc", "-O2", "-fPIC", "-shared", "-fopenmp", "-std=c11", str(src), "-o", str(tmp),
+           "-lm"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"oracle build failed: {' '.join(cmd)}\n{r.stdout}{r.stderr}")
+    os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
 def lib() -> ctypes.CDLL:
     global _lib
     if _lib is None:
-        import sys
-
-        sys.path.insert(0, str(HERE.parent))
-        from paper_1904_12380_b200._build import build_oracle
-
-        build_oracle()  # no-op unless missing or older than sk_oracle.c
+        build()  # no-op unless missing or older than sk_oracle.c
         L = ctypes.CDLL(str(LIB_PATH))
         L.sko_softmax_f32.restype = c_int64
         L.sko_softmax_f32.argtypes = [c_void_p, c_void_p, c_int64, c_int64, c_int, c_int]
@@ -56,6 +71,13 @@ def lib() -> ctypes.CDLL:
         L.sko_seq_max.argtypes = [c_void_p, c_int64]
         L.sko_seq_sum_wide.restype = c_float
         L.sko_seq_sum_wide.argtypes = [c_void_p, c_int64]
+        L.sko_fill_uniform_f32.restype = None
+        L.sko_fill_uniform_f32.argtypes = [c_void_p, c_int64, c_uint64, c_double, c_double,
+                                           c_uint64, c_int]
+        L.sko_fill_normal_f32.restype = None
+        L.sko_fill_normal_f32.argtypes = [c_void_p, c_int64, c_uint64, c_double, c_uint64, c_int]
+        L.sko_plant_f32.restype = c_int
+        L.sko_plant_f32.argtypes = [c_void_p, c_int64, c_int64, c_uint64, c_float]
         _lib = L
     return _lib
 

@@ -30,6 +30,7 @@
 #include <float.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 #ifdef _OPENMP
 #include <omp.h>
@@ -198,4 +199,94 @@ void sko_philox_raw(uint64_t seed, uint64_t start, uint64_t* out, int64_t n) {
     if (i == 0 || (k & 3) == 0) sko_philox_block(k >> 2, seed, buf);
     out[i] = buf[k & 3];
   }
+}
+
+/* --- the BASELINE config generators (test side) ------------------------- *
+ * configs.py's input definitions, restated here so the checker and the
+ * `bench.py --impl reference` arm build the exact input bytes without the
+ * product library (tests/test_oracle_golden.py pins both against the input
+ * SHA-256 recorded in tests/golden/golden.json):
+ *   uniform  reference fill_uniform, tensor.py:106-121: raw u64 ->
+ *            ((u>>11)+0.5)*2^-53 -> low+(high-low)u (f64) -> fp32 -> clamp into
+ *            the open interval
+ *   normal   element i: Box-Muller on raw pair (2*(i/2), 2*(i/2)+1):
+ *            r = sqrt(-2 ln u1), th = 2 pi u2; even i -> sigma*r*cos(th),
+ *            odd i -> sigma*r*sin(th) (f64, then fp32)
+ *   plant    count distinct flat positions from the raw stream keyed by
+ *            seed ^ 0x5EEDC0FFEE, position = raw % total, first-come order.  */
+static inline double sko_open_unit(uint64_t u) {
+  return ((double)(u >> 11) + 0.5) * 0x1.0p-53;
+}
+
+static inline uint64_t sko_raw_at(uint64_t seed, uint64_t k, uint64_t buf[4], uint64_t* blk) {
+  if (*blk != (k >> 2)) {
+    *blk = k >> 2;
+    sko_philox_block(*blk, seed, buf);
+  }
+  return buf[k & 3];
+}
+
+void sko_fill_uniform_f32(float* dst, int64_t n, uint64_t seed, double low, double high,
+                          uint64_t start, int nthreads) {
+  const float lo = (float)low, hi = (float)high;
+  const float lo_in = ((double)lo <= low) ? nextafterf(lo, hi) : lo;
+  const float hi_in = ((double)hi >= high) ? nextafterf(hi, lo) : hi;
+#ifdef _OPENMP
+  if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel num_threads(nthreads)
+#endif
+  {
+    uint64_t buf[4], blk = UINT64_MAX;
+#ifdef _OPENMP
+#pragma omp for schedule(static)
+#endif
+    for (int64_t i = 0; i < n; ++i) {
+      const double u = sko_open_unit(sko_raw_at(seed, start + (uint64_t)i, buf, &blk));
+      float v = (float)(low + (high - low) * u);
+      dst[i] = v < lo_in ? lo_in : (v > hi_in ? hi_in : v);
+    }
+  }
+  (void)nthreads;
+}
+
+void sko_fill_normal_f32(float* dst, int64_t n, uint64_t seed, double sigma, uint64_t start,
+                         int nthreads) {
+  const double two_pi = 6.283185307179586476925286766559;
+#ifdef _OPENMP
+  if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel num_threads(nthreads)
+#endif
+  {
+    uint64_t buf[4], blk = UINT64_MAX;
+#ifdef _OPENMP
+#pragma omp for schedule(static)
+#endif
+    for (int64_t i = 0; i < n; ++i) {
+      const uint64_t g = start + (uint64_t)i, p = g >> 1;
+      const double u1 = sko_open_unit(sko_raw_at(seed, 2 * p, buf, &blk));
+      const double u2 = sko_open_unit(sko_raw_at(seed, 2 * p + 1, buf, &blk));
+      const double rad = sqrt(-2.0 * log(u1)), th = two_pi * u2;
+      dst[i] = (float)(sigma * ((g & 1) ? rad * sin(th) : rad * cos(th)));
+    }
+  }
+  (void)nthreads;
+}
+
+int sko_plant_f32(float* x, int64_t total, int64_t count, uint64_t seed, float value) {
+  if (count > total || total <= 0) return count == 0 ? 0 : -1;
+  uint8_t* seen = (uint8_t*)calloc((size_t)total, 1);
+  if (!seen) return -1;
+  uint64_t buf[4], blk = UINT64_MAX, k = 0;
+  const uint64_t key = seed ^ 0x5EEDC0FFEEULL;
+  int64_t placed = 0;
+  while (placed < count) {
+    const uint64_t idx = sko_raw_at(key, k++, buf, &blk) % (uint64_t)total;
+    if (!seen[idx]) {
+      seen[idx] = 1;
+      x[idx] = value;
+      ++placed;
+    }
+  }
+  free(seen);
+  return 0;
 }

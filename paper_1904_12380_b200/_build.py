@@ -123,18 +123,14 @@ def build_torch_ops(force: bool = False) -> Path:
 
 
 def build_oracle(force: bool = False) -> Path:
-    """Compile the C restatement of the reference (test infrastructure only)."""
-    src = ORACLE_DIR / "sk_oracle.c"
-    if not force and not _stale(ORACLE_LIB, [src]):
-        return ORACLE_LIB
-    tmp = ORACLE_LIB.with_suffix(".so.tmp")
-    # -O2, no -ffast-math: the f64 left-to-right sum and IEEE reciprocal are the contract.
-    cmd = ["gcc", "-O2", "-fPIC", "-shared", "-fopenmp", "-std=c11", str(src), "-o", str(tmp), "-lm"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError(f"oracle build failed: {' '.join(cmd)}\n{r.stdout}{r.stderr}")
-    os.replace(tmp, ORACLE_LIB)
-    return ORACLE_LIB
+    """Compile the C restatement of the reference (test infrastructure only;
+    the recipe lives with the oracle, oracle/oracle.py:build)."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("_sk_oracle_build", ORACLE_DIR / "oracle.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.build(force)
 
 
 if __name__ == "__main__":

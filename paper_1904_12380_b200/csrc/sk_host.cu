@@ -5,9 +5,13 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "sk_internal.h"
@@ -33,6 +37,9 @@ struct HostCtx {
   unsigned long long* hbad = nullptr;  // pinned mirror
   int64_t flag_cap = 0;
   size_t cap_bytes = 0;
+  float* pin_in[kRing] = {};   // page-locked staging (pageable caller buffers)
+  float* pin_out[kRing] = {};
+  size_t pin_bytes = 0;
 };
 std::mutex g_host_mu;
 std::map<int, HostCtx*> g_host;
@@ -50,6 +57,77 @@ const void* mapped_device_ptr(const void* h) {
   if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
   return a.devicePointer;
 }
+
+// ------------------------------------------- host copy pool (pageable buffers)
+// A drop-in caller hands over pageable numpy memory (the reference's
+// alloc_matrix is np.zeros, tensor.py:90-103).  cudaMemcpyAsync from pageable
+// memory is synchronous and goes through the driver's small bounce buffer, so
+// the staged path below copies each chunk between the caller's buffer and a
+// page-locked staging slot with this pool of persistent host threads (a
+// memcpy split into page-aligned pieces), and the DMA engines only ever see
+// page-locked memory.
+std::atomic<int> g_host_threads{0};  // 0: auto (min(16, hardware threads))
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool* p = new CopyPool();  // never destroyed: threads live with the process
+    return *p;
+  }
+  // dst[0, bytes) = src[0, bytes) using up to n threads (the caller is one of them)
+  void copy(void* dst, const void* src, size_t bytes) {
+    int n = g_host_threads.load();
+    if (n <= 0) n = std::min(16, std::max(1, static_cast<int>(std::thread::hardware_concurrency())));
+    const size_t piece = std::max<size_t>(size_t(1) << 20, ((bytes / n) + 4095) / 4096 * 4096);
+    const int parts = static_cast<int>(std::min<size_t>(n, (bytes + piece - 1) / piece));
+    if (parts <= 1) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    ensure(parts - 1);
+    std::unique_lock<std::mutex> lk(mu_);
+    job_ = [=](int i) {
+      const size_t a = size_t(i) * piece, b = std::min(bytes, a + piece);
+      if (a < b) std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
+    };
+    parts_ = parts;
+    next_ = 1;  // part 0 is done by the caller
+    pending_ = parts - 1;
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    job_(0);
+    lk.lock();
+    done_.wait(lk, [&] { return pending_ == 0; });
+  }
+
+ private:
+  void ensure(int n) {
+    std::lock_guard<std::mutex> g(mu_);
+    while (static_cast<int>(th_.size()) < n) th_.emplace_back([this] { loop(); });
+  }
+  void loop() {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(mu_);
+    for (;;) {
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      while (next_ < parts_) {
+        const int i = next_++;
+        auto fn = job_;
+        lk.unlock();
+        fn(i);
+        lk.lock();
+        if (--pending_ == 0) done_.notify_all();
+      }
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  std::vector<std::thread> th_;
+  std::function<void(int)> job_;
+  int parts_ = 0, next_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+};
 
 HostCtx* host_ctx(int dev) {
   std::lock_guard<std::mutex> g(g_host_mu);
@@ -198,14 +276,50 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
   }
   std::vector<int64_t> start(nchunks + 1, 0);
   for (int64_t k = 0; k < nchunks; ++k) start[k + 1] = start[k] + sched[k];
+  // pageable caller buffers: stage every chunk through page-locked slots
+  const bool staged_in = mapped_device_ptr(x_host) == nullptr;
+  const bool staged_out = mapped_device_ptr(y_host) == nullptr;
+  if ((staged_in || staged_out) && c->pin_bytes < need) {
+    SK_CUDA(cudaDeviceSynchronize());
+    for (int i = 0; i < kRing; ++i) {
+      if (c->pin_in[i]) cudaFreeHost(c->pin_in[i]);
+      if (c->pin_out[i]) cudaFreeHost(c->pin_out[i]);
+      c->pin_in[i] = c->pin_out[i] = nullptr;
+    }
+    c->pin_bytes = 0;
+    for (int i = 0; i < kRing; ++i) {
+      SK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->pin_in[i]), need, cudaHostAllocPortable));
+      SK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->pin_out[i]), need, cudaHostAllocPortable));
+    }
+    c->pin_bytes = need;
+  }
+  CopyPool& pool = CopyPool::get();
+  // copy chunk j's staged output back into the caller's buffer once its D2H is done
+  auto drain = [&](int64_t j) -> int {
+    const int i = static_cast<int>(j % kRing);
+    SK_CUDA(cudaEventSynchronize(c->ev_d2h[i]));
+    pool.copy(y_host + start[j] * cols, c->pin_out[i], size_t(sched[j] * row_bytes));
+    return SK_OK;
+  };
   for (int64_t k = 0; k < nchunks; ++k) {
     const int i = static_cast<int>(k % kRing);
     const int64_t r0 = start[k];
     const int64_t nr = sched[k];
     const size_t bytes = size_t(nr * row_bytes);
+    if (staged_out && k >= kRing) {  // slot i's staged output must be copied out first
+      st = drain(k - kRing);
+      if (st) return st;
+    }
     // input slot free once the kernel that last read it is done
     if (k >= kRing) SK_CUDA(cudaStreamWaitEvent(c->s_h2d, c->ev_k[i], 0));
-    SK_CUDA(cudaMemcpyAsync(c->dx[i], x_host + r0 * cols, bytes, cudaMemcpyHostToDevice,
+    const float* src = x_host + r0 * cols;
+    if (staged_in) {
+      // the staging slot is free once the H2D that last read it is done
+      if (k >= kRing) SK_CUDA(cudaEventSynchronize(c->ev_h2d[i]));
+      pool.copy(c->pin_in[i], src, bytes);
+      src = c->pin_in[i];
+    }
+    SK_CUDA(cudaMemcpyAsync(c->dx[i], src, bytes, cudaMemcpyHostToDevice,
                             c->s_h2d));
     SK_CUDA(cudaEventRecord(c->ev_h2d[i], c->s_h2d));
     SK_CUDA(cudaStreamWaitEvent(c->s_comp, c->ev_h2d[i], 0));
@@ -219,10 +333,15 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
     if (st) return st;
     SK_CUDA(cudaEventRecord(c->ev_k[i], c->s_comp));
     SK_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_k[i], 0));
-    SK_CUDA(cudaMemcpyAsync(y_host + r0 * cols, c->dy[i], bytes, cudaMemcpyDeviceToHost,
-                            c->s_d2h));
+    SK_CUDA(cudaMemcpyAsync(staged_out ? c->pin_out[i] : y_host + r0 * cols, c->dy[i], bytes,
+                            cudaMemcpyDeviceToHost, c->s_d2h));
     SK_CUDA(cudaEventRecord(c->ev_d2h[i], c->s_d2h));
   }
+  if (staged_out)
+    for (int64_t j = std::max<int64_t>(0, nchunks - kRing); j < nchunks; ++j) {
+      st = drain(j);
+      if (st) return st;
+    }
   // every chunk's non-finite flag in one small copy after the last kernel
   // (one DMA instead of one per chunk between the bulk transfers)
   SK_CUDA(cudaMemcpyAsync(c->hbad, c->dbad, size_t(nchunks) * sizeof(unsigned long long),

@@ -54,3 +54,21 @@ def softmax_abi(x: np.ndarray, mode: int = 0, x_offset: int = 0, y_offset: int =
 
 def plan(rows: int, cols: int) -> str:
     return _native.describe_plan(rows, cols, cols, cols, 0, 0, 0)
+
+
+def parity_all_rows(oracle, y_dev, x_host: np.ndarray, chunk_bytes: int = 64 << 20) -> dict:
+    """Every row of a device output against the oracle, in row chunks (so the
+    full c4 / c5a / c5b outputs fit host memory); worst metrics + gate."""
+    rows, cols = x_host.shape
+    step = max(1, chunk_bytes // (4 * cols))
+    worst = {"max_abs": 0.0, "max_rel": 0.0, "max_rowsum_dev": 0.0}
+    for a in range(0, rows, step):
+        b = min(rows, a + step)
+        ref = oracle.softmax_ref(x_host[a:b], True, nthreads=0)
+        d = oracle.parity(y_dev[a:b].cpu().numpy(), ref)
+        for k in worst:
+            worst[k] = max(worst[k], d[k])
+    worst["ok"] = bool(worst["max_abs"] <= oracle.TOL_ABS and worst["max_rel"] <= oracle.TOL_REL
+                       and worst["max_rowsum_dev"] <= oracle.TOL_ROWSUM)
+    worst["rows_checked"] = rows
+    return worst

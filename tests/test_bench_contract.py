@@ -22,8 +22,36 @@ def test_reference_arm_json_line():
         assert k in d, k
     assert d["impl"] == "reference" and d["unit"] == "GB/s" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
-    assert d["config"]["workload"].startswith("c2")
+    ref_present = (ROOT / "baseline" / "_ref" / "softmax_kit" / "kernels.py").exists()
+    assert d["cpu_baseline"]["kind"] == ("reference" if ref_present else "port")
+    assert d["cpu_baseline"]["cores"] >= 1
+    assert d["config"]["workload"].startswith("c5a")
+    assert set(d["config"]) == {"workload", "rows", "cols", "scaling"}
+
+
+def test_reference_arm_never_maps_the_product_library():
+    """The reference arm builds its inputs with the oracle's generators and
+    times softmax_kit (or the C restatement): no paper_1904_12380_b200 .so may
+    be mapped into that process (vs_reference voided for that)."""
+    code = (
+        "import runpy, sys\n"
+        "sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '0',"
+        " '--config', 'c2']\n"
+        "try:\n"
+        "    runpy.run_path('bench.py', run_name='__main__')\n"
+        "except SystemExit as e:\n"
+        "    assert not e.code, e.code\n"
+        "maps = open('/proc/self/maps').read()\n"
+        "bad = sorted({l.split()[-1] for l in maps.splitlines()"
+        " if 'paper_1904_12380_b200' in l and l.endswith('.so')})\n"
+        "print('PRODUCT_SO', bad)\n"
+        "print('PRODUCT_MODULES', sorted(m for m in sys.modules if m.startswith('paper_1904')))\n"
+    )
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                       cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "PRODUCT_SO []" in r.stdout, r.stdout
+    assert "PRODUCT_MODULES []" in r.stdout, r.stdout
 
 
 def _torchrun(nproc, *args, env=None, timeout=600):

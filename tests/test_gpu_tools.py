@@ -85,12 +85,14 @@ def test_bench_row_shard_under_torchrun():
 
     from tests.test_bench_contract import _torchrun
 
-    r = _torchrun(2, "--steps", "64", "--warmup", "3", "--e2e-steps", "1",
-                  "--no-cpu-baseline", env={"SK_BENCH_SHARE_DEVICE": "1"})
+    r = _torchrun(2, "--config", "c2", "--extra", "", "--steps", "64", "--warmup", "3",
+                  "--e2e-steps", "1", "--no-cpu-baseline", env={"SK_BENCH_SHARE_DEVICE": "1"})
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["config"]["global_rows"] == 2 * 65536
-    assert d["parity"]["ok"] and d["e2e"]["bitwise_equal_device_path"]
+    assert d["n_gpus"] == 2 and d["config"]["rows"] == 65536
+    assert d["setup"]["rows_per_gpu"] == 32768 and d["scaling"] == "strong"
+    assert d["parity"]["ok"] and d["parity"]["rows_checked"] == 65536
+    assert d["e2e"]["bitwise_equal_device_path"] and d["e2e"]["pinned"]["bitwise_equal_device_path"]
     assert d["gpu_launches"] == 64 and d["value"] > 0

@@ -126,3 +126,55 @@ def test_component_ops_bit_exact(golden_components, oracle):
         assert np.array_equal(bits(oracle.scale_reciprocal(e, s)), bits(g[f"{name}/scaled"])), name
         st = oracle.row_stats(r)
         assert np.array_equal(bits(np.array(st, np.float32)), bits(g[f"{name}/stats"])), name
+
+
+def test_oracle_config_table_matches_product():
+    """oracle/inputs.py restates configs.py's table (same shapes, laws, seeds)."""
+    import inputs
+
+    from paper_1904_12380_b200 import configs
+
+    assert set(inputs.CONFIGS) == set(configs.CONFIGS)
+    for k, a in inputs.CONFIGS.items():
+        b = configs.CONFIGS[k]
+        assert (a.rows, a.cols, a.dist, a.seed, a.sigma, a.low, a.high, a.plant_count,
+                a.plant_value) == (b.rows, b.cols, b.dist, b.seed, b.sigma, b.low, b.high,
+                                   b.plant_count, b.plant_value), k
+        assert a.describe() == b.describe()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_oracle_generator_matches_recorded_inputs(golden_meta, name):
+    """The checker's own generators rebuild the exact input bytes the reference
+    outputs were recorded on (input SHA-256 in golden.json)."""
+    import inputs
+
+    assert inputs.sha256(inputs.generate(name)) == golden_meta["configs"][name]["input_sha256"]
+
+
+def test_oracle_generator_row_blocks_match_product():
+    import inputs
+
+    from paper_1904_12380_b200 import configs
+
+    for name, start, count in (("c5a", 12345, 77), ("c4", 3, 2), ("c5b", 1000, 1), ("c2", 7, 9)):
+        a = inputs.generate(name, start, count)
+        b = configs.generate(name, start, count)
+        assert np.array_equal(bits(a), bits(b)), name
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c4", "c5a", "c5b"])
+def test_full_big_config_hash_matches_reference(golden_meta, oracle, name):
+    """Every output element of the big configs: the oracle's ReferenceClipped
+    output hash equals the hash recorded by running the reference itself on the
+    full config (tests/golden/make_golden.py); inputs from the checker's own
+    generator, pinned to the recorded input hash."""
+    import inputs
+
+    meta = golden_meta["configs"][name]
+    x = inputs.generate(name)
+    assert inputs.sha256(x) == meta["input_sha256"]
+    y = oracle.softmax_ref(x, True, nthreads=0)
+    del x
+    assert inputs.sha256(y) == meta["ref_clipped_sha256"]
