@@ -58,6 +58,15 @@ enum sk_mode { SK_MODE_CLIPPED = 0, SK_MODE_EXACT = 1, SK_MODE_APPROX = 2 };
  * timed out (a peer never arrived); the output is then undefined. */
 #define SK_EXCHANGE_ABORTED 0xFFFFFFFFFFFFFFFEull
 
+/* The library's per-device non-finite flag (a device uint64, SK_NO_BAD_ROW
+ * when clear): what the torch ops (torch_ops/sk_torch_ops.cpp) and the Python
+ * wrappers pass as bad_row, so an asynchronous call's bad row is seen by
+ * whoever checks the flag next (kernels.check_device_flag()).
+ * sk_flag_read copies *flag to the host on `stream` (waiting for the stream)
+ * and, with reset, clears it again. */
+int sk_device_flag(int device, unsigned long long** flag);
+int sk_flag_read(unsigned long long* flag, void* stream, int reset, unsigned long long* value);
+
 int sk_abi_version(void);
 const char* sk_status_string(int status);
 /* Last CUDA error text seen by this thread (empty if none). */
@@ -142,11 +151,21 @@ int sk_normalize_f32(const float* x, float* y, int64_t rows, int64_t cols, int64
  *       as ONE cooperative kernel on this GPU with `world` local blocks -- the
  *       same kernel and exchange code, for testing with fewer GPUs than ranks.
  *   sk_describe_colshard_plan: the per-rank plan (cols = shard width).
+ *   sk_xchg_reset: zero an exchange block on `stream` (epoch back to 0).  The
+ *       slot tags carry a 23-bit launch epoch, so a block must be reset at
+ *       least every sk_xchg_reset_period() launches; sk_colshard_softmax_f32
+ *       refuses (SK_ERR_ARGUMENT) a launch past that on a multi-rank block.
+ *       With peers in other processes every rank must be quiescent around the
+ *       reset (barrier, reset own block, synchronise, barrier);
+ *       sharding.FusedColumnShard does this itself.  Single-process blocks
+ *       (world 1, emulation) are reset automatically.
  */
 #define SK_IPC_HANDLE_BYTES 64
 size_t sk_xchg_block_bytes(void);
 int sk_xchg_alloc(int device, void** block);
 int sk_xchg_free(void* block);
+int sk_xchg_reset(void* block, void* stream);
+unsigned long long sk_xchg_reset_period(void);
 int sk_ipc_handle(const void* dev_ptr, void* handle);
 int sk_ipc_open(const void* handle, void** dev_ptr);
 int sk_ipc_close(void* dev_ptr);
@@ -184,6 +203,12 @@ int sk_sumscale_f32(float* buf, int64_t rows, int64_t cols, int64_t ld, void* st
  */
 int sk_row_sum_f32(const float* x, int64_t rows, int64_t cols, int64_t ldx, double* row_sum,
                    void* stream);
+/* row_max_scalar / row_stats of one row (kernels.py:119-126, 272-276) with
+ * the reference's results for ANY input: max = NaN if x[0] is NaN, else the
+ * largest non-NaN value; sum = f64 sum of expf(x - max), NaN / inf
+ * propagating.  One block; the component ops use it for non-finite rows. */
+int sk_row_stats_ref_f32(const float* x, int64_t n, float* row_max, double* row_sum,
+                         void* stream);
 int sk_shift_scale_f32(const float* x, float* y, int64_t n, float shift, float scale,
                        void* stream);
 
@@ -239,6 +264,9 @@ void sk_free_pinned(void* p);
  *                    latency path (cluster / split kernels) instead (default 3;
  *                    4-6 measured no better, profiles/r1d_latency_threshold_ab.jsonl)
  *   "host_chunk_kb"  sk_softmax_f32_host chunk size in KiB (0 = auto, ~1/4 of the job)
+ *   "gres_epoch_reset" launches between zeroings of a K3g exchange block (the
+ *                    library's per-stream block; the column-shard period); 0 =
+ *                    default 2^22, the maximum (the 23-bit slot epoch never wraps)
  *   "host_threads"   host threads copying pageable caller buffers through the
  *                    page-locked staging slots of sk_softmax_f32_host (0 = auto,
  *                    min(16, hardware threads))

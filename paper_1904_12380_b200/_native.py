@@ -65,6 +65,7 @@ SIGNATURES: dict[str, tuple] = {
     "sk_exp_f32": (c_int, [c_void_p, c_int64, c_int, c_void_p]),
     "sk_sumscale_f32": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p]),
     "sk_row_sum_f32": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p]),
+    "sk_row_stats_ref_f32": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "sk_shift_scale_f32": (c_int, [c_void_p, c_void_p, c_int64, c_float, c_float, c_void_p]),
     "sk_alloc_pinned": (c_void_p, [c_size_t]),
     "sk_free_pinned": (None, [c_void_p]),
@@ -80,6 +81,10 @@ SIGNATURES: dict[str, tuple] = {
     "sk_xchg_block_bytes": (c_size_t, []),
     "sk_xchg_alloc": (c_int, [c_int, POINTER(c_void_p)]),
     "sk_xchg_free": (c_int, [c_void_p]),
+    "sk_xchg_reset": (c_int, [c_void_p, c_void_p]),
+    "sk_device_flag": (c_int, [c_int, POINTER(c_void_p)]),
+    "sk_flag_read": (c_int, [c_void_p, c_void_p, c_int, POINTER(c_uint64)]),
+    "sk_xchg_reset_period": (c_uint64, []),
     "sk_ipc_handle": (c_int, [c_void_p, c_void_p]),
     "sk_ipc_open": (c_int, [c_void_p, POINTER(c_void_p)]),
     "sk_ipc_close": (c_int, [c_void_p]),

@@ -75,8 +75,11 @@ def _stats(x, op: str):
             x.data_ptr(), 1, x.numel(), x.numel(), _native.SK_MODE_EXACT, rmax.data_ptr(),
             rsum.data_ptr(), flag.data_ptr(), None, 0, _stream(x)), op)
         if int(flag.item()) != -1:
+            # a NaN / inf in the row: the reference returns its scan result
+            # (no error), so recompute with the NaN / inf-propagating kernel
             flag.fill_(-1)
-            raise NumericDomainError(f"{op}: non-finite value in the row")
+            _native.check(_native.lib().sk_row_stats_ref_f32(
+                x.data_ptr(), x.numel(), rmax.data_ptr(), rsum.data_ptr(), _stream(x)), op)
     return rmax, rsum
 
 

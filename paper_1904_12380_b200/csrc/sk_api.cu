@@ -706,7 +706,9 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     // profiles/r1d_k1m_block_size_ab.jsonl; same bits); the k1m_threads knob
     // forces a size that still holds a whole row
     const int kt = g_k1m_threads.load();
-    p.threads = (kt >= 32 * wpr && kt <= kRowsThreads) ? kt : 32 * wpr;
+    // whole rows per block: a multiple of 32 * WPR threads (a partial row would
+    // read reduction slots no warp wrote)
+    p.threads = (kt >= 32 * wpr && kt <= kRowsThreads) ? kt / (32 * wpr) * (32 * wpr) : 32 * wpr;
     const int64_t rpc = p.threads / 32 / wpr;
     p.grid = std::max<int64_t>(1, std::min<int64_t>((rows + rpc - 1) / rpc, INT32_MAX));
     return SK_OK;
@@ -727,7 +729,8 @@ int make_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint64_t xa,
     // block size: 256 threads, halved (to 64) while the job would occupy fewer
     // CTAs than SMs -- a small job then spreads over the chip.  Each row is one
     // warp's work whatever the block size, so the bits do not change.
-    int threads = std::max(32, std::min(g_k1_threads.load(), kRowsThreads));
+    // a whole number of warps (K1 numbers warps as (blockIdx*blockDim+tid)>>5)
+    int threads = std::max(32, std::min(g_k1_threads.load(), kRowsThreads) / 32 * 32);
     auto rows_per = [&](int t) { return int64_t(t / 32) * u * (32 / lpr); };
     while (threads > 64 && (rows + rows_per(threads) - 1) / rows_per(threads) < di.sms) threads /= 2;
     p.threads = threads;
@@ -843,8 +846,16 @@ constexpr size_t kGresWsMax = size_t(1) << 20;  // >= any single-device plan (<=
 
 // Library-owned K3g control block per (device, stream): zeroed once, then
 // only ever advanced by the kernels themselves (other paths never touch it).
+// The kernels zero this block themselves every gres_reset_period() launches
+// (GresComm::reset_words, sk_gres.cuh), so its 23-bit slot epoch never wraps,
+// CUDA-graph replays included.
 std::mutex g_gres_mu;
 std::map<std::pair<int, cudaStream_t>, void*> g_gres_blk;
+std::atomic<unsigned long long> g_gres_epoch_reset{kGresEpochReset};
+unsigned long long gres_reset_period() {
+  const unsigned long long v = g_gres_epoch_reset.load();
+  return (v == 0 || v > kGresEpochReset) ? kGresEpochReset : v;
+}
 int get_gres_block(int dev, cudaStream_t s, char** out) {
   std::lock_guard<std::mutex> g(g_gres_mu);
   void*& b = g_gres_blk[{dev, s}];
@@ -1037,6 +1048,10 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
       comm.nvr = 1;
       comm.sys = 0;
       comm.spin_limit = g_gres_spins.load();
+      // the library block: self-reset by the kernel; a caller's workspace is
+      // cleared before every launch (above)
+      comm.reset_words = user_ws ? 0ull : (kGresWsMax - w.slots) / 8;
+      comm.reset_period = static_cast<unsigned>(gres_reset_period());
       int P = p.nseg, slice = p.seglen, nst = p.lag;
       SK_CUDA(launch_k(gres_fn(mode, p.glag, p.threads == kGresBlock, p.unal), dim3(static_cast<unsigned>(p.grid)),
                        dim3(p.threads), p.smem, s, true, x, y, rows, cols, ldx, ldy, P, slice, nst, comm,
@@ -1134,6 +1149,10 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "gres_sleep") g_gres_sleep = value;
   else if (k == "gres_split") g_gres_split = value;
   else if (k == "gres_lag") g_gres_lag = value;
+  else if (k == "gres_epoch_reset") {
+    if (value < 0) return arg_fail("gres_epoch_reset: launches between exchange-block resets (0 = default)");
+    g_gres_epoch_reset = static_cast<unsigned long long>(value);
+  }
   else if (k == "k1m") g_k1m = value;
   else if (k == "k1_fit") g_k1_fit = value;
   else if (k == "k1_threads") g_k1_threads = value;
@@ -1194,6 +1213,42 @@ int sk_describe_plan(int64_t rows, int64_t cols, int64_t ldx, int64_t ldy, uint6
     const size_t n = strlen(buf);
     if (n < size_t(buflen)) snprintf(buf + n, size_t(buflen) - n, " lag=%d", p.glag);
   }
+  return SK_OK;
+}
+
+int sk_device_flag(int device, unsigned long long** flag) {
+  if (!flag) return arg_fail("null output pointer");
+  static std::mutex mu;
+  static std::map<int, unsigned long long*> flags;
+  std::lock_guard<std::mutex> g(mu);
+  unsigned long long*& f = flags[device];
+  if (!f) {
+    int prev = 0;
+    SK_CUDA(cudaGetDevice(&prev));
+    SK_CUDA(cudaSetDevice(device));
+    cudaError_t e = cudaMalloc(&f, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(f, 0xFF, sizeof(unsigned long long));  // SK_NO_BAD_ROW
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) {
+      f = nullptr;
+      return cuda_fail(e, "sk_device_flag");
+    }
+  }
+  *flag = f;
+  return SK_OK;
+}
+
+int sk_flag_read(unsigned long long* flag, void* stream, int reset, unsigned long long* value) {
+  if (!flag || !value) return arg_fail("null pointer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned long long v = SK_NO_BAD_ROW;
+  SK_CUDA(cudaMemcpyAsync(&v, flag, sizeof(v), cudaMemcpyDeviceToHost, s));
+  SK_CUDA(cudaStreamSynchronize(s));
+  if (reset && v != SK_NO_BAD_ROW) {
+    SK_CUDA(cudaMemsetAsync(flag, 0xFF, sizeof(v), s));
+    SK_CUDA(cudaStreamSynchronize(s));
+  }
+  *value = v;
   return SK_OK;
 }
 

@@ -6,6 +6,9 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
 
 #include "sk_gres.cuh"
 #include "sk_internal.h"
@@ -22,6 +25,16 @@ namespace detail {
 // the kernel, overlapped with the streaming -- no NCCL call on the data path.
 constexpr size_t kXBlockBytes = size_t(2) << 20;
 constexpr size_t kXSlots = 256;
+
+// Cross-GPU blocks (peers in other processes write into them) are reset by
+// their owner through sk_xchg_reset with every rank quiescent
+// (sharding.FusedColumnShard does it every gres_reset_period() calls between
+// two barriers); this counts launches per owned block and refuses one past
+// the period rather than risk a wrapped epoch.  Blocks no other process
+// writes (world 1, emulation) are reset by the kernel itself
+// (GresComm::reset_words), CUDA-graph replays included.
+std::mutex g_xchg_mu;
+std::map<const void*, unsigned long long> g_xchg_launches;
 
 int colshard_launch(const float* x, float* y, int64_t rows, int64_t cols, int64_t ldx,
                     int64_t ldy, int mode, int rank, int world, int nvr, void* const* blocks,
@@ -55,6 +68,16 @@ int colshard_launch(const float* x, float* y, int64_t rows, int64_t cols, int64_
     return SK_OK;
   }
   if (rows == 0) return SK_OK;
+  const bool cross_gpu = world > 1 && nvr == 1;
+  if (cross_gpu) {
+    std::lock_guard<std::mutex> g(g_xchg_mu);
+    unsigned long long& n = g_xchg_launches[blocks[rank]];
+    const unsigned long long period = gres_reset_period();
+    if (n >= period)
+      return arg_fail("exchange block needs sk_xchg_reset: " + std::to_string(n) +
+                      " launches since the last reset (limit " + std::to_string(period) + ")");
+    ++n;
+  }
   GresComm comm = {};
   for (int r = 0; r < world; ++r)
     comm.dst[r] = reinterpret_cast<unsigned long long*>(static_cast<char*>(blocks[r]) + kXSlots);
@@ -65,6 +88,8 @@ int colshard_launch(const float* x, float* y, int64_t rows, int64_t cols, int64_
   comm.nvr = nvr;
   comm.sys = (world > 1 && nvr == 1) ? 1 : 0;  // peers are other GPUs
   comm.spin_limit = g_gres_spins.load();
+  comm.reset_words = cross_gpu ? 0ull : (kXBlockBytes - kXSlots) / 8;
+  comm.reset_period = static_cast<unsigned>(gres_reset_period());
   const size_t smem = size_t(gc.st) * gc.slice * sizeof(float);
   int P = gc.P, slice = static_cast<int>(gc.slice), nst = gc.st;
   const int grid = gc.groups * gc.P * nvr;
@@ -100,9 +125,25 @@ int sk_xchg_alloc(int device, void** block) {
 }
 
 int sk_xchg_free(void* block) {
-  if (block) SK_CUDA(cudaFree(block));
+  if (block) {
+    {
+      std::lock_guard<std::mutex> g(g_xchg_mu);
+      g_xchg_launches.erase(block);
+    }
+    SK_CUDA(cudaFree(block));
+  }
   return SK_OK;
 }
+
+int sk_xchg_reset(void* block, void* stream) {
+  if (!block) return arg_fail("null exchange block");
+  SK_CUDA(cudaMemsetAsync(block, 0, kXBlockBytes, static_cast<cudaStream_t>(stream)));
+  std::lock_guard<std::mutex> g(g_xchg_mu);
+  g_xchg_launches[block] = 0;
+  return SK_OK;
+}
+
+unsigned long long sk_xchg_reset_period(void) { return gres_reset_period(); }
 
 int sk_ipc_handle(const void* dev_ptr, void* handle) {
   if (!dev_ptr || !handle) return arg_fail("null pointer");

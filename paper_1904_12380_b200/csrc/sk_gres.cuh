@@ -91,6 +91,14 @@ struct GresComm {
   int64_t shard_stride;
   int world, rank0, nvr, sys;
   unsigned spin_limit;  // polls before a missing peer aborts the exchange
+  // Device-side epoch reset (blocks no other process writes: the library's
+  // per-stream block, a world-1 or emulated column shard): every
+  // reset_period launches the launch's last CTA zeroes reset_words 64-bit
+  // words of slots in each of the launch's blocks and restarts the epoch at
+  // 0, so the 23-bit slot epoch never wraps -- CUDA-graph replays included.
+  // 0: the host resets the block (cross-GPU column shards, sk_xchg_reset).
+  unsigned long long reset_words;
+  unsigned reset_period;
 };
 
 // comm.dst[i] without dynamic indexing of the parameter array (which would
@@ -106,13 +114,22 @@ __device__ __forceinline__ unsigned long long* gres_dst(const GresComm& c, int i
 // A CTA's row pair as one 16-B slot of two independently tagged 64-bit words:
 // tag << 32 | bits(m) and tag << 32 | bits(s) -- the CTA's partial sum rounded
 // to fp32 (2^-24 relative; the row sum S itself is still accumulated in f64
-// over the pairs).  tag = epoch << 16 | 0x8000 | (k & 0x7fff): never 0 (zeroed
-// memory is "not yet"), unique against the slot's previous row (k - 2L-2)
-// and previous launches (epoch), so the data IS the flag -- no counter, no
-// fence, no per-launch memset for a peer to race.  One store, one load.
+// over the pairs).  tag = 0x80000000 | (epoch mod 2^23) << 8 | (k mod 256):
+// never 0 (zeroed memory is "not yet"); the row bits only have to tell k from
+// the slot set's previous row in this launch, k - (2L+2) with 2L+2 <= 8; the
+// 23 epoch bits tell this launch from every earlier one, because the host
+// zeroes an exchange block (epoch back to 0, every slot "not yet") at least
+// every kGresEpochReset < 2^23 launches -- so the epoch never wraps and a slot
+// left over from an older launch can never carry a matching tag.  The data IS
+// the flag -- no counter, no fence, no per-launch memset for a peer to race.
+// One store, one load.
+constexpr unsigned kGresEpochBits = 23;
+constexpr unsigned long long kGresEpochReset = 1ull << 22;  // default reset period (launches)
+static_assert(kGresEpochReset < (1ull << kGresEpochBits), "the epoch must never wrap");
 __device__ __forceinline__ unsigned gres_tag(unsigned epoch, unsigned k) {
-  return (epoch << 16) | 0x8000u | (k & 0x7fffu);
+  return 0x80000000u | ((epoch & ((1u << kGresEpochBits) - 1u)) << 8) | (k & 0xFFu);
 }
+static_assert(2 * 3 + 2 <= 256, "row tag bits must cover the slot-set rotation");
 __device__ __forceinline__ void gres_publish(unsigned long long* slot, float m, double s,
                                              unsigned tag, bool sys) {
   const unsigned long long t = static_cast<unsigned long long>(tag) << 32;
@@ -461,12 +478,30 @@ __global__ void __launch_bounds__(kGresBlock, 1)
   // The launch's last CTA advances the epoch (every CTA has read it by now)
   // and turns an exchange timeout into a status the host can see.
   __syncthreads();
+  __shared__ int last_s;
   if (tid == 0) {
     __threadfence();
-    if (atomicAdd(comm.ctl + 1, 1u) == gridDim.x - 1) {
+    last_s = atomicAdd(comm.ctl + 1, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last_s) {
+    // every other CTA of the launch is done with the slots; the next launch
+    // reads them only after griddepcontrol.wait, i.e. after this grid completes
+    const bool wipe = comm.reset_words != 0 && comm.reset_period != 0 &&
+                      (epoch + 1u) % comm.reset_period == 0u;
+    if (wipe) {
+      const int nb = comm.nvr == comm.world ? comm.world : 1;
+      for (int r = 0; r < nb; ++r) {
+        unsigned long long* d = comm.nvr == comm.world ? gres_dst(comm, r) : gres_dst(comm, comm.rank0);
+        for (unsigned long long i = tid; i < comm.reset_words; i += blockDim.x) d[i] = 0ull;
+      }
+      __threadfence();
+      __syncthreads();
+    }
+    if (tid == 0) {
       if (atomicExch(comm.ctl + 2, 0u)) atomicMin(bad_row, kExchangeAborted);
       comm.ctl[1] = 0;
-      comm.ctl[0] = epoch + 1u;
+      comm.ctl[0] = wipe ? 0u : epoch + 1u;
     }
   }
 }

@@ -86,6 +86,9 @@ GresChoice plan_gres(int64_t rows, int64_t cols, int mode, const DevInfo& di, in
                      bool unal);
 const void* gres_fn(int mode, int lag, bool split);
 bool gres_split(int lag);
+// exchange blocks are zeroed every gres_reset_period() launches (<= 2^22) so the
+// slot tags' 23-bit epoch never wraps (sk_gres.cuh, gres_tag)
+unsigned long long gres_reset_period();
 // the K3g plan is modelled at this row count: plans (hence bits) depend on C only
 inline constexpr int64_t kGresPlanRows = 2048;
 

@@ -118,6 +118,41 @@ __global__ void k_shift_scale(const float* __restrict__ x, float* __restrict__ y
     y[i] = __fmul_rn(__fsub_rn(x[i], shift), scale);
 }
 
+// row_max_scalar / row_stats of ONE row with the reference's semantics for
+// ANY input (kernels.py:119-126 strict '>' scan from a[0]; kernels.py:272-276
+// sum of np.exp(row - max) in f64): max = NaN if a[0] is NaN, else the largest
+// non-NaN value (-inf for an all -inf row); sum = sum of expf(a - max) with
+// IEEE propagation (NaN / inf in, NaN / inf out).  The component ops take it
+// for rows the fast stats kernel flagged as non-finite.
+__global__ void __launch_bounds__(kPhaseThreads)
+    k_row_stats_ref(const float* __restrict__ x, int64_t n, float* __restrict__ out_max,
+                    double* __restrict__ out_sum) {
+  __shared__ float redf[kPhaseThreads / 32];
+  __shared__ double red[kPhaseThreads / 32];
+  __shared__ float mb;
+  float m = -INFINITY;
+  for (int64_t i = threadIdx.x; i < n; i += kPhaseThreads) m = fmaxf(m, x[i]);  // NaN ignored
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) redf[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float v = redf[0];
+    for (int w = 1; w < kPhaseThreads / 32; ++w) v = fmaxf(v, redf[w]);
+    mb = isnan(x[0]) ? x[0] : v;
+  }
+  __syncthreads();
+  const float M = mb;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += kPhaseThreads)
+    s += static_cast<double>(expf(__fsub_rn(x[i], M)));
+  s = cta_reduce_sum(s, red);
+  if (threadIdx.x == 0) {
+    *out_max = M;
+    *out_sum = s;
+  }
+}
+
 unsigned elementwise_grid(int64_t n) {
   int sms = 148;
   int dev = 0;
@@ -174,6 +209,14 @@ int sk_row_sum_f32(const float* x, int64_t rows, int64_t cols, int64_t ldx, doub
   if (rows == 0) return SK_OK;
   sk::k_rowsum<<<static_cast<unsigned>(rows), sk::kPhaseThreads, 0,
                  static_cast<cudaStream_t>(stream)>>>(x, cols, ldx, row_sum);
+  return cudaGetLastError() == cudaSuccess ? SK_OK : SK_ERR_CUDA;
+}
+
+int sk_row_stats_ref_f32(const float* x, int64_t n, float* row_max, double* row_sum,
+                         void* stream) {
+  if (n < 1 || !x || !row_max || !row_sum) return SK_ERR_ARGUMENT;
+  sk::k_row_stats_ref<<<1, sk::kPhaseThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      x, n, row_max, row_sum);
   return cudaGetLastError() == cudaSuccess ? SK_OK : SK_ERR_CUDA;
 }
 

@@ -9,14 +9,18 @@ Mirror of /root/reference/pkg/src/softmax_kit/kernels.py:
 * ``softmax(m, variant, cfg=LaneConfig())`` (kernels.py:350-362): same
   signature and error behaviour.  ``m`` may be
 
-  - a ``Matrix2D`` (the reference's type): copied to the GPU in row chunks,
-    computed, copied back into a fresh ``Matrix2D`` (H2D/compute/D2H
-    pipelined over streams inside the native library);
+  - a ``Matrix2D`` -- this package's, or the reference's own
+    ``softmax_kit.tensor.Matrix2D`` (duck-typed: rows / cols / flat float32
+    ``data`` / ``view2d``, validated like tensor.py:43-57): copied to the GPU
+    in row chunks, computed, copied back into a fresh Matrix2D of the
+    caller's class (H2D/compute/D2H pipelined over streams inside the native
+    library; pageable buffers are staged through page-locked slots);
   - a CUDA ``torch.Tensor[N, C]`` float32 with unit column stride (the hot
     path): returns a same-shape CUDA tensor on the current stream;
   - a 2-D float32 ``numpy.ndarray``: like ``Matrix2D``, returns an ndarray.
 
-  ``variant`` selects the arithmetic: ReferenceClipped clamps shifted logits
+  ``variant`` (this package's KernelVariant or the reference's, matched by
+  value) selects the arithmetic: ReferenceClipped clamps shifted logits
   at -64 (kernels.py:147); every other rung is the same math without the clip
   (SPEC.md:97 invariant); FullVectorizedApproxExp uses the ex2.approx
   exponential (tolerance 1e-5, bench.py:52).  ``cfg`` is validated but has no
@@ -90,10 +94,24 @@ class RowStats(NamedTuple):
     sum: Any
 
 
+def as_variant(variant) -> KernelVariant:
+    """This package's KernelVariant for ``variant``: its own members, or the
+    reference's own enum (softmax_kit.kernels.KernelVariant, kernels.py:76-93 --
+    same member values), so a caller that swaps only the ``softmax`` import
+    keeps passing its variants; anything else is an ArgumentError
+    (kernels.py:304-305)."""
+    if isinstance(variant, KernelVariant):
+        return variant
+    if isinstance(variant, enum.Enum) and isinstance(variant.value, str):
+        for v in KernelVariant:
+            if v.value == variant.value:
+                return v
+    raise ArgumentError(f"expected a KernelVariant, got {variant!r}")
+
+
 def variant_mode(variant: KernelVariant) -> int:
     """Variant -> native arithmetic mode (include/softmax_b200.h, sk_mode)."""
-    if not isinstance(variant, KernelVariant):
-        raise ArgumentError(f"expected a KernelVariant, got {variant!r}")  # kernels.py:304-305
+    variant = as_variant(variant)
     if variant is KernelVariant.REFERENCE_CLIPPED:
         return _native.SK_MODE_CLIPPED
     if variant is KernelVariant.FULL_VECTORIZED_APPROX_EXP:
@@ -114,8 +132,75 @@ def _sync_fault_hook() -> None:
 
 
 def _check_cfg(cfg: LaneConfig) -> None:
-    if not isinstance(cfg, LaneConfig):
-        raise ArgumentError(f"expected a LaneConfig, got {cfg!r}")
+    """This package's LaneConfig or the reference's (simd_reduce.py:60-75, a
+    frozen dataclass with ``width``): same validation rule, no numeric effect."""
+    if isinstance(cfg, LaneConfig):
+        return
+    w = getattr(cfg, "width", None)
+    if isinstance(w, int) and not isinstance(w, bool):
+        LaneConfig(w)  # same rule, same error
+        return
+    raise ArgumentError(f"expected a LaneConfig, got {cfg!r}")
+
+
+def _is_foreign_matrix(m) -> bool:
+    """A Matrix2D of another class with the reference's interface
+    (tensor.py:31-72: rows, cols, a flat float32 ``data`` buffer, ``view2d``),
+    e.g. softmax_kit.tensor.Matrix2D itself."""
+    return (not isinstance(m, Matrix2D) and isinstance(getattr(m, "data", None), np.ndarray)
+            and isinstance(getattr(m, "rows", None), (int, np.integer))
+            and isinstance(getattr(m, "cols", None), (int, np.integer))
+            and hasattr(type(m), "view2d"))
+
+
+def _foreign_view(m, what: str) -> np.ndarray:
+    """Validate a foreign Matrix2D like Matrix2D.__post_init__ (tensor.py:43-57)
+    and return its (rows, cols) view."""
+    rows, cols, data = int(m.rows), int(m.cols), m.data
+    if rows < 1 or cols < 1:
+        raise ArgumentError(f"matrix dimensions must be >= 1, got {rows}x{cols}")
+    if data.dtype != np.float32:
+        raise ArgumentError(f"expected float32 data, got {data.dtype}")
+    if data.ndim != 1 or not data.flags.c_contiguous:
+        raise ArgumentError("data must be a contiguous 1-D buffer")
+    if data.size != rows * cols:
+        raise ArgumentError(f"data length {data.size} != rows*cols = {rows * cols}")
+    if what == "out" and not data.flags.writeable:
+        raise ArgumentError("out must be writeable")
+    return data.reshape(rows, cols)
+
+
+def _foreign_error(m, e: Exception) -> Exception:
+    """``e`` re-typed so the caller's own error classes catch it too: for a
+    reference Matrix2D (softmax_kit.tensor) the raised class derives from both
+    this package's class and softmax_kit.errors' class of the same name
+    (errors.py:4-21), so ``except softmax_kit.errors.NumericDomainError`` works
+    after swapping only the ``softmax`` import."""
+    import sys
+
+    mod = sys.modules.get(type(m).__module__.rsplit(".", 1)[0] + ".errors")
+    theirs = getattr(mod, type(e).__name__, None) if mod else None
+    if not (isinstance(theirs, type) and issubclass(theirs, Exception)) or isinstance(e, theirs):
+        return e
+    key = (type(e), theirs)
+    cls = _FOREIGN_ERR.get(key)
+    if cls is None:
+        cls = type(type(e).__name__, (type(e), theirs), {"__module__": type(e).__module__})
+        _FOREIGN_ERR[key] = cls
+    return cls(*e.args)
+
+
+_FOREIGN_ERR: dict = {}
+
+
+def _foreign_out(m):
+    """A fresh output of the caller's own Matrix2D class (kernels.py:358 returns
+    a fresh Matrix2D), backed by a 32-B aligned zeroed buffer."""
+    data = alloc_matrix(int(m.rows), int(m.cols)).data
+    try:
+        return type(m)(rows=int(m.rows), cols=int(m.cols), data=data)
+    except Exception:  # noqa: BLE001 -- a class we cannot construct: ours
+        return Matrix2D(rows=int(m.rows), cols=int(m.cols), data=data)
 
 
 # ---------------------------------------------------------------- host path
@@ -134,11 +219,44 @@ def _softmax_host(x2d: np.ndarray, out2d: np.ndarray, mode: int, device: int) ->
 _flags: dict[int, Any] = {}
 
 
+class _DeviceFlag:
+    """The library's per-device non-finite flag (sk_device_flag): one device
+    uint64 shared by every entry point on the device -- the Python wrappers
+    here and the torch.ops launchers (torch_ops/sk_torch_ops.cpp) -- so a bad
+    row recorded by an asynchronous call is raised by the next check.  Reads
+    go through sk_flag_read on the device's current stream (like
+    ``Tensor.item()``, they wait for it)."""
+
+    def __init__(self, torch, index: int):
+        self._torch, self.index = torch, index
+        p = ctypes.c_void_p()
+        _native.check(_native.lib().sk_device_flag(index, ctypes.byref(p)), "device_flag")
+        self.ptr = int(p.value)
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+    def _read(self, reset: int) -> int:
+        v = ctypes.c_uint64()
+        s = self._torch.cuda.current_stream(self.index).cuda_stream
+        _native.check(_native.lib().sk_flag_read(self.ptr, s, reset, ctypes.byref(v)), "flag_read")
+        return ctypes.c_int64(v.value).value  # SK_NO_BAD_ROW -> -1, aborted -> -2
+
+    def item(self) -> int:
+        return self._read(0)
+
+    def fill_(self, value: int) -> "_DeviceFlag":
+        if value != -1:
+            raise ValueError("the device flag can only be cleared")
+        self._read(1)
+        return self
+
+
 def _bad_flag(torch, device):
     idx = device.index if device.index is not None else torch.cuda.current_device()
     f = _flags.get(idx)
     if f is None:
-        f = torch.full((1,), -1, dtype=torch.int64, device=device)  # == SK_NO_BAD_ROW
+        f = _DeviceFlag(torch, idx)
         _flags[idx] = f
     return f
 
@@ -202,16 +320,16 @@ def softmax(m, variant: KernelVariant, cfg: LaneConfig = LaneConfig(), *,
             out=None, device: int | None = None, check_finite: bool = True):
     """Run one softmax variant over ``m`` and return a fresh output
     (kernels.py:350-362).  See the module docstring for accepted types."""
+    if _is_foreign_matrix(m):
+        try:
+            return _softmax_matrix(m, variant, cfg, out, device)
+        except SoftmaxKitError as e:
+            raise _foreign_error(m, e) from None
     mode = variant_mode(variant)
     _check_cfg(cfg)
     _sync_fault_hook()
     if isinstance(m, Matrix2D):
-        if out is None:
-            out = alloc_matrix(m.rows, m.cols)
-        elif not isinstance(out, Matrix2D) or out.shape != m.shape:
-            raise ArgumentError("out must be a Matrix2D of the input's shape")
-        _softmax_host(m.view2d, out.view2d, mode, _host_device(device))
-        return out
+        return _softmax_matrix(m, variant, cfg, out, device)
     if isinstance(m, np.ndarray):
         if m.ndim != 2 or m.dtype != np.float32:
             raise ArgumentError("numpy input must be a 2-D float32 array")
@@ -231,6 +349,26 @@ def softmax(m, variant: KernelVariant, cfg: LaneConfig = LaneConfig(), *,
         softmax_into(m, y, variant, cfg, check_finite=check_finite)
         return y
     raise ArgumentError(f"unsupported input type {type(m).__name__}")
+
+
+def _softmax_matrix(m, variant, cfg, out, device):
+    """The host-buffer path for this package's or a foreign Matrix2D."""
+    mode = variant_mode(variant)
+    _check_cfg(cfg)
+    _sync_fault_hook()
+    x2d = m.view2d if isinstance(m, Matrix2D) else _foreign_view(m, "input")
+    if out is None:
+        out = alloc_matrix(m.rows, m.cols) if isinstance(m, Matrix2D) else _foreign_out(m)
+    if isinstance(out, Matrix2D):
+        y2d = out.view2d
+    elif _is_foreign_matrix(out):
+        y2d = _foreign_view(out, "out")
+    else:
+        raise ArgumentError("out must be a Matrix2D of the input's shape")
+    if y2d.shape != x2d.shape:
+        raise ArgumentError("out must be a Matrix2D of the input's shape")
+    _softmax_host(x2d, y2d, mode, _host_device(device))
+    return out
 
 
 def _host_device(device: int | None) -> int:

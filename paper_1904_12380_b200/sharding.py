@@ -148,6 +148,17 @@ class NativeExchange:
     def free(self, block: int) -> None:
         self._native.check(self.L.sk_xchg_free(block), "xchg_free")
 
+    def reset_period(self) -> int:
+        return int(self.L.sk_xchg_reset_period())
+
+    def reset(self, block: int) -> None:
+        """Zero the block on the current stream and wait for it."""
+        import torch
+
+        s = torch.cuda.current_stream()
+        self._native.check(self.L.sk_xchg_reset(block, s.cuda_stream), "xchg_reset")
+        s.synchronize()
+
     def handle(self, block: int) -> bytes:
         import ctypes
 
@@ -196,7 +207,8 @@ class FusedColumnShard:
     runs on CPU with gloo and a test double (tests/test_sharding_gloo.py).
     """
 
-    def __init__(self, group=None, device: int | None = None, *, native=None, all_gather=None):
+    def __init__(self, group=None, device: int | None = None, *, native=None, all_gather=None,
+                 barrier=None):
         import torch.distributed as dist
 
         if dist.is_available() and dist.is_initialized():
@@ -213,6 +225,14 @@ class FusedColumnShard:
                 out = [None] * self.world
                 dist.all_gather_object(out, obj, group=group)
                 return out
+        if barrier is None:
+            def barrier():
+                if self.world > 1:
+                    dist.barrier(group=group)
+        self._all_gather = all_gather
+        self._barrier = barrier
+        self._agreed = None  # the (rows, cols, mode) every rank last agreed on
+        self._calls = 0
         if device is None:
             import torch
 
@@ -238,7 +258,20 @@ class FusedColumnShard:
             raise ArgumentError("FusedColumnShard is closed")
         if x_local.dim() != 2 or x_local.dtype != torch.float32 or not x_local.is_cuda:
             raise ArgumentError("x_local must be a CUDA float32 [N, C_r] tensor")
-        y = torch.empty_like(x_local) if out is None else out
+        rows, cols = x_local.shape
+        if cols > 1 and x_local.stride(1) != 1:
+            raise ArgumentError("x_local must have unit column stride")
+        if out is None:
+            y = torch.empty_like(x_local)
+        else:
+            if not isinstance(out, torch.Tensor) or not out.is_cuda or out.dtype != torch.float32:
+                raise ArgumentError("out must be a CUDA float32 tensor")
+            if tuple(out.shape) != (rows, cols) or out.device != x_local.device:
+                raise ArgumentError(f"out must be [{rows}, {cols}] on {x_local.device}")
+            if cols > 1 and out.stride(1) != 1:
+                raise ArgumentError("out must have unit column stride")
+            y = out
+        self._prepare(rows, cols, mode, sync=torch.cuda.synchronize)
         flag = _bad_flag(torch, x_local.device)
         self._n.launch(x_local, y, mode, self.rank, self.world, self.blocks, flag)
         if check_finite:
@@ -248,6 +281,38 @@ class FusedColumnShard:
                 flag.fill_(-1)
                 raise NumericDomainError(f"non-finite logits in row {bad}")
         return y
+
+    def _prepare(self, rows: int, cols: int, mode: int, sync=None) -> None:
+        """Host side of one call, in the same order on every rank:
+
+        * the first call, and every call whose (rows, shard width, mode)
+          differs from this rank's previous call, all-gathers it and raises on
+          every rank if any rank differs -- the K3g plan (slot layout, CTAs
+          per row, ring depth) is a function of the shard width, so uneven
+          shards would merge mismatched slots or poll until the exchange
+          timeout.  (Calls, shape changes included, must be issued in the
+          same order on every rank: a rank that changes shape alone waits in
+          the all-gather instead of launching.);
+        * every ``reset_period()`` calls all ranks quiesce and zero their
+          own exchange block (the slot tags' 23-bit epoch then never wraps;
+          sk_gres.cuh, gres_tag)."""
+        key = (int(rows), int(cols), int(mode))
+        if key != self._agreed:
+            seen = [tuple(k) for k in self._all_gather(key)]
+            if any(k != key for k in seen):
+                raise ArgumentError(
+                    "column shards differ across ranks (rows, shard width, mode): "
+                    f"{seen}; every rank needs the same rows, the same number of columns and "
+                    "the same variant")
+            self._agreed = key
+        period = max(1, int(self._n.reset_period()))
+        if self._calls and self._calls % period == 0:
+            if sync is not None:
+                sync()
+            self._barrier()  # no rank is still publishing into a peer's block
+            self._n.reset(self.block)
+            self._barrier()  # every block is zero before any rank launches again
+        self._calls += 1
 
     def close(self) -> None:
         if self._closed:

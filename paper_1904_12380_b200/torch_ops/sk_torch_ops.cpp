@@ -9,8 +9,11 @@
 //                                   (clip = variant is REFERENCE_CLIPPED)
 //   row_max / row_sumexp / normalize_   RowStats pieces, kernels.py:108-112,
 //                                   272-276 (the column-shard building blocks)
-// Non-finite rows are recorded in the library's per-stream device flag (the
-// ops are asynchronous); kernels.check_device_flag() raises for them.
+// Non-finite rows (and a timed-out row-statistics exchange) are recorded in
+// the library's per-device flag (sk_device_flag) -- the flag the Python
+// wrappers use too -- because the ops are asynchronous;
+// kernels.check_device_flag() raises NumericDomainError / SoftmaxKitError
+// for them.
 #include <ATen/ATen.h>
 #include <c10/cuda/CUDAGuard.h>
 #include <c10/cuda/CUDAStream.h>
@@ -38,6 +41,12 @@ void* stream_of(const at::Tensor& x) {
   return static_cast<void*>(c10::cuda::getCurrentCUDAStream(x.device().index()).stream());
 }
 
+unsigned long long* flag_of(const at::Tensor& x) {
+  unsigned long long* f = nullptr;
+  check_status(sk_device_flag(x.device().index(), &f), "device_flag");
+  return f;
+}
+
 void softmax_fwd_out(const at::Tensor& x, at::Tensor& y, bool clip) {
   check_matrix(x, "x");
   check_matrix(y, "y");
@@ -47,7 +56,7 @@ void softmax_fwd_out(const at::Tensor& x, at::Tensor& y, bool clip) {
   if (x.size(0) == 0) return;
   check_status(sk_softmax_f32(x.data_ptr<float>(), y.data_ptr<float>(), x.size(0), x.size(1),
                               pitch(x), pitch(y), clip ? SK_MODE_CLIPPED : SK_MODE_EXACT,
-                              nullptr, nullptr, 0, stream_of(x)),
+                              flag_of(x), nullptr, 0, stream_of(x)),
                "softmax_fwd");
 }
 
@@ -67,7 +76,7 @@ std::tuple<at::Tensor, at::Tensor> stats(const at::Tensor& x, bool clip) {
   if (x.size(0) > 0)
     check_status(sk_row_stats_f32(x.data_ptr<float>(), x.size(0), x.size(1), pitch(x),
                                   clip ? SK_MODE_CLIPPED : SK_MODE_EXACT, m.data_ptr<float>(),
-                                  s.data_ptr<double>(), nullptr, nullptr, 0, stream_of(x)),
+                                  s.data_ptr<double>(), flag_of(x), nullptr, 0, stream_of(x)),
                  "row_stats");
   return {m, s};
 }

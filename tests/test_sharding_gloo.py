@@ -116,7 +116,7 @@ class _FakeExchange:
     MAP = 1 << 40
 
     def __init__(self):
-        self.closed, self.freed = [], []
+        self.closed, self.freed, self.resets = [], [], []
 
     def alloc(self, device):
         return 0x1000 * (1 + int(os.environ["RANK"]))
@@ -132,6 +132,14 @@ class _FakeExchange:
 
     def free(self, block):
         self.freed.append(block)
+
+    PERIOD = 3
+
+    def reset_period(self):
+        return self.PERIOD
+
+    def reset(self, block):
+        self.resets.append(block)
 
 
 def _fused_worker(rank, world, port, out_q):
@@ -180,3 +188,61 @@ def test_fused_column_shard_rejects_more_than_eight_ranks(monkeypatch):
     monkeypatch.setattr(dist, "get_rank", lambda group=None: 0)
     with pytest.raises(Exception, match="at most 8"):
         sharding.FusedColumnShard(device=0, native=_FakeExchange())
+
+
+def _prepare_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["RANK"] = str(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nat = _FakeExchange()
+        fc = sharding.FusedColumnShard(device=0, native=nat)
+        log = []
+        for call in range(8):
+            before = len(nat.resets)
+            fc._prepare(1024, 131072, 0)
+            if len(nat.resets) > before:
+                log.append(call)
+        # a new shape on every rank, but rank 1's shard is wider: every rank refuses
+        err = None
+        try:
+            fc._prepare(512, 131072 + (4 if rank == 1 else 0), 0)
+        except Exception as e:  # noqa: BLE001
+            err = type(e).__name__ + ": " + str(e)
+        # a fresh instance whose very first call disagrees
+        err2 = None
+        fc2 = sharding.FusedColumnShard(device=0, native=_FakeExchange())
+        try:
+            fc2._prepare(1024, 131072, rank % 2)
+        except Exception as e:  # noqa: BLE001
+            err2 = type(e).__name__
+        err = (err, err2)
+        out_q.put((rank, log, nat.resets, err))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_fused_column_shard_reset_schedule_and_shape_agreement_gloo(world):
+    """Host side of FusedColumnShard calls: (1) every
+    reset_period() calls every rank zeroes its own exchange block between two
+    barriers, at the same call index on all ranks (the 23-bit slot epoch never
+    wraps); (2) a rank whose shard differs makes every rank raise instead of
+    launching kernels that would poll mismatched slot layouts until the
+    exchange timeout."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_prepare_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, log, resets, err in res:
+        assert log == [3, 6], (rank, log)
+        assert resets == [0x1000 * (1 + rank)] * 2
+        assert err[0] is not None and err[0].startswith("ArgumentError"), err
+        assert "differ across ranks" in err[0] and err[1] == "ArgumentError"
