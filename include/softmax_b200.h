@@ -270,6 +270,8 @@ void sk_free_pinned(void* p);
  *   "host_threads"   host threads copying pageable caller buffers through the
  *                    page-locked staging slots of sk_softmax_f32_host (0 = auto,
  *                    min(16, hardware threads))
+ *   "host_nt"        1 (default): those copies use non-temporal 16-B stores
+ *                    (no read-for-ownership of the destination); 0: memcpy
  *   "host_zero_copy" 1: pinned host buffers with rows <= 8192 are read and written
  *                    by the kernel directly over PCIe (measured no faster than
  *                    staging on this box, so 0 by default)

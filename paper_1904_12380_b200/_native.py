@@ -123,6 +123,11 @@ def lib() -> ctypes.CDLL:
                 fn = getattr(L, name)
                 fn.restype = res
                 fn.argtypes = args
+            # SK_TUNING="key=value key=value": tuning overrides at load (A/B runs)
+            for kv in os.environ.get("SK_TUNING", "").split():
+                k, _, v = kv.partition("=")
+                if L.sk_set_tuning(k.encode(), int(v)) != 0:
+                    raise ValueError(f"SK_TUNING: bad entry {kv!r}")
             _lib = L
     return _lib
 

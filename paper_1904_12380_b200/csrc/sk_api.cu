@@ -1131,6 +1131,7 @@ int sk_set_tuning(const char* key, int value) {
   else if (k == "pdl") g_pdl = value;
   else if (k == "host_chunk_kb") g_host_chunk_kb = value;
   else if (k == "host_threads") g_host_threads = value;
+  else if (k == "host_nt") g_host_nt = value;
   else if (k == "host_zero_copy") g_host_zero_copy = value;
   else if (k == "cluster_k3") g_cluster_k3 = value;
   else if (k == "cluster_size") g_cluster_size = value;

@@ -36,7 +36,7 @@ inline constexpr int64_t kOneCtaRowMax = 8192;
 
 // tuning knobs read outside sk_api.cu (sk_set_tuning writes them)
 extern std::atomic<int> g_pdl, g_coop_pdl, g_gres_sleep, g_gres_diag, g_host_chunk_kb,
-    g_host_zero_copy, g_host_threads;
+    g_host_zero_copy, g_host_threads, g_host_nt;
 extern std::atomic<unsigned> g_gres_spins;
 
 // Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.

@@ -32,6 +32,7 @@ There is no CPU fallback: without a CUDA device every call raises
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import enum
 import threading
@@ -217,6 +218,7 @@ def _softmax_host(x2d: np.ndarray, out2d: np.ndarray, mode: int, device: int) ->
 
 # -------------------------------------------------------------- device path
 _flags: dict[int, Any] = {}
+_NULL_CTX = contextlib.nullcontext()
 
 
 class _DeviceFlag:
@@ -300,14 +302,19 @@ def softmax_into(x, out, variant: KernelVariant, cfg: LaneConfig = LaneConfig(),
         return
     ldx = x.stride(0) if rows > 1 else cols
     ldy = out.stride(0) if rows > 1 else cols
-    with torch.cuda.device(x.device):
-        s = stream if stream is not None else torch.cuda.current_stream(x.device)
-        flag = _bad_flag(torch, x.device)
+    dev = x.device
+    # the C entry point plans for the CURRENT device: switch only when needed
+    # (the context manager is a visible share of a small call's host cost)
+    ctx = torch.cuda.device(dev) if dev.index != torch.cuda.current_device() else _NULL_CTX
+    with ctx:
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        flag = _bad_flag(torch, dev)
         st = _native.lib().sk_softmax_f32(
-            x.data_ptr(), out.data_ptr(), rows, cols, ldx, ldy, mode, flag.data_ptr(), None, 0,
+            x.data_ptr(), out.data_ptr(), rows, cols, ldx, ldy, mode, flag.ptr, None, 0,
             s.cuda_stream,
         )
-        _native.check(st, "softmax")
+        if st:
+            _native.check(st, "softmax")
         if check_finite:
             bad = int(flag.item())  # syncs the current stream
             _raise_if_aborted(flag, bad)

@@ -40,7 +40,7 @@ def main():
     res = {"_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch of the default "
                     "plan's kernel(s), ncu --cache-control none --clock-control none, launches "
                     "11-20 of bench.py's loop (steady state, rotating buffers). Algorithmic = "
-                    "8 B/element. Built by scripts/traffic_json.py from profiles/r1_traffic_<config>.csv"}
+                    "8 B/element. Built by scripts/traffic_json.py from the ncu CSVs of scripts/r2_profiles.sh (profiles/r2_traffic_<config>.csv)"}
     for c in ("c1", "c2", "c3", "c5a", "c4", "c5b"):
         p = src / f"traffic_{c}.csv"
         if not p.exists():

@@ -199,3 +199,29 @@ def test_component_ops_nonfinite_rows_follow_the_reference(row, oracle):
     # device tensors too
     md = components.row_max_scalar(torch.from_numpy(a).cuda())
     assert (bool(torch.isnan(md)) and np.isnan(m_ref)) or float(md) == float(m_ref)
+
+
+def test_every_plan_kind_interleaved(oracle):
+    """Jobs of every plan kind -- K1, K1m, K2 (k1m off), K3g over aligned and
+    unaligned rows, the split path -- interleaved on one stream, twice: no
+    launch inherits anything from the previous one (workspace, K3g exchange
+    block, plan fields), each result against the oracle.  (A per-thread plan
+    cache tried this round leaked a K3g plan's fields into a K2 launch; it
+    measured no faster and was removed.)"""
+    shapes = [(4096, 128), (64, 4096), (40, 6144), (64, 262144), (400, 50257), (3, 300000),
+              (700, 1000), (33, 16384), (64, 65536), (1500, 50), (20, 8192)]
+    xs = {s: configs.generate("c4", 0, -(-s[0] * s[1] // 262144)).reshape(-1)[:s[0] * s[1]]
+          .reshape(s).copy() for s in shapes}
+    refs = {s: oracle.softmax_ref(xs[s], True, nthreads=0) for s in shapes}
+    _native.set_tuning("k1m", 0)  # 4096 / 6144 / 8192 columns take K2 (kPathSeg, k3 unset)
+    try:
+        kinds = set()
+        for _ in range(2):
+            for s in shapes:
+                kinds.add(gu.plan(*s).split()[0])
+                y, bad = gu.softmax_abi(xs[s])
+                assert bad == gu.NO_BAD
+                assert oracle.parity(y, refs[s])["ok"], (s, gu.plan(*s))
+        assert {"k1", "k2_tma", "k3_gres", "k3_gres_unal", "k4_split"} <= kinds, kinds
+    finally:
+        _native.set_tuning("k1m", 1)
