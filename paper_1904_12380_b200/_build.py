@@ -133,7 +133,36 @@ def build_oracle(force: bool = False) -> Path:
     return mod.build(force)
 
 
+REF_SRC = Path("/root/reference/pkg")
+REF_DST = ROOT / "baseline" / "_ref"
+
+
+def install_reference() -> Path | None:
+    """Install the UNMODIFIED reference package into baseline/_ref (git-ignored,
+    travels with the snapshot) when its sources are present and it is not there
+    yet: the reference arm of bench.py and the live-reference tests use it.  The
+    sources are read-only, so pip builds from a copy under /tmp."""
+    if (REF_DST / "softmax_kit").is_dir():
+        return REF_DST
+    if not REF_SRC.is_dir():
+        return None
+    import tempfile
+
+    with tempfile.TemporaryDirectory(prefix="sk_refpkg_") as tmp:
+        src = Path(tmp) / "pkg"
+        shutil.copytree(REF_SRC, src)
+        cmd = [sys.executable, "-m", "pip", "install", "--no-index", "--no-build-isolation",
+               "--no-deps", "--find-links", "/opt/wheelhouse", "--target", str(REF_DST), str(src)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            print(f"reference install failed (reference arm falls back to the C port):\n"
+                  f"{r.stdout[-2000:]}{r.stderr[-2000:]}", file=sys.stderr)
+            return None
+    return REF_DST
+
+
 if __name__ == "__main__":
+    install_reference()
     build_native(force="--force" in sys.argv, verbose=True)
     build_torch_ops(force="--force" in sys.argv)
     build_oracle(force="--force" in sys.argv)
