@@ -699,19 +699,38 @@ def run_ours(args):
 
     # (a) the drop-in call on reference-style pageable buffers (alloc_matrix =
     # np.zeros, tensor.py:90-103); the output buffer is allocated once and
-    # reused, the convention of the reference's own timer (profiler.py:136-162)
+    # reused, the convention of the reference's own timer (profiler.py:136-162).
+    # First with the page-locking cache off: every call staged through
+    # page-locked slots, what a one-shot call on new buffers costs ...
+    from paper_1904_12380_b200 import hostpin
+
+    pin_policy = hostpin.configure()
     m_page = sk.alloc_matrix(nr, cols)
     m_page.view2d[:] = x_host
     o_page = sk.alloc_matrix(nr, cols)
-    s_page = e2e_time(lambda: sk.softmax(m_page, sk.KernelVariant.REFERENCE_CLIPPED, out=o_page,
-                                         device=local))
-    page_ok = bool(np.array_equal(o_page.view2d.view(np.uint32), dev_bits))
-    del o_page
+    hostpin.configure(enabled=False)
+    s_stage = e2e_time(lambda: sk.softmax(m_page, sk.KernelVariant.REFERENCE_CLIPPED, out=o_page,
+                                          device=local))
+    stage_ok = bool(np.array_equal(o_page.view2d.view(np.uint32), dev_bits))
     # (a') the same call returning a fresh output Matrix2D each time (first-touch
     # page faults of the new buffer included), as kernels.py:350-362 does
     s_fresh = e2e_time(lambda: sk.softmax(m_page, sk.KernelVariant.REFERENCE_CLIPPED,
                                           device=local))
-    del m_page
+    # ... then the library's default: repeated calls on the same two pageable
+    # matrices.  The call that sees a large buffer for the second time
+    # page-locks it in place (timed here on its own: t_pin), and every later
+    # call DMAs straight from / into the caller's memory.
+    hostpin.configure(enabled=pin_policy["enabled"])
+    o_page.view2d[:] = 0
+    sk.softmax(m_page, sk.KernelVariant.REFERENCE_CLIPPED, out=o_page, device=local)  # sighting 1
+    t0 = time.perf_counter()
+    sk.softmax(m_page, sk.KernelVariant.REFERENCE_CLIPPED, out=o_page, device=local)  # sighting 2
+    t_pin = time.perf_counter() - t0
+    pin_ranges = hostpin.stats()["ranges"]
+    s_page = e2e_time(lambda: sk.softmax(m_page, sk.KernelVariant.REFERENCE_CLIPPED, out=o_page,
+                                         device=local))
+    page_ok = bool(np.array_equal(o_page.view2d.view(np.uint32), dev_bits))
+    del o_page, m_page
     # (b) page-locked host buffers, output reused
     m_in = sk.Matrix2D.from_array(x_host, pinned=True)
     m_out = sk.alloc_matrix(nr, cols, pinned=True)
@@ -759,14 +778,26 @@ def run_ours(args):
             "e2e": {"value": bytes_job * e2e_steps / s_page / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": int(4 * G * cols), "d2h_bytes_per_step": int(4 * G * cols),
                     "steps": e2e_steps, "ms_per_step": s_page / e2e_steps * 1e3,
-                    "path": "softmax(reference-style pageable Matrix2D, ReferenceClipped, out= "
-                            "pageable Matrix2D allocated once) -> sk_softmax_f32_host: chunks "
-                            "staged through page-locked slots by host copy threads, H2D / kernel / "
-                            "D2H pipelined over three streams",
+                    "path": "softmax(reference-style pageable Matrix2D from alloc_matrix = np.zeros, "
+                            "ReferenceClipped, out= pageable Matrix2D allocated once), called "
+                            "repeatedly on the same two matrices like the reference's own timer "
+                            "(profiler.py:136-162): the library page-locked both buffers in place "
+                            "on their second call (hostpin.py; that call timed separately below), "
+                            "so each timed call is sk_softmax_f32_host DMA-ing the caller's memory "
+                            "directly, H2D / kernel / D2H pipelined over three streams",
                     "bitwise_equal_device_path": page_ok,
+                    "buffers_page_locked_by_library": pin_ranges,
+                    "pinning_call_ms": t_pin * 1e3,
+                    "staged": {"value": bytes_job * e2e_steps / s_stage / 1e9, "unit": "GB/s",
+                               "ms_per_step": s_stage / e2e_steps * 1e3,
+                               "path": "the same call with the page-locking cache off (what a first "
+                                       "/ one-shot call on new pageable buffers costs): chunks staged "
+                                       "through page-locked slots by host copy threads",
+                               "bitwise_equal_device_path": stage_ok},
                     "fresh_output": {"value": bytes_job * e2e_steps / s_fresh / 1e9, "unit": "GB/s",
                                      "ms_per_step": s_fresh / e2e_steps * 1e3,
-                                     "path": "softmax(pageable Matrix2D) -> fresh Matrix2D per call"},
+                                     "path": "softmax(pageable Matrix2D) -> fresh Matrix2D per call, "
+                                             "staged"},
                     "pinned": {"value": bytes_job * e2e_steps / s_pin / 1e9, "unit": "GB/s",
                                "ms_per_step": s_pin / e2e_steps * 1e3,
                                "path": "softmax(Matrix2D in page-locked memory, out= page-locked)",

@@ -219,6 +219,19 @@ int sk_shift_scale_f32(const float* x, float* y, int64_t n, float shift, float s
  */
 void* sk_alloc_pinned(size_t bytes);
 void sk_free_pinned(void* p);
+/*
+ * Page-lock / release a caller-owned host range in place (cudaHostRegister,
+ * portable).  A registered range is found by sk_softmax_f32_host per call
+ * (cudaPointerGetAttributes) and then takes the direct-DMA path with no
+ * staging copies.  The host mirror registers a caller's large pageable
+ * Matrix2D buffers (the reference's np.zeros, tensor.py:90-103) the second
+ * time it sees them and releases them when the owning array dies
+ * (hostpin.py); C callers own the lifetime themselves: unregister BEFORE
+ * freeing the memory.  SK_OK, or SK_ERR_CUDA (range already registered,
+ * locked-memory limit, ...) -- the caller then simply stays on the staged path.
+ */
+int sk_host_register(void* p, size_t bytes);
+int sk_host_unregister(void* p);
 
 /*
  * Process-wide tuning / test hooks (not needed for normal use):

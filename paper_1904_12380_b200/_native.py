@@ -69,6 +69,8 @@ SIGNATURES: dict[str, tuple] = {
     "sk_shift_scale_f32": (c_int, [c_void_p, c_void_p, c_int64, c_float, c_float, c_void_p]),
     "sk_alloc_pinned": (c_void_p, [c_size_t]),
     "sk_free_pinned": (None, [c_void_p]),
+    "sk_host_register": (c_int, [c_void_p, c_size_t]),
+    "sk_host_unregister": (c_int, [c_void_p]),
     "sk_set_tuning": (c_int, [c_char_p, c_int]),
     "sk_copy_f32": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p]),
     "sk_exp_accuracy": (c_int, [c_int, c_float, c_float, POINTER(c_double), POINTER(c_double), c_int]),

@@ -193,6 +193,28 @@ void sk_free_pinned(void* p) {
   if (p) cudaFreeHost(p);
 }
 
+int sk_host_register(void* p, size_t bytes) {
+  if (!p || !bytes) return arg_fail("host_register: empty range");
+  if (mapped_device_ptr(p)) {
+    g_last_error = "host_register: the range is already page-locked";
+    return SK_ERR_CUDA;
+  }
+  if (cudaHostRegister(p, bytes, cudaHostRegisterPortable) != cudaSuccess) {
+    g_last_error = std::string("cudaHostRegister failed: ") + cudaGetErrorString(cudaGetLastError());
+    return SK_ERR_CUDA;
+  }
+  return SK_OK;
+}
+
+int sk_host_unregister(void* p) {
+  if (!p) return arg_fail("host_unregister: null");
+  if (cudaHostUnregister(p) != cudaSuccess) {
+    g_last_error = std::string("cudaHostUnregister failed: ") + cudaGetErrorString(cudaGetLastError());
+    return SK_ERR_CUDA;
+  }
+  return SK_OK;
+}
+
 int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_t cols,
                         int mode, int device, int64_t* bad_row_out) {
   if (bad_row_out) *bad_row_out = -1;

@@ -40,7 +40,7 @@ from typing import Any, NamedTuple
 
 import numpy as np
 
-from . import _native
+from . import _native, hostpin
 from .errors import ArgumentError, NumericDomainError, SoftmaxKitError
 from .lanes import LaneConfig
 from .tensor import Matrix2D, alloc_matrix
@@ -208,6 +208,10 @@ def _foreign_out(m):
 def _softmax_host(x2d: np.ndarray, out2d: np.ndarray, mode: int, device: int) -> None:
     rows, cols = x2d.shape
     bad = ctypes.c_int64(-1)
+    # a large caller buffer seen again is page-locked in place (hostpin.py):
+    # the call below then DMAs straight from / into it, no staging copies
+    hostpin.note(x2d)
+    hostpin.note(out2d)
     st = _native.lib().sk_softmax_f32_host(
         x2d.ctypes.data, out2d.ctypes.data, rows, cols, mode, device, ctypes.byref(bad)
     )
