@@ -60,6 +60,32 @@ const void* mapped_device_ptr(const void* h) {
   return a.devicePointer;
 }
 
+// Ranges page-locked in place through sk_host_register (start -> bytes).  One
+// cudaMemcpyAsync may not span two registrations (invalid argument), and a
+// caller buffer is registered as up to three adjacent ranges (hostpin.py: the
+// 2 MiB-aligned window and the pages before / after it), so direct copies are
+// cut at the range boundaries found here.
+std::mutex g_reg_mu;
+std::map<uintptr_t, size_t> g_reg;
+
+// [p, p + bytes) as pieces that each lie inside one registered range; false
+// when some byte is in none of the library's registrations.
+bool reg_pieces(const void* p, size_t bytes, std::vector<std::pair<size_t, size_t>>* pieces) {
+  std::lock_guard<std::mutex> g(g_reg_mu);
+  uintptr_t cur = reinterpret_cast<uintptr_t>(p);
+  const uintptr_t base = cur, end = cur + bytes;
+  while (cur < end) {
+    auto it = g_reg.upper_bound(cur);
+    if (it == g_reg.begin()) return false;
+    --it;
+    if (cur >= it->first + it->second) return false;
+    const uintptr_t next = std::min<uintptr_t>(end, it->first + it->second);
+    if (pieces) pieces->emplace_back(size_t(cur - base), size_t(next - cur));
+    cur = next;
+  }
+  return true;
+}
+
 // ------------------------------------------- host copy pool (pageable buffers)
 // A drop-in caller hands over pageable numpy memory (the reference's
 // alloc_matrix is np.zeros, tensor.py:90-103).  cudaMemcpyAsync from pageable
@@ -203,11 +229,17 @@ int sk_host_register(void* p, size_t bytes) {
     g_last_error = std::string("cudaHostRegister failed: ") + cudaGetErrorString(cudaGetLastError());
     return SK_ERR_CUDA;
   }
+  std::lock_guard<std::mutex> g(g_reg_mu);
+  g_reg[reinterpret_cast<uintptr_t>(p)] = bytes;
   return SK_OK;
 }
 
 int sk_host_unregister(void* p) {
   if (!p) return arg_fail("host_unregister: null");
+  {
+    std::lock_guard<std::mutex> g(g_reg_mu);
+    g_reg.erase(reinterpret_cast<uintptr_t>(p));
+  }
   if (cudaHostUnregister(p) != cudaSuccess) {
     g_last_error = std::string("cudaHostUnregister failed: ") + cudaGetErrorString(cudaGetLastError());
     return SK_ERR_CUDA;
@@ -333,9 +365,47 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
   }
   std::vector<int64_t> start(nchunks + 1, 0);
   for (int64_t k = 0; k < nchunks; ++k) start[k + 1] = start[k] + sched[k];
-  // pageable caller buffers: stage every chunk through page-locked slots
-  const bool staged_in = mapped_device_ptr(x_host) == nullptr;
-  const bool staged_out = mapped_device_ptr(y_host) == nullptr;
+  // Pageable caller memory is staged through page-locked slots, decided per
+  // chunk: a buffer page-locked in place by sk_host_register (hostpin.py) is
+  // registered over its inner 2 MiB-aligned window only, so the chunks at
+  // either end can reach into pageable memory while every other chunk is
+  // DMA-ed directly.
+  auto locked = [](const float* p, size_t bytes) {
+    if (reg_pieces(p, bytes, nullptr)) return true;
+    // page-locked by someone else (cudaHostAlloc, the caller's own registration):
+    // taken as one range when both ends are locked
+    return !reg_pieces(p, 1, nullptr) && !reg_pieces(reinterpret_cast<const char*>(p) + bytes - 1, 1, nullptr) &&
+           mapped_device_ptr(p) != nullptr &&
+           mapped_device_ptr(reinterpret_cast<const char*>(p) + bytes - 1) != nullptr;
+  };
+  // one cudaMemcpyAsync per registered range the host side of a direct copy touches
+  auto copy_direct = [](void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
+                        const void* host, cudaStream_t s) -> cudaError_t {
+    std::vector<std::pair<size_t, size_t>> pc;
+    if (!reg_pieces(host, bytes, &pc) || pc.size() <= 1)
+      return cudaMemcpyAsync(dst, src, bytes, kind, s);
+    for (const auto& q : pc) {
+      const cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst) + q.first,
+                                            static_cast<const char*>(src) + q.first, q.second, kind, s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  };
+  std::vector<char> stage_in(nchunks), stage_out(nchunks);
+  bool staged_in = false, staged_out = false;
+  {
+    // whole buffer locked (the common cases: cudaHostAlloc'd or fully pageable)
+    const bool all_in = locked(x_host, size_t(total)), all_out = locked(y_host, size_t(total));
+    const bool mid_in = mapped_device_ptr(x_host + (rows / 2) * cols) != nullptr;
+    const bool mid_out = mapped_device_ptr(y_host + (rows / 2) * cols) != nullptr;
+    for (int64_t k = 0; k < nchunks; ++k) {
+      const size_t b = size_t(sched[k] * row_bytes);
+      stage_in[k] = all_in ? 0 : (!mid_in || !locked(x_host + start[k] * cols, b));
+      stage_out[k] = all_out ? 0 : (!mid_out || !locked(y_host + start[k] * cols, b));
+      staged_in |= stage_in[k] != 0;
+      staged_out |= stage_out[k] != 0;
+    }
+  }
   if ((staged_in || staged_out) && c->pin_bytes < need) {
     SK_CUDA(cudaDeviceSynchronize());
     for (int i = 0; i < kRing; ++i) {
@@ -353,6 +423,7 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
   CopyPool& pool = CopyPool::get();
   // copy chunk j's staged output back into the caller's buffer once its D2H is done
   auto drain = [&](int64_t j) -> int {
+    if (!stage_out[j]) return SK_OK;
     const int i = static_cast<int>(j % kRing);
     SK_CUDA(cudaEventSynchronize(c->ev_d2h[i]));
     pool.copy(y_host + start[j] * cols, c->pin_out[i], size_t(sched[j] * row_bytes));
@@ -370,14 +441,17 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
     // input slot free once the kernel that last read it is done
     if (k >= kRing) SK_CUDA(cudaStreamWaitEvent(c->s_h2d, c->ev_k[i], 0));
     const float* src = x_host + r0 * cols;
-    if (staged_in) {
+    // (placing the chunk at the host address's phase within a 4 KiB page on
+    // the device side does not speed the DMA up: profiles/r2_hostpin_ab.jsonl)
+    float* const dxk = c->dx[i];
+    float* const dyk = c->dy[i];
+    if (stage_in[k]) {
       // the staging slot is free once the H2D that last read it is done
       if (k >= kRing) SK_CUDA(cudaEventSynchronize(c->ev_h2d[i]));
       pool.copy(c->pin_in[i], src, bytes);
       src = c->pin_in[i];
     }
-    SK_CUDA(cudaMemcpyAsync(c->dx[i], src, bytes, cudaMemcpyHostToDevice,
-                            c->s_h2d));
+    SK_CUDA(copy_direct(dxk, src, bytes, cudaMemcpyHostToDevice, src, c->s_h2d));
     SK_CUDA(cudaEventRecord(c->ev_h2d[i], c->s_h2d));
     SK_CUDA(cudaStreamWaitEvent(c->s_comp, c->ev_h2d[i], 0));
     // output slot free once the D2H that last read it is done
@@ -385,13 +459,13 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
     // a chunk of this job: the job's throughput plan (never the latency path a
     // small standalone call would take), so every chunk keeps the whole job's bits
     const bool whole = nr == rows;
-    st = softmax_dev(c->dx[i], c->dy[i], nr, cols, cols, cols, mode, c->dbad + k, nullptr, 0,
-                     c->s_comp, !whole);
+    st = softmax_dev(dxk, dyk, nr, cols, cols, cols, mode, c->dbad + k, nullptr, 0, c->s_comp,
+                     !whole);
     if (st) return st;
     SK_CUDA(cudaEventRecord(c->ev_k[i], c->s_comp));
     SK_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_k[i], 0));
-    SK_CUDA(cudaMemcpyAsync(staged_out ? c->pin_out[i] : y_host + r0 * cols, c->dy[i], bytes,
-                            cudaMemcpyDeviceToHost, c->s_d2h));
+    float* const dsty = stage_out[k] ? c->pin_out[i] : y_host + r0 * cols;
+    SK_CUDA(copy_direct(dsty, dyk, bytes, cudaMemcpyDeviceToHost, dsty, c->s_d2h));
     SK_CUDA(cudaEventRecord(c->ev_d2h[i], c->s_d2h));
   }
   if (staged_out)

@@ -5,11 +5,14 @@ The reference's ``alloc_matrix`` hands out pageable ``np.zeros`` memory
 over and over (profiler.py:136-162).  From pageable memory every call pays two
 host-side staging copies (sk_host.cu); from page-locked memory the DMA engines
 read and write the caller's buffers directly (~95 vs ~53 GB/s on c5a).  Pinning
-a buffer in place costs about as much as two staged calls (cudaHostRegister:
-~85 ms per GiB), so this cache does it only for a large buffer seen for the
-SECOND time -- a one-shot call never pays it -- and releases the registration
-when the owning ndarray dies (``weakref.finalize`` runs before numpy frees the
-data), so no range stays registered past its memory.
+a buffer in place costs about as much as a staged call (cudaHostRegister of
+2 GiB: ~35 ms for whole 2 MiB pages, ~160 ms when the range ends inside a huge
+page -- profiles/r2_hostreg_align.jsonl -- so only the buffer's inner 2 MiB-
+aligned window is registered; sk_softmax_f32_host stages the chunk at either
+end that reaches outside it), so this cache does it only for a large buffer
+seen for the SECOND time -- a one-shot call never pays it -- and releases the
+registration when the owning ndarray dies (``weakref.finalize`` runs before
+numpy frees the data), so no range stays registered past its memory.
 
 Only memory an ndarray keeps alive is ever registered: the key is the topmost
 ndarray of the view chain (the owner, or the array wrapping a foreign buffer
@@ -34,24 +37,31 @@ _state = {
     "max_bytes": 64 << 30,        # never lock more than this in one range
     "sightings": 2,               # register on the N-th call that uses the buffer
     "budget_bytes": 0,            # 0: half of physical memory
+    "edges": True,                # also lock the < 2 MiB before / after the aligned window
 }
+_HUGE = 2 << 20
 _entries: dict[int, "_Entry"] = {}
 _pinned_total = 0
 
 
 class _Entry:
-    __slots__ = ("ptr", "nbytes", "seen", "registered", "failed", "fin")
+    __slots__ = ("ptr", "nbytes", "lo", "hi", "seen", "box", "failed", "fin", "ranges")
 
     def __init__(self, ptr: int, nbytes: int):
         self.ptr, self.nbytes = ptr, nbytes
+        # the registered window: whole 2 MiB pages inside the buffer
+        self.lo = (ptr + _HUGE - 1) // _HUGE * _HUGE
+        self.hi = (ptr + nbytes) // _HUGE * _HUGE
+        self.ranges = []  # [(address, bytes)] registered: shared with the finalizer
         self.seen = 0
-        self.registered = False
+        self.box = [False]  # [registered]: shared with the owner's finalizer
         self.failed = False
         self.fin = None
 
 
 def configure(enabled: bool | None = None, min_bytes: int | None = None,
-              sightings: int | None = None, budget_bytes: int | None = None) -> dict:
+              sightings: int | None = None, budget_bytes: int | None = None,
+              edges: bool | None = None) -> dict:
     """Set the cache policy; returns the policy in force."""
     with _lock:
         if enabled is not None:
@@ -62,12 +72,14 @@ def configure(enabled: bool | None = None, min_bytes: int | None = None,
             _state["sightings"] = max(1, int(sightings))
         if budget_bytes is not None:
             _state["budget_bytes"] = max(0, int(budget_bytes))
+        if edges is not None:
+            _state["edges"] = bool(edges)
         return dict(_state)
 
 
 def stats() -> dict:
     with _lock:
-        return {"ranges": sum(1 for e in _entries.values() if e.registered),
+        return {"ranges": sum(1 for e in _entries.values() if e.box[0]),
                 "bytes": _pinned_total, "tracked": len(_entries)}
 
 
@@ -87,18 +99,20 @@ def _budget() -> int:
         return 16 << 30
 
 
-def _release(key: int, ptr: int, nbytes: int, registered_box: list) -> None:
+def _release(key: int, ranges: list, registered_box: list) -> None:
     """Finalizer of the owning ndarray: runs before numpy frees the data."""
     global _pinned_total
     with _lock:
         _entries.pop(key, None)
         if registered_box[0]:
             registered_box[0] = False
-            _pinned_total -= nbytes
-            try:
-                _native.lib().sk_host_unregister(ptr)
-            except Exception:  # noqa: BLE001 -- interpreter teardown
-                pass
+            for lo, n in ranges:
+                _pinned_total -= n
+                try:
+                    _native.lib().sk_host_unregister(lo)
+                except Exception:  # noqa: BLE001 -- interpreter teardown
+                    pass
+            del ranges[:]
 
 
 def note(view: np.ndarray) -> bool:
@@ -116,28 +130,39 @@ def note(view: np.ndarray) -> bool:
         e = _entries.get(key)
         if e is None or e.ptr != own.ctypes.data or e.nbytes != nbytes:
             e = _Entry(int(own.ctypes.data), nbytes)
-            box = [False]
             try:
-                e.fin = weakref.finalize(own, _release, key, e.ptr, nbytes, box)
+                e.fin = weakref.finalize(own, _release, key, e.ranges, e.box)
             except TypeError:
                 return False
             e.fin.atexit = False  # process teardown releases every registration
-            e.registered = box  # shared with the finalizer
             _entries[key] = e
-        box = e.registered
+        box = e.box
         if box[0]:
             return True
         if e.failed:
             return False
         e.seen += 1
-        if e.seen < _state["sightings"] or _pinned_total + nbytes > _budget():
+        win = e.hi - e.lo
+        if e.seen < _state["sightings"] or _pinned_total + win > _budget():
             return False
-        st = _native.lib().sk_host_register(e.ptr, nbytes)
+        st = _native.lib().sk_host_register(e.lo, win) if win > 0 else 1
         if st != 0:
             e.failed = True  # already registered by the caller, locked-memory limit, ...
             return False
         box[0] = True
-        _pinned_total += nbytes
+        e.ranges.append((e.lo, win))
+        _pinned_total += win
+        if _state["edges"]:
+            # the pages before / after the window, as two small registrations of
+            # their own (a range ending inside a huge page registers slowly as a
+            # whole, so they are kept apart from the window); a failure here only
+            # leaves the end chunks on the staged path
+            page = 4096
+            for a, b in ((e.ptr // page * page, e.lo),
+                         (e.hi, (e.ptr + nbytes + page - 1) // page * page)):
+                if b > a and _native.lib().sk_host_register(a, b - a) == 0:
+                    e.ranges.append((a, b - a))
+                    _pinned_total += b - a
         return True
 
 

@@ -77,3 +77,39 @@ for name, rows in (("c5a", None), ("c2", None)):
     emit(what="calls", config=name, ms=[round(t, 2) for t in ts],
          gbs=[round(byts / t / 1e6, 1) for t in ts], stats=hostpin.stats())
     del m, o
+
+
+def huge_kb(addr, nbytes):
+    """AnonHugePages (kB) of the mappings overlapping [addr, addr + nbytes)."""
+    tot, inside = 0, False
+    for line in open("/proc/self/smaps"):
+        f = line.split()
+        if "-" in f[0] and len(f) >= 5 and not f[0].endswith(":"):
+            lo, hi = (int(v, 16) for v in f[0].split("-"))
+            inside = lo < addr + nbytes and hi > addr
+        elif inside and f[0] == "AnonHugePages:":
+            tot += int(f[1])
+    return tot
+
+
+# where the registration time goes in the call flow: the input (filled by one
+# numpy copy) and the output (first touched by the staging threads)
+hostpin.configure(enabled=False)
+x = configs.generate("c5a")
+m = sk.alloc_matrix(*x.shape)
+m.view2d[:] = x
+o = sk.alloc_matrix(*x.shape)
+emit(what="huge_before_call", m_kb=huge_kb(m.data.ctypes.data, m.data.nbytes),
+     o_kb=huge_kb(o.data.ctypes.data, o.data.nbytes))
+sk.softmax(m, sk.KernelVariant.REFERENCE_CLIPPED, out=o)
+emit(what="huge_after_call", m_kb=huge_kb(m.data.ctypes.data, m.data.nbytes),
+     o_kb=huge_kb(o.data.ctypes.data, o.data.nbytes))
+for name, a in (("m", m.data.base), ("o", o.data.base), ("x", x)):
+    for rep in range(2):
+        t0 = time.perf_counter()
+        st = L.sk_host_register(a.ctypes.data, a.nbytes)
+        t1 = time.perf_counter()
+        L.sk_host_unregister(a.ctypes.data)
+        t2 = time.perf_counter()
+        emit(what="register_in_flow", buf=name, rep=rep, status=st, register_ms=(t1 - t0) * 1e3,
+             unregister_ms=(t2 - t1) * 1e3, huge_kb=huge_kb(a.ctypes.data, a.nbytes))

@@ -11,6 +11,9 @@ import paper_1904_12380_b200 as sk
 from paper_1904_12380_b200 import hostpin
 
 
+_M2 = 2 << 20
+
+
 class _FakeLib:
     def __init__(self, fail=False):
         self.reg, self.unreg, self.fail = [], [], fail
@@ -29,33 +32,64 @@ def fake(monkeypatch):
     lib = _FakeLib()
     monkeypatch.setattr(hostpin._native, "lib", lambda: lib)
     before = hostpin.configure()
-    hostpin.configure(enabled=True, min_bytes=1 << 10, sightings=2, budget_bytes=1 << 30)
+    hostpin.configure(enabled=True, min_bytes=1 << 20, sightings=2, budget_bytes=1 << 30,
+                      edges=False)
     yield lib
     hostpin.release_all()
     hostpin.configure(enabled=before["enabled"], min_bytes=before["min_bytes"],
-                      sightings=before["sightings"], budget_bytes=before["budget_bytes"])
+                      sightings=before["sightings"], budget_bytes=before["budget_bytes"],
+                      edges=before["edges"])
+
+
+def _window(a):
+    """The whole 2 MiB pages inside ``a``'s buffer: what gets registered."""
+    lo = (a.ctypes.data + _M2 - 1) // _M2 * _M2
+    hi = (a.ctypes.data + a.nbytes) // _M2 * _M2
+    return lo, hi - lo
 
 
 def test_registers_on_second_sighting_and_releases_with_the_owner(fake):
-    m = sk.alloc_matrix(64, 64)  # a view into an over-allocated np.zeros, like the reference's
+    m = sk.alloc_matrix(2048, 2048)  # a view into an over-allocated np.zeros, like the reference's
     own = m.data.base
     assert not hostpin.note(m.view2d) and fake.reg == []
     assert hostpin.note(m.view2d)
-    assert fake.reg == [(own.ctypes.data, own.nbytes)]
-    assert hostpin.note(m.view2d[:40]) and len(fake.reg) == 1  # any view of the owner hits
-    assert hostpin.stats()["bytes"] == own.nbytes
-    ptr = own.ctypes.data
+    lo, n = _window(own)
+    assert fake.reg == [(lo, n)] and n >= own.nbytes - 2 * _M2
+    assert lo % _M2 == 0 and n % _M2 == 0 and lo >= own.ctypes.data
+    assert lo + n <= own.ctypes.data + own.nbytes
+    assert hostpin.note(m.view2d[:1200]) and len(fake.reg) == 1  # any view of the owner hits
+    assert hostpin.stats()["bytes"] == n
     del m, own
     gc.collect()
-    assert fake.unreg == [ptr] and hostpin.stats() == {"ranges": 0, "bytes": 0, "tracked": 0}
+    assert fake.unreg == [lo] and hostpin.stats() == {"ranges": 0, "bytes": 0, "tracked": 0}
+
+
+def test_edges_are_separate_page_aligned_registrations(fake):
+    hostpin.configure(edges=True)
+    m = sk.alloc_matrix(2048, 2048)
+    own = m.data.base
+    hostpin.note(m.view2d), hostpin.note(m.view2d)
+    lo, n = _window(own)
+    assert fake.reg[0] == (lo, n) and 1 <= len(fake.reg) <= 3
+    ranges = sorted(fake.reg)
+    for (a, na), (b, _) in zip(ranges, ranges[1:]):
+        assert a + na == b                       # adjacent, never overlapping
+    assert all(a % 4096 == 0 and na % 4096 == 0 for a, na in ranges)
+    assert ranges[0][0] <= own.ctypes.data < ranges[0][0] + 4096
+    end = ranges[-1][0] + ranges[-1][1]
+    assert end - 4096 < own.ctypes.data + own.nbytes <= end
+    assert hostpin.stats()["bytes"] == sum(na for _, na in ranges)
+    del m, own
+    gc.collect()
+    assert sorted(fake.unreg) == [a for a, _ in ranges] and hostpin.stats()["bytes"] == 0
 
 
 def test_small_buffers_windows_and_disabled_are_left_alone(fake):
-    small = np.zeros(16, np.float32)
-    big = np.zeros(1 << 16, np.float32)
+    small = np.zeros(1 << 10, np.float32)
+    big = np.zeros(8 << 20, np.float32)
     for _ in range(3):
         assert not hostpin.note(small)
-        assert not hostpin.note(big[:1024])  # a small window of a large owner
+        assert not hostpin.note(big[: 1 << 20])  # a small window of a large owner
     hostpin.configure(enabled=False)
     for _ in range(3):
         assert not hostpin.note(big)
@@ -64,25 +98,25 @@ def test_small_buffers_windows_and_disabled_are_left_alone(fake):
 
 def test_failed_registration_is_not_retried_and_budget_is_kept(fake):
     fake.fail = True
-    a = np.zeros(4096, np.float32)
+    a = np.zeros(2 << 20, np.float32)
     assert not hostpin.note(a) and not hostpin.note(a) and not hostpin.note(a)
     assert len(fake.reg) == 1 and fake.unreg == []
     fake.fail = False
-    hostpin.configure(budget_bytes=20000)
-    b, c = np.zeros(4096, np.float32), np.zeros(4096, np.float32)
+    hostpin.configure(budget_bytes=10 << 20)
+    b, c = np.zeros(2 << 20, np.float32), np.zeros(2 << 20, np.float32)
     hostpin.note(b), hostpin.note(c)
-    assert hostpin.note(b) and not hostpin.note(c)  # 16 KiB fits the budget once
+    assert hostpin.note(b) and not hostpin.note(c)  # 8 MiB fits the budget once
     del a, b, c
     gc.collect()
     assert hostpin.stats()["bytes"] == 0
 
 
 def test_reused_address_is_a_new_buffer(fake):
-    a = np.zeros(4096, np.float32)
+    a = np.zeros(2 << 20, np.float32)
     hostpin.note(a), hostpin.note(a)
     del a
     gc.collect()
-    b = np.zeros(4096, np.float32)  # may land on the same address / id
+    b = np.zeros(2 << 20, np.float32)  # may land on the same address / id
     assert not hostpin.note(b)      # first sighting again
     assert len(fake.unreg) == 1
 
