@@ -166,9 +166,67 @@ def note(view: np.ndarray) -> bool:
         return True
 
 
+# ------------------------------------------------------------- output pool
+# ``softmax(m, variant)`` returns a fresh Matrix2D per call (kernels.py:358).
+# For a large result that means 2 GiB of first-touch page faults and a buffer
+# the cache above never sees twice.  The pool keeps a few large output blocks
+# alive and hands one out again once nothing but the pool references it (every
+# view of a block -- the Matrix2D's data, its view2d, any slice the caller
+# kept -- holds a reference to the block itself, so the block's reference
+# count says exactly whether a caller can still see it).  A recycled block was
+# seen before: note() page-locks it, and the call DMAs straight into it.
+# Blocks are carved at a 2 MiB boundary, so the whole result is one aligned
+# registration.  The result is fully overwritten by the call; it is NOT zeroed
+# (alloc_matrix, which promises zeros, never uses the pool).
+import sys  # noqa: E402
+
+_POOL_MAX_BLOCKS = 4
+_pool: list[np.ndarray] = []
+
+
+def pooled_output(nfloats: int) -> np.ndarray | None:
+    """A float32 buffer of ``nfloats`` (2 MiB-aligned, uninitialised) from the
+    pool, or None when the pool does not apply (small result, pool disabled or
+    exhausted): the caller then allocates as usual."""
+    nbytes = nfloats * 4
+    if not _state["enabled"] or nbytes < _state["min_bytes"]:
+        return None
+    need = nfloats + _HUGE // 4
+    with _lock:
+        for i in range(len(_pool)):
+            # references: the pool's list slot + getrefcount's argument
+            if _pool[i].size == need and sys.getrefcount(_pool[i]) == 2:
+                raw = _pool[i]
+                break
+        else:
+            # drop blocks of other sizes nobody uses; allocate while under the cap
+            for i in range(len(_pool) - 1, -1, -1):
+                if _pool[i].size != need and sys.getrefcount(_pool[i]) == 2:
+                    del _pool[i]
+            held = sum(b.nbytes for b in _pool)
+            if len(_pool) >= _POOL_MAX_BLOCKS or held + need * 4 > _budget() // 2:
+                return None
+            try:
+                raw = np.empty(need, dtype=np.float32)
+            except MemoryError:
+                return None
+            _pool.append(raw)
+    off = (-raw.ctypes.data) % _HUGE // 4
+    return raw[off: off + nfloats]
+
+
+def pool_stats() -> dict:
+    with _lock:
+        return {"blocks": len(_pool), "bytes": sum(b.nbytes for b in _pool),
+                "in_use": sum(1 for i in range(len(_pool)) if sys.getrefcount(_pool[i]) > 2)}
+
+
 def release_all() -> None:
     """Drop every registration now (tests; a caller about to fork)."""
     with _lock:
+        for i in range(len(_pool) - 1, -1, -1):
+            if sys.getrefcount(_pool[i]) == 2:
+                del _pool[i]
         fins = [e.fin for e in _entries.values() if e.fin is not None]
     for f in fins:
         f()

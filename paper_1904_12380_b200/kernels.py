@@ -194,10 +194,20 @@ def _foreign_error(m, e: Exception) -> Exception:
 _FOREIGN_ERR: dict = {}
 
 
+def _fresh_out(rows: int, cols: int) -> Matrix2D:
+    """The fresh output of a host call (kernels.py:358).  Every element is
+    overwritten by the call, so a large result comes from hostpin's pool of
+    recycled, page-locked blocks when one is free; otherwise alloc_matrix."""
+    data = hostpin.pooled_output(rows * cols)
+    if data is None:
+        return alloc_matrix(rows, cols)
+    return Matrix2D(rows=rows, cols=cols, data=data)
+
+
 def _foreign_out(m):
     """A fresh output of the caller's own Matrix2D class (kernels.py:358 returns
-    a fresh Matrix2D), backed by a 32-B aligned zeroed buffer."""
-    data = alloc_matrix(int(m.rows), int(m.cols)).data
+    a fresh Matrix2D), backed by a 32-B aligned buffer."""
+    data = _fresh_out(int(m.rows), int(m.cols)).data
     try:
         return type(m)(rows=int(m.rows), cols=int(m.cols), data=data)
     except Exception:  # noqa: BLE001 -- a class we cannot construct: ours
@@ -369,7 +379,7 @@ def _softmax_matrix(m, variant, cfg, out, device):
     _sync_fault_hook()
     x2d = m.view2d if isinstance(m, Matrix2D) else _foreign_view(m, "input")
     if out is None:
-        out = alloc_matrix(m.rows, m.cols) if isinstance(m, Matrix2D) else _foreign_out(m)
+        out = _fresh_out(m.rows, m.cols) if isinstance(m, Matrix2D) else _foreign_out(m)
     if isinstance(out, Matrix2D):
         y2d = out.view2d
     elif _is_foreign_matrix(out):

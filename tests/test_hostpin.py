@@ -121,6 +121,72 @@ def test_reused_address_is_a_new_buffer(fake):
     assert len(fake.unreg) == 1
 
 
+def test_output_pool_recycles_only_blocks_nobody_can_see(fake):
+    n = 1 << 20  # 4 MiB results
+    assert hostpin.pooled_output(1 << 10) is None              # small: not pooled
+    a = hostpin.pooled_output(n)
+    assert a.size == n and a.ctypes.data % (2 << 20) == 0 and a.dtype == np.float32
+    b = hostpin.pooled_output(n)
+    assert b.base is not a.base and hostpin.pool_stats()["in_use"] == 2
+    a[:] = 7.0
+    keep = a.reshape(1024, 1024)[5]                             # a slice the caller kept
+    block = a.base
+    del a
+    c = hostpin.pooled_output(n)
+    assert c.base is not block and float(keep[0]) == 7.0        # still visible: not reused
+    del keep, block
+    d = hostpin.pooled_output(n)
+    assert d.base is not b.base and d.base is not c.base        # the released block comes back
+    assert hostpin.pool_stats()["blocks"] == 3
+    e = hostpin.pooled_output(n)
+    assert e is not None and hostpin.pool_stats()["blocks"] == 4
+    assert hostpin.pooled_output(n) is None                     # pool exhausted: caller allocates
+    del b, c, d, e
+    assert hostpin.pool_stats()["in_use"] == 0
+    f = hostpin.pooled_output(2 * n)                            # another size evicts idle blocks
+    assert f is not None and hostpin.pool_stats()["blocks"] == 1
+    hostpin.configure(enabled=False)
+    assert hostpin.pooled_output(n) is None
+    del f
+    hostpin.release_all()
+    assert hostpin.pool_stats()["blocks"] == 0
+
+
+@pytest.mark.gpu
+def test_fresh_outputs_come_from_the_pool_and_stay_valid():
+    import torch
+
+    from paper_1904_12380_b200 import configs
+
+    before = hostpin.configure()
+    hostpin.configure(enabled=True, min_bytes=1 << 20, sightings=2)
+    try:
+        x = configs.generate("c2")
+        ref = sk.softmax(torch.from_numpy(x).cuda(), sk.KernelVariant.REFERENCE_CLIPPED).cpu().numpy()
+        m = sk.Matrix2D.from_array(x)
+        outs = [sk.softmax(m, sk.KernelVariant.REFERENCE_CLIPPED) for _ in range(3)]  # all alive
+        assert len({o.data.base.ctypes.data for o in outs}) == 3
+        y = None
+        for _ in range(6):                                       # the usual loop: y rebound
+            y = sk.softmax(m, sk.KernelVariant.REFERENCE_CLIPPED)
+            assert np.array_equal(y.view2d.view(np.uint32), ref.view(np.uint32))
+        for o in outs:                                           # never overwritten meanwhile
+            assert np.array_equal(o.view2d.view(np.uint32), ref.view(np.uint32))
+        assert hostpin.pool_stats()["blocks"] <= 4
+        assert hostpin.stats()["ranges"] >= 2                    # input + a recycled block
+        # the reference's own Matrix2D class gets pooled outputs too (duck-typed path)
+        x2 = x.copy()
+        x2[7, 3] = np.nan
+        with pytest.raises(sk.NumericDomainError, match="row 7"):
+            sk.softmax(sk.Matrix2D.from_array(x2), sk.KernelVariant.REFERENCE_CLIPPED)
+    finally:
+        del outs, y, m
+        gc.collect()
+        hostpin.release_all()
+        hostpin.configure(enabled=before["enabled"], min_bytes=before["min_bytes"],
+                          sightings=before["sightings"])
+
+
 @pytest.mark.gpu
 def test_pageable_matrix_is_pinned_on_second_call_same_bits():
     import torch
