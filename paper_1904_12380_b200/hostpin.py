@@ -30,7 +30,9 @@ import numpy as np
 
 from . import _native
 
-_lock = threading.Lock()
+# re-entrant: dropping a pooled block (or any collection) under the lock can run
+# an owner's finalizer (_release) on the same thread
+_lock = threading.RLock()
 _state = {
     "enabled": os.environ.get("SK_HOST_PIN", "1") != "0",
     "min_bytes": 64 << 20,        # smaller calls are latency-bound either way

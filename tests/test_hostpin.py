@@ -121,6 +121,7 @@ def test_reused_address_is_a_new_buffer(fake):
     assert len(fake.unreg) == 1
 
 
+@pytest.mark.timeout(60)
 def test_output_pool_recycles_only_blocks_nobody_can_see(fake):
     n = 1 << 20  # 4 MiB results
     assert hostpin.pooled_output(1 << 10) is None              # small: not pooled
@@ -141,9 +142,12 @@ def test_output_pool_recycles_only_blocks_nobody_can_see(fake):
     e = hostpin.pooled_output(n)
     assert e is not None and hostpin.pool_stats()["blocks"] == 4
     assert hostpin.pooled_output(n) is None                     # pool exhausted: caller allocates
+    hostpin.note(e), hostpin.note(e)                            # registered: has a finalizer
+    assert len(fake.reg) == 1
     del b, c, d, e
     assert hostpin.pool_stats()["in_use"] == 0
     f = hostpin.pooled_output(2 * n)                            # another size evicts idle blocks
+    assert len(fake.unreg) == 1                                 # ... and releases them (no deadlock)
     assert f is not None and hostpin.pool_stats()["blocks"] == 1
     hostpin.configure(enabled=False)
     assert hostpin.pooled_output(n) is None
