@@ -35,7 +35,7 @@ from . import _native
 _lock = threading.RLock()
 _state = {
     "enabled": os.environ.get("SK_HOST_PIN", "1") != "0",
-    "min_bytes": 64 << 20,        # smaller calls are latency-bound either way
+    "min_bytes": 8 << 20,         # smaller calls are latency-bound either way
     "max_bytes": 64 << 30,        # never lock more than this in one range
     "sightings": 2,               # register on the N-th call that uses the buffer
     "budget_bytes": 0,            # 0: half of physical memory
