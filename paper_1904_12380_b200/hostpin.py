@@ -195,11 +195,15 @@ def pooled_output(nfloats: int) -> np.ndarray | None:
         return None
     need = nfloats + _HUGE // 4
     with _lock:
-        for i in range(len(_pool)):
-            # references: the pool's list slot + getrefcount's argument
-            if _pool[i].size == need and sys.getrefcount(_pool[i]) == 2:
-                raw = _pool[i]
-                break
+        free = [i for i in range(len(_pool))
+                # references: the pool's list slot + getrefcount's argument
+                if _pool[i].size == need and sys.getrefcount(_pool[i]) == 2]
+        if free:
+            raw = _pool[free[0]]
+            # a y = f(x) loop alternates between two blocks: keep one spare, let
+            # the memory of any further idle block go
+            for i in reversed(free[2:]):
+                del _pool[i]
         else:
             # drop blocks of other sizes nobody uses; allocate while under the cap
             for i in range(len(_pool) - 1, -1, -1):

@@ -146,8 +146,11 @@ def test_output_pool_recycles_only_blocks_nobody_can_see(fake):
     assert len(fake.reg) == 1
     del b, c, d, e
     assert hostpin.pool_stats()["in_use"] == 0
+    g = hostpin.pooled_output(n)                                # 4 idle blocks: one handed out,
+    assert hostpin.pool_stats()["blocks"] == 2                  # one spare kept, two released
+    del g
     f = hostpin.pooled_output(2 * n)                            # another size evicts idle blocks
-    assert len(fake.unreg) == 1                                 # ... and releases them (no deadlock)
+    assert len(fake.unreg) == 1                                 # ... releasing them (no deadlock)
     assert f is not None and hostpin.pool_stats()["blocks"] == 1
     hostpin.configure(enabled=False)
     assert hostpin.pooled_output(n) is None
