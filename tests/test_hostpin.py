@@ -235,3 +235,47 @@ def test_pageable_matrix_is_pinned_on_second_call_same_bits():
     finally:
         hostpin.configure(enabled=before["enabled"], min_bytes=before["min_bytes"],
                           sightings=before["sightings"])
+
+
+@pytest.mark.gpu
+def test_host_path_fuzz_pinned_views_and_edges():
+    """Random shapes / views through the host path while buffers move from
+    staged to page-locked (whole owner, sub-views, odd byte offsets inside the
+    registered window and across its edges): always the device path's bits."""
+    import torch
+
+    before = hostpin.configure()
+    hostpin.configure(enabled=True, min_bytes=1 << 20, sightings=2)
+    rng = np.random.default_rng(20260710)
+    try:
+        for case in range(24):
+            cols = int(rng.choice([50, 128, 256, 1000, 1501, 4096, 20000, 70001]))
+            rows = max(2, int((rng.integers(3, 40) << 20) // (4 * cols)))
+            lead = int(rng.integers(0, 3)) * int(rng.choice([1, 8, 1024, 524288]))  # floats before the data
+            raw_x = np.zeros(rows * cols + lead + 16, np.float32)
+            raw_y = np.zeros(rows * cols + lead + 16, np.float32)
+            x = raw_x[lead:lead + rows * cols].reshape(rows, cols)
+            y = raw_y[lead:lead + rows * cols].reshape(rows, cols)
+            x[:] = rng.standard_normal((rows, cols), dtype=np.float32) * 4
+            ref = sk.softmax(torch.from_numpy(x).cuda(), sk.KernelVariant.REFERENCE_CLIPPED).cpu().numpy()
+            for call in range(3):                      # staged, pinning, direct
+                y[:] = -1.0
+                out = sk.softmax(x, sk.KernelVariant.REFERENCE_CLIPPED, out=y)
+                assert out is y
+                assert np.array_equal(y.view(np.uint32), ref.view(np.uint32)), (case, call, rows, cols, lead)
+            # a row block of the (now page-locked) buffers: same bits as those rows of the whole
+            r0, r1 = sorted(int(v) for v in rng.integers(0, rows + 1, 2))
+            if r1 - r0 >= 1:
+                y[:] = -1.0
+                sk.softmax(x[r0:r1], sk.KernelVariant.REFERENCE_CLIPPED, out=y[r0:r1])
+                got = sk.softmax(torch.from_numpy(x[r0:r1]).cuda(),
+                                 sk.KernelVariant.REFERENCE_CLIPPED).cpu().numpy()
+                assert np.array_equal(y[r0:r1].view(np.uint32), got.view(np.uint32)), (case, r0, r1)
+                assert (y[:r0] == -1.0).all() and (y[r1:] == -1.0).all()
+            del x, y, raw_x, raw_y
+            gc.collect()
+        assert hostpin.stats()["bytes"] == 0
+    finally:
+        hostpin.release_all()
+        hostpin.configure(enabled=before["enabled"], min_bytes=before["min_bytes"],
+                          sightings=before["sightings"])
