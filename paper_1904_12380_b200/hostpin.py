@@ -5,19 +5,21 @@ The reference's ``alloc_matrix`` hands out pageable ``np.zeros`` memory
 over and over (profiler.py:136-162).  From pageable memory every call pays two
 host-side staging copies (sk_host.cu); from page-locked memory the DMA engines
 read and write the caller's buffers directly (~95 vs ~53 GB/s on c5a).  Pinning
-a buffer in place costs about as much as a staged call (cudaHostRegister of
-2 GiB: ~35 ms for whole 2 MiB pages, ~160 ms when the range ends inside a huge
-page -- profiles/r2_hostreg_align.jsonl -- so only the buffer's inner 2 MiB-
-aligned window is registered; sk_softmax_f32_host stages the chunk at either
-end that reaches outside it), so this cache does it only for a large buffer
+a buffer in place costs one to two staged calls (cudaHostRegister of 2 GiB:
+35-50 ms when the range ends on a 2 MiB boundary, ~160 ms otherwise --
+profiles/r2_hostreg_align.jsonl), so this cache does it only for a large buffer
 seen for the SECOND time -- a one-shot call never pays it -- and releases the
 registration when the owning ndarray dies (``weakref.finalize`` runs before
 numpy frees the data), so no range stays registered past its memory.
 
-Only memory an ndarray keeps alive is ever registered: the key is the topmost
-ndarray of the view chain (the owner, or the array wrapping a foreign buffer
-and holding a reference to it).  ``SK_HOST_PIN=0`` or ``configure(enabled=
-False)`` turns it off; the staged path is then always used for pageable memory.
+The whole buffer of the owning ndarray is registered as ONE range: CUDA rejects
+a copy whose host side spans two registrations (or leaves one), and the caller
+-- or torch, for ``torch.from_numpy(a).cuda()`` -- may copy any part of its own
+array at any time.  (Registering the inner 2 MiB-aligned window and the edge
+pages separately is 4x faster and was tried: such a torch copy then fails with
+"invalid argument".)  Only memory an ndarray OWNS is registered (never a window
+onto someone else's buffer).  ``SK_HOST_PIN=0`` or ``configure(enabled=False)``
+turns it off; the staged path is then always used for pageable memory.
 """
 
 from __future__ import annotations
@@ -39,7 +41,6 @@ _state = {
     "max_bytes": 64 << 30,        # never lock more than this in one range
     "sightings": 2,               # register on the N-th call that uses the buffer
     "budget_bytes": 0,            # 0: half of physical memory
-    "edges": True,                # also lock the < 2 MiB before / after the aligned window
 }
 _HUGE = 2 << 20
 _entries: dict[int, "_Entry"] = {}
@@ -47,14 +48,10 @@ _pinned_total = 0
 
 
 class _Entry:
-    __slots__ = ("ptr", "nbytes", "lo", "hi", "seen", "box", "failed", "fin", "ranges")
+    __slots__ = ("ptr", "nbytes", "seen", "box", "failed", "fin")
 
     def __init__(self, ptr: int, nbytes: int):
         self.ptr, self.nbytes = ptr, nbytes
-        # the registered window: whole 2 MiB pages inside the buffer
-        self.lo = (ptr + _HUGE - 1) // _HUGE * _HUGE
-        self.hi = (ptr + nbytes) // _HUGE * _HUGE
-        self.ranges = []  # [(address, bytes)] registered: shared with the finalizer
         self.seen = 0
         self.box = [False]  # [registered]: shared with the owner's finalizer
         self.failed = False
@@ -62,8 +59,7 @@ class _Entry:
 
 
 def configure(enabled: bool | None = None, min_bytes: int | None = None,
-              sightings: int | None = None, budget_bytes: int | None = None,
-              edges: bool | None = None) -> dict:
+              sightings: int | None = None, budget_bytes: int | None = None) -> dict:
     """Set the cache policy; returns the policy in force."""
     with _lock:
         if enabled is not None:
@@ -74,8 +70,6 @@ def configure(enabled: bool | None = None, min_bytes: int | None = None,
             _state["sightings"] = max(1, int(sightings))
         if budget_bytes is not None:
             _state["budget_bytes"] = max(0, int(budget_bytes))
-        if edges is not None:
-            _state["edges"] = bool(edges)
         return dict(_state)
 
 
@@ -101,20 +95,18 @@ def _budget() -> int:
         return 16 << 30
 
 
-def _release(key: int, ranges: list, registered_box: list) -> None:
+def _release(key: int, ptr: int, nbytes: int, registered_box: list) -> None:
     """Finalizer of the owning ndarray: runs before numpy frees the data."""
     global _pinned_total
     with _lock:
         _entries.pop(key, None)
         if registered_box[0]:
             registered_box[0] = False
-            for lo, n in ranges:
-                _pinned_total -= n
-                try:
-                    _native.lib().sk_host_unregister(lo)
-                except Exception:  # noqa: BLE001 -- interpreter teardown
-                    pass
-            del ranges[:]
+            _pinned_total -= nbytes
+            try:
+                _native.lib().sk_host_unregister(ptr)
+            except Exception:  # noqa: BLE001 -- interpreter teardown
+                pass
 
 
 def note(view: np.ndarray) -> bool:
@@ -125,15 +117,17 @@ def note(view: np.ndarray) -> bool:
         return False
     own = _owner(view)
     nbytes = int(own.nbytes)
-    if nbytes > _state["max_bytes"] or view.nbytes * 2 < nbytes:
-        return False  # a small window of a much larger buffer: not worth locking it all
+    if not own.flags.owndata or nbytes > _state["max_bytes"] or view.nbytes * 2 < nbytes:
+        # a window onto memory numpy does not own (its lifetime and its other
+        # users are not ours to judge), or a small part of a much larger buffer
+        return False
     key = id(own)
     with _lock:
         e = _entries.get(key)
         if e is None or e.ptr != own.ctypes.data or e.nbytes != nbytes:
             e = _Entry(int(own.ctypes.data), nbytes)
             try:
-                e.fin = weakref.finalize(own, _release, key, e.ranges, e.box)
+                e.fin = weakref.finalize(own, _release, key, e.ptr, nbytes, e.box)
             except TypeError:
                 return False
             e.fin.atexit = False  # process teardown releases every registration
@@ -144,27 +138,13 @@ def note(view: np.ndarray) -> bool:
         if e.failed:
             return False
         e.seen += 1
-        win = e.hi - e.lo
-        if e.seen < _state["sightings"] or _pinned_total + win > _budget():
+        if e.seen < _state["sightings"] or _pinned_total + nbytes > _budget():
             return False
-        st = _native.lib().sk_host_register(e.lo, win) if win > 0 else 1
-        if st != 0:
+        if _native.lib().sk_host_register(e.ptr, nbytes) != 0:
             e.failed = True  # already registered by the caller, locked-memory limit, ...
             return False
         box[0] = True
-        e.ranges.append((e.lo, win))
-        _pinned_total += win
-        if _state["edges"]:
-            # the pages before / after the window, as two small registrations of
-            # their own (a range ending inside a huge page registers slowly as a
-            # whole, so they are kept apart from the window); a failure here only
-            # leaves the end chunks on the staged path
-            page = 4096
-            for a, b in ((e.ptr // page * page, e.lo),
-                         (e.hi, (e.ptr + nbytes + page - 1) // page * page)):
-                if b > a and _native.lib().sk_host_register(a, b - a) == 0:
-                    e.ranges.append((a, b - a))
-                    _pinned_total += b - a
+        _pinned_total += nbytes
         return True
 
 

@@ -32,20 +32,11 @@ def fake(monkeypatch):
     lib = _FakeLib()
     monkeypatch.setattr(hostpin._native, "lib", lambda: lib)
     before = hostpin.configure()
-    hostpin.configure(enabled=True, min_bytes=1 << 20, sightings=2, budget_bytes=1 << 30,
-                      edges=False)
+    hostpin.configure(enabled=True, min_bytes=1 << 20, sightings=2, budget_bytes=1 << 30)
     yield lib
     hostpin.release_all()
     hostpin.configure(enabled=before["enabled"], min_bytes=before["min_bytes"],
-                      sightings=before["sightings"], budget_bytes=before["budget_bytes"],
-                      edges=before["edges"])
-
-
-def _window(a):
-    """The whole 2 MiB pages inside ``a``'s buffer: what gets registered."""
-    lo = (a.ctypes.data + _M2 - 1) // _M2 * _M2
-    hi = (a.ctypes.data + a.nbytes) // _M2 * _M2
-    return lo, hi - lo
+                      sightings=before["sightings"], budget_bytes=before["budget_bytes"])
 
 
 def test_registers_on_second_sighting_and_releases_with_the_owner(fake):
@@ -53,35 +44,23 @@ def test_registers_on_second_sighting_and_releases_with_the_owner(fake):
     own = m.data.base
     assert not hostpin.note(m.view2d) and fake.reg == []
     assert hostpin.note(m.view2d)
-    lo, n = _window(own)
-    assert fake.reg == [(lo, n)] and n >= own.nbytes - 2 * _M2
-    assert lo % _M2 == 0 and n % _M2 == 0 and lo >= own.ctypes.data
-    assert lo + n <= own.ctypes.data + own.nbytes
+    # the owner's whole buffer as ONE range: a copy of any part of the caller's
+    # array (torch.from_numpy(a).cuda()) must never straddle a registration
+    assert fake.reg == [(own.ctypes.data, own.nbytes)]
     assert hostpin.note(m.view2d[:1200]) and len(fake.reg) == 1  # any view of the owner hits
-    assert hostpin.stats()["bytes"] == n
+    assert hostpin.stats()["bytes"] == own.nbytes
+    ptr = own.ctypes.data
     del m, own
     gc.collect()
-    assert fake.unreg == [lo] and hostpin.stats() == {"ranges": 0, "bytes": 0, "tracked": 0}
+    assert fake.unreg == [ptr] and hostpin.stats() == {"ranges": 0, "bytes": 0, "tracked": 0}
 
 
-def test_edges_are_separate_page_aligned_registrations(fake):
-    hostpin.configure(edges=True)
-    m = sk.alloc_matrix(2048, 2048)
-    own = m.data.base
-    hostpin.note(m.view2d), hostpin.note(m.view2d)
-    lo, n = _window(own)
-    assert fake.reg[0] == (lo, n) and 1 <= len(fake.reg) <= 3
-    ranges = sorted(fake.reg)
-    for (a, na), (b, _) in zip(ranges, ranges[1:]):
-        assert a + na == b                       # adjacent, never overlapping
-    assert all(a % 4096 == 0 and na % 4096 == 0 for a, na in ranges)
-    assert ranges[0][0] <= own.ctypes.data < ranges[0][0] + 4096
-    end = ranges[-1][0] + ranges[-1][1]
-    assert end - 4096 < own.ctypes.data + own.nbytes <= end
-    assert hostpin.stats()["bytes"] == sum(na for _, na in ranges)
-    del m, own
-    gc.collect()
-    assert sorted(fake.unreg) == [a for a, _ in ranges] and hostpin.stats()["bytes"] == 0
+def test_memory_numpy_does_not_own_is_never_registered(fake):
+    backing = bytearray(8 << 20)
+    a = np.frombuffer(backing, dtype=np.float32)
+    for _ in range(3):
+        assert not hostpin.note(a)
+    assert fake.reg == []
 
 
 def test_small_buffers_windows_and_disabled_are_left_alone(fake):
@@ -258,11 +237,32 @@ def test_host_path_fuzz_pinned_views_and_edges():
             y = raw_y[lead:lead + rows * cols].reshape(rows, cols)
             x[:] = rng.standard_normal((rows, cols), dtype=np.float32) * 4
             ref = sk.softmax(torch.from_numpy(x).cuda(), sk.KernelVariant.REFERENCE_CLIPPED).cpu().numpy()
+            # Long rows: a small standalone device call takes the latency path
+            # (split) where the host path's chunks keep the throughput plan (K3g),
+            # and K3g's unaligned variant cuts slices at each row's 16-B phase,
+            # which differs between a chunk in a staging slot and the whole matrix
+            # on the device (DESIGN sections 4-5): same values within the gate
+            # there, the same bits for every row one CTA holds (<= 16384 floats)
+            exact = cols <= 16384
+
+            def same(a, b):
+                if exact:
+                    return np.array_equal(a.view(np.uint32), b.view(np.uint32))
+                return bool((np.abs(a - b) <= 1e-5 * b).all())
+
+            first = None
             for call in range(3):                      # staged, pinning, direct
                 y[:] = -1.0
                 out = sk.softmax(x, sk.KernelVariant.REFERENCE_CLIPPED, out=y)
                 assert out is y
-                assert np.array_equal(y.view(np.uint32), ref.view(np.uint32)), (case, call, rows, cols, lead)
+                assert same(y, ref), (case, call, rows, cols, lead)
+                if first is None:
+                    first = y.copy()
+                # staged or direct, the host path itself always gives the same bits
+                assert np.array_equal(y.view(np.uint32), first.view(np.uint32)), (case, call)
+            # other CUDA users of the caller's memory keep working on the page-locked
+            # buffer: any part of it, the whole owner included, copies in one piece
+            assert torch.equal(torch.from_numpy(raw_y).cuda().cpu(), torch.from_numpy(raw_y))
             # a row block of the (now page-locked) buffers: same bits as those rows of the whole
             r0, r1 = sorted(int(v) for v in rng.integers(0, rows + 1, 2))
             if r1 - r0 >= 1:
@@ -270,9 +270,9 @@ def test_host_path_fuzz_pinned_views_and_edges():
                 sk.softmax(x[r0:r1], sk.KernelVariant.REFERENCE_CLIPPED, out=y[r0:r1])
                 got = sk.softmax(torch.from_numpy(x[r0:r1]).cuda(),
                                  sk.KernelVariant.REFERENCE_CLIPPED).cpu().numpy()
-                assert np.array_equal(y[r0:r1].view(np.uint32), got.view(np.uint32)), (case, r0, r1)
+                assert same(y[r0:r1], got), (case, r0, r1)
                 assert (y[:r0] == -1.0).all() and (y[r1:] == -1.0).all()
-            del x, y, raw_x, raw_y
+            del x, y, raw_x, raw_y, out
             gc.collect()
         assert hostpin.stats()["bytes"] == 0
     finally:
