@@ -40,19 +40,37 @@ def fake(monkeypatch):
 
 
 def test_registers_on_second_sighting_and_releases_with_the_owner(fake):
-    m = sk.alloc_matrix(2048, 2048)  # a view into an over-allocated np.zeros, like the reference's
-    own = m.data.base
+    raw = np.zeros(4 * 1024 * 1024 + 8, np.float32)  # the reference allocator's layout
+    off = (-raw.ctypes.data) % 32 // 4
+    m = sk.Matrix2D(rows=2048, cols=2048, data=raw[off:off + 4 * 1024 * 1024])
     assert not hostpin.note(m.view2d) and fake.reg == []
     assert hostpin.note(m.view2d)
     # the owner's whole buffer as ONE range: a copy of any part of the caller's
     # array (torch.from_numpy(a).cuda()) must never straddle a registration
-    assert fake.reg == [(own.ctypes.data, own.nbytes)]
+    assert fake.reg == [(raw.ctypes.data, raw.nbytes)]
     assert hostpin.note(m.view2d[:1200]) and len(fake.reg) == 1  # any view of the owner hits
-    assert hostpin.stats()["bytes"] == own.nbytes
-    ptr = own.ctypes.data
-    del m, own
+    assert hostpin.stats()["bytes"] == raw.nbytes
+    ptr = raw.ctypes.data
+    del m, raw
     gc.collect()
     assert fake.unreg == [ptr] and hostpin.stats() == {"ranges": 0, "bytes": 0, "tracked": 0}
+
+
+def test_this_packages_matrices_are_aligned_windows_of_whole_huge_pages(fake):
+    m = sk.alloc_matrix(2048, 2049)                  # 16 MiB + 8 KiB: zero-filled, 2 MiB-aligned
+    assert m.data.ctypes.data % _M2 == 0 and not m.data.any() and m.data.flags.writeable
+    m.view2d[5, 7] = 3.0
+    assert float(m.data[5 * 2049 + 7]) == 3.0
+    hostpin.note(m.view2d), hostpin.note(m.view2d)
+    win = (m.data.nbytes + _M2 - 1) // _M2 * _M2
+    assert fake.reg == [(m.data.ctypes.data, win)]   # exactly the window, nothing outside it
+    assert hostpin.note(m.view2d[100:1900])
+    ptr = m.data.ctypes.data
+    del m
+    gc.collect()
+    assert fake.unreg == [ptr] and hostpin.stats()["tracked"] == 0
+    small = sk.alloc_matrix(64, 64)                  # small matrices stay plain numpy
+    assert small.data.base.flags.owndata and small.data.ctypes.data % 32 == 0
 
 
 def test_memory_numpy_does_not_own_is_never_registered(fake):
