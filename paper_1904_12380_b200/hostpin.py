@@ -38,7 +38,8 @@ from . import _native
 _lock = threading.RLock()
 _state = {
     "enabled": os.environ.get("SK_HOST_PIN", "1") != "0",
-    "min_bytes": 8 << 20,         # smaller calls are latency-bound either way
+    "min_bytes": 512 << 10,       # below this the staging copy costs less than the bookkeeping
+    "pool_min_bytes": 8 << 20,    # results at least this large come from the block pool
     "max_bytes": 64 << 30,        # never lock more than this in one range
     "sightings": 2,               # register on the N-th call that uses the buffer
     "budget_bytes": 0,            # 0: half of physical memory
@@ -60,7 +61,8 @@ class _Entry:
 
 
 def configure(enabled: bool | None = None, min_bytes: int | None = None,
-              sightings: int | None = None, budget_bytes: int | None = None) -> dict:
+              sightings: int | None = None, budget_bytes: int | None = None,
+              pool_min_bytes: int | None = None) -> dict:
     """Set the cache policy; returns the policy in force."""
     with _lock:
         if enabled is not None:
@@ -71,6 +73,8 @@ def configure(enabled: bool | None = None, min_bytes: int | None = None,
             _state["sightings"] = max(1, int(sightings))
         if budget_bytes is not None:
             _state["budget_bytes"] = max(0, int(budget_bytes))
+        if pool_min_bytes is not None:
+            _state["pool_min_bytes"] = max(0, int(pool_min_bytes))
         return dict(_state)
 
 
@@ -219,7 +223,7 @@ def pooled_output(nfloats: int) -> np.ndarray | None:
     pool, or None when the pool does not apply (small result, pool disabled or
     exhausted): the caller then allocates as usual."""
     nbytes = nfloats * 4
-    if not _state["enabled"] or nbytes < _state["min_bytes"]:
+    if not _state["enabled"] or nbytes < max(_state["min_bytes"], _state["pool_min_bytes"]):
         return None
     with _lock:
         free = [i for i in range(len(_pool)) if _pool[i][1] == nfloats and _idle(i)]

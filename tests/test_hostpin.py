@@ -32,11 +32,13 @@ def fake(monkeypatch):
     lib = _FakeLib()
     monkeypatch.setattr(hostpin._native, "lib", lambda: lib)
     before = hostpin.configure()
-    hostpin.configure(enabled=True, min_bytes=1 << 20, sightings=2, budget_bytes=1 << 30)
+    hostpin.configure(enabled=True, min_bytes=1 << 20, sightings=2, budget_bytes=1 << 30,
+                      pool_min_bytes=1 << 20)
     yield lib
     hostpin.release_all()
     hostpin.configure(enabled=before["enabled"], min_bytes=before["min_bytes"],
-                      sightings=before["sightings"], budget_bytes=before["budget_bytes"])
+                      sightings=before["sightings"], budget_bytes=before["budget_bytes"],
+                      pool_min_bytes=before["pool_min_bytes"])
 
 
 def test_registers_on_second_sighting_and_releases_with_the_owner(fake):
@@ -163,7 +165,7 @@ def test_fresh_outputs_come_from_the_pool_and_stay_valid():
     from paper_1904_12380_b200 import configs
 
     before = hostpin.configure()
-    hostpin.configure(enabled=True, min_bytes=1 << 20, sightings=2)
+    hostpin.configure(enabled=True, min_bytes=1 << 20, sightings=2, pool_min_bytes=1 << 20)
     try:
         x = configs.generate("c2")
         ref = sk.softmax(torch.from_numpy(x).cuda(), sk.KernelVariant.REFERENCE_CLIPPED).cpu().numpy()
@@ -188,7 +190,7 @@ def test_fresh_outputs_come_from_the_pool_and_stay_valid():
         gc.collect()
         hostpin.release_all()
         hostpin.configure(enabled=before["enabled"], min_bytes=before["min_bytes"],
-                          sightings=before["sightings"])
+                          sightings=before["sightings"], pool_min_bytes=before["pool_min_bytes"])
 
 
 @pytest.mark.gpu
