@@ -255,6 +255,22 @@ def pool_stats() -> dict:
                 "in_use": sum(1 for i in range(len(_pool)) if not _idle(i))}
 
 
+def _after_fork_in_child() -> None:
+    """A forked child has no CUDA context: its copies of the registrations are
+    not its to release (the pages stay locked for the parent), so forget them
+    rather than call the driver from the child when the arrays die."""
+    global _pinned_total, _lock
+    _lock = threading.RLock()
+    for e in _entries.values():
+        e.box[0] = False
+        e.failed = True  # never try to lock the parent's buffers from the child
+    _pinned_total = 0
+
+
+if hasattr(os, "register_at_fork"):
+    os.register_at_fork(after_in_child=_after_fork_in_child)
+
+
 def release_all() -> None:
     """Drop every registration now (tests; a caller about to fork)."""
     with _lock:

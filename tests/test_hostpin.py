@@ -110,6 +110,29 @@ def test_failed_registration_is_not_retried_and_budget_is_kept(fake):
     assert hostpin.stats()["bytes"] == 0
 
 
+def test_forked_child_forgets_the_parents_registrations(fake):
+    import os
+
+    a = np.zeros(2 << 20, np.float32)
+    hostpin.note(a), hostpin.note(a)
+    assert hostpin.stats()["ranges"] == 1
+    r, w = os.pipe()
+    pid = os.fork()
+    if pid == 0:  # child: no CUDA context of its own
+        try:
+            ok = hostpin.stats()["ranges"] == 0 and not hostpin.note(a)
+            del a
+            gc.collect()
+            ok = ok and fake.unreg == []  # the child never calls the driver for them
+            os.write(w, b"1" if ok else b"0")
+        finally:
+            os._exit(0)
+    os.close(w)
+    assert os.read(r, 1) == b"1"
+    os.waitpid(pid, 0)
+    assert hostpin.stats()["ranges"] == 1  # the parent's registration is untouched
+
+
 def test_reused_address_is_a_new_buffer(fake):
     a = np.zeros(2 << 20, np.float32)
     hostpin.note(a), hostpin.note(a)
