@@ -122,8 +122,13 @@ def shard(total: int, world: int, rank: int) -> tuple[int, int]:
 
 def common_config(spec_name: str, rows: int, cols: int, workload: str) -> dict:
     """The config dict both arms print (identical by construction)."""
+    mib = 8 * rows * cols >> 20
+    # the device arm's L2 policy (setup.l2 has the per-rank detail): a step's
+    # buffers exceed 3x the 126 MiB L2, or that many buffer pairs are rotated
+    l2 = (f"inputs larger than L2: {mib} MiB read + written per step"
+          if mib >= 3 * 126 else "rotating resident buffer pairs totalling > 3x the 126 MiB L2")
     return {"workload": workload, "rows": rows, "cols": cols,
-            "scaling": "strong: rows split across ranks"}
+            "scaling": "strong: rows split across ranks", "l2": l2}
 
 
 # ------------------------------------------------------------------ clocks

@@ -26,7 +26,7 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == ("reference" if ref_present else "port")
     assert d["cpu_baseline"]["cores"] >= 1
     assert d["config"]["workload"].startswith("c5a")
-    assert set(d["config"]) == {"workload", "rows", "cols", "scaling"}
+    assert set(d["config"]) == {"workload", "rows", "cols", "scaling", "l2"}
 
 
 def test_reference_arm_never_maps_the_product_library():
