@@ -1022,10 +1022,11 @@ int launch_plan(const Plan& p, const float* x, float* y, int64_t rows, int64_t c
       }
       cfg.attrs = a;
       cfg.numAttrs = na;
-      int slice = p.seglen, nst = p.lag;
+      int slice = p.seglen, nst = p.lag, dg = g_gres_diag.load();
       float shv = sh;
       void* args[] = {(void*)&x, (void*)&y, (void*)&rows, (void*)&cols, (void*)&ldx,
-                      (void*)&ldy, (void*)&slice, (void*)&nst, (void*)&bad, (void*)&shv};
+                      (void*)&ldy, (void*)&slice, (void*)&nst, (void*)&bad, (void*)&shv,
+                      (void*)&dg};
       SK_CUDA(cudaLaunchKernelExC(&cfg, cluster_fn(mode), args));
     } else if (p.k3 == 7) {
       const GresWs w = gres_ws(p);

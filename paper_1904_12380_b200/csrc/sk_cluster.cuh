@@ -91,7 +91,7 @@ template <int MODE, bool ONEX, int TPB = kClusterThreads>
 __global__ void __launch_bounds__(TPB, 1)
     k3_cluster(const float* __restrict__ x, float* __restrict__ y, int64_t rows, int64_t cols,
                int64_t ldx, int64_t ldy, int slice, int nstages,
-               unsigned long long* __restrict__ bad_row, float shift_scale) {
+               unsigned long long* __restrict__ bad_row, float shift_scale, int diag) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage_buf = reinterpret_cast<float*>(smem_raw);
   __shared__ uint64_t bars[kClusterStages];
@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(TPB, 1)
   int k = 0;
   for (int64_t row = cid; row < rows; row += ncl, ++k) {
     const int stage = k % nstages;
+    timing_chaos(diag, 8, k);  // diag bit 6: timing chaos (sk_common.cuh), results unchanged
     mbar_wait(&bars[stage], (k / nstages) & 1);
     float4* sb = reinterpret_cast<float4*>(stage_buf + size_t(stage) * slice);
 
@@ -168,6 +169,7 @@ __global__ void __launch_bounds__(TPB, 1)
       M = bc_m;  // local max of this slice for now
     } else {
       if (tid == 0) mbar_arrive_expect_tx(&xbar_max[par], cs * 4u);
+      timing_chaos(diag, 2, k);
       if (warp == 0) {
         float m = lane < NW ? red_f[lane] : kPadLogit;
         m = group_max<32>(m);
@@ -198,6 +200,7 @@ __global__ void __launch_bounds__(TPB, 1)
       if (ONEX) mbar_arrive_expect_tx(&xbar_max[par], cs * 4u);
       mbar_arrive_expect_tx(&xbar_sum[par], cs * 8u);
     }
+    timing_chaos(diag, 3, k);
     if (warp == 0) {
       double t = lane < NW ? red_d[lane] : 0.0;
       t = group_sum<32>(t);
@@ -209,6 +212,7 @@ __global__ void __launch_bounds__(TPB, 1)
                      dsmem_addr(&xbar_sum[par], lane));
       }
     }
+    timing_chaos(diag, 4, k);
     if (ONEX) mbar_wait(&xbar_max[par], xpar);
     mbar_wait(&xbar_sum[par], xpar);
     double S;
@@ -226,6 +230,7 @@ __global__ void __launch_bounds__(TPB, 1)
     const float rcp = recip_of_sum(S);
 
     // ---- y = e * r, streaming stores
+    timing_chaos(diag, 6, k);
     float* yr = y + row * ldy + c0;
 #pragma unroll 4
     for (int q = tid; q < nvec; q += TPB) {
@@ -240,6 +245,7 @@ __global__ void __launch_bounds__(TPB, 1)
       }
       st_stream4(yr + 4 * q, make_float4(a.x, a.y, b.x, b.y));
     }
+    timing_chaos(diag, 7, k);
     __syncthreads();  // stage fully consumed
     if (tid == 0) {
       const int64_t rn = row + int64_t(nstages) * ncl;

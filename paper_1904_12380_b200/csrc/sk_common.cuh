@@ -288,6 +288,27 @@ __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// ---- timing chaos for the barrier-heavy kernels (K3g, K3c) ------------------
+// Timing chaos (gres_diag bit 6; bits 8.. seed it): pseudo-random per-warp
+// delays of up to ~4 us at every hand-off point -- before waiting for a stage,
+// arriving at a named barrier, publishing, refilling, polling, writing out --
+// so the tests can shake the schedule the barriers, mbarriers and tagged slots
+// must hold under (the pool's GPUs refuse compute-sanitizer's racecheck).
+// Results must not change by a bit; a missed dependency shows as wrong output
+// or as the exchange timing out.
+__device__ __forceinline__ void timing_chaos(int diag, unsigned point, unsigned k) {
+  if (diag & 64) {
+    unsigned h = (blockIdx.x * 2654435761u) ^ ((threadIdx.x >> 5) * 0x9E3779B1u) ^
+                 (point * 0x85EBCA6Bu) ^ (k * 0xC2B2AE35u) ^ (static_cast<unsigned>(diag) >> 8);
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    h *= 0x297A2D39u;
+    h ^= h >> 15;
+    if ((h & 3u) == 0u) __nanosleep(100u + ((h >> 8) & 4095u));
+  }
+}
+
 // ---- global-scope acquire/release for cross-CTA row statistics --------------
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   unsigned v;

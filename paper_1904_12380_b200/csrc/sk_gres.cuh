@@ -77,26 +77,6 @@ __device__ __forceinline__ void ld_slot2(const unsigned long long* p, unsigned l
     asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 
-// Timing chaos (gres_diag bit 6; bits 8.. seed it): pseudo-random per-warp
-// delays of up to ~4 us at every hand-off point -- before waiting for a stage,
-// arriving at a named barrier, publishing, refilling, polling, writing out --
-// so the tests can shake the schedule the barriers, mbarriers and tagged slots
-// must hold under (the pool's GPUs refuse compute-sanitizer's racecheck).
-// Results must not change by a bit; a missed dependency shows as wrong output
-// or as the exchange timing out.
-__device__ __forceinline__ void gres_chaos(int diag, unsigned point, unsigned k) {
-  if (diag & 64) {
-    unsigned h = (blockIdx.x * 2654435761u) ^ ((threadIdx.x >> 5) * 0x9E3779B1u) ^
-                 (point * 0x85EBCA6Bu) ^ (k * 0xC2B2AE35u) ^ (static_cast<unsigned>(diag) >> 8);
-    h ^= h >> 15;
-    h *= 0x2C1B3C6Du;
-    h ^= h >> 12;
-    h *= 0x297A2D39u;
-    h ^= h >> 15;
-    if ((h & 3u) == 0u) __nanosleep(100u + ((h >> 8) & 4095u));
-  }
-}
-
 constexpr int kGresMaxSlots = 160;  // pairs merged per row (world x P), 5 per poller lane
 constexpr int kGresMaxWorld = 8;
 
@@ -356,7 +336,7 @@ __global__ void __launch_bounds__(kGresBlock, 1)
     for (int64_t row = g; row < rows; row += G, ++k) {
       const int b = static_cast<int>(k % unsigned(NB));
       // CTA pair (m, s) of row k from the 16 warp pairs, fixed order
-      gres_chaos(diag, 1, k);
+      timing_chaos(diag, 1, k);
       bar_sync_n(gres_bar1<L>(k), kGresThreads);
       const float mw = lane < NW ? red_f[b][lane] : kPadLogit;
       const float mc = group_max<32>(mw);
@@ -364,21 +344,21 @@ __global__ void __launch_bounds__(kGresBlock, 1)
       if (lane < NW && mw != mc) sw *= static_cast<double>(expf(mw - mc));
       const double sc = group_sum<32>(sw);
       // lane r stores the pair into rank r's slot array (a peer's, over NVLink)
-      gres_chaos(diag, 2, k);
+      timing_chaos(diag, 2, k);
       if (lane < comm.world)
         gres_publish(slot_set(gres_dst(comm, lane), k) + 2 * gi, mc, sc, gres_tag(epoch, k), sys);
       // refill the stage row k-L released
       if (k >= unsigned(L)) {
         const unsigned j = k - unsigned(L);
         bar_sync_n(gres_bar3<L>(j), kGresThreads);
-        gres_chaos(diag, 3, k);
+        timing_chaos(diag, 3, k);
         const int64_t rn = row - int64_t(L) * G + int64_t(nstages) * G;
         if (lane == 0 && rn < rows) issue(rn, static_cast<int>(j % unsigned(nstages)));
       }
       if (!SPLIT) {
-        gres_chaos(diag, 4, k);
+        timing_chaos(diag, 4, k);
         poll_merge(k);
-        gres_chaos(diag, 5, k);
+        timing_chaos(diag, 5, k);
         bar_arrive_n(gres_bar2<L>(k), kGresThreads);
       }
     }
@@ -389,9 +369,9 @@ __global__ void __launch_bounds__(kGresBlock, 1)
     if (SPLIT) {
       unsigned k = 0;
       for (int64_t row = g; row < rows; row += G, ++k) {
-        gres_chaos(diag, 4, k);
+        timing_chaos(diag, 4, k);
         poll_merge(k);
-        gres_chaos(diag, 5, k);
+        timing_chaos(diag, 5, k);
         bar_arrive_n(gres_bar2<L>(k), kGresThreads);
       }
     }
@@ -400,7 +380,7 @@ __global__ void __launch_bounds__(kGresBlock, 1)
     // row k's output pass runs after row k+L's local pass, so the group
     // exchange of row k overlaps L full rows of streaming work.
     auto output = [&](unsigned j) {
-      gres_chaos(diag, 6, j);
+      timing_chaos(diag, 6, j);
       bar_sync_n(gres_bar2<L>(j), kGresThreads);
       const int b = static_cast<int>(j % unsigned(NB));
       const float M = bc_m[b];
@@ -450,14 +430,14 @@ __global__ void __launch_bounds__(kGresBlock, 1)
         }
       }
       fence_proxy_async_smem();  // generic smem reads before the TMA refill
-      gres_chaos(diag, 7, j);
+      timing_chaos(diag, 7, j);
       bar_arrive_n(gres_bar3<L>(j), kGresThreads);
     };
 
     unsigned k = 0;
     for (int64_t row = g; row < rows; row += G, ++k) {
       const int stage = static_cast<int>(k % unsigned(nstages));
-      gres_chaos(diag, 8, k);
+      timing_chaos(diag, 8, k);
       mbar_wait(&bars[stage], (k / unsigned(nstages)) & 1u);
       const float4* sb = reinterpret_cast<const float4*>(stage_buf + size_t(stage) * slice);
       int nq = nvec;  // staged float4 groups
@@ -499,7 +479,7 @@ __global__ void __launch_bounds__(kGresBlock, 1)
         red_f[b][warp] = mw;
         red_d[b][warp] = sw;
       }
-      gres_chaos(diag, 9, k);
+      timing_chaos(diag, 9, k);
       bar_arrive_n(gres_bar1<L>(k), kGresThreads);
       if (k >= unsigned(L)) output(k - unsigned(L));
     }

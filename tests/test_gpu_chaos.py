@@ -78,3 +78,27 @@ def test_fused_column_shard_bits_do_not_depend_on_timing(tuning, oracle):
         x, sk.KernelVariant.REFERENCE_CLIPPED, 4), seeds=(5, 6, 7))
     d = oracle.parity(y0[:16].cpu().numpy(), oracle.softmax_ref(x_host[:16], True))
     assert d["ok"], d
+
+
+@pytest.mark.timeout(600)
+def test_k3c_cluster_rows_bits_do_not_depend_on_timing(tuning, oracle):
+    """The cluster-resident fallback (K3c: DSMEM st.async pushes completing
+    peers' mbarriers, a TMA ring per CTA) under the same shaken schedules."""
+    import torch
+
+    import paper_1904_12380_b200 as sk
+
+    rows, cols = 160, 131072
+    tuning.set_tuning("gres", 0)
+    tuning.set_tuning("k3_impl", 5)
+    try:
+        plan = tuning.describe_plan(rows, cols)
+        assert plan.startswith("k3_cluster"), plan
+        rng = np.random.default_rng(5)
+        x_host = (rng.standard_normal((rows, cols), dtype=np.float32) * 5).astype(np.float32)
+        x = torch.from_numpy(x_host).cuda()
+        y0 = _chaos_runs(tuning, lambda: sk.softmax(x, sk.KernelVariant.REFERENCE_CLIPPED))
+        d = oracle.parity(y0[:16].cpu().numpy(), oracle.softmax_ref(x_host[:16], True))
+        assert d["ok"], d
+    finally:
+        tuning.set_tuning("k3_impl", 3)
