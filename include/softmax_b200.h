@@ -263,7 +263,11 @@ int sk_host_unregister(void* p);
  *   "gres_sleep"     K3g poller back-off (ns, default 128)
  *   "gres_timeout_spins"  polls before a missing peer aborts an exchange (0 = default)
  *   "gres_diag"      1: K3g waits for its own slot only, 2: K3g skips the math
- *                    (timing diagnostics; wrong results)
+ *                    (timing diagnostics; wrong results); 64 | seed << 8: timing
+ *                    chaos -- pseudo-random per-warp delays at every hand-off of
+ *                    K3g / K3c, results unchanged (tests/test_gpu_chaos.py)
+ *   "colshard_sys"   1: the one-GPU column-shard emulation uses the cross-GPU
+ *                    launch's system-scope slot stores / loads (test hook)
  *   "cluster_k3"     1 (default): K3c may serve rows K3g cannot (fallback)
  *   "cluster_size"   force the K3c cluster size (0 = auto: most SMs covered)
  *   "cluster_onex"   1: K3c exchanges one (max, sum) pair per row and recomputes

@@ -105,6 +105,7 @@ std::atomic<int> g_gres_sleep{128};  // poller back-off between polls (ns)
 std::atomic<int> g_latency_steps{3};  // K3g row steps per group up to which the latency path is taken
 std::atomic<int> g_gres_diag{0};     // timing diagnostics (1: wait only for the own slot -- wrong results)
 std::atomic<unsigned> g_gres_spins{kGresSpinLimit};  // exchange timeout (polls), tests shorten it
+std::atomic<int> g_colshard_sys{0};  // 1: the emulated column shard uses the cross-GPU (.sys) slot accesses
 bool gres_split(int lag) {
   const int v = g_gres_split.load();
   return v < 0 ? lag >= 2 : v != 0;
@@ -1146,6 +1147,7 @@ int sk_set_tuning(const char* key, int value) {
   }
   else if (k == "gres") g_gres = value;
   else if (k == "gres_p") g_gres_p = value;
+  else if (k == "colshard_sys") g_colshard_sys = value;
   else if (k == "gres_st") g_gres_st = value;
   else if (k == "gres_diag") g_gres_diag = value;
   else if (k == "gres_sleep") g_gres_sleep = value;

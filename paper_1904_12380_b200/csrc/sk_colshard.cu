@@ -86,7 +86,9 @@ int colshard_launch(const float* x, float* y, int64_t rows, int64_t cols, int64_
   comm.world = world;
   comm.rank0 = nvr == 1 ? rank : 0;
   comm.nvr = nvr;
-  comm.sys = (world > 1 && nvr == 1) ? 1 : 0;  // peers are other GPUs
+  // peers are other GPUs (or the test hook asks the emulation for the same
+  // st / ld.relaxed.sys slot accesses the cross-GPU launch uses)
+  comm.sys = (world > 1 && (nvr == 1 || g_colshard_sys.load())) ? 1 : 0;
   comm.spin_limit = g_gres_spins.load();
   comm.reset_words = cross_gpu ? 0ull : (kXBlockBytes - kXSlots) / 8;
   comm.reset_period = static_cast<unsigned>(gres_reset_period());

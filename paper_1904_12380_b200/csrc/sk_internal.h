@@ -38,6 +38,7 @@ inline constexpr int64_t kOneCtaRowMax = 8192;
 extern std::atomic<int> g_pdl, g_coop_pdl, g_gres_sleep, g_gres_diag, g_host_chunk_kb,
     g_host_zero_copy, g_host_threads, g_host_nt;
 extern std::atomic<unsigned> g_gres_spins;
+extern std::atomic<int> g_colshard_sys;  // test hook: .sys-scope slot accesses in the one-GPU emulation too
 
 // Launch helper: cudaLaunchKernelExC with PDL (and cooperative) attributes.
 template <typename... Args>

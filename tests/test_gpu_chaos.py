@@ -102,3 +102,30 @@ def test_k3c_cluster_rows_bits_do_not_depend_on_timing(tuning, oracle):
         assert d["ok"], d
     finally:
         tuning.set_tuning("k3_impl", 3)
+
+
+@pytest.mark.timeout(600)
+def test_fused_column_shard_with_system_scope_slot_accesses(tuning, oracle):
+    """The cross-GPU launch publishes and polls its slots with st / ld.relaxed.sys
+    (peer memory over NVLink).  One GPU cannot run two ranks' kernels that wait
+    on each other, so the emulated 4-rank launch is switched to the same
+    system-scope accesses (colshard_sys): same bits as the .gpu-scope run, also
+    under shaken schedules."""
+    import torch
+
+    import paper_1904_12380_b200 as sk
+    from paper_1904_12380_b200 import sharding
+
+    rng = np.random.default_rng(91)
+    x_host = (rng.standard_normal((40, 4 * 50000), dtype=np.float32) * 3).astype(np.float32)
+    x = torch.from_numpy(x_host).cuda()
+    fn = lambda: sharding.emulate_column_shards(x, sk.KernelVariant.REFERENCE_CLIPPED, 4)  # noqa: E731
+    y_gpu = fn()
+    tuning.set_tuning("colshard_sys", 1)
+    try:
+        y_sys = _chaos_runs(tuning, fn, seeds=(11, 12, 13))
+    finally:
+        tuning.set_tuning("colshard_sys", 0)
+    assert torch.equal(y_sys, y_gpu)
+    d = oracle.parity(y_sys[:16].cpu().numpy(), oracle.softmax_ref(x_host[:16], True))
+    assert d["ok"], d
