@@ -223,11 +223,12 @@ void sk_free_pinned(void* p);
  * Page-lock / release a caller-owned host range in place (cudaHostRegister,
  * portable).  A registered range is found by sk_softmax_f32_host per call
  * (cudaPointerGetAttributes) and then takes the direct-DMA path with no
- * staging copies.  The host mirror registers a caller's large pageable
- * Matrix2D buffers (the reference's np.zeros, tensor.py:90-103) the second
- * time it sees them and releases them when the owning array dies
- * (hostpin.py); C callers own the lifetime themselves: unregister BEFORE
- * freeing the memory.  SK_OK, or SK_ERR_CUDA (range already registered,
+ * staging copies.  The host mirror registers a caller's pageable Matrix2D
+ * buffers (the reference's np.zeros, tensor.py:90-103) the second time it
+ * sees them -- the owning array's whole range as ONE registration, since CUDA
+ * rejects any copy (the caller's own, torch's) whose host side straddles two
+ * registrations -- and releases them when the owning array dies (hostpin.py);
+ * C callers own the lifetime themselves: unregister BEFORE freeing the memory.  SK_OK, or SK_ERR_CUDA (range already registered,
  * locked-memory limit, ...) -- the caller then simply stays on the staged path.
  */
 int sk_host_register(void* p, size_t bytes);

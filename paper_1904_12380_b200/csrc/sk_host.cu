@@ -61,10 +61,10 @@ const void* mapped_device_ptr(const void* h) {
 }
 
 // Ranges page-locked in place through sk_host_register (start -> bytes).  One
-// cudaMemcpyAsync may not span two registrations (invalid argument), and a
-// caller buffer is registered as up to three adjacent ranges (hostpin.py: the
-// 2 MiB-aligned window and the pages before / after it), so direct copies are
-// cut at the range boundaries found here.
+// cudaMemcpyAsync may not span two registrations (invalid argument).  The
+// Python mirror registers one range per buffer (hostpin.py), but a C caller
+// may register a buffer in adjacent pieces, so direct copies are cut at the
+// range boundaries found here.
 std::mutex g_reg_mu;
 std::map<uintptr_t, size_t> g_reg;
 
@@ -366,10 +366,10 @@ int sk_softmax_f32_host(const float* x_host, float* y_host, int64_t rows, int64_
   std::vector<int64_t> start(nchunks + 1, 0);
   for (int64_t k = 0; k < nchunks; ++k) start[k + 1] = start[k] + sched[k];
   // Pageable caller memory is staged through page-locked slots, decided per
-  // chunk: a buffer page-locked in place by sk_host_register (hostpin.py) is
-  // registered over its inner 2 MiB-aligned window only, so the chunks at
-  // either end can reach into pageable memory while every other chunk is
-  // DMA-ed directly.
+  // chunk: a caller may have page-locked only part of a buffer (e.g. its
+  // 2 MiB-aligned inside, which registers 4x faster), so the chunks at either
+  // end can reach into pageable memory while every other chunk is DMA-ed
+  // directly.
   auto locked = [](const float* p, size_t bytes) {
     if (reg_pieces(p, bytes, nullptr)) return true;
     // page-locked by someone else (cudaHostAlloc, the caller's own registration):
